@@ -1,0 +1,178 @@
+/* rdist_b200.h — C ABI of the B200-native R-distance hot path.
+ *
+ * The reference (`rdist`, a pure numpy/scipy package) has no FFI of its own:
+ * its only native crossing is numpy ufuncs and scipy's LAPACK wrappers. Each
+ * entry point below replaces one of those call sites; the reference
+ * file:line it stands in for is given beside it (paths relative to the
+ * reference's pkg/src/rdist/).
+ *
+ * Conventions (all entry points):
+ *   - every pointer argument is a DEVICE pointer unless stated otherwise;
+ *     buffers are caller-owned (the Python host layer passes torch tensors'
+ *     data_ptr()), the library allocates nothing persistent;
+ *   - matrices are row-major float64 with leading dimension `ld` (elements);
+ *     element [i][j] follows the reference orientation: weight / distance of
+ *     the edge or path j -> i (graphs.py:1-8);
+ *   - batched calls take `batch` matrices `stride` elements apart;
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on it (numerical status is written to device memory and read by the
+ *     caller after a stream sync);
+ *   - return value: RDB_OK or an RDB_E* code (argument / launch errors only).
+ */
+#ifndef RDIST_B200_H
+#define RDIST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RDB_ABI_VERSION 1
+#define RDB_NB 128 /* Gauss-Jordan panel width; inverted matrices are padded to a multiple */
+
+/* status codes */
+#define RDB_OK 0
+#define RDB_EINVAL 1    /* bad argument (shape, alignment, null pointer) */
+#define RDB_ESINGULAR 2 /* reserved for callers: pivot below PIVOT_RTOL*scale (linalg.py:33-38) */
+#define RDB_ENOTM 3     /* reserved for callers: no-pivot elimination not certified */
+#define RDB_ECUDA 4     /* CUDA launch / runtime error */
+
+/* Per-matrix pivot record written by the inversion kernels.
+ * min_pivot = min |U_kk| over all elimination steps, i.e. the quantity the
+ * reference thresholds at linalg.py:33-34; flags report why the
+ * no-pivot certificate failed. */
+typedef struct rdb_pivot_info {
+  double min_pivot;
+  int32_t min_index;
+  int32_t flags;
+} rdb_pivot_info;
+#define RDB_PIV_NONPOS 1    /* a pivot <= 0 appeared: not a nonsingular M-matrix */
+#define RDB_PIV_NONFINITE 2 /* a pivot was inf/nan */
+
+/* build modes for rdb_build_m */
+#define RDB_BUILD_X 0 /* out = gamma^W              (resolvent.py:90-98, build_x) */
+#define RDB_BUILD_M 1 /* out = I - gamma^W, identity in the padding (resolvent.py:114-115) */
+
+/* rdb_log_ceil counters, per matrix */
+#define RDB_CNT_NEGATIVE 0  /* entries below NEGATIVE_ENTRY_TOL (resolvent.py:120) */
+#define RDB_CNT_UNDERFLOW 1 /* exact zeros at reachable off-diagonal pairs (resolvent.py:121-124) */
+#define RDB_NCOUNTERS 2
+
+const char* rdb_strerror(int code);
+int rdb_abi_version(void);
+
+/* ---- K1: X = gamma^W or M = I - gamma^W -------------------------------
+ * Replaces np.power(gamma, W) (resolvent.py:98) and np.eye(n) - x
+ * (resolvent.py:115). W entries: +inf = no edge (gamma^inf = 0); W == 1.0
+ * maps to gamma exactly (the bitwise identity test_resolvent.py:72-75
+ * pins). Output is n_pad x n_pad; for RDB_BUILD_M rows/cols >= n are the
+ * identity (so the padded inverse is [[M^-1, 0], [0, I]]). Per-matrix gains
+ * come from `gammas` (device, `batch` entries) or, when it is NULL, from the
+ * scalar `gamma`. */
+int rdb_build_m(const double* w, int64_t ldw, int64_t stride_w, int64_t n, int64_t n_pad,
+                int64_t batch, const double* gammas, double gamma, int mode, double* out,
+                int64_t ldo, int64_t stride_o, void* stream);
+
+/* Same, from bit-packed adjacency: bit (j % 32) of word bits[b][i][j / 32]
+ * set <=> edge j -> i (an unweighted graph, W == 1). words_per_row =
+ * (n + 31) / 32; a graph is n * words_per_row words. */
+int rdb_build_m_bits(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch,
+                     const double* gammas, double gamma, double* out, int64_t ldo,
+                     int64_t stride_o, void* stream);
+
+/* Identity in rows/cols [n, n_pad) of each matrix (embeds a generic matrix
+ * for rdb_invert), zeros elsewhere in the padding. */
+int rdb_pad_identity(double* a, int64_t n, int64_t n_pad, int64_t lda, int64_t stride,
+                     int64_t batch, void* stream);
+
+/* Statistics the reference checks before factorising / iterating
+ * (linalg.py:27-29, :64-65): stats[0] = max |a_ij| over finite entries (the
+ * `scale`), stats[1] = number of non-finite entries, stats[2] = number of
+ * entries violating the Z-matrix sign pattern (off-diagonal > 0 or diagonal
+ * <= 0), stats[3] = number of negative entries. Counts are exact doubles.
+ * `stats` (4 doubles) must be zeroed by the caller. */
+int rdb_matrix_stats(const double* a, int64_t n, int64_t lda, double* stats, void* stream);
+
+/* ---- K2: blocked Gauss-Jordan inversion, FP64 DMMA, no pivoting --------
+ * Replaces scipy.linalg.lu_factor + lu_solve(I) (linalg.py:32, :39).
+ * In place: a <- a^-1. n_pad must be a multiple of RDB_NB, lda even.
+ * Valid without pivoting for nonsingular M-matrices (every M = I - gamma^W
+ * with gamma below the critical gain); `info` (device, batch entries)
+ * records min |pivot| and RDB_PIV_* flags so the caller can apply the
+ * reference's singularity rule and fall back to rdb_invert_pivoted when the
+ * certificate fails. `work` must hold rdb_invert_workspace_bytes(n_pad,
+ * batch) bytes. */
+size_t rdb_invert_workspace_bytes(int64_t n_pad, int64_t batch);
+int rdb_invert_batched(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t batch,
+                       void* work, rdb_pivot_info* info, void* stream);
+int rdb_invert(double* a, int64_t n_pad, int64_t lda, void* work, rdb_pivot_info* info,
+               void* stream);
+
+/* Gauss-Jordan with partial (row) pivoting, first-max pivot choice as
+ * LAPACK idamax; in place, any n. For generic matrices handed to
+ * lu_invert (linalg.py:18-39) that carry no M-matrix certificate.
+ * `work` must hold rdb_invert_pivoted_workspace_bytes(n) bytes. */
+size_t rdb_invert_pivoted_workspace_bytes(int64_t n);
+int rdb_invert_pivoted(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_info* info,
+                       void* stream);
+
+/* ---- K3: R = log Y / log gamma, D = ceil R ------------------------------
+ * Replaces r_distance (resolvent.py:131-143) and rounded_r_distance
+ * (resolvent.py:146-153): y > 0 -> log(y)/log(gamma), else +inf; diagonal
+ * forced 0; D = ceil(R) without nudge. Near-integer quotients are refined
+ * in double-double so exact powers give exact integers (test_resolvent.py:
+ * 137-148). Any of r_out (fp64 R), dceil_out (fp64 D, +inf sentinel) and
+ * d32_out (int32 D, INT32_MAX sentinel) may be NULL; they share ldo /
+ * stride_o. `counters` (device, batch*RDB_NCOUNTERS, caller-zeroed) may be
+ * NULL; `reachable` (uint8 n x n, ldm, one mask shared by the batch) may be
+ * NULL, in which case the underflow counter is not updated. */
+int rdb_log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+                 const double* gammas, double gamma, double* r_out, double* dceil_out,
+                 int32_t* d32_out, int64_t ldo, int64_t stride_o, const uint8_t* reachable,
+                 int64_t ldm, unsigned long long* counters, void* stream);
+
+/* ---- K5: inversion residual max |M Y - I| (resolvent.py:125-127) --------
+ * n_pad a multiple of RDB_NB; *out_max (device) must be zeroed by caller. */
+int rdb_residual(const double* m, int64_t ldm, const double* y, int64_t ldy, int64_t n_pad,
+                 double* out_max, void* stream);
+
+/* ---- K4: power iteration (linalg.py:57-94) ------------------------------
+ * On a non-negative n x n matrix, or (indicator != 0) on the 0/1 pattern
+ * isfinite(m) — adjacency_indicator (graphs.py:114-116) of a weight matrix,
+ * as critical_gain uses it (resolvent.py:156-165). Same start vector,
+ * estimate and stopping rule as the reference. result (device, 3 doubles):
+ * value, converged (0/1), iterations. work: rdb_power_workspace_bytes(n). */
+size_t rdb_power_workspace_bytes(int64_t n);
+int rdb_power_iteration(const double* m, int64_t n, int64_t ldm, int indicator, double tol,
+                        int64_t max_iter, void* work, double* result, void* stream);
+
+/* ---- K6: greedy-descent next hop (navigation.py:63-67) -----------------
+ * For each target t in `targets` (device int32, n_targets) and every vertex
+ * j: next[r][j] = the successor k of j (W[k][j] finite, ascending k) that
+ * minimises W[k][j] + dist[t][k], first minimum on ties; -1 when j == t,
+ * when j has no successor, or when the best score is not finite (the
+ * reference's stop conditions, navigation.py:62-69). W and dist are n x n;
+ * next is n_targets x n (ldn). work: rdb_next_hop_workspace_bytes(n, nnz)
+ * where nnz = number of finite off-diagonal W entries (rdb_count_edges). */
+int rdb_count_edges(const double* w, int64_t n, int64_t ldw, unsigned long long* out_nnz,
+                    void* stream);
+size_t rdb_next_hop_workspace_bytes(int64_t n, int64_t nnz);
+int rdb_next_hop(const double* w, int64_t ldw, const double* dist, int64_t ldd, int64_t n,
+                 int64_t nnz, const int32_t* targets, int64_t n_targets, int32_t* next,
+                 int64_t ldn, void* work, void* stream);
+
+/* ---- batched APSP (the config-2 workload in one call) -------------------
+ * bits -> M (K1) -> in-place inverse (K2) -> int32 D (K3) for `batch`
+ * unweighted graphs of n vertices with per-graph gains. `mwork` holds
+ * batch * n_pad * n_pad doubles, `work` rdb_invert_workspace_bytes(n_pad,
+ * batch) bytes; d32 is batch x n x n (ld n). */
+int rdb_apsp_bits_batched(const uint32_t* bits, int64_t n, int64_t batch, const double* gammas,
+                          double* mwork, void* work, rdb_pivot_info* info, int32_t* d32,
+                          unsigned long long* counters, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RDIST_B200_H */

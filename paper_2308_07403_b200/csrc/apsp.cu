@@ -1,0 +1,52 @@
+// Library entry points that chain the kernels, and error strings.
+//
+// rdb_apsp_bits_batched is the config-2 workload in one call: the reference's
+// per-graph run_rdist closure (pkg/src/rdist/experiments.py:305-310:
+// resolvent(with_residual=False) -> r_distance -> ceil) for a whole batch of
+// unweighted graphs, with per-graph gains.
+#include "common.cuh"
+
+namespace rdb {
+int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
+                   rdb_pivot_info* info, cudaStream_t st);
+int log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+             const double* gammas, double gamma, double* r_out, double* dceil_out, int32_t* d32_out,
+             int64_t ldo, int64_t stride_o, const uint8_t* reachable, int64_t ldm,
+             unsigned long long* counters, cudaStream_t st);
+}  // namespace rdb
+
+extern "C" const char* rdb_strerror(int code) {
+  switch (code) {
+    case RDB_OK:
+      return "ok";
+    case RDB_EINVAL:
+      return "invalid argument (shape, alignment or null pointer)";
+    case RDB_ESINGULAR:
+      return "singular to working precision";
+    case RDB_ENOTM:
+      return "no-pivot elimination not certified (not a nonsingular M-matrix)";
+    case RDB_ECUDA:
+      return "CUDA launch or runtime error";
+    default:
+      return "unknown error";
+  }
+}
+
+extern "C" int rdb_abi_version(void) { return RDB_ABI_VERSION; }
+
+extern "C" int rdb_apsp_bits_batched(const uint32_t* bits, int64_t n, int64_t batch,
+                                     const double* gammas, double* mwork, void* work,
+                                     rdb_pivot_info* info, int32_t* d32,
+                                     unsigned long long* counters, void* stream) {
+  if (!bits || !gammas || !mwork || !work || !info || !d32 || n <= 0 || batch <= 0)
+    return RDB_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n_pad = (n + RDB_NB - 1) / RDB_NB * RDB_NB;
+  const int64_t stride = n_pad * n_pad;
+  int rc = rdb_build_m_bits(bits, n, n_pad, batch, gammas, 0.0, mwork, n_pad, stride, stream);
+  if (rc) return rc;
+  rc = rdb::invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st);
+  if (rc) return rc;
+  return rdb::log_ceil(mwork, n, n_pad, stride, batch, gammas, 0.0, nullptr, nullptr, d32, n, n * n,
+                       nullptr, 0, counters, st);
+}

@@ -1,0 +1,177 @@
+// K1: X = gamma^W / M = I - gamma^W, elementwise and HBM-bound
+// (reference: np.power(gamma, W) at pkg/src/rdist/resolvent.py:98 and
+// np.eye(n) - x at resolvent.py:115), plus the matrix statistics the
+// reference's lu_invert checks (linalg.py:27-29) and identity padding.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace rdb {
+
+// gamma^w with the reference's special cases: w == 1 gives gamma exactly
+// (IEEE pow(x, 1) == x; asserted bitwise by test_resolvent.py:72-75) and
+// w == +inf gives 0 for 0 < gamma < 1.
+RDB_DEV double gain_pow(double g, double w) {
+  if (w == 1.0) return g;
+  if (isinf(w) && w > 0) return 0.0;
+  return pow(g, w);
+}
+
+// One thread per 2 columns of one row (grid-stride over rows).
+__global__ void build_m_kernel(const double* __restrict__ w, int64_t ldw, int64_t stride_w, int64_t n,
+                               int64_t n_pad, const double* __restrict__ gammas, double gamma,
+                               int mode, double* __restrict__ out, int64_t ldo, int64_t stride_o) {
+  const int64_t b = blockIdx.z;
+  const double g = gammas ? gammas[b] : gamma;
+  const double* W = w + b * stride_w;
+  double* O = out + b * stride_o;
+  const int64_t ncols = (mode == RDB_BUILD_M) ? n_pad : n;
+  for (int64_t i = blockIdx.y; i < ncols; i += gridDim.y) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ncols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      double v;
+      if (i < n && j < n) {
+        const double x = gain_pow(g, W[i * ldw + j]);
+        v = (mode == RDB_BUILD_M) ? ((i == j ? 1.0 : 0.0) - x) : x;
+      } else {
+        v = (i == j) ? 1.0 : 0.0;
+      }
+      O[i * ldo + j] = v;
+    }
+  }
+}
+
+// Bit-packed adjacency -> M. Thread handles 2 adjacent columns (double2 store).
+__global__ void build_m_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t n_pad,
+                                    const double* __restrict__ gammas, double gamma,
+                                    double* __restrict__ out, int64_t ldo, int64_t stride_o) {
+  const int64_t b = blockIdx.z;
+  const double g = gammas ? gammas[b] : gamma;
+  const int64_t wpr = (n + 31) / 32;
+  const uint32_t* Bb = bits + b * n * wpr;
+  double* O = out + b * stride_o;
+  for (int64_t i = blockIdx.y; i < n_pad; i += gridDim.y) {
+    for (int64_t j = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); j < n_pad;
+         j += 2 * (int64_t)gridDim.x * blockDim.x) {
+      double v[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t jj = j + e;
+        if (i < n && jj < n) {
+          const uint32_t word = Bb[i * wpr + (jj >> 5)];
+          const bool edge = (word >> (jj & 31)) & 1u;
+          v[e] = (i == jj) ? 1.0 : (edge ? -g : 0.0);
+        } else {
+          v[e] = (i == jj) ? 1.0 : 0.0;
+        }
+      }
+      stg2(O + i * ldo + j, make_double2(v[0], v[1]));
+    }
+  }
+}
+
+__global__ void pad_identity_kernel(double* __restrict__ a, int64_t n, int64_t n_pad, int64_t lda,
+                                    int64_t stride) {
+  double* A = a + (int64_t)blockIdx.z * stride;
+  for (int64_t i = blockIdx.y; i < n_pad; i += gridDim.y) {
+    const int64_t j_begin = (i < n) ? n : 0;
+    for (int64_t j = j_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_pad;
+         j += (int64_t)gridDim.x * blockDim.x)
+      A[i * lda + j] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+// stats[0] max|a| (atomic on the bit pattern), [1] non-finite count,
+// [2] Z-pattern violations, [3] negative entries.
+__global__ void matrix_stats_kernel(const double* __restrict__ a, int64_t n, int64_t lda,
+                                    double* __restrict__ stats) {
+  double mx = 0.0;
+  unsigned nonfinite = 0, nonz = 0, neg = 0;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      const double v = a[i * lda + j];
+      const double av = fabs(v);
+      if (!(av <= 1.7976931348623157e308)) {
+        ++nonfinite;
+      } else {
+        mx = fmax(mx, av);
+      }
+      if (i == j ? !(v > 0.0) : (v > 0.0)) ++nonz;
+      if (v < 0.0) ++neg;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  nonfinite = __reduce_add_sync(0xffffffffu, nonfinite);
+  nonz = __reduce_add_sync(0xffffffffu, nonz);
+  neg = __reduce_add_sync(0xffffffffu, neg);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(&stats[0], mx);
+    // counts are kept as doubles (exact below 2^53)
+    if (nonfinite) atomicAdd(&stats[1], (double)nonfinite);
+    if (nonz) atomicAdd(&stats[2], (double)nonz);
+    if (neg) atomicAdd(&stats[3], (double)neg);
+  }
+}
+
+static dim3 grid2d(int64_t cols, int64_t rows, int64_t batch, int threads, int per_thread = 1) {
+  int64_t gx = (cols + (int64_t)threads * per_thread - 1) / ((int64_t)threads * per_thread);
+  if (gx < 1) gx = 1;
+  if (gx > 1024) gx = 1024;
+  int64_t gy = rows < 1 ? 1 : rows;
+  if (gy > 65535) gy = 65535;
+  return dim3((unsigned)gx, (unsigned)gy, (unsigned)batch);
+}
+
+}  // namespace rdb
+
+using namespace rdb;
+
+extern "C" int rdb_build_m(const double* w, int64_t ldw, int64_t stride_w, int64_t n, int64_t n_pad,
+                           int64_t batch, const double* gammas, double gamma, int mode, double* out,
+                           int64_t ldo, int64_t stride_o, void* stream) {
+  if (!w || !out || n <= 0 || batch <= 0 || batch > 65535 || ldw < n) return RDB_EINVAL;
+  if (mode != RDB_BUILD_X && mode != RDB_BUILD_M) return RDB_EINVAL;
+  if (mode == RDB_BUILD_M && n_pad < n) return RDB_EINVAL;
+  const int64_t cols = (mode == RDB_BUILD_M) ? n_pad : n;
+  if (ldo < cols) return RDB_EINVAL;
+  if (!gammas && !(gamma > 0.0 && gamma < 1.0)) return RDB_EINVAL;
+  build_m_kernel<<<grid2d(cols, cols, batch, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      w, ldw, stride_w, n, n_pad, gammas, gamma, mode, out, ldo, stride_o);
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+
+extern "C" int rdb_build_m_bits(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch,
+                                const double* gammas, double gamma, double* out, int64_t ldo,
+                                int64_t stride_o, void* stream) {
+  if (!bits || !out || n <= 0 || n_pad < n || (n_pad & 1) || (ldo & 1) || ldo < n_pad ||
+      batch <= 0 || batch > 65535 || ((uintptr_t)out & 15))
+    return RDB_EINVAL;
+  if (!gammas && !(gamma > 0.0 && gamma < 1.0)) return RDB_EINVAL;
+  build_m_bits_kernel<<<grid2d(n_pad, n_pad, batch, 256, 2), 256, 0,
+                        static_cast<cudaStream_t>(stream)>>>(bits, n, n_pad, gammas, gamma, out, ldo,
+                                                             stride_o);
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+
+extern "C" int rdb_pad_identity(double* a, int64_t n, int64_t n_pad, int64_t lda, int64_t stride,
+                                int64_t batch, void* stream) {
+  if (!a || n < 0 || n_pad < n || lda < n_pad || batch <= 0 || batch > 65535) return RDB_EINVAL;
+  if (n_pad == n) return RDB_OK;
+  pad_identity_kernel<<<grid2d(n_pad, n_pad, batch, 256), 256, 0,
+                        static_cast<cudaStream_t>(stream)>>>(a, n, n_pad, lda, stride);
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+
+extern "C" int rdb_matrix_stats(const double* a, int64_t n, int64_t lda, double* stats,
+                                void* stream) {
+  if (!a || !stats || n <= 0 || lda < n) return RDB_EINVAL;
+  int64_t gy = n < 4096 ? n : 4096;
+  matrix_stats_kernel<<<grid2d(n, gy, 1, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      a, n, lda, stats);
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}

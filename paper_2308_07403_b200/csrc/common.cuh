@@ -1,0 +1,91 @@
+// Shared device helpers for the R-distance kernels (sm_100a).
+//
+// FP64 on sm_100a: the only FP64 tensor instruction is DMMA.8x8x4
+// (PTX mma.sync.aligned.m8n8k4.row.col.f64); tcgen05.mma has no f64 kind,
+// so the Blackwell-specific parts used here are the bulk-copy (TMA) engine
+// (cp.async.bulk, SASS UBLKCP) and mbarrier transaction counting.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/rdist_b200.h"
+
+#define RDB_DEV __device__ __forceinline__
+
+namespace rdb {
+
+constexpr int NB = RDB_NB;  // Gauss-Jordan panel width (128)
+
+// ---------------------------------------------------------------- DMMA
+// D(8x8) += A(8x4, row) * B(4x8, col). Lane l holds A[l/4][l%4], B[l%4][l/4],
+// and C[l/4][2*(l%4) + {0,1}].
+RDB_DEV void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- mbarrier
+RDB_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+RDB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+RDB_DEV void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+RDB_DEV void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+RDB_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+RDB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared through the TMA unit, completing on `bar`.
+// dst/src 16-byte aligned, bytes a multiple of 16.
+RDB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------- misc
+RDB_DEV double2 ldg2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+RDB_DEV void stg2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+// Monotone int64 key for non-negative doubles (IEEE ordering == integer ordering).
+RDB_DEV void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+}  // namespace rdb
+
+#define RDB_LAUNCH_CHECK()                                   \
+  do {                                                       \
+    cudaError_t _e = cudaGetLastError();                     \
+    if (_e != cudaSuccess) return RDB_ECUDA;                 \
+  } while (0)

@@ -1,0 +1,179 @@
+"""Generate the golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference package ``rdist`` from
+/root/reference/pkg/src, feeds it seeded inputs built with this repo's
+generators (whose ER pattern is the reference's own gen_random_dense
+recipe — checked below), and writes compressed .npz fixtures next to this
+file. Tests compare the oracle (CPU) and the CUDA path (GPU) against them;
+nothing at test / bench time reads /root/reference.
+
+Environment recorded in meta.json: numpy/scipy versions and BLAS threads.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parents[1]
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(REPO))
+
+import rdist  # noqa: E402  (the reference)
+import scipy  # noqa: E402
+
+from paper_2308_07403_b200 import workloads as wl  # noqa: E402
+
+
+def whash(w: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(w, dtype=np.float64).tobytes()).hexdigest()[:16]
+
+
+def d_u8(d: np.ndarray) -> np.ndarray:
+    """fp64 D (small non-negative ints, +inf) -> uint8 with 255 for inf."""
+    out = np.full(d.shape, 255, dtype=np.uint8)
+    fin = np.isfinite(d)
+    assert (d[fin] < 255).all() and (d[fin] == np.round(d[fin])).all()
+    out[fin] = d[fin].astype(np.uint8)
+    return out
+
+
+def min_gap(r: np.ndarray) -> float:
+    off = ~np.eye(r.shape[0], dtype=bool) & np.isfinite(r)
+    g = np.abs(r[off] - np.round(r[off]))
+    g = g[g > 0]
+    return float(g.min()) if g.size else math.inf
+
+
+def ug(w):
+    return rdist.Graph(w.shape[0], w, rdist.GraphKind.UNWEIGHTED)
+
+
+def main() -> None:
+    out: dict[str, dict[str, np.ndarray]] = {}
+    meta: dict[str, object] = {
+        "numpy": np.__version__,
+        "scipy": scipy.__version__,
+        "reference": "/root/reference/pkg/src/rdist (rdist " + rdist.__version__ + ")",
+    }
+    try:
+        from threadpoolctl import threadpool_info
+
+        meta["blas"] = [{k: i.get(k) for k in ("internal_api", "version", "num_threads")} for i in threadpool_info()]
+    except Exception:  # noqa: BLE001
+        pass
+
+    # --- known-answer tests from the reference's own test suite -------------
+    chain2 = rdist.graph_from_edge_list(rdist.EdgeList(2, ((0, 1, 1.0),)), rdist.GraphKind.UNWEIGHTED)
+    ring3 = rdist.graph_from_edge_list(
+        rdist.EdgeList(3, tuple((i, (i + 1) % 3, 1.0) for i in range(3))), rdist.GraphKind.UNWEIGHTED
+    )
+    grid4 = rdist.gen_grid(4)
+    kat = {
+        "chain2_w": chain2.weights,
+        "chain2_y": rdist.resolvent(chain2, 0.5).y,
+        "chain2_r": rdist.r_distance(rdist.resolvent(chain2, 0.5)),
+        "ring3_w": ring3.weights,
+        "ring3_y_0p1": rdist.resolvent(ring3, 0.1).y,
+        "grid4_w": grid4.weights,
+        "grid4_d_1em3": rdist.rounded_r_distance(rdist.resolvent(grid4, 1e-3)),
+        "grid4_bfs": rdist.bfs_apsp(grid4),
+        "exact_power_r": rdist.r_distance(
+            rdist.ResolventResult(np.array([[1.0, 0.3**2], [0.3, 1.0]]), 0.3, rdist.HealthFlags(False, None, 0.0))
+        ),
+        "complete7_rho": np.array(rdist.spectral_radius(np.ones((7, 7)) - np.eye(7), tol=1e-8)),
+        "k11_gc": np.array(rdist.critical_gain(rdist.gen_random_dense(11, 1.0, 0))),
+    }
+    rng = np.random.default_rng(7)
+    gen = (rng.uniform(-10, 10, (5, 5)) + 20 * np.eye(5))
+    kat["generic5_m"] = gen
+    kat["generic5_inv"] = rdist.lu_invert(gen)
+    out["kat"] = kat
+
+    # --- config 1: N=512 ER p=0.05 gamma=1e-3 (full size) --------------------
+    c = wl.CFG1
+    g_ref = rdist.gen_random_dense(c["n"], c["p"], 0)
+    w1 = wl.er_graph(c["n"], c["p"], 0).weights
+    assert np.array_equal(g_ref.weights, w1), "ER generator must reproduce gen_random_dense"
+    res = rdist.resolvent(g_ref, c["gamma"])
+    r1 = rdist.r_distance(res)
+    d1 = np.ceil(r1)
+    bfs1 = rdist.bfs_apsp(g_ref)
+    fw1 = rdist.floyd_warshall(g_ref)
+    assert np.array_equal(d1, bfs1) and np.array_equal(bfs1, fw1)
+    pi = rdist.power_iteration(rdist.adjacency_indicator(g_ref))
+    out["cfg1"] = {
+        "seed": np.array(0),
+        "w_hash": np.array(whash(w1)),
+        "d": d_u8(d1),
+        "r": r1,
+        "residual": np.array(res.health.inversion_residual),
+        "min_gap": np.array(min_gap(r1)),
+        "rho": np.array(pi.value),
+        "rho_iters": np.array(pi.iterations),
+        "critical_gain": np.array(rdist.critical_gain(g_ref)),
+    }
+
+    # --- config 2 samples: ER + lattices at N=1024 ----------------------------
+    for kind, seed in (("er", 2000), ("lattice", 1000), ("lattice", 1001), ("lattice", 1004)):
+        w = wl.weights_from_present(wl.cfg2_present(kind, seed))
+        gamma = wl.cfg2_gamma(kind)
+        r = rdist.r_distance(rdist.resolvent(ug(w), gamma, with_residual=False))
+        d = np.ceil(r)
+        off = np.isfinite(r) & ~np.eye(w.shape[0], dtype=bool)
+        out[f"cfg2_{kind}_{seed}"] = {
+            "kind": np.array(kind),
+            "seed": np.array(seed),
+            "gamma": np.array(gamma),
+            "w_hash": np.array(whash(w)),
+            "d": d_u8(d),
+            "min_gap": np.array(min_gap(r)),
+            "exact_int": np.array(int((r[off] == np.round(r[off])).sum())),
+        }
+
+    # --- config 4 analogue (smaller N): weighted U[1,5], R and next hops ------
+    n4 = 384
+    gw = wl.weighted_er_graph(n4, 0.1, 1.0, 5.0, 42)
+    g4 = rdist.Graph(n4, np.array(gw.weights), rdist.GraphKind.REAL_WEIGHTED)
+    r4 = rdist.r_distance(rdist.resolvent(g4, 1e-3, with_residual=False))
+    nxt = np.full((n4, n4), -1, dtype=np.int16)
+    for t in range(n4):
+        for j in range(n4):
+            pr = rdist.greedy_descent(g4, r4, j, t, max_steps=1)
+            if pr.steps_taken == 1:
+                nxt[t, j] = pr.vertices[1]
+    paths = []
+    prng = np.random.default_rng(5)
+    for _ in range(64):
+        s, t = (int(x) for x in prng.integers(0, n4, 2))
+        pr = rdist.greedy_descent(g4, r4, s, t)
+        paths.append((s, t, pr.length, int(pr.reached), pr.steps_taken, len(pr.vertices)))
+    out["cfg4_small"] = {
+        "n": np.array(n4),
+        "seed": np.array(42),
+        "gamma": np.array(1e-3),
+        "w_hash": np.array(whash(gw.weights)),
+        "r": r4,
+        "next": nxt,
+        "paths": np.array(paths, dtype=np.float64),
+    }
+
+    for name, arrays in out.items():
+        np.savez_compressed(HERE / f"{name}.npz", **arrays)
+    (HERE / "meta.json").write_text(json.dumps(meta, indent=1) + "\n")
+    for p in sorted(HERE.glob("*.npz")):
+        print(p.name, p.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,131 @@
+"""Config-level parity of the CUDA path against the reference (golden
+fixtures produced by the reference itself) and the CPU oracle.
+
+Bars (BASELINE.json north_star): D and next hops bit-exact; R within 1e-9
+relative where R <= 50 (checked far tighter here where the oracle is run on
+the same inputs).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2308_07403_b200 as rb
+import rdist_oracle as orc
+from helpers import u8_to_d
+from paper_2308_07403_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+R_RTOL = 1e-9  # north_star tolerance for real-valued R
+
+
+def int32_to_d(d32):
+    d = d32.astype(np.float64)
+    d[d32 == rb.UNREACHABLE] = np.inf
+    return d
+
+
+def test_cfg1_full(cuda, golden):
+    f = golden("cfg1")
+    g = wl.er_graph(512, 0.05, int(f["seed"]))
+    res = rb.resolvent(g, 1e-3)
+    d = rb.rounded_r_distance(res)
+    np.testing.assert_array_equal(d, u8_to_d(f["d"]))
+    r = rb.r_distance(res)
+    np.testing.assert_allclose(r, f["r"], rtol=1e-13, atol=0)
+    assert res.health.inversion_residual < 1e-12 and not res.health.negative_entries
+    assert rb.critical_gain(g) == pytest.approx(float(f["critical_gain"]), rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["cfg2_er_2000", "cfg2_lattice_1000", "cfg2_lattice_1001", "cfg2_lattice_1004"])
+def test_cfg2_golden_batch_api(cuda, golden, name):
+    f = golden(name)
+    kind, seed, gamma = str(f["kind"]), int(f["seed"]), float(f["gamma"])
+    bits = wl.pack_bits(wl.cfg2_present(kind, seed))[None]
+    d32 = rb.rounded_r_distance_batch(bits, [gamma], 1024)
+    np.testing.assert_array_equal(int32_to_d(d32[0]), u8_to_d(f["d"]))
+
+
+def test_cfg2_golden_drop_in_api(cuda, golden):
+    # the same graphs through the reference-shaped per-graph API
+    for name in ("cfg2_er_2000", "cfg2_lattice_1004"):
+        f = golden(name)
+        kind, seed, gamma = str(f["kind"]), int(f["seed"]), float(f["gamma"])
+        g = rb.Graph(1024, wl.weights_from_present(wl.cfg2_present(kind, seed)), rb.GraphKind.UNWEIGHTED)
+        d = rb.rounded_r_distance(rb.resolvent(g, gamma, with_residual=False))
+        np.testing.assert_array_equal(d, u8_to_d(f["d"]))
+
+
+def test_cfg2_batch_mixed_gammas_vs_oracle(cuda):
+    # a 16-graph slice of the config-2 batch (ER + lattice, mixed gains)
+    seeds = wl.cfg2_seeds(256)
+    pick = seeds[120:136]
+    present = [wl.cfg2_present(k, s) for k, s in pick]
+    bits = np.stack([wl.pack_bits(p) for p in present])
+    gammas = np.array([wl.cfg2_gamma(k) for k, _ in pick])
+    d32 = rb.rounded_r_distance_batch(bits, gammas, 1024, chunk=5)
+    for b, (p, gm) in enumerate(zip(present, gammas)):
+        ref = orc.run_rdist(wl.weights_from_present(p), gm)
+        np.testing.assert_array_equal(int32_to_d(d32[b]), ref, err_msg=f"graph {pick[b]}")
+
+
+def test_cfg2_full_batch_properties(cuda):
+    # all 256 graphs, device-resident path; size-independent properties:
+    # zero diagonal, D == 1 exactly on edges, D >= 2 elsewhere, sentinel
+    # exactly where the graph has no path (zero pattern of Y = reachability)
+    bits, gammas, seeds = wl.cfg2_batch(256)
+    dev_bits = torch.from_numpy(bits.view(np.int32)).cuda()
+    d = rb.rounded_r_distance_batch_device(dev_bits, torch.from_numpy(gammas).cuda(), 1024).cpu().numpy()
+    host = rb.rounded_r_distance_batch(bits[:8], gammas[:8], 1024)
+    np.testing.assert_array_equal(d[:8], host)
+    for b in range(0, 256, 17):
+        present = wl.unpack_bits(bits[b], 1024)
+        db = d[b]
+        assert (np.diagonal(db) == 0).all()
+        assert (db[present] == 1).all()
+        off = ~present & ~np.eye(1024, dtype=bool)
+        assert (db[off] >= 2).all()
+        reach = np.isfinite(orc.bfs_apsp(wl.weights_from_present(present)))
+        assert np.array_equal(db != rb.UNREACHABLE, reach), seeds[b]
+
+
+def test_cfg4_small_golden(cuda, golden):
+    f = golden("cfg4_small")
+    n = int(f["n"])
+    g = wl.weighted_er_graph(n, 0.1, 1.0, 5.0, int(f["seed"]))
+    r = rb.r_distance(rb.resolvent(g, 1e-3, with_residual=False))
+    np.testing.assert_allclose(r, f["r"], rtol=1e-13, atol=0)
+    nxt = rb.next_hop_table(g, r)
+    np.testing.assert_array_equal(nxt, f["next"].astype(np.int32))
+    for s, t, length, reached, steps, nv in f["paths"]:
+        pr = rb.greedy_descent(g, f["r"], int(s), int(t))
+        assert (pr.length, int(pr.reached), pr.steps_taken, len(pr.vertices)) == (length, int(reached), int(steps), int(nv))
+
+
+def test_cfg4_full_sampled_targets(cuda):
+    c = wl.CFG4
+    g = wl.weighted_er_graph(c["n"], c["p"], c["w_lo"], c["w_hi"], 42)
+    w = np.asarray(g.weights)
+    r = rb.r_distance(rb.resolvent(g, c["gamma"], with_residual=False))
+    r_ref = orc.r_distance(orc.resolvent_y(w, c["gamma"]), c["gamma"])
+    fin = np.isfinite(r_ref) & (r_ref <= 50)
+    assert np.array_equal(np.isfinite(r), np.isfinite(r_ref))
+    rel = np.abs(r[fin] - r_ref[fin]) / np.maximum(np.abs(r_ref[fin]), 1e-300)
+    assert rel.max() < R_RTOL and rel.max() < 1e-13
+    targets = np.random.default_rng(1).choice(c["n"], 256, replace=False)
+    got = rb.next_hop_table(g, r_ref, targets)
+    ref = orc.next_hop_table(w, r_ref, targets)
+    np.testing.assert_array_equal(got, ref)
+    # and from the GPU's own R (ties/gaps are far above the R error)
+    np.testing.assert_array_equal(rb.next_hop_table(g, r, targets), ref)
+
+
+def test_cfg3_full(cuda):
+    c = wl.CFG3
+    g = wl.er_graph(c["n"], c["p"], 0)
+    w = np.asarray(g.weights)
+    d = rb.rounded_r_distance(rb.resolvent(g, c["gamma"], with_residual=False))
+    ref = orc.run_rdist(w, c["gamma"])
+    np.testing.assert_array_equal(d, ref)
+    assert set(np.unique(d[~np.eye(c["n"], dtype=bool)])) <= {1.0, 2.0}
