@@ -10,56 +10,63 @@
 // reference's diag(U) (linalg.py:33-34).
 //
 // Per panel p = [k*NB, (k+1)*NB), r = all other indices, in place on A:
-//   P1  D = A_pp^-1            (one CTA per matrix, unblocked GJ, pivots recorded)
-//   P2  A_pr = D * A_pr        (DMMA tiles over the row panel)
-//       Cw   = A_rp (copy)     (the update overwrites A_rp)
-//   U   A_rr = A_rr - Cw * A_pr ;  A_rp = -Cw * D   (one DMMA tile kernel)
-// After the last panel A = M^-1 (2n^3 flop in total).
+//   P1 (gj_panel_kernel, block x = 0)  D = A_pp^-1, pivots recorded; Dt = D^T
+//   P1 (gj_panel_kernel, blocks x > 0) CwT = -(A_rp)^T   (the update overwrites A_rp)
+//   P2 (engine, store)                 A_pJ = D * A_pJ             for J != p
+//   U  (engine, reduce-add / store)    A_IJ += CwT^T * A_pJ        for I != p, J != p
+//                                      A_Ip  = CwT^T * D           (= -A_Ip D)
+// After the last panel A = M^-1 (2n^3 flop in total). P2 and U run on the
+// persistent warp-specialised DMMA engine (dmma_engine.cuh).
 #include <cmath>
 
-#include "tile_mma.cuh"
+#include "dmma_engine.cuh"
 
 namespace rdb {
 
 // ------------------------------------------------------------------ P1
-// Unblocked Gauss-Jordan inverse of the NB x NB diagonal block, in place.
-// 512 threads; thread (rg = t/128, j = t%128) keeps column j, rows 32*rg..+32
-// of the block in registers. Each step publishes the pivot row and column
-// through shared memory (double-buffered) and applies a rank-1 update.
+// Block x = 0: unblocked Gauss-Jordan inverse of the NB x NB diagonal block,
+// in place; thread (rg = t/128, j = t%128) keeps column j, rows 32*rg..+32 in
+// registers; each step publishes the pivot row / column through shared memory.
+// Blocks x > 0: rows [64(x-1), 64x) of the column panel, negated and
+// transposed into CwT (128 x n per matrix).
 constexpr int P1_THREADS = 512;
+constexpr int CP_ROWS = 64;
+constexpr int CP_ST = CP_ROWS + 1;
+constexpr size_t P1_SMEM = (size_t)NB * CP_ST * sizeof(double);
 
-__global__ void __launch_bounds__(P1_THREADS, 1)
-    gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int p0,
-                    rdb_pivot_info* __restrict__ info, int first) {
-  __shared__ double prow[2][NB];
-  __shared__ double pcol[2][NB];
+__device__ __noinline__ void panel_inverse(double* __restrict__ A, int64_t lda, int p0,
+                                           rdb_pivot_info* __restrict__ inf, int first,
+                                           double* __restrict__ dt, double* smem) {
+  double* prow = smem;           // [2][NB]
+  double* pcol = smem + 2 * NB;  // [2][NB]
+  double* pinv_s = smem + 4 * NB;  // [2]
   const int t = threadIdx.x;
   const int j = t & (NB - 1);
   const int rg = t >> 7;
-  double* A = a + (int64_t)blockIdx.x * stride + (int64_t)p0 * lda + p0;
   double v[32];
 #pragma unroll
   for (int r = 0; r < 32; ++r) v[r] = A[(int64_t)(32 * rg + r) * lda + j];
 
   double minp = INFINITY;
   int mini = -1, flags = 0;
-
   int buf = 0;
 #pragma unroll 1
   for (int q = 0; q < 4; ++q) {
 #pragma unroll
     for (int s = 0; s < 32; ++s) {
       const int kk = 32 * q + s;
-      // publish pivot row kk and pivot column kk
-      if (rg == q) prow[buf][j] = v[s];
+      if (rg == q) {
+        prow[buf * NB + j] = v[s];
+        if (j == kk) pinv_s[buf] = 1.0 / v[s];
+      }
       if (j == kk) {
 #pragma unroll
-        for (int r = 0; r < 32; ++r) pcol[buf][32 * rg + r] = v[r];
+        for (int r = 0; r < 32; ++r) pcol[buf * NB + 32 * rg + r] = v[r];
       }
       __syncthreads();
-      const double p = prow[buf][kk];
-      const double pinv = 1.0 / p;
+      const double pinv = pinv_s[buf];
       if (t == 0) {
+        const double p = prow[buf * NB + kk];
         const double ap = fabs(p);
         if (!(ap < INFINITY)) flags |= RDB_PIV_NONFINITE;
         if (!(p > 0.0)) flags |= RDB_PIV_NONPOS;
@@ -68,30 +75,31 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
           mini = kk;
         }
       }
-      const double u = (j == kk) ? pinv : prow[buf][j] * pinv;
+      const double u = (j == kk) ? pinv : prow[buf * NB + j] * pinv;
       if (j == kk) {
         // column kk of the result is -f_i * pinv: start from 0 so the common
         // fma(-f, u, v) below produces exactly that.
 #pragma unroll
         for (int r = 0; r < 32; ++r) v[r] = 0.0;
       }
+      const double* pc = pcol + buf * NB + 32 * rg;
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         if (r == s && rg == q) {
           v[r] = u;
         } else {
-          const double f = pcol[buf][32 * rg + r];
-          v[r] = fma(-f, u, v[r]);
+          v[r] = fma(-pc[r], u, v[r]);
         }
       }
       buf ^= 1;
     }
   }
 #pragma unroll
-  for (int r = 0; r < 32; ++r) A[(int64_t)(32 * rg + r) * lda + j] = v[r];
-
+  for (int r = 0; r < 32; ++r) {
+    A[(int64_t)(32 * rg + r) * lda + j] = v[r];
+    dt[(int64_t)j * NB + 32 * rg + r] = v[r];
+  }
   if (t == 0) {
-    rdb_pivot_info* inf = info + blockIdx.x;
     if (first) {
       inf->min_pivot = minp;
       inf->min_index = p0 + mini;
@@ -106,86 +114,121 @@ __global__ void __launch_bounds__(P1_THREADS, 1)
   }
 }
 
-// ------------------------------------------------------------------ P2
-// grid (n/TN, batch). Column tile J (TN wide):
-//   * copy Cw[i][0:NB] = A[i][p0:p0+NB] for rows i in [J*TN, J*TN+TN) outside p;
-//   * if J is outside p: A[p0:p0+NB][J] = D * A[p0:p0+NB][J] (DMMA tile, K = NB).
-__global__ void __launch_bounds__(TILE_THREADS, 2)
-    gj_rowpanel_kernel(double* __restrict__ a, int64_t n, int64_t lda, int64_t stride, int p0,
-                       double* __restrict__ cw_all) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  TileSmem& s = *reinterpret_cast<TileSmem*>(smem_raw);
-  const int J = blockIdx.x;
+__global__ void __launch_bounds__(P1_THREADS, 1)
+    gj_panel_kernel(double* __restrict__ a, int64_t n, int64_t lda, int64_t stride, int p0,
+                    rdb_pivot_info* __restrict__ info, int first, double* __restrict__ cwt_all,
+                    double* __restrict__ dt_all) {
+  extern __shared__ __align__(16) double smem[];
   const int64_t b = blockIdx.y;
   double* A = a + b * stride;
-  double* cw = cw_all + b * n * NB;
-  const int col0 = J * TN;
-  const bool in_panel = (col0 >= p0) && (col0 < p0 + NB);
-
-  // column-panel copy (rows col0 .. col0+TN; row-tile and column-tile index sets coincide)
-  if (!in_panel) {
-    const int tid = threadIdx.x;
-    // TN rows x NB cols = TN * NB/2 double2
-    for (int e = tid; e < TN * (NB / 2); e += TILE_THREADS) {
-      const int r = e / (NB / 2), c2 = e % (NB / 2);
-      const int64_t i = col0 + r;
-      stg2(cw + i * NB + 2 * c2, ldg2(A + i * lda + p0 + 2 * c2));
-    }
+  if (blockIdx.x == 0) {
+    panel_inverse(A + (int64_t)p0 * lda + p0, lda, p0, info + b, first, dt_all + b * NB * NB, smem);
+    return;
   }
-  if (in_panel) return;
-
-  Acc acc;
-  acc_zero(acc);
-  const double* D = A + (int64_t)p0 * lda + p0;
-  const double* Bp = A + (int64_t)p0 * lda + col0;
-  tile_mainloop(s, acc, D, lda, Bp, lda, NB);
-  double* out = A + (int64_t)p0 * lda + col0;
-  tile_epilogue(acc, [&](int r, int c, double x0, double x1) {
-    stg2(out + (int64_t)r * lda + c, make_double2(x0, x1));
-  });
+  const int64_t i0 = (int64_t)(blockIdx.x - 1) * CP_ROWS;
+  if (i0 >= p0 && i0 < p0 + NB) return;  // rows of the panel itself: not needed by the update
+  // load A[i0 + il][p0 + k] (coalesced along k) -> T[k][il]
+  for (int e = threadIdx.x; e < CP_ROWS * NB; e += P1_THREADS) {
+    const int il = e / NB, k = e % NB;
+    smem[k * CP_ST + il] = A[(i0 + il) * lda + p0 + k];
+  }
+  __syncthreads();
+  double* cwt = cwt_all + b * NB * n;
+  for (int e = threadIdx.x; e < CP_ROWS * NB; e += P1_THREADS) {
+    const int k = e / CP_ROWS, il = e % CP_ROWS;
+    cwt[(int64_t)k * n + i0 + il] = -smem[k * CP_ST + il];
+  }
 }
 
-// ------------------------------------------------------------------ U
-// grid (n/TN, n/TM, batch). Tile (I, J), I != panel row tile:
-//   A_IJ = (J in p ? 0 : A_IJ) - Cw_I * A_pJ.
-__global__ void __launch_bounds__(TILE_THREADS, 2)
-    gj_update_kernel(double* __restrict__ a, int64_t n, int64_t lda, int64_t stride, int p0,
-                     const double* __restrict__ cw_all) {
-  const int row0 = blockIdx.y * TM;
-  if (row0 == p0) return;  // TM == NB: the panel row tile was written by P2
+// ------------------------------------------------------------------ schedulers
+struct RowPanelSched {
+  double* a;
+  const double* dt_all;
+  int64_t lda, stride;
+  int nt, pt, batch;
+  RDB_DEV int count() const { return batch * (nt - 1); }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int g = t / (nt - 1);
+    int J = t - g * (nt - 1);
+    J += (J >= pt);
+    double* A = a + (int64_t)g * stride;
+    double* rowp = A + (int64_t)pt * NB * lda + (int64_t)J * NB;
+    eng::Tile T;
+    T.a = dt_all + (int64_t)g * NB * NB;
+    T.lda = NB;
+    T.b = rowp;
+    T.ldb = lda;
+    T.c = rowp;
+    T.ldc = lda;
+    T.nk = NB / eng::BK;
+    T.mode = eng::EPI_STORE;
+    return T;
+  }
+};
+
+struct UpdateSched {
+  double* a;
+  const double* cwt_all;
+  int64_t n, lda, stride;
+  int nt, pt, batch;
+  RDB_DEV int count() const { return batch * (nt - 1) * nt; }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int per = (nt - 1) * nt;
+    const int g = t / per;
+    const int rem = t - g * per;
+    int I = rem / nt;
+    const int J = rem - I * nt;
+    I += (I >= pt);
+    double* A = a + (int64_t)g * stride;
+    eng::Tile T;
+    T.a = cwt_all + (int64_t)g * NB * n + (int64_t)I * NB;
+    T.lda = n;
+    T.b = A + (int64_t)pt * NB * lda + (int64_t)J * NB;
+    T.ldb = lda;
+    T.c = A + (int64_t)I * NB * lda + (int64_t)J * NB;
+    T.ldc = lda;
+    T.nk = NB / eng::BK;
+    T.mode = (J == pt) ? eng::EPI_STORE : eng::EPI_REDUCE;
+    return T;
+  }
+};
+
+__global__ void __launch_bounds__(eng::THREADS, 1) gj_rowpanel_kernel(RowPanelSched sched) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  TileSmem& s = *reinterpret_cast<TileSmem*>(smem_raw);
-  const int col0 = blockIdx.x * TN;
-  const int64_t b = blockIdx.z;
-  double* A = a + b * stride;
-  const double* cw = cw_all + b * n * NB;
-  const bool in_panel = (col0 >= p0) && (col0 < p0 + NB);
-
-  Acc acc;
-  acc_zero(acc);
-  tile_mainloop(s, acc, cw + (int64_t)row0 * NB, NB, A + (int64_t)p0 * lda + col0, lda, NB);
-  double* C = A + (int64_t)row0 * lda + col0;
-  tile_epilogue(acc, [&](int r, int c, double x0, double x1) {
-    double* p = C + (int64_t)r * lda + c;
-    double2 o = in_panel ? make_double2(0.0, 0.0) : ldg2(p);
-    o.x -= x0;
-    o.y -= x1;
-    stg2(p, o);
-  });
+  eng::run<true>(*reinterpret_cast<eng::Smem*>(smem_raw), sched);
 }
 
-static bool g_attr_set = false;
+__global__ void __launch_bounds__(eng::THREADS, 1) gj_update_kernel(UpdateSched sched) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  eng::run<true>(*reinterpret_cast<eng::Smem*>(smem_raw), sched);
+}
 
-static int set_attrs() {
-  if (g_attr_set) return RDB_OK;
+static int g_sms = 0;
+
+static int setup() {
+  if (g_sms) return RDB_OK;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return RDB_ECUDA;
+  if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return RDB_ECUDA;
   if (cudaFuncSetAttribute(gj_rowpanel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TILE_SMEM_BYTES) != cudaSuccess)
+                           (int)eng::SMEM_BYTES) != cudaSuccess ||
+      cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)eng::SMEM_BYTES) != cudaSuccess ||
+      cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)P1_SMEM) != cudaSuccess)
     return RDB_ECUDA;
-  if (cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TILE_SMEM_BYTES) != cudaSuccess)
-    return RDB_ECUDA;
-  g_attr_set = true;
   return RDB_OK;
+}
+
+int sm_count() {
+  setup();
+  return g_sms > 0 ? g_sms : 148;
+}
+
+static unsigned persistent_grid(int64_t tiles) {
+  const int64_t sms = sm_count();
+  return (unsigned)(tiles < sms ? tiles : sms);
 }
 
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
@@ -193,49 +236,82 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   if (!a || !work || !info || n <= 0 || batch <= 0) return RDB_EINVAL;
   if (n % NB != 0 || lda < n || (lda & 1) || (batch > 1 && stride < n * lda)) return RDB_EINVAL;
   if (((uintptr_t)a & 15) || ((uintptr_t)work & 15)) return RDB_EINVAL;
-  if (batch > 65535 || n / TN > 2147483647) return RDB_EINVAL;
-  int rc = set_attrs();
+  if (batch > 65535) return RDB_EINVAL;
+  const int nt = (int)(n / NB);
+  if ((int64_t)batch * nt * nt > 2147483647LL) return RDB_EINVAL;
+  int rc = setup();
   if (rc) return rc;
-  double* cw = static_cast<double*>(work);
-  const int nsteps = (int)(n / NB);
-  for (int k = 0; k < nsteps; ++k) {
+  double* cwt = static_cast<double*>(work);
+  double* dt = cwt + batch * NB * n;
+  for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
-    gj_panel_kernel<<<(unsigned)batch, P1_THREADS, 0, st>>>(a, lda, stride, p0, info, k == 0);
-    gj_rowpanel_kernel<<<dim3((unsigned)(n / TN), (unsigned)batch), TILE_THREADS, TILE_SMEM_BYTES,
-                         st>>>(a, n, lda, stride, p0, cw);
-    gj_update_kernel<<<dim3((unsigned)(n / TN), (unsigned)(n / TM), (unsigned)batch), TILE_THREADS,
-                       TILE_SMEM_BYTES, st>>>(a, n, lda, stride, p0, cw);
+    gj_panel_kernel<<<dim3((unsigned)(1 + n / CP_ROWS), (unsigned)batch), P1_THREADS, P1_SMEM, st>>>(
+        a, n, lda, stride, p0, info, k == 0, cwt, dt);
+    if (nt > 1) {
+      RowPanelSched rp{a, dt, lda, stride, nt, k, (int)batch};
+      gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), eng::THREADS, eng::SMEM_BYTES,
+                           st>>>(rp);
+      UpdateSched up{a, cwt, n, lda, stride, nt, k, (int)batch};
+      gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), eng::THREADS,
+                         eng::SMEM_BYTES, st>>>(up);
+    }
   }
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
 
 // ------------------------------------------------------------------ K5 residual
-// max |M Y - I| over the n_pad x n_pad product (resolvent.py:125-127). The
-// padding is identity in both factors, so it contributes exact zeros.
-__global__ void __launch_bounds__(TILE_THREADS, 2)
-    residual_kernel(const double* __restrict__ m, int64_t ldm, const double* __restrict__ y,
-                    int64_t ldy, int64_t n, double* __restrict__ out_max) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  TileSmem& s = *reinterpret_cast<TileSmem*>(smem_raw);
-  const int row0 = blockIdx.y * TM, col0 = blockIdx.x * TN;
-  Acc acc;
-  acc_zero(acc);
-  tile_mainloop(s, acc, m + (int64_t)row0 * ldm, ldm, y + col0, ldy, (int)n);
-  double mx = 0.0;
-  tile_epilogue(acc, [&](int r, int c, double x0, double x1) {
-    const int gi = row0 + r, gj = col0 + c;
-    const double e0 = fabs(x0 - (gi == gj ? 1.0 : 0.0));
-    const double e1 = fabs(x1 - (gi == gj + 1 ? 1.0 : 0.0));
-    // NaN must win the max, as numpy's max does
-    mx = (e0 > mx || e0 != e0) ? e0 : mx;
-    mx = (e1 > mx || e1 != e1) ? e1 : mx;
-  });
-  for (int o = 16; o > 0; o >>= 1) {
-    const double other = __shfl_xor_sync(0xffffffffu, mx, o);
-    mx = (other > mx || other != other) ? other : mx;
+// max |M Y - I| (resolvent.py:125-127) with M row-major as the A operand; the
+// epilogue reduces |acc - delta_ij| instead of storing.
+struct ResidualSched {
+  const double* m;
+  const double* y;
+  int64_t ldm, ldy;
+  int nt, nk;
+  RDB_DEV int count() const { return nt * nt; }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int I = t / nt, J = t - (t / nt) * nt;
+    eng::Tile T;
+    T.a = m + (int64_t)I * NB * ldm;
+    T.lda = ldm;
+    T.b = y + (int64_t)J * NB;
+    T.ldb = ldy;
+    T.c = nullptr;
+    T.ldc = I;  // row tile index (the epilogue needs the origin only)
+    T.nk = nk;
+    T.mode = J;
+    return T;
   }
-  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out_max, mx);
+};
+
+struct ResidualEpi {
+  double* out_max;
+  RDB_DEV void operator()(const eng::Tile& T, double (&acc)[8][4][2], int wr, int wc, int lane,
+                          double*) const {
+    const int64_t row0 = T.ldc * NB + wr * 64, col0 = (int64_t)T.mode * NB + wc * 32;
+    double mx = 0.0;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int64_t gi = row0 + mi * 8 + (lane >> 2);
+        const int64_t gj = col0 + ni * 8 + 2 * (lane & 3);
+        const double e0 = fabs(acc[mi][ni][0] - (gi == gj ? 1.0 : 0.0));
+        const double e1 = fabs(acc[mi][ni][1] - (gi == gj + 1 ? 1.0 : 0.0));
+        mx = (e0 > mx || e0 != e0) ? e0 : mx;  // NaN wins, as in numpy's max
+        mx = (e1 > mx || e1 != e1) ? e1 : mx;
+      }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double other = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = (other > mx || other != other) ? other : mx;
+    }
+    if (lane == 0) atomic_max_nonneg(out_max, mx);
+  }
+};
+
+__global__ void __launch_bounds__(eng::THREADS, 1) residual_kernel(ResidualSched sched, ResidualEpi epi) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  eng::run<false>(*reinterpret_cast<eng::Smem*>(smem_raw), sched, epi);
 }
 
 }  // namespace rdb
@@ -244,7 +320,7 @@ using namespace rdb;
 
 extern "C" size_t rdb_invert_workspace_bytes(int64_t n_pad, int64_t batch) {
   if (n_pad <= 0 || batch <= 0) return 0;
-  return (size_t)batch * (size_t)n_pad * NB * sizeof(double);
+  return (size_t)batch * ((size_t)n_pad * NB + (size_t)NB * NB) * sizeof(double);
 }
 
 extern "C" int rdb_invert_batched(double* a, int64_t n_pad, int64_t lda, int64_t stride,
@@ -265,11 +341,13 @@ extern "C" int rdb_residual(const double* m, int64_t ldm, const double* y, int64
       ldy < n_pad)
     return RDB_EINVAL;
   if (cudaFuncSetAttribute(residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TILE_SMEM_BYTES) != cudaSuccess)
+                           (int)eng::SMEM_BYTES) != cudaSuccess)
     return RDB_ECUDA;
-  residual_kernel<<<dim3((unsigned)(n_pad / TN), (unsigned)(n_pad / TM)), TILE_THREADS,
-                    TILE_SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(m, ldm, y, ldy, n_pad,
-                                                                           out_max);
+  const int nt = (int)(n_pad / NB);
+  ResidualSched sched{m, y, ldm, ldy, nt, (int)(n_pad / eng::BK)};
+  ResidualEpi epi{out_max};
+  residual_kernel<<<persistent_grid((int64_t)nt * nt), eng::THREADS, eng::SMEM_BYTES,
+                    static_cast<cudaStream_t>(stream)>>>(sched, epi);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
