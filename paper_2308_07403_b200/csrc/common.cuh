@@ -72,6 +72,19 @@ RDB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
       : "memory");
 }
 
+// Reciprocal without the IEEE-division slow-path call (whose ABI call site
+// forces register spills in fully unrolled loops): MUFU.RCP64H seed and two
+// Newton steps with FMA. Within 1 ulp (exact for powers of two) for normal p;
+// 0 or non-finite p yield a non-finite result, which the callers flag.
+RDB_DEV double rcp_nr(double p) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
+  double e = fma(-p, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-p, y, 1.0);
+  return fma(y, e, y);
+}
+
 // ---------------------------------------------------------------- misc
 RDB_DEV double2 ldg2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 RDB_DEV void stg2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }

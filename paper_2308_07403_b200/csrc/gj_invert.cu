@@ -20,124 +20,28 @@
 #include <cmath>
 
 #include "dmma_engine.cuh"
+#include "gj_panel.cuh"
 
 namespace rdb {
 
 // ------------------------------------------------------------------ P1
-// Block x = 0: unblocked Gauss-Jordan inverse of the NB x NB diagonal block,
-// in place; thread (rg = t/128, j = t%128) keeps column j, rows 32*rg..+32 in
-// registers; each step publishes the pivot row / column through shared memory.
-// Blocks x > 0: rows [64(x-1), 64x) of the column panel, negated and
-// transposed into CwT (128 x n per matrix).
-constexpr int P1_THREADS = 512;
-constexpr int CP_ROWS = 64;
-constexpr int CP_ST = CP_ROWS + 1;
-constexpr size_t P1_SMEM = (size_t)NB * CP_ST * sizeof(double);
-
-__device__ __noinline__ void panel_inverse(double* __restrict__ A, int64_t lda, int p0,
-                                           rdb_pivot_info* __restrict__ inf, int first,
-                                           double* __restrict__ dt, double* smem) {
-  double* prow = smem;           // [2][NB]
-  double* pcol = smem + 2 * NB;  // [2][NB]
-  double* pinv_s = smem + 4 * NB;  // [2]
-  const int t = threadIdx.x;
-  const int j = t & (NB - 1);
-  const int rg = t >> 7;
-  double v[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) v[r] = A[(int64_t)(32 * rg + r) * lda + j];
-
-  double minp = INFINITY;
-  int mini = -1, flags = 0;
-  int buf = 0;
-#pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
-#pragma unroll
-    for (int s = 0; s < 32; ++s) {
-      const int kk = 32 * q + s;
-      if (rg == q) {
-        prow[buf * NB + j] = v[s];
-        if (j == kk) pinv_s[buf] = 1.0 / v[s];
-      }
-      if (j == kk) {
-#pragma unroll
-        for (int r = 0; r < 32; ++r) pcol[buf * NB + 32 * rg + r] = v[r];
-      }
-      __syncthreads();
-      const double pinv = pinv_s[buf];
-      if (t == 0) {
-        const double p = prow[buf * NB + kk];
-        const double ap = fabs(p);
-        if (!(ap < INFINITY)) flags |= RDB_PIV_NONFINITE;
-        if (!(p > 0.0)) flags |= RDB_PIV_NONPOS;
-        if (ap < minp || mini < 0) {
-          minp = ap;
-          mini = kk;
-        }
-      }
-      const double u = (j == kk) ? pinv : prow[buf * NB + j] * pinv;
-      if (j == kk) {
-        // column kk of the result is -f_i * pinv: start from 0 so the common
-        // fma(-f, u, v) below produces exactly that.
-#pragma unroll
-        for (int r = 0; r < 32; ++r) v[r] = 0.0;
-      }
-      const double* pc = pcol + buf * NB + 32 * rg;
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        if (r == s && rg == q) {
-          v[r] = u;
-        } else {
-          v[r] = fma(-pc[r], u, v[r]);
-        }
-      }
-      buf ^= 1;
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    A[(int64_t)(32 * rg + r) * lda + j] = v[r];
-    dt[(int64_t)j * NB + 32 * rg + r] = v[r];
-  }
-  if (t == 0) {
-    if (first) {
-      inf->min_pivot = minp;
-      inf->min_index = p0 + mini;
-      inf->flags = flags;
-    } else {
-      if (minp < inf->min_pivot) {
-        inf->min_pivot = minp;
-        inf->min_index = p0 + mini;
-      }
-      inf->flags |= flags;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(P1_THREADS, 1)
+// Block x = 0: D = A_pp^-1 in place (+ D^T, pivots), see gj_panel.cuh.
+// Blocks x > 0: rows [128(x-1), 128x) of the column panel -> CwT = -(A_rp)^T.
+__global__ void __launch_bounds__(p1::THREADS, 1)
     gj_panel_kernel(double* __restrict__ a, int64_t n, int64_t lda, int64_t stride, int p0,
                     rdb_pivot_info* __restrict__ info, int first, double* __restrict__ cwt_all,
                     double* __restrict__ dt_all) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t b = blockIdx.y;
   double* A = a + b * stride;
   if (blockIdx.x == 0) {
-    panel_inverse(A + (int64_t)p0 * lda + p0, lda, p0, info + b, first, dt_all + b * NB * NB, smem);
+    p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), A + (int64_t)p0 * lda + p0, lda, p0,
+                      info + b, first, dt_all + b * NB * NB);
     return;
   }
-  const int64_t i0 = (int64_t)(blockIdx.x - 1) * CP_ROWS;
-  if (i0 >= p0 && i0 < p0 + NB) return;  // rows of the panel itself: not needed by the update
-  // load A[i0 + il][p0 + k] (coalesced along k) -> T[k][il]
-  for (int e = threadIdx.x; e < CP_ROWS * NB; e += P1_THREADS) {
-    const int il = e / NB, k = e % NB;
-    smem[k * CP_ST + il] = A[(i0 + il) * lda + p0 + k];
-  }
-  __syncthreads();
-  double* cwt = cwt_all + b * NB * n;
-  for (int e = threadIdx.x; e < CP_ROWS * NB; e += P1_THREADS) {
-    const int k = e / CP_ROWS, il = e % CP_ROWS;
-    cwt[(int64_t)k * n + i0 + il] = -smem[k * CP_ST + il];
-  }
+  const int64_t i0 = (int64_t)(blockIdx.x - 1) * p1::CP_ROWS;
+  if (i0 >= p0 && i0 < p0 + NB) return;  // the panel's own rows: not used by the update
+  p1::panel_copy(reinterpret_cast<double*>(smem_raw), A, n, lda, p0, i0, cwt_all + b * NB * n);
 }
 
 // ------------------------------------------------------------------ schedulers
@@ -216,7 +120,7 @@ static int setup() {
       cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)eng::SMEM_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)P1_SMEM) != cudaSuccess)
+                           (int)p1::SMEM_BYTES) != cudaSuccess)
     return RDB_ECUDA;
   return RDB_OK;
 }
@@ -245,7 +149,8 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   double* dt = cwt + batch * NB * n;
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
-    gj_panel_kernel<<<dim3((unsigned)(1 + n / CP_ROWS), (unsigned)batch), P1_THREADS, P1_SMEM, st>>>(
+    gj_panel_kernel<<<dim3((unsigned)(1 + n / p1::CP_ROWS), (unsigned)batch), p1::THREADS, p1::SMEM_BYTES,
+                      st>>>(
         a, n, lda, stride, p0, info, k == 0, cwt, dt);
     if (nt > 1) {
       RowPanelSched rp{a, dt, lda, stride, nt, k, (int)batch};
