@@ -43,29 +43,34 @@ __global__ void build_m_kernel(const double* __restrict__ w, int64_t ldw, int64_
 
 // Bit-packed adjacency -> M. Thread handles 2 adjacent columns (double2 store).
 __global__ void build_m_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t n_pad,
-                                    const double* __restrict__ gammas, double gamma,
+                                    int64_t batch, const double* __restrict__ gammas, double gamma,
                                     double* __restrict__ out, int64_t ldo, int64_t stride_o) {
-  const int64_t b = blockIdx.z;
-  const double g = gammas ? gammas[b] : gamma;
+  // one warp per output row (grid-stride over batch * n_pad rows); lane l
+  // writes columns 2l, 2l+1 of every 64-column chunk: 512 B per store wave.
+  const int lane = threadIdx.x & 31;
   const int64_t wpr = (n + 31) / 32;
-  const uint32_t* Bb = bits + b * n * wpr;
-  double* O = out + b * stride_o;
-  for (int64_t i = blockIdx.y; i < n_pad; i += gridDim.y) {
-    for (int64_t j = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); j < n_pad;
-         j += 2 * (int64_t)gridDim.x * blockDim.x) {
-      double v[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t jj = j + e;
-        if (i < n && jj < n) {
-          const uint32_t word = Bb[i * wpr + (jj >> 5)];
-          const bool edge = (word >> (jj & 31)) & 1u;
-          v[e] = (i == jj) ? 1.0 : (edge ? -g : 0.0);
-        } else {
-          v[e] = (i == jj) ? 1.0 : 0.0;
-        }
+  const int64_t rows = n_pad * batch;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += nwarps) {
+    const int64_t b = w / n_pad, i = w - b * n_pad;
+    const double ng = -(gammas ? gammas[b] : gamma);
+    const uint32_t* row = bits + (b * n + i) * wpr;
+    double* O = out + b * stride_o + i * ldo;
+    for (int64_t j0 = 0; j0 < n_pad; j0 += 64) {
+      const int64_t j = j0 + 2 * lane;
+      const int64_t wi = j0 >> 5;  // two words cover this 64-column chunk
+      uint32_t w0 = 0, w1 = 0;
+      if (i < n) {
+        if (wi < wpr) w0 = __ldg(row + wi);
+        if (wi + 1 < wpr) w1 = __ldg(row + wi + 1);
       }
-      stg2(O + i * ldo + j, make_double2(v[0], v[1]));
+      const uint32_t word = (lane < 16) ? w0 : w1;
+      const int sh = (2 * lane) & 31;
+      double v0 = ((word >> sh) & 1u) && (j < n) ? ng : 0.0;
+      double v1 = ((word >> (sh + 1)) & 1u) && (j + 1 < n) ? ng : 0.0;
+      if (j == i) v0 = 1.0;
+      if (j + 1 == i) v1 = 1.0;
+      stg2(O + j, make_double2(v0, v1));
     }
   }
 }
@@ -149,9 +154,11 @@ extern "C" int rdb_build_m_bits(const uint32_t* bits, int64_t n, int64_t n_pad, 
       batch <= 0 || batch > 65535 || ((uintptr_t)out & 15))
     return RDB_EINVAL;
   if (!gammas && !(gamma > 0.0 && gamma < 1.0)) return RDB_EINVAL;
-  build_m_bits_kernel<<<grid2d(n_pad, n_pad, batch, 256, 2), 256, 0,
-                        static_cast<cudaStream_t>(stream)>>>(bits, n, n_pad, gammas, gamma, out, ldo,
-                                                             stride_o);
+  if (n_pad % 64) return RDB_EINVAL;
+  const int64_t rows = n_pad * batch;
+  const int64_t blocks = (rows + 7) / 8 < 148 * 32 ? (rows + 7) / 8 : 148 * 32;
+  build_m_bits_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      bits, n, n_pad, batch, gammas, gamma, out, ldo, stride_o);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }

@@ -3,13 +3,16 @@
 // pkg/src/rdist/resolvent.py:131-153, counters at resolvent.py:120-124).
 //
 // Exactness: ceil has no nudge (resolvent.py:146-153), so a quotient that
-// should be an exact integer must come out exact. Both logs use the same
-// device log, and any quotient within 1e-9 of an integer k is recomputed as
-// k + log1p((y - gamma^k)/gamma^k)/log(gamma) with gamma^k in double-double:
-// the result is then correctly rounded, so y == gamma^k (as in the lone-edge
-// lattice case y == gamma) gives exactly k, and log(0.09)/log(0.3) gives 2.0
-// (test_resolvent.py:137-148).
-#include <algorithm>
+// should be an exact integer must come out exact. R is first formed as
+// log(y) * (1 / log gamma) (within a few ulp of the reference's quotient); any
+// value within 1e-9 of an integer k is then recomputed as
+// k + log1p((y - gamma^k)/gamma^k)/log(gamma) with gamma^k in double-double,
+// which is correctly rounded: y == gamma^k (the lone-edge lattice case
+// y == gamma) gives exactly k, and log(0.09)/log(0.3) gives 2.0
+// (test_resolvent.py:137-148). Away from integers the ceil cannot change.
+//
+// Layout: one warp per matrix row, lane l handles columns 2l, 2l+1 of every
+// 64-column chunk (16-byte loads of Y, 8-byte int32 pair stores).
 #include <climits>
 #include <cmath>
 
@@ -39,80 +42,117 @@ RDB_DEV double refine_near_integer(double y, double g, double lg, double r) {
   return k + delta;
 }
 
+RDB_DEV double rdist_value(double v, bool diag, double g, double lg, double inv_lg) {
+  if (diag) return 0.0;
+  if (!(v > 0.0)) return INFINITY;
+  return refine_near_integer(v, g, lg, log(v) * inv_lg);
+}
+
 template <bool HAS_R, bool HAS_DC, bool HAS_D32>
-__global__ void log_ceil_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y,
-                                const double* __restrict__ gammas, double gamma,
-                                double* __restrict__ r_out, double* __restrict__ dc_out,
-                                int32_t* __restrict__ d32_out, int64_t ldo, int64_t stride_o,
-                                const uint8_t* __restrict__ reach, int64_t ldm,
-                                unsigned long long* __restrict__ counters) {
-  const int64_t b = blockIdx.z;
-  const double g = gammas ? gammas[b] : gamma;
-  const double lg = log(g);
-  const double* Y = y + b * stride_y;
-  unsigned neg = 0, under = 0;
-  for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-         j += (int64_t)gridDim.x * blockDim.x) {
-      const double v = Y[i * ldy + j];
-      double r;
-      if (i == j) {
-        r = 0.0;
-      } else if (v > 0.0) {
-        r = refine_near_integer(v, g, lg, log(v) / lg);
-      } else {
-        r = INFINITY;
-      }
-      neg += (v < NEGATIVE_ENTRY_TOL);
-      if (reach) under += (v == 0.0 && i != j && reach[i * ldm + j] != 0);
-      const int64_t o = b * stride_o + i * ldo + j;
-      if (HAS_R) r_out[o] = r;
-      const double dcv = ceil(r);
-      if (HAS_DC) dc_out[o] = dcv;
-      if (HAS_D32) d32_out[o] = (dcv < 2147483647.0) ? (int32_t)dcv : INT_MAX;
-    }
+struct Sink {
+  double* r;
+  double* dc;
+  int32_t* d32;
+  RDB_DEV static int32_t to_i32(double dcv) { return (dcv < 2147483647.0) ? (int32_t)dcv : INT_MAX; }
+  RDB_DEV void put1(int64_t o, double rv) const {
+    const double dcv = ceil(rv);
+    if (HAS_R) r[o] = rv;
+    if (HAS_DC) dc[o] = dcv;
+    if (HAS_D32) d32[o] = to_i32(dcv);
   }
-  if (counters) {
-    neg = __reduce_add_sync(0xffffffffu, neg);
-    under = __reduce_add_sync(0xffffffffu, under);
-    if ((threadIdx.x & 31) == 0) {
-      if (neg) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_NEGATIVE], (unsigned long long)neg);
-      if (under)
-        atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_UNDERFLOW], (unsigned long long)under);
+  RDB_DEV void put2(int64_t o, double r0, double r1) const {
+    const double c0 = ceil(r0), c1 = ceil(r1);
+    if (HAS_R) *reinterpret_cast<double2*>(r + o) = make_double2(r0, r1);
+    if (HAS_DC) *reinterpret_cast<double2*>(dc + o) = make_double2(c0, c1);
+    if (HAS_D32) *reinterpret_cast<int2*>(d32 + o) = make_int2(to_i32(c0), to_i32(c1));
+  }
+};
+
+template <bool HAS_R, bool HAS_DC, bool HAS_D32, bool VEC>
+__global__ void __launch_bounds__(256)
+    log_ceil_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y,
+                    int64_t batch, const double* __restrict__ gammas, double gamma,
+                    Sink<HAS_R, HAS_DC, HAS_D32> sink, int64_t ldo, int64_t stride_o,
+                    const uint8_t* __restrict__ reach, int64_t ldm,
+                    unsigned long long* __restrict__ counters) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = n * batch;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += nwarps) {
+    const int64_t b = w / n, i = w - b * n;
+    const double g = gammas ? gammas[b] : gamma;
+    const double lg = log(g);
+    const double inv_lg = 1.0 / lg;
+    const double* Y = y + b * stride_y + i * ldy;
+    const int64_t orow = b * stride_o + i * ldo;
+    const uint8_t* M = reach ? reach + i * ldm : nullptr;
+    unsigned neg = 0, under = 0;
+    for (int64_t j0 = 0; j0 < n; j0 += 64) {
+      const int64_t j = j0 + 2 * lane;
+      if (VEC && j + 1 < n) {
+        const double2 v = ldg2(Y + j);
+        const double r0 = rdist_value(v.x, i == j, g, lg, inv_lg);
+        const double r1 = rdist_value(v.y, i == j + 1, g, lg, inv_lg);
+        sink.put2(orow + j, r0, r1);
+        neg += (v.x < NEGATIVE_ENTRY_TOL) + (v.y < NEGATIVE_ENTRY_TOL);
+        if (M) under += (v.x == 0.0 && i != j && M[j]) + (v.y == 0.0 && i != j + 1 && M[j + 1]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t jj = j + e;
+          if (jj < n) {
+            const double v = Y[jj];
+            sink.put1(orow + jj, rdist_value(v, i == jj, g, lg, inv_lg));
+            neg += (v < NEGATIVE_ENTRY_TOL);
+            if (M) under += (v == 0.0 && i != jj && M[jj]);
+          }
+        }
+      }
+    }
+    if (counters) {
+      neg = __reduce_add_sync(0xffffffffu, neg);
+      under = __reduce_add_sync(0xffffffffu, under);
+      if (lane == 0) {
+        if (neg) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_NEGATIVE], (unsigned long long)neg);
+        if (under) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_UNDERFLOW], (unsigned long long)under);
+      }
     }
   }
 }
 
 template <bool A, bool B, bool C>
-static void launch(dim3 grid, cudaStream_t st, const double* y, int64_t n, int64_t ldy,
-                   int64_t stride_y, const double* gammas, double gamma, double* r, double* dc,
-                   int32_t* d32, int64_t ldo, int64_t stride_o, const uint8_t* reach, int64_t ldm,
-                   unsigned long long* counters) {
-  log_ceil_kernel<A, B, C><<<grid, 256, 0, st>>>(y, n, ldy, stride_y, gammas, gamma, r, dc, d32, ldo,
-                                                 stride_o, reach, ldm, counters);
+static void launch(bool vec, unsigned blocks, cudaStream_t st, const double* y, int64_t n, int64_t ldy,
+                   int64_t stride_y, int64_t batch, const double* gammas, double gamma, double* r,
+                   double* dc, int32_t* d32, int64_t ldo, int64_t stride_o, const uint8_t* reach,
+                   int64_t ldm, unsigned long long* counters) {
+  Sink<A, B, C> sink{r, dc, d32};
+  if (vec)
+    log_ceil_kernel<A, B, C, true><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, sink,
+                                                           ldo, stride_o, reach, ldm, counters);
+  else
+    log_ceil_kernel<A, B, C, false><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, sink,
+                                                            ldo, stride_o, reach, ldm, counters);
 }
 
 int log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
              const double* gammas, double gamma, double* r_out, double* dceil_out, int32_t* d32_out,
              int64_t ldo, int64_t stride_o, const uint8_t* reachable, int64_t ldm,
              unsigned long long* counters, cudaStream_t st) {
-  if (!y || n <= 0 || ldy < n || batch <= 0 || batch > 65535) return RDB_EINVAL;
+  if (!y || n <= 0 || ldy < n || batch <= 0) return RDB_EINVAL;
   if ((r_out || dceil_out || d32_out) && ldo < n) return RDB_EINVAL;
   if (reachable && ldm < n) return RDB_EINVAL;
   if (!gammas && !(gamma > 0.0 && gamma < 1.0)) return RDB_EINVAL;
-  int64_t gx = (n + 255) / 256;
-  int64_t gy = n;
-  // aim for ~8 waves of 148 SMs in total
-  const int64_t target = 148 * 16;
-  int64_t total = gx * gy * batch;
-  if (total > target * 64) gy = std::max<int64_t>(1, (target * 64) / (gx * batch));
-  if (gy > 65535) gy = 65535;
-  dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)batch);
+  auto al = [](const void* p, uintptr_t a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
+  const bool vec = !(ldy & 1) && !(stride_y & 1) && !(ldo & 1) && !(stride_o & 1) && al(y, 16) &&
+                   al(r_out, 16) && al(dceil_out, 16) && al(d32_out, 8);
+  const int64_t rows = n * batch;
+  const int64_t want = (rows + 7) / 8;
+  const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
   const int key = (r_out ? 4 : 0) | (dceil_out ? 2 : 0) | (d32_out ? 1 : 0);
-#define RDB_LC(K, A, B, C)                                                                      \
-  case K:                                                                                       \
-    launch<A, B, C>(grid, st, y, n, ldy, stride_y, gammas, gamma, r_out, dceil_out, d32_out, ldo, \
-                    stride_o, reachable, ldm, counters);                                        \
+#define RDB_LC(K, A, B, C)                                                                       \
+  case K:                                                                                        \
+    launch<A, B, C>(vec, blocks, st, y, n, ldy, stride_y, batch, gammas, gamma, r_out, dceil_out, \
+                    d32_out, ldo, stride_o, reachable, ldm, counters);                           \
     break;
   switch (key) {
     RDB_LC(0, false, false, false)
