@@ -62,6 +62,8 @@ typedef struct rdb_pivot_info {
 
 const char* rdb_strerror(int code);
 int rdb_abi_version(void);
+/* cudaGetErrorString of the last CUDA error an entry point returned RDB_ECUDA for (this thread). */
+const char* rdb_last_cuda_error(void);
 
 /* ---- K1: X = gamma^W or M = I - gamma^W -------------------------------
  * Replaces np.power(gamma, W) (resolvent.py:98) and np.eye(n) - x

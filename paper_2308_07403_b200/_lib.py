@@ -52,6 +52,7 @@ _sz = ctypes.c_size_t
 SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "rdb_strerror": (ctypes.c_char_p, [_int]),
     "rdb_abi_version": (_int, []),
+    "rdb_last_cuda_error": (ctypes.c_char_p, []),
     "rdb_build_m": (_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _dbl, _int, _vp, _i64, _i64, _vp]),
     "rdb_build_m_bits": (_int, [_vp, _i64, _i64, _i64, _vp, _dbl, _vp, _i64, _i64, _vp]),
     "rdb_pad_identity": (_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp]),
@@ -121,6 +122,8 @@ def ptr(t: torch.Tensor | None) -> int | None:
 def check(rc: int, what: str) -> None:
     if rc != RDB_OK:
         msg = lib().rdb_strerror(rc).decode()
+        if rc == 4:
+            msg += f" [{lib().rdb_last_cuda_error().decode()}]"
         raise NativeCallError(f"{what} failed: {msg} (code {rc})")
 
 

@@ -34,6 +34,13 @@ extern "C" const char* rdb_strerror(int code) {
 
 extern "C" int rdb_abi_version(void) { return RDB_ABI_VERSION; }
 
+namespace rdb {
+static thread_local cudaError_t g_last_err = cudaSuccess;
+void set_cuda_error(cudaError_t e) { g_last_err = e; }
+}  // namespace rdb
+
+extern "C" const char* rdb_last_cuda_error(void) { return cudaGetErrorString(rdb::g_last_err); }
+
 extern "C" int rdb_apsp_bits_batched(const uint32_t* bits, int64_t n, int64_t batch,
                                      const double* gammas, double* mwork, void* work,
                                      rdb_pivot_info* info, int32_t* d32,

@@ -97,8 +97,15 @@ RDB_DEV void atomic_max_nonneg(double* addr, double v) {
 
 }  // namespace rdb
 
+namespace rdb {
+void set_cuda_error(cudaError_t e);  // remembered for rdb_last_cuda_error()
+}
+
 #define RDB_LAUNCH_CHECK()                                   \
   do {                                                       \
     cudaError_t _e = cudaGetLastError();                     \
-    if (_e != cudaSuccess) return RDB_ECUDA;                 \
+    if (_e != cudaSuccess) {                                 \
+      rdb::set_cuda_error(_e);                               \
+      return RDB_ECUDA;                                      \
+    }                                                        \
   } while (0)

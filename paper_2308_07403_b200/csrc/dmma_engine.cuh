@@ -2,65 +2,98 @@
 //
 //   for every tile t assigned to this CTA (t = blockIdx.x, += gridDim.x):
 //     acc(128x128) = sum_k A(rows, k) * B(k, cols)          (DMMA.8x8x4)
-//     C(rows, cols)  = acc   (EPI_STORE)   or   C += acc (EPI_REDUCE)
+//     C(rows, cols)  = +-acc (EPI_STORE)   or   C += +-acc (EPI_REDUCE)
 //
 // * warps 0-7 (MMA): 2 x 4 grid of 64x32 warp tiles, 64 fp64 accumulators per
-//   lane; fragments from padded shared memory (bank-conflict free for the
-//   m8n8k4 lane layout).
-// * warp 8 (producer): streams BK=16-deep k-chunks of A and B into a
-//   STAGES-deep ring with 1-D bulk copies (TMA engine, cp.async.bulk), one
-//   full/empty mbarrier pair per stage; it runs ahead across tile boundaries,
-//   so the next tile's operands arrive while the MMA warps drain the epilogue.
-// * epilogue: each MMA warp stages 32x32 sub-tiles in shared memory and
-//   writes them back with bulk stores or bulk reduce-adds
-//   (cp.reduce.async.bulk .add.f64, SASS UBLKRED.ADD.F64.RN): C is never read
-//   by the SM, the L2 applies C + acc with one IEEE rounding.
-//
-// A is either k-major in memory (A^T row-major: element (i,k) at A[k*lda+i];
-// 16 bulk copies of 1 KB per chunk) or row-major (element (i,k) at
-// A[i*lda+k]; 128 copies of 128 B). B is row-major (element (k,j) at
-// B[k*ldb+j]).
+//   lane.
+// * warp 8 (producer): streams BK=16-deep k-chunks into a STAGES-deep ring,
+//   one full/empty mbarrier pair per stage, running ahead across tile
+//   boundaries so the next tile's operands arrive during the epilogue.
+//   - A (row-major in global memory) arrives as ONE 2-D/3-D TMA tensor tile
+//     (cp.async.bulk.tensor, SASS UTMALDG): 128 rows x 16 doubles, 128-byte
+//     swizzle. The MMA row -> smem row map pi(r) = 2(r%4) + (r%8)/4 (within
+//     each 8-row group) makes the m8n8k4 A-fragment loads bank-conflict free
+//     under that swizzle; the epilogue writes accumulator row r to C row pi(r).
+//   - B (row-major) arrives as 16 one-dimensional bulk copies of 1 KB into a
+//     padded layout (row stride 132 doubles, conflict free).
+// * epilogue: each MMA warp stages 32x32 sub-tiles in shared memory and writes
+//   them back with bulk stores or bulk reduce-adds (cp.reduce.async.bulk
+//   .add.f64, SASS UBLKRED.ADD.F64.RN): C is never read by the SM; the L2
+//   applies C + acc with one IEEE rounding.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace rdb {
 namespace eng {
 
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
-constexpr int AST_K = BM + 4;  // k-major A row stride (132 = 4 mod 16)
-constexpr int AST_R = BK + 4;  // row-major A row stride (20 = 4 mod 16)
-constexpr int BST = BN + 4;    // B row stride (132)
-constexpr int OST = 40;        // epilogue staging row stride (STS.128 conflict free)
+constexpr int BST = BN + 4;  // B row stride (132 = 4 mod 16)
+constexpr int OST = 36;      // epilogue staging row stride (STS.128 conflict free for the pi row map)
 constexpr int MMA_WARPS = 8;
 constexpr int THREADS = (MMA_WARPS + 1) * 32;
+constexpr uint32_t A_STAGE_BYTES = BM * BK * 8;  // 16 KB, 1024-aligned (swizzle atom)
 constexpr uint32_t STAGE_BYTES = (BM * BK + BK * BN) * 8;
-constexpr int A_STAGE_DOUBLES = (BM * AST_R > BK * AST_K) ? BM * AST_R : BK * AST_K;
 
 enum { EPI_STORE = 0, EPI_REDUCE = 1 };
 
 struct Smem {
-  alignas(128) double a[STAGES][A_STAGE_DOUBLES];
+  alignas(1024) double a[STAGES][BM * BK];
   alignas(128) double b[STAGES][BK * BST];
   alignas(128) double out[MMA_WARPS][32 * OST];
   alignas(8) uint64_t full[STAGES];
   alignas(8) uint64_t empty[STAGES];
 };
-constexpr size_t SMEM_BYTES = sizeof(Smem);
+constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;  // + alignment slack
 
-// A tile job produced by a scheduler: operand origins for this tile, K, output.
+// A tile job produced by a scheduler.
 struct Tile {
-  const double* a;  // k-major: &A^T[0][row0]; row-major: &A[row0][0]
-  int64_t lda;
-  const double* b;  // &B[0][col0]
+  int a_col, a_row, a_mat;  // TMA coordinates of A(row0, k=0): column, row, matrix (batch) index
+  const double* b;          // &B[0][col0]
   int64_t ldb;
-  double* c;        // &C[row0][col0]
+  double* c;                // &C[row0][col0]
   int64_t ldc;
-  int nk;           // number of BK chunks
-  int mode;         // EPI_STORE / EPI_REDUCE
+  int nk;                   // number of BK chunks
+  int mode;                 // EPI_STORE / EPI_REDUCE
+  int neg;                  // write -acc instead of acc
+  // Optional in-kernel dependency (tiles that overwrite another tile's A
+  // operand): after its last k-chunk has landed in shared memory a tile
+  // increments *signal; a tile with wait != nullptr holds its epilogue until
+  // *wait >= wait_target. Waits only ever point at tiles with a smaller index,
+  // and every CTA processes its tiles in increasing order, so the smallest
+  // unfinished tile can always progress (no deadlock).
+  int* signal;
+  const int* wait;
+  int wait_target;
 };
+
+RDB_DEV int pi_row(int r) { return 2 * (r & 3) + ((r >> 2) & 1); }
+
+RDB_DEV void signal_done(int* cnt) {
+  fence_proxy_async();
+  __threadfence();
+  atomicAdd(cnt, 1);
+}
+
+RDB_DEV void wait_count(const int* cnt, int target) {
+  int v;
+  do {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+  } while (v < target);
+  fence_proxy_async();
+}
 
 RDB_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+RDB_DEV void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
 
 RDB_DEV void bulk_s2g(double* dst, const void* src, uint32_t bytes) {
@@ -79,12 +112,13 @@ RDB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "m
 RDB_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 RDB_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
-// Default epilogue: C = acc (EPI_STORE) or C += acc (EPI_REDUCE) through two
-// 32x32 halves of the per-warp staging buffer and bulk stores / reduce-adds.
+// Default epilogue: C = +-acc (EPI_STORE) or C += +-acc (EPI_REDUCE) through two
+// 32-row halves of the per-warp staging buffer and bulk stores / reduce-adds.
 struct BulkEpilogue {
-  RDB_DEV void operator()(const Tile& T, double (&acc)[8][4][2], int wr, int wc, int lane,
+  RDB_DEV void operator()(Tile T, double (&acc)[8][4][2], int wr, int wc, int lane,
                           double* stage_out) const {
     const int lr = lane >> 2, lk = lane & 3;
+    const int pr = pi_row(lr);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       bulk_wait_read0();  // this lane's previous bulk op has finished reading staging
@@ -93,10 +127,11 @@ struct BulkEpilogue {
       for (int m = 0; m < 4; ++m)
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) {
-          const int row = m * 8 + lr;
+          const int row = m * 8 + pr;
           const int col = ni * 8 + 2 * lk;
+          const double x0 = acc[4 * h + m][ni][0], x1 = acc[4 * h + m][ni][1];
           *reinterpret_cast<double2*>(&stage_out[row * OST + col]) =
-              make_double2(acc[4 * h + m][ni][0], acc[4 * h + m][ni][1]);
+              T.neg ? make_double2(-x0, -x1) : make_double2(x0, x1);
         }
       fence_proxy_async();
       __syncwarp();
@@ -112,8 +147,13 @@ struct BulkEpilogue {
 
 // Sched must provide: int count() and Tile tile(int t) (identical in every warp).
 // Epi: callable (Tile, acc, wr, wc, lane, staging) run by each MMA warp per tile.
-template <bool A_KMAJOR, class Sched, class Epi = BulkEpilogue>
-__device__ __forceinline__ void run(Smem& s, const Sched& sched, const Epi& epi = Epi()) {
+template <class Sched, class Epi = BulkEpilogue>
+__device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* amap, const Sched& sched,
+                                    const Epi& epi = Epi()) {
+  // the 128-byte TMA swizzle atom needs a 1024-byte aligned destination: align
+  // the dynamic shared memory base (pointer arithmetic keeps the shared space)
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw + pad);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -128,29 +168,21 @@ __device__ __forceinline__ void run(Smem& s, const Sched& sched, const Epi& epi 
 
   if (warp == MMA_WARPS) {
     // ------------------------------------------------------------ producer
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(amap)) : "memory");
     int st = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const Tile T = sched.tile(t);
       for (int c = 0; c < T.nk; ++c) {
         mbar_wait(&s.empty[st], ph ^ 1);
-        if (lane == 0) mbar_arrive_expect_tx(&s.full[st], STAGE_BYTES);
-        __syncwarp();
         const int k0 = c * BK;
-        if (A_KMAJOR) {
-          if (lane < BK)
-            bulk_g2s(&s.a[st][lane * AST_K], T.a + (int64_t)(k0 + lane) * T.lda, BM * 8, &s.full[st]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < BM / 32; ++q) {
-            const int i = lane + 32 * q;
-            bulk_g2s(&s.a[st][i * AST_R], T.a + (int64_t)i * T.lda + k0, BK * 8, &s.full[st]);
-          }
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&s.full[st], STAGE_BYTES);
+          tma_load_3d(s.a[st], amap, T.a_col + k0, T.a_row, T.a_mat, &s.full[st]);
         }
-        if (lane >= 32 - BK) {
-          const int kk = lane - (32 - BK);
-          bulk_g2s(&s.b[st][kk * BST], T.b + (int64_t)(k0 + kk) * T.ldb, BN * 8, &s.full[st]);
-        }
+        __syncwarp();
+        if (lane < BK)
+          bulk_g2s(&s.b[st][lane * BST], T.b + (int64_t)(k0 + lane) * T.ldb, BN * 8, &s.full[st]);
         if (++st == STAGES) {
           st = 0;
           ph ^= 1;
@@ -164,6 +196,10 @@ __device__ __forceinline__ void run(Smem& s, const Sched& sched, const Epi& epi 
   const int wr = warp >> 2;  // 0..1 : rows 64*wr
   const int wc = warp & 3;   // 0..3 : cols 32*wc
   const int lr = lane >> 2, lk = lane & 3;
+  // A fragment byte offsets within a stage for (mi, kk): physical row
+  // pr = 64wr + 8mi + pi(lr); 16-byte chunk ((kk+lk)/2) ^ (pr%8); +8 if odd k.
+  const int prow = wr * 64 + pi_row(lr);
+  const int psw = pi_row(lr);  // == prow % 8
   double* stage_out = s.out[warp];
   int st = 0;
   uint32_t ph = 0;
@@ -177,16 +213,18 @@ __device__ __forceinline__ void run(Smem& s, const Sched& sched, const Epi& epi 
 
     for (int c = 0; c < T.nk; ++c) {
       mbar_wait(&s.full[st], ph);
-      const double* sa = s.a[st];
+      // all of this tile's operands are in shared memory: release dependents
+      if (c == T.nk - 1 && T.signal && warp == 0 && lane == 0) signal_done(T.signal);
+      const char* sa = reinterpret_cast<const char*>(s.a[st]);
       const double* sb = s.b[st] + lk * BST + wc * 32 + lr;
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
         double af[8], bf[4];
+        const int kq = kk + lk;
+        const int off = (((kq >> 1) ^ psw) << 4) + ((kq & 1) << 3);
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi) {
-          const int r = wr * 64 + mi * 8 + lr;
-          af[mi] = A_KMAJOR ? sa[(kk + lk) * AST_K + r] : sa[r * AST_R + kk + lk];
-        }
+        for (int mi = 0; mi < 8; ++mi)
+          af[mi] = *reinterpret_cast<const double*>(sa + (prow + mi * 8) * 128 + off);
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) bf[ni] = sb[kk * BST + ni * 8];
 #pragma unroll
@@ -202,10 +240,21 @@ __device__ __forceinline__ void run(Smem& s, const Sched& sched, const Epi& epi 
       }
     }
 
+    if (T.wait) {
+      if (lane == 0) wait_count(T.wait, T.wait_target);
+      __syncwarp();
+    }
     epi(T, acc, wr, wc, lane, stage_out);
   }
   bulk_wait0();
 }
 
 }  // namespace eng
+
+// Host: a 3-D tensor map over `batch` row-major fp64 matrices (rows x cols,
+// row stride ld, matrix stride `stride` elements) with 128 x 16 boxes and
+// 128-byte swizzle — the engine's A operand. Returns RDB_OK or an error.
+int make_a_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+               int64_t stride, int64_t batch);
+
 }  // namespace rdb

@@ -10,13 +10,18 @@
 // reference's diag(U) (linalg.py:33-34).
 //
 // Per panel p = [k*NB, (k+1)*NB), r = all other indices, in place on A:
-//   P1 (gj_panel_kernel, block x = 0)  D = A_pp^-1, pivots recorded; Dt = D^T
-//   P1 (gj_panel_kernel, blocks x > 0) CwT = -(A_rp)^T   (the update overwrites A_rp)
-//   P2 (engine, store)                 A_pJ = D * A_pJ             for J != p
-//   U  (engine, reduce-add / store)    A_IJ += CwT^T * A_pJ        for I != p, J != p
-//                                      A_Ip  = CwT^T * D           (= -A_Ip D)
+//   P1 (gj_panel_kernel)             D = A_pp^-1, pivots recorded (gj_panel.cuh)
+//   P2 (engine, store)               A_pJ = D * A_pJ                 for J != p
+//   U  (engine, reduce-add / store)  A_IJ += -(A_Ip * A_pJ)          for I != p, J != p
+//                                    A_Ip  = -(A_Ip * D)             (last in row block I)
 // After the last panel A = M^-1 (2n^3 flop in total). P2 and U run on the
-// persistent warp-specialised DMMA engine (dmma_engine.cuh).
+// persistent warp-specialised DMMA engine (dmma_engine.cuh). U reads the
+// column panel A_Ip straight from A; the one tile per row block that
+// overwrites it is enumerated last in that row block and holds its epilogue
+// until the other tiles of the row block have their operands in shared
+// memory (in-kernel counters, no copy of the panel).
+#include <cudaTypedefs.h>
+
 #include <cmath>
 
 #include "dmma_engine.cuh"
@@ -24,30 +29,18 @@
 
 namespace rdb {
 
-// ------------------------------------------------------------------ P1
-// Block x = 0: D = A_pp^-1 in place (+ D^T, pivots), see gj_panel.cuh.
-// Blocks x > 0: rows [128(x-1), 128x) of the column panel -> CwT = -(A_rp)^T.
 __global__ void __launch_bounds__(p1::THREADS, 1)
-    gj_panel_kernel(double* __restrict__ a, int64_t n, int64_t lda, int64_t stride, int p0,
-                    rdb_pivot_info* __restrict__ info, int first, double* __restrict__ cwt_all,
-                    double* __restrict__ dt_all) {
+    gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int p0,
+                    rdb_pivot_info* __restrict__ info, int first) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int64_t b = blockIdx.y;
-  double* A = a + b * stride;
-  if (blockIdx.x == 0) {
-    p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), A + (int64_t)p0 * lda + p0, lda, p0,
-                      info + b, first, dt_all + b * NB * NB);
-    return;
-  }
-  const int64_t i0 = (int64_t)(blockIdx.x - 1) * p1::CP_ROWS;
-  if (i0 >= p0 && i0 < p0 + NB) return;  // the panel's own rows: not used by the update
-  p1::panel_copy(reinterpret_cast<double*>(smem_raw), A, n, lda, p0, i0, cwt_all + b * NB * n);
+  const int64_t b = blockIdx.x;
+  p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), a + b * stride + (int64_t)p0 * lda + p0,
+                    lda, p0, info + b, first, nullptr);
 }
 
 // ------------------------------------------------------------------ schedulers
 struct RowPanelSched {
   double* a;
-  const double* dt_all;
   int64_t lda, stride;
   int nt, pt, batch;
   RDB_DEV int count() const { return batch * (nt - 1); }
@@ -58,22 +51,27 @@ struct RowPanelSched {
     double* A = a + (int64_t)g * stride;
     double* rowp = A + (int64_t)pt * NB * lda + (int64_t)J * NB;
     eng::Tile T;
-    T.a = dt_all + (int64_t)g * NB * NB;
-    T.lda = NB;
+    T.a_col = pt * NB;  // A operand: D = A_pp
+    T.a_row = pt * NB;
+    T.a_mat = g;
     T.b = rowp;
     T.ldb = lda;
     T.c = rowp;
     T.ldc = lda;
     T.nk = NB / eng::BK;
     T.mode = eng::EPI_STORE;
+    T.neg = 0;
+    T.signal = nullptr;
+    T.wait = nullptr;
+    T.wait_target = 0;
     return T;
   }
 };
 
 struct UpdateSched {
   double* a;
-  const double* cwt_all;
-  int64_t n, lda, stride;
+  int* cnt;  // [batch][nt] row-block counters, zeroed before step 0
+  int64_t lda, stride;
   int nt, pt, batch;
   RDB_DEV int count() const { return batch * (nt - 1) * nt; }
   RDB_DEV eng::Tile tile(int t) const {
@@ -81,30 +79,73 @@ struct UpdateSched {
     const int g = t / per;
     const int rem = t - g * per;
     int I = rem / nt;
-    const int J = rem - I * nt;
+    const int jj = rem - I * nt;
     I += (I >= pt);
+    // column order pt+1, ..., nt-1, 0, ..., pt: the panel column comes last
+    int J = pt + 1 + jj;
+    if (J >= nt) J -= nt;
     double* A = a + (int64_t)g * stride;
     eng::Tile T;
-    T.a = cwt_all + (int64_t)g * NB * n + (int64_t)I * NB;
-    T.lda = n;
+    T.a_col = pt * NB;  // A operand: A_Ip
+    T.a_row = I * NB;
+    T.a_mat = g;
     T.b = A + (int64_t)pt * NB * lda + (int64_t)J * NB;
     T.ldb = lda;
     T.c = A + (int64_t)I * NB * lda + (int64_t)J * NB;
     T.ldc = lda;
     T.nk = NB / eng::BK;
-    T.mode = (J == pt) ? eng::EPI_STORE : eng::EPI_REDUCE;
+    T.neg = 1;
+    int* c = cnt + (int64_t)g * nt + I;
+    // completed steps j < pt touched row block I unless j == I
+    const int base = (pt - (I < pt ? 1 : 0)) * (nt - 1);
+    if (J == pt) {
+      T.mode = eng::EPI_STORE;
+      T.signal = nullptr;
+      T.wait = c;
+      T.wait_target = base + (nt - 1);
+    } else {
+      T.mode = eng::EPI_REDUCE;
+      T.signal = c;
+      T.wait = nullptr;
+      T.wait_target = 0;
+    }
     return T;
   }
 };
 
-__global__ void __launch_bounds__(eng::THREADS, 1) gj_rowpanel_kernel(RowPanelSched sched) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  eng::run<true>(*reinterpret_cast<eng::Smem*>(smem_raw), sched);
+__global__ void __launch_bounds__(eng::THREADS, 1)
+    gj_rowpanel_kernel(const __grid_constant__ CUtensorMap amap, RowPanelSched sched) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run(smem_raw, &amap, sched);
 }
 
-__global__ void __launch_bounds__(eng::THREADS, 1) gj_update_kernel(UpdateSched sched) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  eng::run<true>(*reinterpret_cast<eng::Smem*>(smem_raw), sched);
+__global__ void __launch_bounds__(eng::THREADS, 1)
+    gj_update_kernel(const __grid_constant__ CUtensorMap amap, UpdateSched sched) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run(smem_raw, &amap, sched);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int make_a_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+               int64_t stride, int64_t batch) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return RDB_ECUDA;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (((uintptr_t)base & 15) || (ld & 1) || (stride & 1)) return RDB_EINVAL;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)stride * 8};
+  const cuuint32_t box[3] = {eng::BK, eng::BM, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? RDB_OK : RDB_EINVAL;
 }
 
 static int g_sms = 0;
@@ -145,20 +186,22 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   if ((int64_t)batch * nt * nt > 2147483647LL) return RDB_EINVAL;
   int rc = setup();
   if (rc) return rc;
-  double* cwt = static_cast<double*>(work);
-  double* dt = cwt + batch * NB * n;
+  int* cnt = static_cast<int*>(work);
+  CUtensorMap amap;
+  rc = make_a_map(&amap, a, n, n, lda, batch > 1 ? stride : n * lda, batch);
+  if (rc) return rc;
+  if (cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)batch * nt, st) != cudaSuccess) return RDB_ECUDA;
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
-    gj_panel_kernel<<<dim3((unsigned)(1 + n / p1::CP_ROWS), (unsigned)batch), p1::THREADS, p1::SMEM_BYTES,
-                      st>>>(
-        a, n, lda, stride, p0, info, k == 0, cwt, dt);
+    gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, info,
+                                                                          k == 0);
     if (nt > 1) {
-      RowPanelSched rp{a, dt, lda, stride, nt, k, (int)batch};
+      RowPanelSched rp{a, lda, stride, nt, k, (int)batch};
       gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), eng::THREADS, eng::SMEM_BYTES,
-                           st>>>(rp);
-      UpdateSched up{a, cwt, n, lda, stride, nt, k, (int)batch};
+                           st>>>(amap, rp);
+      UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch};
       gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), eng::THREADS,
-                         eng::SMEM_BYTES, st>>>(up);
+                         eng::SMEM_BYTES, st>>>(amap, up);
     }
   }
   RDB_LAUNCH_CHECK();
@@ -177,21 +220,26 @@ struct ResidualSched {
   RDB_DEV eng::Tile tile(int t) const {
     const int I = t / nt, J = t - (t / nt) * nt;
     eng::Tile T;
-    T.a = m + (int64_t)I * NB * ldm;
-    T.lda = ldm;
+    T.a_col = 0;  // A operand: M rows I
+    T.a_row = I * NB;
+    T.a_mat = 0;
     T.b = y + (int64_t)J * NB;
     T.ldb = ldy;
     T.c = nullptr;
     T.ldc = I;  // row tile index (the epilogue needs the origin only)
     T.nk = nk;
     T.mode = J;
+    T.neg = 0;
+    T.signal = nullptr;
+    T.wait = nullptr;
+    T.wait_target = 0;
     return T;
   }
 };
 
 struct ResidualEpi {
   double* out_max;
-  RDB_DEV void operator()(const eng::Tile& T, double (&acc)[8][4][2], int wr, int wc, int lane,
+  RDB_DEV void operator()(eng::Tile T, double (&acc)[8][4][2], int wr, int wc, int lane,
                           double*) const {
     const int64_t row0 = T.ldc * NB + wr * 64, col0 = (int64_t)T.mode * NB + wc * 32;
     double mx = 0.0;
@@ -199,7 +247,7 @@ struct ResidualEpi {
     for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
-        const int64_t gi = row0 + mi * 8 + (lane >> 2);
+        const int64_t gi = row0 + mi * 8 + eng::pi_row(lane >> 2);
         const int64_t gj = col0 + ni * 8 + 2 * (lane & 3);
         const double e0 = fabs(acc[mi][ni][0] - (gi == gj ? 1.0 : 0.0));
         const double e1 = fabs(acc[mi][ni][1] - (gi == gj + 1 ? 1.0 : 0.0));
@@ -214,9 +262,10 @@ struct ResidualEpi {
   }
 };
 
-__global__ void __launch_bounds__(eng::THREADS, 1) residual_kernel(ResidualSched sched, ResidualEpi epi) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  eng::run<false>(*reinterpret_cast<eng::Smem*>(smem_raw), sched, epi);
+__global__ void __launch_bounds__(eng::THREADS, 1)
+    residual_kernel(const __grid_constant__ CUtensorMap amap, ResidualSched sched, ResidualEpi epi) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run(smem_raw, &amap, sched, epi);
 }
 
 }  // namespace rdb
@@ -225,7 +274,8 @@ using namespace rdb;
 
 extern "C" size_t rdb_invert_workspace_bytes(int64_t n_pad, int64_t batch) {
   if (n_pad <= 0 || batch <= 0) return 0;
-  return (size_t)batch * ((size_t)n_pad * NB + (size_t)NB * NB) * sizeof(double);
+  const size_t nt = (size_t)((n_pad + NB - 1) / NB);
+  return ((size_t)batch * nt * sizeof(int) + 255) & ~(size_t)255;
 }
 
 extern "C" int rdb_invert_batched(double* a, int64_t n_pad, int64_t lda, int64_t stride,
@@ -251,8 +301,11 @@ extern "C" int rdb_residual(const double* m, int64_t ldm, const double* y, int64
   const int nt = (int)(n_pad / NB);
   ResidualSched sched{m, y, ldm, ldy, nt, (int)(n_pad / eng::BK)};
   ResidualEpi epi{out_max};
+  CUtensorMap amap;
+  int rc = make_a_map(&amap, m, n_pad, n_pad, ldm, n_pad * ldm, 1);
+  if (rc) return rc;
   residual_kernel<<<persistent_grid((int64_t)nt * nt), eng::THREADS, eng::SMEM_BYTES,
-                    static_cast<cudaStream_t>(stream)>>>(sched, epi);
+                    static_cast<cudaStream_t>(stream)>>>(amap, sched, epi);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }

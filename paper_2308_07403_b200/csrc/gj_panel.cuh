@@ -180,9 +180,11 @@ RDB_DEV void panel_inverse(Smem& s, double* __restrict__ A, int64_t lda, int p0,
     const int r = e / (NB / 2), c2 = e % (NB / 2);
     stg2(A + (int64_t)r * lda + 2 * c2, *reinterpret_cast<const double2*>(&s.S[r * SST + 2 * c2]));
   }
-  for (int e = t; e < NB * NB; e += THREADS) {
-    const int r = e / NB, c = e % NB;  // dt[r][c] = D[c][r]; coalesced write
-    dt[e] = s.S[c * SST + r];
+  if (dt) {
+    for (int e = t; e < NB * NB; e += THREADS) {
+      const int r = e / NB, c = e % NB;  // dt[r][c] = D[c][r]; coalesced write
+      dt[e] = s.S[c * SST + r];
+    }
   }
   if (t == 0) {
     if (first) {

@@ -44,7 +44,7 @@ def test_abi_version_and_errors_without_gpu():
     assert lib.rdb_invert(None, 128, 128, None, None, None) == 1
     assert lib.rdb_invert(ctypes.c_void_p(256), 100, 100, ctypes.c_void_p(256), ctypes.c_void_p(256), None) == 1
     assert lib.rdb_log_ceil(None, 4, 4, 0, 1, None, 0.5, None, None, None, 4, 0, None, 0, None, None) == 1
-    assert lib.rdb_invert_workspace_bytes(1024, 256) == 256 * (1024 * 128 + 128 * 128) * 8
+    assert lib.rdb_invert_workspace_bytes(1024, 256) == 256 * 8 * 4  # row-block counters
     assert lib.rdb_invert_workspace_bytes(0, 1) == 0
 
 
