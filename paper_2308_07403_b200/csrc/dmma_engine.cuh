@@ -4,22 +4,22 @@
 //     acc(128x128) = sum_k A(rows, k) * B(k, cols)          (DMMA.8x8x4)
 //     C(rows, cols)  = +-acc (EPI_STORE)   or   C += +-acc (EPI_REDUCE)
 //
-// * warps 0-7 (MMA): 2 x 4 grid of 64x32 warp tiles, 64 fp64 accumulators per
-//   lane.
-// * warp 8 (producer): streams BK=16-deep k-chunks into a STAGES-deep ring,
+// * MMA warps: a WGM x WGN grid of warp tiles ((128/WGM) x (128/WGN)),
+//   accumulators in registers (Cfg below).
+// * one producer warp: streams BK=16-deep k-chunks into a STAGES-deep ring,
 //   one full/empty mbarrier pair per stage, running ahead across tile
 //   boundaries so the next tile's operands arrive during the epilogue.
-//   - A (row-major in global memory) arrives as ONE 2-D/3-D TMA tensor tile
+//   - A (row-major in global memory) arrives as ONE 3-D TMA tensor tile
 //     (cp.async.bulk.tensor, SASS UTMALDG): 128 rows x 16 doubles, 128-byte
 //     swizzle. The MMA row -> smem row map pi(r) = 2(r%4) + (r%8)/4 (within
 //     each 8-row group) makes the m8n8k4 A-fragment loads bank-conflict free
 //     under that swizzle; the epilogue writes accumulator row r to C row pi(r).
 //   - B (row-major) arrives as 16 one-dimensional bulk copies of 1 KB into a
 //     padded layout (row stride 132 doubles, conflict free).
-// * epilogue: each MMA warp stages 32x32 sub-tiles in shared memory and writes
-//   them back with bulk stores or bulk reduce-adds (cp.reduce.async.bulk
-//   .add.f64, SASS UBLKRED.ADD.F64.RN): C is never read by the SM; the L2
-//   applies C + acc with one IEEE rounding.
+// * epilogue: each MMA warp stages its tile in 16-/32-row pieces in shared
+//   memory and writes them back with bulk stores or bulk reduce-adds
+//   (cp.reduce.async.bulk .add.f64, SASS UBLKRED.ADD.F64.RN): C is never read
+//   by the SM; the L2 applies C + acc with one IEEE rounding.
 #pragma once
 #include <cuda.h>
 
@@ -31,21 +31,32 @@ namespace eng {
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
 constexpr int BST = BN + 4;  // B row stride (132 = 4 mod 16)
 constexpr int OST = 36;      // epilogue staging row stride (STS.128 conflict free for the pi row map)
-constexpr int MMA_WARPS = 8;
-constexpr int THREADS = (MMA_WARPS + 1) * 32;
-constexpr uint32_t A_STAGE_BYTES = BM * BK * 8;  // 16 KB, 1024-aligned (swizzle atom)
 constexpr uint32_t STAGE_BYTES = (BM * BK + BK * BN) * 8;
 
-enum { EPI_STORE = 0, EPI_REDUCE = 1 };
-
-struct Smem {
-  alignas(1024) double a[STAGES][BM * BK];
-  alignas(128) double b[STAGES][BK * BST];
-  alignas(128) double out[MMA_WARPS][32 * OST];
-  alignas(8) uint64_t full[STAGES];
-  alignas(8) uint64_t empty[STAGES];
+// Warp layout: WGM x WGN MMA warps, warp tile (8*MI) x (8*NI).
+template <int WGM_, int WGN_>
+struct Cfg {
+  static constexpr int WGM = WGM_, WGN = WGN_;
+  static constexpr int MMA_WARPS = WGM * WGN;
+  static constexpr int THREADS = (MMA_WARPS + 1) * 32;
+  static constexpr int MI = BM / WGM / 8;   // 8-row groups per warp
+  static constexpr int NI = BN / WGN / 8;   // 8-col groups per warp
+  static constexpr int WCOLS = NI * 8;      // warp tile width (doubles)
+  static constexpr int HROWS = MI * 8 / 2;  // staging piece height (half the warp tile)
+  struct Smem {
+    alignas(1024) double a[STAGES][BM * BK];
+    alignas(128) double b[STAGES][BK * BST];
+    alignas(128) double out[MMA_WARPS][HROWS * OST];
+    alignas(8) uint64_t full[STAGES];
+    alignas(8) uint64_t empty[STAGES];
+  };
+  static constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;  // + alignment slack
+  static_assert(WCOLS <= OST, "staging row holds a warp-tile row");
 };
-constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;  // + alignment slack
+
+using Default = Cfg<4, 4>;  // 16 MMA warps, 32x32 warp tiles
+
+enum { EPI_STORE = 0, EPI_REDUCE = 1 };
 
 // A tile job produced by a scheduler.
 struct Tile {
@@ -112,10 +123,12 @@ RDB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "m
 RDB_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 RDB_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
-// Default epilogue: C = +-acc (EPI_STORE) or C += +-acc (EPI_REDUCE) through two
-// 32-row halves of the per-warp staging buffer and bulk stores / reduce-adds.
+// Default epilogue: C = +-acc (EPI_STORE) or C += +-acc (EPI_REDUCE), the warp
+// tile staged in two halves through the per-warp staging buffer, written back
+// by per-row bulk stores / reduce-adds (one lane per row).
+template <class C>
 struct BulkEpilogue {
-  RDB_DEV void operator()(Tile T, double (&acc)[8][4][2], int wr, int wc, int lane,
+  RDB_DEV void operator()(Tile T, double (&acc)[C::MI][C::NI][2], int wr, int wc, int lane,
                           double* stage_out) const {
     const int lr = lane >> 2, lk = lane & 3;
     const int pr = pi_row(lr);
@@ -124,32 +137,35 @@ struct BulkEpilogue {
       bulk_wait_read0();  // this lane's previous bulk op has finished reading staging
       __syncwarp();
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < C::MI / 2; ++m)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
+        for (int ni = 0; ni < C::NI; ++ni) {
           const int row = m * 8 + pr;
           const int col = ni * 8 + 2 * lk;
-          const double x0 = acc[4 * h + m][ni][0], x1 = acc[4 * h + m][ni][1];
+          const double x0 = acc[(C::MI / 2) * h + m][ni][0], x1 = acc[(C::MI / 2) * h + m][ni][1];
           *reinterpret_cast<double2*>(&stage_out[row * OST + col]) =
               T.neg ? make_double2(-x0, -x1) : make_double2(x0, x1);
         }
       fence_proxy_async();
       __syncwarp();
-      double* dst = T.c + (int64_t)(wr * 64 + 32 * h + lane) * T.ldc + wc * 32;
-      if (T.mode == EPI_REDUCE)
-        bulk_s2g_add(dst, &stage_out[lane * OST], 32 * 8);
-      else
-        bulk_s2g(dst, &stage_out[lane * OST], 32 * 8);
-      bulk_commit();
+      if (lane < C::HROWS) {
+        double* dst = T.c + (int64_t)(wr * C::MI * 8 + C::HROWS * h + lane) * T.ldc + wc * C::WCOLS;
+        if (T.mode == EPI_REDUCE)
+          bulk_s2g_add(dst, &stage_out[lane * OST], C::WCOLS * 8);
+        else
+          bulk_s2g(dst, &stage_out[lane * OST], C::WCOLS * 8);
+        bulk_commit();
+      }
     }
   }
 };
 
 // Sched must provide: int count() and Tile tile(int t) (identical in every warp).
 // Epi: callable (Tile, acc, wr, wc, lane, staging) run by each MMA warp per tile.
-template <class Sched, class Epi = BulkEpilogue>
+template <class C, class Sched, class Epi>
 __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* amap, const Sched& sched,
-                                    const Epi& epi = Epi()) {
+                                    const Epi& epi) {
+  using Smem = typename C::Smem;
   // the 128-byte TMA swizzle atom needs a 1024-byte aligned destination: align
   // the dynamic shared memory base (pointer arithmetic keeps the shared space)
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -159,14 +175,14 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
   if (tid == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&s.full[i], 1);
-      mbar_init(&s.empty[i], MMA_WARPS);
+      mbar_init(&s.empty[i], C::MMA_WARPS);
     }
     fence_mbar_init();
   }
   __syncthreads();
   const int ntiles = sched.count();
 
-  if (warp == MMA_WARPS) {
+  if (warp == C::MMA_WARPS) {
     // ------------------------------------------------------------ producer
     if (lane == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(amap)) : "memory");
     int st = 0;
@@ -193,44 +209,44 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
   }
 
   // -------------------------------------------------------------- MMA warps
-  const int wr = warp >> 2;  // 0..1 : rows 64*wr
-  const int wc = warp & 3;   // 0..3 : cols 32*wc
+  const int wr = warp / C::WGN;
+  const int wc = warp % C::WGN;
   const int lr = lane >> 2, lk = lane & 3;
   // A fragment byte offsets within a stage for (mi, kk): physical row
-  // pr = 64wr + 8mi + pi(lr); 16-byte chunk ((kk+lk)/2) ^ (pr%8); +8 if odd k.
-  const int prow = wr * 64 + pi_row(lr);
+  // pr = 8*MI*wr + 8mi + pi(lr); 16-byte chunk ((kk+lk)/2) ^ (pr%8); +8 if odd k.
+  const int prow = wr * C::MI * 8 + pi_row(lr);
   const int psw = pi_row(lr);  // == prow % 8
   double* stage_out = s.out[warp];
   int st = 0;
   uint32_t ph = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile T = sched.tile(t);
-    double acc[8][4][2];
+    double acc[C::MI][C::NI][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     for (int c = 0; c < T.nk; ++c) {
       mbar_wait(&s.full[st], ph);
       // all of this tile's operands are in shared memory: release dependents
       if (c == T.nk - 1 && T.signal && warp == 0 && lane == 0) signal_done(T.signal);
       const char* sa = reinterpret_cast<const char*>(s.a[st]);
-      const double* sb = s.b[st] + lk * BST + wc * 32 + lr;
+      const double* sb = s.b[st] + lk * BST + wc * C::WCOLS + lr;
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
-        double af[8], bf[4];
+        double af[C::MI], bf[C::NI];
         const int kq = kk + lk;
         const int off = (((kq >> 1) ^ psw) << 4) + ((kq & 1) << 3);
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
+        for (int mi = 0; mi < C::MI; ++mi)
           af[mi] = *reinterpret_cast<const double*>(sa + (prow + mi * 8) * 128 + off);
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] = sb[kk * BST + ni * 8];
+        for (int ni = 0; ni < C::NI; ++ni) bf[ni] = sb[kk * BST + ni * 8];
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
+        for (int mi = 0; mi < C::MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.empty[st]);

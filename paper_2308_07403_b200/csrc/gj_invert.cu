@@ -29,6 +29,8 @@
 
 namespace rdb {
 
+using EC = eng::Default;  // engine warp layout
+
 __global__ void __launch_bounds__(p1::THREADS, 1)
     gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int p0,
                     rdb_pivot_info* __restrict__ info, int first) {
@@ -113,16 +115,16 @@ struct UpdateSched {
   }
 };
 
-__global__ void __launch_bounds__(eng::THREADS, 1)
+__global__ void __launch_bounds__(EC::THREADS, 1)
     gj_rowpanel_kernel(const __grid_constant__ CUtensorMap amap, RowPanelSched sched) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  eng::run(smem_raw, &amap, sched);
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>());
 }
 
-__global__ void __launch_bounds__(eng::THREADS, 1)
+__global__ void __launch_bounds__(EC::THREADS, 1)
     gj_update_kernel(const __grid_constant__ CUtensorMap amap, UpdateSched sched) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  eng::run(smem_raw, &amap, sched);
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>());
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -157,9 +159,9 @@ static int setup() {
   if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return RDB_ECUDA;
   if (cudaFuncSetAttribute(gj_rowpanel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)eng::SMEM_BYTES) != cudaSuccess ||
+                           (int)EC::SMEM_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)eng::SMEM_BYTES) != cudaSuccess ||
+                           (int)EC::SMEM_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)p1::SMEM_BYTES) != cudaSuccess)
     return RDB_ECUDA;
@@ -197,11 +199,11 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
                                                                           k == 0);
     if (nt > 1) {
       RowPanelSched rp{a, lda, stride, nt, k, (int)batch};
-      gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), eng::THREADS, eng::SMEM_BYTES,
+      gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES,
                            st>>>(amap, rp);
       UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch};
-      gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), eng::THREADS,
-                         eng::SMEM_BYTES, st>>>(amap, up);
+      gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), EC::THREADS,
+                         EC::SMEM_BYTES, st>>>(amap, up);
     }
   }
   RDB_LAUNCH_CHECK();
@@ -239,14 +241,14 @@ struct ResidualSched {
 
 struct ResidualEpi {
   double* out_max;
-  RDB_DEV void operator()(eng::Tile T, double (&acc)[8][4][2], int wr, int wc, int lane,
+  RDB_DEV void operator()(eng::Tile T, double (&acc)[EC::MI][EC::NI][2], int wr, int wc, int lane,
                           double*) const {
-    const int64_t row0 = T.ldc * NB + wr * 64, col0 = (int64_t)T.mode * NB + wc * 32;
+    const int64_t row0 = T.ldc * NB + wr * EC::MI * 8, col0 = (int64_t)T.mode * NB + wc * EC::WCOLS;
     double mx = 0.0;
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
+    for (int mi = 0; mi < EC::MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
+      for (int ni = 0; ni < EC::NI; ++ni) {
         const int64_t gi = row0 + mi * 8 + eng::pi_row(lane >> 2);
         const int64_t gj = col0 + ni * 8 + 2 * (lane & 3);
         const double e0 = fabs(acc[mi][ni][0] - (gi == gj ? 1.0 : 0.0));
@@ -262,10 +264,10 @@ struct ResidualEpi {
   }
 };
 
-__global__ void __launch_bounds__(eng::THREADS, 1)
+__global__ void __launch_bounds__(EC::THREADS, 1)
     residual_kernel(const __grid_constant__ CUtensorMap amap, ResidualSched sched, ResidualEpi epi) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  eng::run(smem_raw, &amap, sched, epi);
+  eng::run<EC>(smem_raw, &amap, sched, epi);
 }
 
 }  // namespace rdb
@@ -296,7 +298,7 @@ extern "C" int rdb_residual(const double* m, int64_t ldm, const double* y, int64
       ldy < n_pad)
     return RDB_EINVAL;
   if (cudaFuncSetAttribute(residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)eng::SMEM_BYTES) != cudaSuccess)
+                           (int)EC::SMEM_BYTES) != cudaSuccess)
     return RDB_ECUDA;
   const int nt = (int)(n_pad / NB);
   ResidualSched sched{m, y, ldm, ldy, nt, (int)(n_pad / eng::BK)};
@@ -304,7 +306,7 @@ extern "C" int rdb_residual(const double* m, int64_t ldm, const double* y, int64
   CUtensorMap amap;
   int rc = make_a_map(&amap, m, n_pad, n_pad, ldm, n_pad * ldm, 1);
   if (rc) return rc;
-  residual_kernel<<<persistent_grid((int64_t)nt * nt), eng::THREADS, eng::SMEM_BYTES,
+  residual_kernel<<<persistent_grid((int64_t)nt * nt), EC::THREADS, EC::SMEM_BYTES,
                     static_cast<cudaStream_t>(stream)>>>(amap, sched, epi);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
