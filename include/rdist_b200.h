@@ -135,6 +135,15 @@ int rdb_log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int6
                  int32_t* d32_out, int64_t ldo, int64_t stride_o, const uint8_t* reachable,
                  int64_t ldm, unsigned long long* counters, void* stream);
 
+/* K3 over a rows x cols block of a larger Y (e.g. sampled columns, or a rank's
+ * block-cyclic tiles): local row i is global row row0 + i, local column j is
+ * global column gcol[j] (device int64, or col0 + j when gcol is NULL); the
+ * forced-zero diagonal is where the two coincide. Outputs as rdb_log_ceil. */
+int rdb_log_ceil_block(const double* y, int64_t rows, int64_t cols, int64_t ldy, int64_t row0,
+                       int64_t col0, const int64_t* gcol, double gamma, double* r_out,
+                       double* dceil_out, int32_t* d32_out, int64_t ldo,
+                       unsigned long long* counters, void* stream);
+
 /* ---- K5: inversion residual max |M Y - I| (resolvent.py:125-127) --------
  * n_pad a multiple of RDB_NB; *out_max (device) must be zeroed by caller. */
 int rdb_residual(const double* m, int64_t ldm, const double* y, int64_t ldy, int64_t n_pad,

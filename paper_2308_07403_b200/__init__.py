@@ -30,6 +30,7 @@ from .resolvent import (
     gamma_bounds,
     precision_floor,
     r_distance,
+    r_distance_device,
     resolvent,
     rounded_r_distance,
     suggest_gamma,
@@ -69,6 +70,7 @@ __all__ = [
     "power_iteration",
     "precision_floor",
     "r_distance",
+    "r_distance_device",
     "resolvent",
     "rounded_r_distance",
     "rounded_r_distance_batch",

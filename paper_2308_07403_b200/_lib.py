@@ -66,6 +66,10 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
         _int,
         [_vp, _i64, _i64, _i64, _i64, _vp, _dbl, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp],
     ),
+    "rdb_log_ceil_block": (
+        _int,
+        [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _dbl, _vp, _vp, _vp, _i64, _vp, _vp],
+    ),
     "rdb_residual": (_int, [_vp, _i64, _vp, _i64, _i64, _vp, _vp]),
     "rdb_power_workspace_bytes": (_sz, [_i64]),
     "rdb_power_iteration": (_int, [_vp, _i64, _i64, _int, _dbl, _i64, _vp, _vp, _vp]),

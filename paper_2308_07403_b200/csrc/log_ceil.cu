@@ -68,18 +68,29 @@ struct Sink {
   }
 };
 
+// rows x cols block of a larger matrix: global row of local row i is row0 + i,
+// global column of local column j is gcol[j] (or col0 + j); the distance
+// diagonal (forced 0) is where they coincide.
+struct Shape {
+  int64_t rows, cols, row0, col0;
+  const int64_t* gcol;
+  RDB_DEV int64_t gc(int64_t j) const { return gcol ? gcol[j] : col0 + j; }
+};
+
 template <bool HAS_R, bool HAS_DC, bool HAS_D32, bool VEC>
 __global__ void __launch_bounds__(256)
-    log_ceil_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y,
+    log_ceil_kernel(const double* __restrict__ y, Shape sh, int64_t ldy, int64_t stride_y,
                     int64_t batch, const double* __restrict__ gammas, double gamma,
                     Sink<HAS_R, HAS_DC, HAS_D32> sink, int64_t ldo, int64_t stride_o,
                     const uint8_t* __restrict__ reach, int64_t ldm,
                     unsigned long long* __restrict__ counters) {
   const int lane = threadIdx.x & 31;
-  const int64_t rows = n * batch;
+  const int64_t n = sh.cols;
+  const int64_t rows = sh.rows * batch;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += nwarps) {
-    const int64_t b = w / n, i = w - b * n;
+    const int64_t b = w / sh.rows, i = w - b * sh.rows;
+    const int64_t gi = sh.row0 + i;
     const double g = gammas ? gammas[b] : gamma;
     const double lg = log(g);
     const double inv_lg = 1.0 / lg;
@@ -91,20 +102,22 @@ __global__ void __launch_bounds__(256)
       const int64_t j = j0 + 2 * lane;
       if (VEC && j + 1 < n) {
         const double2 v = ldg2(Y + j);
-        const double r0 = rdist_value(v.x, i == j, g, lg, inv_lg);
-        const double r1 = rdist_value(v.y, i == j + 1, g, lg, inv_lg);
+        const bool d0 = gi == sh.gc(j), d1 = gi == sh.gc(j + 1);
+        const double r0 = rdist_value(v.x, d0, g, lg, inv_lg);
+        const double r1 = rdist_value(v.y, d1, g, lg, inv_lg);
         sink.put2(orow + j, r0, r1);
         neg += (v.x < NEGATIVE_ENTRY_TOL) + (v.y < NEGATIVE_ENTRY_TOL);
-        if (M) under += (v.x == 0.0 && i != j && M[j]) + (v.y == 0.0 && i != j + 1 && M[j + 1]);
+        if (M) under += (v.x == 0.0 && !d0 && M[j]) + (v.y == 0.0 && !d1 && M[j + 1]);
       } else {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t jj = j + e;
           if (jj < n) {
             const double v = Y[jj];
-            sink.put1(orow + jj, rdist_value(v, i == jj, g, lg, inv_lg));
+            const bool dg = gi == sh.gc(jj);
+            sink.put1(orow + jj, rdist_value(v, dg, g, lg, inv_lg));
             neg += (v < NEGATIVE_ENTRY_TOL);
-            if (M) under += (v == 0.0 && i != jj && M[jj]);
+            if (M) under += (v == 0.0 && !dg && M[jj]);
           }
         }
       }
@@ -121,7 +134,7 @@ __global__ void __launch_bounds__(256)
 }
 
 template <bool A, bool B, bool C>
-static void launch(bool vec, unsigned blocks, cudaStream_t st, const double* y, int64_t n, int64_t ldy,
+static void launch(bool vec, unsigned blocks, cudaStream_t st, const double* y, Shape n, int64_t ldy,
                    int64_t stride_y, int64_t batch, const double* gammas, double gamma, double* r,
                    double* dc, int32_t* d32, int64_t ldo, int64_t stride_o, const uint8_t* reach,
                    int64_t ldm, unsigned long long* counters) {
@@ -134,24 +147,25 @@ static void launch(bool vec, unsigned blocks, cudaStream_t st, const double* y, 
                                                             ldo, stride_o, reach, ldm, counters);
 }
 
-int log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
-             const double* gammas, double gamma, double* r_out, double* dceil_out, int32_t* d32_out,
-             int64_t ldo, int64_t stride_o, const uint8_t* reachable, int64_t ldm,
-             unsigned long long* counters, cudaStream_t st) {
-  if (!y || n <= 0 || ldy < n || batch <= 0) return RDB_EINVAL;
+int log_ceil_shaped(const double* y, Shape sh, int64_t ldy, int64_t stride_y, int64_t batch,
+                    const double* gammas, double gamma, double* r_out, double* dceil_out,
+                    int32_t* d32_out, int64_t ldo, int64_t stride_o, const uint8_t* reachable,
+                    int64_t ldm, unsigned long long* counters, cudaStream_t st) {
+  const int64_t n = sh.cols;
+  if (!y || sh.rows <= 0 || n <= 0 || ldy < n || batch <= 0) return RDB_EINVAL;
   if ((r_out || dceil_out || d32_out) && ldo < n) return RDB_EINVAL;
   if (reachable && ldm < n) return RDB_EINVAL;
   if (!gammas && !(gamma > 0.0 && gamma < 1.0)) return RDB_EINVAL;
   auto al = [](const void* p, uintptr_t a) { return p == nullptr || ((uintptr_t)p % a) == 0; };
   const bool vec = !(ldy & 1) && !(stride_y & 1) && !(ldo & 1) && !(stride_o & 1) && al(y, 16) &&
                    al(r_out, 16) && al(dceil_out, 16) && al(d32_out, 8);
-  const int64_t rows = n * batch;
+  const int64_t rows = sh.rows * batch;
   const int64_t want = (rows + 7) / 8;
   const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
   const int key = (r_out ? 4 : 0) | (dceil_out ? 2 : 0) | (d32_out ? 1 : 0);
 #define RDB_LC(K, A, B, C)                                                                       \
   case K:                                                                                        \
-    launch<A, B, C>(vec, blocks, st, y, n, ldy, stride_y, batch, gammas, gamma, r_out, dceil_out, \
+    launch<A, B, C>(vec, blocks, st, y, sh, ldy, stride_y, batch, gammas, gamma, r_out, dceil_out, \
                     d32_out, ldo, stride_o, reachable, ldm, counters);                           \
     break;
   switch (key) {
@@ -169,7 +183,24 @@ int log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t 
   return RDB_OK;
 }
 
+int log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+             const double* gammas, double gamma, double* r_out, double* dceil_out, int32_t* d32_out,
+             int64_t ldo, int64_t stride_o, const uint8_t* reachable, int64_t ldm,
+             unsigned long long* counters, cudaStream_t st) {
+  return log_ceil_shaped(y, Shape{n, n, 0, 0, nullptr}, ldy, stride_y, batch, gammas, gamma, r_out,
+                         dceil_out, d32_out, ldo, stride_o, reachable, ldm, counters, st);
+}
+
 }  // namespace rdb
+
+extern "C" int rdb_log_ceil_block(const double* y, int64_t rows, int64_t cols, int64_t ldy,
+                                  int64_t row0, int64_t col0, const int64_t* gcol, double gamma,
+                                  double* r_out, double* dceil_out, int32_t* d32_out, int64_t ldo,
+                                  unsigned long long* counters, void* stream) {
+  return rdb::log_ceil_shaped(y, rdb::Shape{rows, cols, row0, col0, gcol}, ldy, 0, 1, nullptr, gamma, r_out,
+                              dceil_out, d32_out, ldo, 0, nullptr, 0, counters,
+                              static_cast<cudaStream_t>(stream));
+}
 
 extern "C" int rdb_log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
                             const double* gammas, double gamma, double* r_out, double* dceil_out,
