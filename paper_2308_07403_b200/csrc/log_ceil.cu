@@ -17,6 +17,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "log_table.cuh"
 
 namespace rdb {
 
@@ -42,10 +43,50 @@ RDB_DEV double refine_near_integer(double y, double g, double lg, double r) {
   return k + delta;
 }
 
-RDB_DEV double rdist_value(double v, bool diag, double g, double lg, double inv_lg) {
-  if (diag) return 0.0;
+// Natural log of a positive finite double in ~18 FP64 operations (within ~1
+// ulp): y = 2^e m, m in [1, 2); a 128-entry table (log_table.cuh, staged in
+// shared memory) gives c ~ 1/m and L = -log c (double-double, folded with ln 2;
+// c = 1 and 1/2 exactly in the two intervals around y = 1, so no term cancels
+// there); log1p(m c - 1), |m c - 1| <= 2^-7, by its Taylor series to r^8.
+struct LogTab {
+  double c[128], hi[128], lo[128];
+};
+
+RDB_DEV double fast_log(double y, const LogTab& T) {
+  long long b = __double_as_longlong(y);
+  int ex = (int)(b >> 52);
+  int esub = 0;
+  if (ex == 0) {  // subnormal: scale by 2^54
+    b = __double_as_longlong(y * 18014398509481984.0);
+    ex = (int)(b >> 52);
+    esub = 54;
+  }
+  const int idx = (int)((b >> 45) & 127);
+  const double m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  const double e = (double)(ex - 1023 - esub + (idx >= 53 ? 1 : 0));
+  const double r = fma(m, T.c[idx], -1.0);
+  double p = fma(r, -0.125, 1.0 / 7.0);
+  p = fma(r, p, -1.0 / 6.0);
+  p = fma(r, p, 1.0 / 5.0);
+  p = fma(r, p, -0.25);
+  p = fma(r, p, 1.0 / 3.0);
+  p = fma(r, p, -0.5);
+  p = fma(r * r, p, r);
+  const double a = e * logtab::LN2_HI;  // exact (LN2_HI has 21 significant bits)
+  const double bh = T.hi[idx];
+  const double s = a + bh;
+  // Fast2Sum error: valid as |a| >= ln2/2 > |bh| when e != 0, and exactly 0 when e == 0
+  const double t = (a - s) + bh;
+  return s + (t + fma(e, logtab::LN2_LO, T.lo[idx]) + p);
+}
+
+RDB_DEV double rdist_value(double v, double g, double lg, double inv_lg, const LogTab& T) {
   if (!(v > 0.0)) return INFINITY;
-  return refine_near_integer(v, g, lg, log(v) * inv_lg);
+  if (!(v < INFINITY)) return -INFINITY;  // log(inf) / log(gamma), as numpy
+  const double r = fast_log(v, T) * inv_lg;
+  // only quotients within 1e-9 of an integer can change the ceil: refine those
+  if (fabs(r - rint(r)) <= 1e-9 * fmax(1.0, r)) return refine_near_integer(v, g, lg, r);
+  return r;
 }
 
 template <bool HAS_R, bool HAS_DC, bool HAS_D32>
@@ -53,18 +94,17 @@ struct Sink {
   double* r;
   double* dc;
   int32_t* d32;
-  RDB_DEV static int32_t to_i32(double dcv) { return (dcv < 2147483647.0) ? (int32_t)dcv : INT_MAX; }
+  // ceil to int32 in one saturating conversion: +inf -> INT_MAX (the sentinel)
+  RDB_DEV static int32_t to_i32(double rv) { return __double2int_ru(rv); }
   RDB_DEV void put1(int64_t o, double rv) const {
-    const double dcv = ceil(rv);
     if (HAS_R) r[o] = rv;
-    if (HAS_DC) dc[o] = dcv;
-    if (HAS_D32) d32[o] = to_i32(dcv);
+    if (HAS_DC) dc[o] = ceil(rv);
+    if (HAS_D32) d32[o] = to_i32(rv);
   }
   RDB_DEV void put2(int64_t o, double r0, double r1) const {
-    const double c0 = ceil(r0), c1 = ceil(r1);
     if (HAS_R) *reinterpret_cast<double2*>(r + o) = make_double2(r0, r1);
-    if (HAS_DC) *reinterpret_cast<double2*>(dc + o) = make_double2(c0, c1);
-    if (HAS_D32) *reinterpret_cast<int2*>(d32 + o) = make_int2(to_i32(c0), to_i32(c1));
+    if (HAS_DC) *reinterpret_cast<double2*>(dc + o) = make_double2(ceil(r0), ceil(r1));
+    if (HAS_D32) *reinterpret_cast<int2*>(d32 + o) = make_int2(to_i32(r0), to_i32(r1));
   }
 };
 
@@ -84,6 +124,13 @@ __global__ void __launch_bounds__(256)
                     Sink<HAS_R, HAS_DC, HAS_D32> sink, int64_t ldo, int64_t stride_o,
                     const uint8_t* __restrict__ reach, int64_t ldm,
                     unsigned long long* __restrict__ counters) {
+  __shared__ LogTab tab;
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+    tab.c[i] = logtab::kC[i];
+    tab.hi[i] = logtab::kLhi[i];
+    tab.lo[i] = logtab::kLlo[i];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t n = sh.cols;
   const int64_t rows = sh.rows * batch;
@@ -91,6 +138,8 @@ __global__ void __launch_bounds__(256)
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += nwarps) {
     const int64_t b = w / sh.rows, i = w - b * sh.rows;
     const int64_t gi = sh.row0 + i;
+    const bool mapped = sh.gcol != nullptr;
+    const int64_t dj = gi - sh.col0;  // local diagonal column when not mapped
     const double g = gammas ? gammas[b] : gamma;
     const double lg = log(g);
     const double inv_lg = 1.0 / lg;
@@ -98,13 +147,40 @@ __global__ void __launch_bounds__(256)
     const int64_t orow = b * stride_o + i * ldo;
     const uint8_t* M = reach ? reach + i * ldm : nullptr;
     unsigned neg = 0, under = 0;
-    for (int64_t j0 = 0; j0 < n; j0 += 64) {
+    int64_t jstart = 0;
+    if (VEC) {
+      // main body: 4 chunks of 64 columns per pass, all loads issued before any
+      // math (memory-level parallelism for an HBM-bound row sweep)
+      constexpr int U = 4;
+      for (; jstart + 64 * U <= n; jstart += 64 * U) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ldg2(Y + jstart + 64 * u + 2 * lane);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = jstart + 64 * u + 2 * lane;
+          const bool d0 = mapped ? gi == sh.gcol[j] : j == dj;
+          const bool d1 = mapped ? gi == sh.gcol[j + 1] : j + 1 == dj;
+          double r0 = rdist_value(v[u].x, g, lg, inv_lg, tab);
+          double r1 = rdist_value(v[u].y, g, lg, inv_lg, tab);
+          r0 = d0 ? 0.0 : r0;
+          r1 = d1 ? 0.0 : r1;
+          sink.put2(orow + j, r0, r1);
+          neg += (v[u].x < NEGATIVE_ENTRY_TOL) + (v[u].y < NEGATIVE_ENTRY_TOL);
+          if (M) under += (v[u].x == 0.0 && !d0 && M[j]) + (v[u].y == 0.0 && !d1 && M[j + 1]);
+        }
+      }
+    }
+    for (int64_t j0 = jstart; j0 < n; j0 += 64) {
       const int64_t j = j0 + 2 * lane;
       if (VEC && j + 1 < n) {
         const double2 v = ldg2(Y + j);
-        const bool d0 = gi == sh.gc(j), d1 = gi == sh.gc(j + 1);
-        const double r0 = rdist_value(v.x, d0, g, lg, inv_lg);
-        const double r1 = rdist_value(v.y, d1, g, lg, inv_lg);
+        const bool d0 = mapped ? gi == sh.gcol[j] : j == dj;
+        const bool d1 = mapped ? gi == sh.gcol[j + 1] : j + 1 == dj;
+        double r0 = rdist_value(v.x, g, lg, inv_lg, tab);
+        double r1 = rdist_value(v.y, g, lg, inv_lg, tab);
+        r0 = d0 ? 0.0 : r0;
+        r1 = d1 ? 0.0 : r1;
         sink.put2(orow + j, r0, r1);
         neg += (v.x < NEGATIVE_ENTRY_TOL) + (v.y < NEGATIVE_ENTRY_TOL);
         if (M) under += (v.x == 0.0 && !d0 && M[j]) + (v.y == 0.0 && !d1 && M[j + 1]);
@@ -114,8 +190,8 @@ __global__ void __launch_bounds__(256)
           const int64_t jj = j + e;
           if (jj < n) {
             const double v = Y[jj];
-            const bool dg = gi == sh.gc(jj);
-            sink.put1(orow + jj, rdist_value(v, dg, g, lg, inv_lg));
+            const bool dg = mapped ? gi == sh.gcol[jj] : jj == dj;
+            sink.put1(orow + jj, dg ? 0.0 : rdist_value(v, g, lg, inv_lg, tab));
             neg += (v < NEGATIVE_ENTRY_TOL);
             if (M) under += (v == 0.0 && !dg && M[jj]);
           }

@@ -151,6 +151,26 @@ class TestRDistance:
                 assert r[1, 0] == 1.0
                 assert abs(r[0, 1] - ref[0, 1]) <= 4e-16 * k
 
+    def test_log_accuracy_full_range(self, cuda):
+        # K3's table logarithm over subnormals .. 1e300, and near 1 (no cancellation)
+        rng = np.random.default_rng(11)
+        e = rng.uniform(-1074, 1000, size=20000)
+        y = np.exp2(e) * rng.uniform(1, 2, size=e.size)
+        y = np.concatenate([y, 1 + rng.uniform(-1e-3, 1e-3, 4000), 1 - np.geomspace(1e-16, 0.3, 4000),
+                            [5e-324, 1e-310, 2.2250738585072014e-308, 0.7071067811865476, 1.4142135623730951]])
+        y = y[np.isfinite(y) & (y > 0) & (y != 1.0)]
+        k = int(np.ceil(np.sqrt(y.size)))
+        mat = np.full(k * k, 0.5)
+        mat[: y.size] = y
+        mat = mat.reshape(k, k)
+        np.fill_diagonal(mat, 1.0)
+        for gamma in (0.3, 1e-3):
+            r = rb.r_distance(rb.ResolventResult(mat, gamma, rb.HealthFlags(False, None, 0.0)))
+            ref = orc.r_distance(mat, gamma)
+            off = ~np.eye(k, dtype=bool)
+            rel = np.abs(r[off] - ref[off]) / np.abs(ref[off])
+            assert rel.max() < 2e-15, rel.max()
+
     def test_matches_oracle_logs(self, cuda):
         rng = np.random.default_rng(3)
         y = np.exp(rng.uniform(-120, 0, size=(200, 200)))
