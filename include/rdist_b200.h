@@ -112,6 +112,23 @@ int rdb_invert_batched(double* a, int64_t n_pad, int64_t lda, int64_t stride, in
 int rdb_invert(double* a, int64_t n_pad, int64_t lda, void* work, rdb_pivot_info* info,
                void* stream);
 
+/* Building blocks of the distributed (2D block-cyclic) inversion, where each
+ * rank holds a local matrix of NB x NB tiles and receives the panels by NCCL
+ * broadcast (paper_2308_07403_b200/distributed.py):
+ *   rdb_gj_panel_inverse: D = A^-1 in place for one NB x NB block (P1); pivot
+ *     record as rdb_invert (first != 0 resets it; p0 = the block's global
+ *     index for min_index);
+ *   rdb_gemm_local: C (m x n) op= (negate ? -1 : 1) * A (m x k) * B (k x n),
+ *     A, B, C row-major, m, n multiples of NB and k of 16; op is += (TMA
+ *     reduce-add) when accumulate != 0, else =; row tile skip_row_tile and
+ *     column tile skip_col_tile are left untouched (-1: none); column tile
+ *     store_col_tile is always stored (=). Same DMMA engine as rdb_invert. */
+int rdb_gj_panel_inverse(double* a, int64_t lda, rdb_pivot_info* info, int first, int64_t p0,
+                         void* stream);
+int rdb_gemm_local(const double* a, int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+                   int64_t m, int64_t n, int64_t k, int64_t skip_row_tile, int64_t skip_col_tile,
+                   int64_t store_col_tile, int accumulate, int negate, void* stream);
+
 /* Gauss-Jordan with partial (row) pivoting, first-max pivot choice as
  * LAPACK idamax; in place, any n. For generic matrices handed to
  * lu_invert (linalg.py:18-39) that carry no M-matrix certificate.

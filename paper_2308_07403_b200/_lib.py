@@ -60,6 +60,11 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "rdb_invert_workspace_bytes": (_sz, [_i64, _i64]),
     "rdb_invert_batched": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "rdb_invert": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
+    "rdb_gj_panel_inverse": (_int, [_vp, _i64, _vp, _int, _i64, _vp]),
+    "rdb_gemm_local": (
+        _int,
+        [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _int, _int, _vp],
+    ),
     "rdb_invert_pivoted_workspace_bytes": (_sz, [_i64]),
     "rdb_invert_pivoted": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "rdb_log_ceil": (

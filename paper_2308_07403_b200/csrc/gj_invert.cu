@@ -32,12 +32,13 @@ namespace rdb {
 using EC = eng::Default;  // engine warp layout
 
 __global__ void __launch_bounds__(p1::THREADS, 1)
-    gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int p0,
+    gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int64_t off, int idx0,
                     rdb_pivot_info* __restrict__ info, int first) {
+  // block at a + b*stride + off*(lda + 1); pivot indices recorded from idx0
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
-  p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), a + b * stride + (int64_t)p0 * lda + p0,
-                    lda, p0, info + b, first, nullptr);
+  p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), a + b * stride + off * lda + off, lda, idx0,
+                    info + b, first, nullptr);
 }
 
 // ------------------------------------------------------------------ schedulers
@@ -195,7 +196,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   if (cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)batch * nt, st) != cudaSuccess) return RDB_ECUDA;
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
-    gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, info,
+    gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, p0, info,
                                                                           k == 0);
     if (nt > 1) {
       RowPanelSched rp{a, lda, stride, nt, k, (int)batch};
@@ -208,6 +209,49 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   }
   RDB_LAUNCH_CHECK();
   return RDB_OK;
+}
+
+// ------------------------------------------------------------------ local GEMM (distributed GJ)
+// C (m x n tiles of 128) op= sign * A (m x K) * B (K x n) for a rank's local
+// tiles of the 2D block-cyclic inversion: A = the received column panel, B =
+// the received row panel (or D and the local row block for the row-panel
+// product). Row tile skip_row and column tile skip_col are left out; column
+// tile store_col is stored instead of accumulated.
+struct LocalSched {
+  const double* b;
+  double* c;
+  int64_t ldb, ldc;
+  int mt, nt, nk, skip_row, skip_col, store_col, mode, neg;
+  RDB_DEV int rows() const { return mt - (skip_row >= 0 ? 1 : 0); }
+  RDB_DEV int cols() const { return nt - (skip_col >= 0 ? 1 : 0); }
+  RDB_DEV int count() const { return rows() * cols(); }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int nc = cols();
+    int I = t / nc, J = t - (t / nc) * nc;
+    if (skip_row >= 0 && I >= skip_row) ++I;
+    if (skip_col >= 0 && J >= skip_col) ++J;
+    eng::Tile T;
+    T.a_col = 0;
+    T.a_row = I * NB;
+    T.a_mat = 0;
+    T.b = b + (int64_t)J * NB;
+    T.ldb = ldb;
+    T.c = c + (int64_t)I * NB * ldc + (int64_t)J * NB;
+    T.ldc = ldc;
+    T.nk = nk;
+    T.mode = (J == store_col) ? eng::EPI_STORE : mode;
+    T.neg = neg;
+    T.signal = nullptr;
+    T.wait = nullptr;
+    T.wait_target = 0;
+    return T;
+  }
+};
+
+__global__ void __launch_bounds__(EC::THREADS, 1)
+    local_gemm_kernel(const __grid_constant__ CUtensorMap amap, LocalSched sched) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>());
 }
 
 // ------------------------------------------------------------------ K5 residual
@@ -290,6 +334,51 @@ extern "C" int rdb_invert(double* a, int64_t n_pad, int64_t lda, void* work, rdb
                           void* stream) {
   return invert_batched(a, n_pad, lda, n_pad * lda, 1, work, info,
                         static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int rdb_gj_panel_inverse(double* a, int64_t lda, rdb_pivot_info* info, int first, int64_t p0,
+                                    void* stream) {
+  if (!a || !info || lda < NB || (lda & 1) || ((uintptr_t)a & 15)) return RDB_EINVAL;
+  int rc = setup();
+  if (rc) return rc;
+  // the block is at `a`; p0 is its global index, used only for the recorded pivot index
+  gj_panel_kernel<<<1, p1::THREADS, p1::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(a, lda, 0, 0, (int)p0,
+                                                                                         info, first);
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+
+extern "C" int rdb_gemm_local(const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                              int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t skip_row_tile,
+                              int64_t skip_col_tile, int64_t store_col_tile, int accumulate, int negate,
+                              void* stream) {
+  if (!a || !b || !c || m <= 0 || n <= 0 || k <= 0 || m % NB || n % NB || k % eng::BK) return RDB_EINVAL;
+  if ((lda & 1) || (ldb & 1) || (ldc & 1) || lda < k || ldb < n || ldc < n) return RDB_EINVAL;
+  if (((uintptr_t)b & 15) || ((uintptr_t)c & 15)) return RDB_EINVAL;
+  int rc = setup();
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(local_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)EC::SMEM_BYTES) != cudaSuccess)
+      return RDB_ECUDA;
+    attr = true;
+  }
+  CUtensorMap amap;
+  rc = make_a_map(&amap, a, m, k, lda, m * lda, 1);
+  if (rc) return rc;
+  const int mt = (int)(m / NB), nt = (int)(n / NB);
+  LocalSched sched{b, c, ldb, ldc, mt, nt, (int)(k / eng::BK),
+                   (int)(skip_row_tile >= 0 && skip_row_tile < mt ? skip_row_tile : -1),
+                   (int)(skip_col_tile >= 0 && skip_col_tile < nt ? skip_col_tile : -1),
+                   (int)(store_col_tile >= 0 && store_col_tile < nt ? store_col_tile : -1),
+                   accumulate ? eng::EPI_REDUCE : eng::EPI_STORE, negate ? 1 : 0};
+  const int64_t tiles = (int64_t)(mt - (sched.skip_row >= 0)) * (nt - (sched.skip_col >= 0));
+  if (tiles <= 0) return RDB_OK;
+  local_gemm_kernel<<<persistent_grid(tiles), EC::THREADS, EC::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
+      amap, sched);
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
 }
 
 extern "C" int rdb_residual(const double* m, int64_t ldm, const double* y, int64_t ldy,
