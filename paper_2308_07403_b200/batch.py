@@ -119,19 +119,37 @@ def check_infos(infos: list[L.PivotInfo], gammas: np.ndarray, first_index: int =
 class APSPBatchEngine:
     """Reusable pipeline: pinned host bits -> device -> int32 D -> pinned host.
 
-    Chunks alternate between two streams so the device->host copy of one
-    chunk overlaps the kernels of the next.
+    All kernels run back to back on one compute stream, chunk by chunk; a copy
+    stream moves each chunk's int32 D to pinned host memory as soon as its K3
+    finishes (CUDA events), so the device->host transfer of chunk i overlaps
+    the kernels of chunks i+1, i+2, ... Two D slots ping-pong; the M / work
+    buffers are reused by every chunk (the compute stream orders them).
     """
 
-    def __init__(self, n: int, max_batch: int, chunk: int = 64):
+    def __init__(self, n: int, max_batch: int, chunk: int = 128):
         self.dev = L.device()
         self.n = n
+        self.n_pad = L.pad_to_nb(n)
         self.max_batch = max_batch
         self.chunk = max(1, min(chunk, max_batch))
-        self.bufs = [BatchBuffers.allocate(n, self.chunk, self.dev) for _ in range(2)]
-        self.streams = [torch.cuda.Stream(device=self.dev) for _ in range(2)]
-        self.out = torch.empty((max_batch, n, n), dtype=torch.int32).pin_memory()
-        self.info_host = torch.empty(max_batch * 16, dtype=torch.uint8).pin_memory()
+        wpr = (n + 31) // 32
+        dev = self.dev
+        self.bits = torch.empty((max_batch, n, wpr), dtype=torch.int32, device=dev)
+        self.gammas = torch.empty(max_batch, dtype=torch.float64, device=dev)
+        self.m = torch.empty((self.chunk, self.n_pad, self.n_pad), dtype=torch.float64, device=dev)
+        self.work = torch.empty(L.lib().rdb_invert_workspace_bytes(self.n_pad, self.chunk), dtype=torch.uint8,
+                                device=dev)
+        self.infos = [L.pivot_info_tensor(max_batch, dev) for _ in range(2)]
+        self.counters = torch.zeros((max_batch, L.RDB_NCOUNTERS), dtype=torch.int64, device=dev)
+        self.d = [torch.empty((self.chunk, n, n), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.cs = torch.cuda.Stream(device=dev)
+        self.xs = torch.cuda.Stream(device=dev)
+        self.computed = [torch.cuda.Event() for _ in range(2)]
+        self.copied = [torch.cuda.Event() for _ in range(2)]
+        self.outs = [torch.empty((max_batch, n, n), dtype=torch.int32).pin_memory() for _ in range(2)]
+        self.info_hosts = [torch.empty(max_batch * 16, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        self.pending = [0, 0]
         self.launches = 0
 
     def pin(self, bits: np.ndarray, gammas) -> tuple[torch.Tensor, torch.Tensor]:
@@ -142,36 +160,64 @@ class APSPBatchEngine:
             raise ValueError("every gamma must be in (0, 1)")
         return torch.from_numpy(bits.view(np.int32)).pin_memory(), torch.from_numpy(g).pin_memory()
 
-    def submit(self, bits_pin: torch.Tensor, gammas_pin: torch.Tensor) -> int:
-        """Enqueue the whole batch; returns its size. Call :meth:`finish` to wait."""
+    def submit(self, bits_pin: torch.Tensor, gammas_pin: torch.Tensor, slot: int = 0) -> int:
+        """Enqueue the whole batch into output slot ``slot`` (0 or 1) and return
+        its size; :meth:`wait` (or :meth:`finish`) collects it. Batches
+        submitted to alternating slots stream back to back: the kernels of one
+        overlap the device->host copy of the previous one."""
         batch = bits_pin.shape[0]
         if batch > self.max_batch:
             raise ValueError(f"batch {batch} exceeds engine capacity {self.max_batch}")
+        if self.pending[slot]:
+            raise RuntimeError(f"slot {slot} still holds an uncollected batch")
+        self.pending[slot] = batch
+        out, info_host, info = self.outs[slot], self.info_hosts[slot], self.infos[slot]
         cur = torch.cuda.current_stream(self.dev)
-        for s in self.streams:
-            s.wait_stream(cur)
+        self.cs.wait_stream(cur)
+        self.xs.wait_stream(cur)
+        lib = L.lib()
         for idx, c0 in enumerate(range(0, batch, self.chunk)):
-            k = idx % 2
+            s = idx % 2
             cnt = min(self.chunk, batch - c0)
-            buf, s = self.bufs[k], self.streams[k]
-            with torch.cuda.stream(s):
-                buf.bits[:cnt].copy_(bits_pin[c0 : c0 + cnt], non_blocking=True)
-                buf.gammas[:cnt].copy_(gammas_pin[c0 : c0 + cnt], non_blocking=True)
-                run_chunk(buf, cnt, s.cuda_stream)
+            with torch.cuda.stream(self.cs):
+                self.bits[c0 : c0 + cnt].copy_(bits_pin[c0 : c0 + cnt], non_blocking=True)
+                self.gammas[c0 : c0 + cnt].copy_(gammas_pin[c0 : c0 + cnt], non_blocking=True)
+                if idx >= 2:
+                    self.cs.wait_event(self.copied[s])  # slot s drained to the host
+                L.check(
+                    lib.rdb_apsp_bits_batched(
+                        self.bits[c0].data_ptr(), self.n, cnt, self.gammas[c0:].data_ptr(), self.m.data_ptr(),
+                        self.work.data_ptr(), info[c0 * 16 :].data_ptr(), self.d[s].data_ptr(),
+                        self.counters[c0].data_ptr(), self.cs.cuda_stream),
+                    "rdb_apsp_bits_batched",
+                )
                 self.launches += launches_per_call(self.n)
-                self.out[c0 : c0 + cnt].copy_(buf.d[:cnt], non_blocking=True)
-                self.info_host[c0 * 16 : (c0 + cnt) * 16].copy_(buf.info[: cnt * 16], non_blocking=True)
+                self.computed[s].record(self.cs)
+            with torch.cuda.stream(self.xs):
+                self.xs.wait_event(self.computed[s])
+                out[c0 : c0 + cnt].copy_(self.d[s][:cnt], non_blocking=True)
+                self.copied[s].record(self.xs)
+        with torch.cuda.stream(self.xs):
+            self.xs.wait_stream(self.cs)
+            info_host[: batch * 16].copy_(info[: batch * 16], non_blocking=True)
+            self.done[slot].record(self.xs)
         return batch
 
-    def finish(self, batch: int, gammas_pin: torch.Tensor, check: bool = True) -> np.ndarray:
-        for s in self.streams:
-            s.synchronize()
+    def wait(self, slot: int, gammas_pin: torch.Tensor, check: bool = True) -> np.ndarray:
+        """Block until slot ``slot``'s batch is in host memory; its int32 D."""
+        batch = self.pending[slot]
+        self.done[slot].synchronize()
+        self.pending[slot] = 0
         if check:
-            check_infos(L.read_pivot_info(self.info_host[: batch * 16]), gammas_pin.numpy())
-        return self.out[:batch].numpy()
+            check_infos(L.read_pivot_info(self.info_hosts[slot][: batch * 16]), gammas_pin.numpy())
+        return self.outs[slot][:batch].numpy()
+
+    def finish(self, batch: int, gammas_pin: torch.Tensor, check: bool = True) -> np.ndarray:
+        return self.wait(0, gammas_pin, check)
 
     def run(self, bits_pin: torch.Tensor, gammas_pin: torch.Tensor, check: bool = True) -> np.ndarray:
-        return self.finish(self.submit(bits_pin, gammas_pin), gammas_pin, check)
+        self.submit(bits_pin, gammas_pin, 0)
+        return self.wait(0, gammas_pin, check)
 
 
 def rounded_r_distance_batch(bits: np.ndarray, gammas, n: int, *, chunk: int = 64) -> np.ndarray:
