@@ -46,12 +46,11 @@ struct Cfg {
   struct Smem {
     alignas(1024) double a[STAGES][BM * BK];
     alignas(128) double b[STAGES][BK * BST];
-    alignas(128) double out[MMA_WARPS][HROWS * OST];
+    alignas(128) double out[MMA_WARPS][HROWS * WCOLS];  // dense HROWS x WCOLS TMA box per warp
     alignas(8) uint64_t full[STAGES];
     alignas(8) uint64_t empty[STAGES];
   };
   static constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;  // + alignment slack
-  static_assert(WCOLS <= OST, "staging row holds a warp-tile row");
 };
 
 using Default = Cfg<4, 4>;  // 16 MMA warps, 32x32 warp tiles
@@ -63,8 +62,7 @@ struct Tile {
   int a_col, a_row, a_mat;  // TMA coordinates of A(row0, k=0): column, row, matrix (batch) index
   const double* b;          // &B[0][col0]
   int64_t ldb;
-  double* c;                // &C[row0][col0]
-  int64_t ldc;
+  int c_col, c_row, c_mat;  // TMA coordinates of C(row0, col0) in the C tensor map
   int nk;                   // number of BK chunks
   int mode;                 // EPI_STORE / EPI_REDUCE
   int neg;                  // write -acc instead of acc
@@ -120,17 +118,34 @@ RDB_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\
 RDB_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 // Default epilogue: C = +-acc (EPI_STORE) or C += +-acc (EPI_REDUCE), the warp
-// tile staged in two halves through the per-warp staging buffer, written back
-// by per-row bulk stores / reduce-adds (one lane per row).
+// tile staged in two HROWS x WCOLS halves through the per-warp staging buffer
+// (dense, the TMA box layout), each written back by ONE tensor store / tensor
+// reduce-add (SASS UTMASTG / UTMAREDG.ADD) issued by lane 0.
+RDB_DEV void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+
+RDB_DEV void tma_reduce_add_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+      : "memory");
+}
+
 template <class C>
 struct BulkEpilogue {
+  const CUtensorMap* cmap;  // box HROWS x WCOLS over the output matrices
   RDB_DEV void operator()(Tile T, double (&acc)[C::MI][C::NI][2], int wr, int wc, int lane,
                           double* stage_out) const {
     const int lr = lane >> 2, lk = lane & 3;
     const int pr = pi_row(lr);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      bulk_wait_read0();  // this lane's previous bulk op has finished reading staging
+      if (lane == 0) bulk_wait_read0();  // the previous piece has left the staging buffer
       __syncwarp();
 #pragma unroll
       for (int m = 0; m < C::MI / 2; ++m)
@@ -139,17 +154,18 @@ struct BulkEpilogue {
           const int row = m * 8 + pr;
           const int col = ni * 8 + 2 * lk;
           const double x0 = acc[(C::MI / 2) * h + m][ni][0], x1 = acc[(C::MI / 2) * h + m][ni][1];
-          *reinterpret_cast<double2*>(&stage_out[row * OST + col]) =
+          *reinterpret_cast<double2*>(&stage_out[row * C::WCOLS + col]) =
               T.neg ? make_double2(-x0, -x1) : make_double2(x0, x1);
         }
       fence_proxy_async();
       __syncwarp();
-      if (lane < C::HROWS) {
-        double* dst = T.c + (int64_t)(wr * C::MI * 8 + C::HROWS * h + lane) * T.ldc + wc * C::WCOLS;
+      if (lane == 0) {
+        const int c0 = T.c_col + wc * C::WCOLS;
+        const int c1 = T.c_row + wr * C::MI * 8 + C::HROWS * h;
         if (T.mode == EPI_REDUCE)
-          bulk_s2g_add(dst, &stage_out[lane * OST], C::WCOLS * 8);
+          tma_reduce_add_3d(cmap, c0, c1, T.c_mat, stage_out);
         else
-          bulk_s2g(dst, &stage_out[lane * OST], C::WCOLS * 8);
+          tma_store_3d(cmap, c0, c1, T.c_mat, stage_out);
         bulk_commit();
       }
     }
@@ -268,5 +284,9 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
 // 128-byte swizzle — the engine's A operand. Returns RDB_OK or an error.
 int make_a_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
                int64_t stride, int64_t batch);
+// Host: the epilogue's C map over the same kind of 3-D layout, box
+// box_rows x box_cols, no swizzle (the staging buffer is the dense box).
+int make_c_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+               int64_t stride, int64_t batch, int box_rows, int box_cols);
 
 }  // namespace rdb

@@ -59,8 +59,9 @@ struct RowPanelSched {
     T.a_mat = g;
     T.b = rowp;
     T.ldb = lda;
-    T.c = rowp;
-    T.ldc = lda;
+    T.c_col = J * NB;
+    T.c_row = pt * NB;
+    T.c_mat = g;
     T.nk = NB / eng::BK;
     T.mode = eng::EPI_STORE;
     T.neg = 0;
@@ -94,8 +95,9 @@ struct UpdateSched {
     T.a_mat = g;
     T.b = A + (int64_t)pt * NB * lda + (int64_t)J * NB;
     T.ldb = lda;
-    T.c = A + (int64_t)I * NB * lda + (int64_t)J * NB;
-    T.ldc = lda;
+    T.c_col = J * NB;
+    T.c_row = I * NB;
+    T.c_mat = g;
     T.nk = NB / eng::BK;
     T.neg = 1;
     int* c = cnt + (int64_t)g * nt + I;
@@ -117,21 +119,23 @@ struct UpdateSched {
 };
 
 __global__ void __launch_bounds__(EC::THREADS, 1)
-    gj_rowpanel_kernel(const __grid_constant__ CUtensorMap amap, RowPanelSched sched) {
+    gj_rowpanel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
+                       RowPanelSched sched) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>());
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
 
 __global__ void __launch_bounds__(EC::THREADS, 1)
-    gj_update_kernel(const __grid_constant__ CUtensorMap amap, UpdateSched sched) {
+    gj_update_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
+                     UpdateSched sched) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>());
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-int make_a_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
-               int64_t stride, int64_t batch) {
+static int encode_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                      int64_t stride, int64_t batch, int box_rows, int box_cols, CUtensorMapSwizzle swz) {
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -143,12 +147,27 @@ int make_a_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols,
   if (((uintptr_t)base & 15) || (ld & 1) || (stride & 1)) return RDB_EINVAL;
   const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)batch};
   const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)stride * 8};
-  const cuuint32_t box[3] = {eng::BK, eng::BM, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? RDB_OK : RDB_EINVAL;
+}
+
+int make_a_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+               int64_t stride, int64_t batch) {
+  return encode_map(map, base, rows, cols, ld, stride, batch, eng::BM, eng::BK, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+int make_c_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+               int64_t stride, int64_t batch, int box_rows, int box_cols) {
+  return encode_map(map, base, rows, cols, ld, stride, batch, box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+static int make_ec_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                       int64_t stride, int64_t batch) {
+  return make_c_map(map, base, rows, cols, ld, stride, batch, EC::HROWS, EC::WCOLS);
 }
 
 static int g_sms = 0;
@@ -190,8 +209,10 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   int rc = setup();
   if (rc) return rc;
   int* cnt = static_cast<int*>(work);
-  CUtensorMap amap;
+  CUtensorMap amap, cmap;
   rc = make_a_map(&amap, a, n, n, lda, batch > 1 ? stride : n * lda, batch);
+  if (rc) return rc;
+  rc = make_ec_map(&cmap, a, n, n, lda, batch > 1 ? stride : n * lda, batch);
   if (rc) return rc;
   if (cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)batch * nt, st) != cudaSuccess) return RDB_ECUDA;
   for (int k = 0; k < nt; ++k) {
@@ -201,10 +222,10 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     if (nt > 1) {
       RowPanelSched rp{a, lda, stride, nt, k, (int)batch};
       gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES,
-                           st>>>(amap, rp);
+                           st>>>(amap, cmap, rp);
       UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch};
       gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), EC::THREADS,
-                         EC::SMEM_BYTES, st>>>(amap, up);
+                         EC::SMEM_BYTES, st>>>(amap, cmap, up);
     }
   }
   RDB_LAUNCH_CHECK();
@@ -219,8 +240,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
 // tile store_col is stored instead of accumulated.
 struct LocalSched {
   const double* b;
-  double* c;
-  int64_t ldb, ldc;
+  int64_t ldb;
   int mt, nt, nk, skip_row, skip_col, store_col, mode, neg;
   RDB_DEV int rows() const { return mt - (skip_row >= 0 ? 1 : 0); }
   RDB_DEV int cols() const { return nt - (skip_col >= 0 ? 1 : 0); }
@@ -236,8 +256,9 @@ struct LocalSched {
     T.a_mat = 0;
     T.b = b + (int64_t)J * NB;
     T.ldb = ldb;
-    T.c = c + (int64_t)I * NB * ldc + (int64_t)J * NB;
-    T.ldc = ldc;
+    T.c_col = J * NB;
+    T.c_row = I * NB;
+    T.c_mat = 0;
     T.nk = nk;
     T.mode = (J == store_col) ? eng::EPI_STORE : mode;
     T.neg = neg;
@@ -249,9 +270,10 @@ struct LocalSched {
 };
 
 __global__ void __launch_bounds__(EC::THREADS, 1)
-    local_gemm_kernel(const __grid_constant__ CUtensorMap amap, LocalSched sched) {
+    local_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
+                      LocalSched sched) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>());
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
 
 // ------------------------------------------------------------------ K5 residual
@@ -271,10 +293,11 @@ struct ResidualSched {
     T.a_mat = 0;
     T.b = y + (int64_t)J * NB;
     T.ldb = ldy;
-    T.c = nullptr;
-    T.ldc = I;  // row tile index (the epilogue needs the origin only)
+    T.c_col = J * NB;  // the epilogue needs the tile origin only
+    T.c_row = I * NB;
+    T.c_mat = 0;
     T.nk = nk;
-    T.mode = J;
+    T.mode = eng::EPI_STORE;
     T.neg = 0;
     T.signal = nullptr;
     T.wait = nullptr;
@@ -287,7 +310,7 @@ struct ResidualEpi {
   double* out_max;
   RDB_DEV void operator()(eng::Tile T, double (&acc)[EC::MI][EC::NI][2], int wr, int wc, int lane,
                           double*) const {
-    const int64_t row0 = T.ldc * NB + wr * EC::MI * 8, col0 = (int64_t)T.mode * NB + wc * EC::WCOLS;
+    const int64_t row0 = T.c_row + wr * EC::MI * 8, col0 = (int64_t)T.c_col + wc * EC::WCOLS;
     double mx = 0.0;
 #pragma unroll
     for (int mi = 0; mi < EC::MI; ++mi)
@@ -368,7 +391,10 @@ extern "C" int rdb_gemm_local(const double* a, int64_t lda, const double* b, int
   rc = make_a_map(&amap, a, m, k, lda, m * lda, 1);
   if (rc) return rc;
   const int mt = (int)(m / NB), nt = (int)(n / NB);
-  LocalSched sched{b, c, ldb, ldc, mt, nt, (int)(k / eng::BK),
+  CUtensorMap cmap;
+  rc = make_ec_map(&cmap, c, m, n, ldc, m * ldc, 1);
+  if (rc) return rc;
+  LocalSched sched{b, ldb, mt, nt, (int)(k / eng::BK),
                    (int)(skip_row_tile >= 0 && skip_row_tile < mt ? skip_row_tile : -1),
                    (int)(skip_col_tile >= 0 && skip_col_tile < nt ? skip_col_tile : -1),
                    (int)(store_col_tile >= 0 && store_col_tile < nt ? store_col_tile : -1),
@@ -376,7 +402,7 @@ extern "C" int rdb_gemm_local(const double* a, int64_t lda, const double* b, int
   const int64_t tiles = (int64_t)(mt - (sched.skip_row >= 0)) * (nt - (sched.skip_col >= 0));
   if (tiles <= 0) return RDB_OK;
   local_gemm_kernel<<<persistent_grid(tiles), EC::THREADS, EC::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
-      amap, sched);
+      amap, cmap, sched);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
