@@ -16,10 +16,11 @@
 //     under that swizzle; the epilogue writes accumulator row r to C row pi(r).
 //   - B (row-major) arrives as 16 one-dimensional bulk copies of 1 KB into a
 //     padded layout (row stride 132 doubles, conflict free).
-// * epilogue: each MMA warp stages its tile in 16-/32-row pieces in shared
-//   memory and writes them back with bulk stores or bulk reduce-adds
-//   (cp.reduce.async.bulk .add.f64, SASS UBLKRED.ADD.F64.RN): C is never read
-//   by the SM; the L2 applies C + acc with one IEEE rounding.
+// * epilogue: each MMA warp stages its tile in two 16 x 32 pieces in shared
+//   memory and writes each back with ONE TMA tensor store or tensor reduce-add
+//   (cp.reduce.async.bulk.tensor .add, SASS UTMAREDG.ADD on an FP64 tensor
+//   map): C is never read by the SM; the L2 applies C + acc with one IEEE
+//   rounding.
 #pragma once
 #include <cuda.h>
 
@@ -28,9 +29,8 @@
 namespace rdb {
 namespace eng {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
 constexpr int BST = BN + 4;  // B row stride (132 = 4 mod 16)
-constexpr int OST = 36;      // epilogue staging row stride (STS.128 conflict free for the pi row map)
 constexpr uint32_t STAGE_BYTES = (BM * BK + BK * BN) * 8;
 
 // Warp layout: WGM x WGN MMA warps, warp tile (8*MI) x (8*NI).
