@@ -17,7 +17,7 @@
 namespace rdb {
 
 constexpr int NH_T = 8;      // targets per CTA
-constexpr int NH_KB = 1024;  // k-block (rows of dist staged per pass)
+constexpr int NH_KB = 128;   // k-block (rows of dist staged per pass)
 constexpr int NH_THREADS = 256;
 constexpr int CSC_SPLIT = 8;  // row-range splits per column group when building the CSC
 
@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(NH_THREADS)
     next_hop_kernel(const int64_t* __restrict__ seg, const int32_t* __restrict__ idx,
                     const double* __restrict__ val, const double* __restrict__ dist, int64_t ldd,
                     int64_t n, int64_t nkb, const int32_t* __restrict__ targets, int64_t n_targets,
-                    int32_t* __restrict__ next, int64_t ldn) {
+                    int32_t* __restrict__ next, int64_t ldn, const int* __restrict__ only_if) {
+  // the exact NaN-aware kernel; with only_if != nullptr it runs only when the
+  // fast kernel flagged a NaN among the dist values
+  if (only_if && *only_if == 0) return;
   extern __shared__ double ds[];  // ds[k][q], NH_KB x NH_T
   const int64_t j = (int64_t)blockIdx.x * NH_THREADS + threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.y * NH_T;
@@ -169,11 +172,199 @@ __global__ void __launch_bounds__(NH_THREADS)
   }
 }
 
+// Warp-cooperative variant: a CTA owns 32 targets (one per lane) x 128 source
+// vertices (16 per warp, running minima in registers). Per k-block the 32
+// targets' dist rows are staged transposed in shared memory (dsT[k][lane]), and
+// a warp walks one column's CSC entries with warp-uniform (broadcast) loads of
+// (k, w), every lane scoring its own target: 32 (target, successor) pairs per
+// entry load, conflict-free shared-memory reads.
+constexpr int NW_T = 32;
+constexpr int NW_COLS = 16;  // columns per warp
+constexpr int NW_WARPS = 8;
+constexpr int NW_ST = NW_T + 1;
+
+__global__ void __launch_bounds__(NW_WARPS * 32)
+    next_hop_warp_kernel(const int64_t* __restrict__ seg, const int32_t* __restrict__ idx,
+                         const double* __restrict__ val, const double* __restrict__ dist, int64_t ldd,
+                         int64_t n, int64_t nkb, const int32_t* __restrict__ targets, int64_t n_targets,
+                         int32_t* __restrict__ next, int64_t ldn) {
+  extern __shared__ double dsT[];  // [NH_KB][NW_ST]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.y * NW_T;
+  const int64_t j0 = (int64_t)blockIdx.x * (NW_COLS * NW_WARPS) + warp * NW_COLS;
+  double best[NW_COLS];
+  int32_t bk[NW_COLS];
+  unsigned nanmask = 0;
+#pragma unroll
+  for (int c = 0; c < NW_COLS; ++c) {
+    best[c] = INFINITY;
+    bk[c] = -1;
+  }
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    const int64_t k0 = kb * NH_KB;
+    const int kl = (int)((n - k0) < NH_KB ? (n - k0) : NH_KB);
+    __syncthreads();
+    for (int e = threadIdx.x; e < NW_T * NH_KB; e += NW_WARPS * 32) {
+      const int q = e / NH_KB, k = e - (e / NH_KB) * NH_KB;
+      dsT[k * NW_ST + q] = (t0 + q < n_targets && k < kl) ? dist[(t0 + q) * ldd + k0 + k] : INFINITY;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NW_COLS; ++c) {
+      const int64_t j = j0 + c;
+      if (j >= n) break;
+      const int64_t eb = seg[j * (nkb + 1) + kb], ee = seg[j * (nkb + 1) + kb + 1];
+#pragma unroll 4
+      for (int64_t e = eb; e < ee; ++e) {
+        const int32_t k = __ldg(idx + e);
+        const double s = __ldg(val + e) + dsT[(k - k0) * NW_ST + lane];
+        if (s < best[c]) {
+          best[c] = s;
+          bk[c] = k;
+        }
+        nanmask |= (unsigned)(s != s) << c;
+      }
+    }
+  }
+  const int64_t r = t0 + lane;
+  if (r >= n_targets) return;
+  const int64_t t = targets[r];
+#pragma unroll
+  for (int c = 0; c < NW_COLS; ++c) {
+    const int64_t j = j0 + c;
+    if (j >= n) break;
+    const bool stop = (t == j) || ((nanmask >> c) & 1u) || !(best[c] < INFINITY);
+    next[r * ldn + j] = stop ? -1 : bk[c];
+  }
+}
+
+// Packed CSC entry: one 16-byte (uniform, broadcast) load per entry.
+struct alignas(16) NhEnt {
+  double w;
+  int32_t k;
+  int32_t pad;
+};
+
+__global__ void csc_pack_kernel(const int32_t* __restrict__ idx, const double* __restrict__ val, int64_t nnz,
+                                NhEnt* __restrict__ pk) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    pk[e] = NhEnt{val[e], idx[e], 0};
+}
+
+// Fast variant: 64 targets per CTA (2 per lane, adjacent in shared memory ->
+// one LDS.128), 8 source vertices per warp, one 16-byte uniform load per CSC
+// entry feeding 64 (target, successor) scores. NaN scores are not tracked per
+// entry: a NaN among the staged dist values raises *nan_flag and the exact
+// NaN-aware kernel (next_hop_kernel) then recomputes the table.
+constexpr int NP_T = 64;
+constexpr int NP_COLS = 8;
+constexpr int NP_WARPS = 8;
+constexpr int NP_ST = NP_T + 2;  // 66 doubles: 16-byte aligned rows
+
+__global__ void __launch_bounds__(NP_WARPS * 32)
+    next_hop_pair_kernel(const int64_t* __restrict__ seg, const NhEnt* __restrict__ pk,
+                         const double* __restrict__ dist, int64_t ldd, int64_t n, int64_t nkb,
+                         const int32_t* __restrict__ targets, int64_t n_targets, int32_t* __restrict__ next,
+                         int64_t ldn, int* __restrict__ nan_flag) {
+  extern __shared__ __align__(16) double dsP[];  // [NH_KB][NP_ST]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.y * NP_T;
+  const int64_t j0 = (int64_t)blockIdx.x * (NP_COLS * NP_WARPS) + warp * NP_COLS;
+  double b0[NP_COLS], b1[NP_COLS];
+  int32_t k0v[NP_COLS], k1v[NP_COLS];
+#pragma unroll
+  for (int c = 0; c < NP_COLS; ++c) {
+    b0[c] = b1[c] = INFINITY;
+    k0v[c] = k1v[c] = -1;
+  }
+  bool nan_here = false;
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    const int64_t k0 = kb * NH_KB;
+    const int kl = (int)((n - k0) < NH_KB ? (n - k0) : NH_KB);
+    // this warp's CSC entries of the k-block, first 32 per column, loaded
+    // cooperatively (one 16-byte load per lane) before the staging barrier
+    int64_t eb[NP_COLS];
+    int cnt[NP_COLS];
+    NhEnt ent[NP_COLS];
+#pragma unroll
+    for (int c = 0; c < NP_COLS; ++c) {
+      const int64_t j = j0 + c;
+      eb[c] = 0;
+      cnt[c] = 0;
+      if (j < n) {
+        eb[c] = seg[j * (nkb + 1) + kb];
+        cnt[c] = (int)(seg[j * (nkb + 1) + kb + 1] - eb[c]);
+      }
+      if (lane < cnt[c]) ent[c] = pk[eb[c] + lane];
+    }
+    __syncthreads();
+    constexpr int SU = 4;  // staging loads in flight per thread
+    for (int e0 = threadIdx.x; e0 < NP_T * NH_KB; e0 += SU * NP_WARPS * 32) {
+      double v[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int e = e0 + u * NP_WARPS * 32;
+        const int q = e / NH_KB, k = e - (e / NH_KB) * NH_KB;
+        v[u] = (e < NP_T * NH_KB && t0 + q < n_targets && k < kl) ? dist[(t0 + q) * ldd + k0 + k] : INFINITY;
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int e = e0 + u * NP_WARPS * 32;
+        if (e < NP_T * NH_KB) {
+          const int q = e / NH_KB, k = e - (e / NH_KB) * NH_KB;
+          nan_here |= (v[u] != v[u]);
+          dsP[k * NP_ST + q] = v[u];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NP_COLS; ++c) {
+      for (int base = 0; base < cnt[c]; base += 32) {
+        NhEnt cur = ent[c];
+        if (base > 0 && lane < cnt[c] - base) cur = pk[eb[c] + base + lane];
+        const int m = (cnt[c] - base) < 32 ? (cnt[c] - base) : 32;
+        for (int i = 0; i < m; ++i) {
+          const double w = __shfl_sync(0xffffffffu, cur.w, i);
+          const int32_t k = __shfl_sync(0xffffffffu, cur.k, i);
+          const double2 d = *reinterpret_cast<const double2*>(&dsP[(k - k0) * NP_ST + 2 * lane]);
+          const double s0 = w + d.x, s1 = w + d.y;
+          if (s0 < b0[c]) {
+            b0[c] = s0;
+            k0v[c] = k;
+          }
+          if (s1 < b1[c]) {
+            b1[c] = s1;
+            k1v[c] = k;
+          }
+        }
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nan_here) && lane == 0) atomicOr(nan_flag, 1);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t r = t0 + 2 * lane + h;
+    if (r >= n_targets) break;
+    const int64_t t = targets[r];
+#pragma unroll
+    for (int c = 0; c < NP_COLS; ++c) {
+      const int64_t j = j0 + c;
+      if (j >= n) break;
+      const double b = h ? b1[c] : b0[c];
+      const int32_t kk = h ? k1v[c] : k0v[c];
+      next[r * ldn + j] = ((t == j) || !(b < INFINITY)) ? -1 : kk;
+    }
+  }
+}
+
 struct NhWork {
   int64_t* offs;  // n*CSC_SPLIT + 1
   int64_t* seg;   // n*(nkb+1)
   int32_t* idx;   // nnz
   double* val;    // nnz
+  NhEnt* pk;      // nnz
+  int* nan_flag;  // 1
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -189,6 +380,10 @@ static NhWork carve(void* work, int64_t n, int64_t nnz) {
   w.val = reinterpret_cast<double*>(p);
   p += align256((size_t)(nnz > 0 ? nnz : 1) * 8);
   w.idx = reinterpret_cast<int32_t*>(p);
+  p += align256((size_t)(nnz > 0 ? nnz : 1) * 4);
+  w.pk = reinterpret_cast<NhEnt*>(p);
+  p += align256((size_t)(nnz > 0 ? nnz : 1) * sizeof(NhEnt));
+  w.nan_flag = reinterpret_cast<int*>(p);
   return w;
 }
 
@@ -210,7 +405,8 @@ extern "C" size_t rdb_next_hop_workspace_bytes(int64_t n, int64_t nnz) {
   if (n <= 0 || nnz < 0) return 0;
   const int64_t nkb = (n + NH_KB - 1) / NH_KB;
   return align256((size_t)(n * CSC_SPLIT + 1) * 8) + align256((size_t)(n * (nkb + 1)) * 8) +
-         align256((size_t)(nnz > 0 ? nnz : 1) * 8) + align256((size_t)(nnz > 0 ? nnz : 1) * 4);
+         align256((size_t)(nnz > 0 ? nnz : 1) * 8) + align256((size_t)(nnz > 0 ? nnz : 1) * 4) +
+         align256((size_t)(nnz > 0 ? nnz : 1) * sizeof(NhEnt)) + 256;
 }
 
 extern "C" int rdb_next_hop(const double* w, int64_t ldw, const double* dist, int64_t ldd, int64_t n,
@@ -228,14 +424,22 @@ extern "C" int rdb_next_hop(const double* w, int64_t ldw, const double* dist, in
   csc_scan_kernel<<<1, 1024, 0, st>>>(wk.offs, n * CSC_SPLIT);
   csc_fill_kernel<<<cg, 32, 0, st>>>(w, n, ldw, wk.offs, wk.idx, wk.val);
   csc_seg_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(wk.offs, wk.idx, n, nkb, wk.seg);
-  const int smem = NH_KB * NH_T * (int)sizeof(double);
-  if (cudaFuncSetAttribute(next_hop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+  csc_pack_kernel<<<592, 256, 0, st>>>(wk.idx, wk.val, nnz, wk.pk);
+  if (cudaMemsetAsync(wk.nan_flag, 0, sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
+  const int smem = NH_KB * NP_ST * (int)sizeof(double);
+  if (cudaFuncSetAttribute(next_hop_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
       cudaSuccess)
     return RDB_ECUDA;
-  next_hop_kernel<<<dim3((unsigned)((n + NH_THREADS - 1) / NH_THREADS),
-                         (unsigned)((n_targets + NH_T - 1) / NH_T)),
-                    NH_THREADS, smem, st>>>(wk.seg, wk.idx, wk.val, dist, ldd, n, nkb, targets,
-                                         n_targets, next, ldn);
+  next_hop_pair_kernel<<<dim3((unsigned)((n + NP_COLS * NP_WARPS - 1) / (NP_COLS * NP_WARPS)),
+                              (unsigned)((n_targets + NP_T - 1) / NP_T)),
+                         NP_WARPS * 32, smem, st>>>(wk.seg, wk.pk, dist, ldd, n, nkb, targets, n_targets, next,
+                                                    ldn, wk.nan_flag);
+  // exact NaN semantics (numpy argmin picks the first NaN and the walk stops):
+  // recompute only when a NaN was seen; otherwise every CTA exits at once
+  const int smem_exact = NH_KB * NH_T * (int)sizeof(double);
+  next_hop_kernel<<<dim3((unsigned)((n + NH_THREADS - 1) / NH_THREADS), (unsigned)((n_targets + NH_T - 1) / NH_T)),
+                    NH_THREADS, smem_exact, st>>>(wk.seg, wk.idx, wk.val, dist, ldd, n, nkb, targets, n_targets,
+                                                  next, ldn, wk.nan_flag);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
