@@ -77,16 +77,21 @@ struct UpdateSched {
   int* cnt;  // [batch][nt] row-block counters, zeroed before step 0
   int64_t lda, stride;
   int nt, pt, batch;
-  RDB_DEV int count() const { return batch * (nt - 1) * nt; }
+  // part 0: every tile; 1: only column block pt+1 (the next panel, look-ahead);
+  // 2: every tile except column block pt+1
+  int part;
+  RDB_DEV int cols() const { return part == 0 ? nt : (part == 1 ? 1 : nt - 1); }
+  RDB_DEV int count() const { return batch * (nt - 1) * cols(); }
   RDB_DEV eng::Tile tile(int t) const {
-    const int per = (nt - 1) * nt;
+    const int nc = cols();
+    const int per = (nt - 1) * nc;
     const int g = t / per;
     const int rem = t - g * per;
-    int I = rem / nt;
-    const int jj = rem - I * nt;
+    int I = rem / nc;
+    const int jj = rem - I * nc;
     I += (I >= pt);
     // column order pt+1, ..., nt-1, 0, ..., pt: the panel column comes last
-    int J = pt + 1 + jj;
+    int J = pt + 1 + jj + (part == 2 ? 1 : 0);
     if (J >= nt) J -= nt;
     double* A = a + (int64_t)g * stride;
     eng::Tile T;
@@ -188,6 +193,22 @@ static int setup() {
   return RDB_OK;
 }
 
+// Side stream + events of the single-matrix look-ahead (one set per process;
+// the library is used from one device per process).
+static cudaStream_t g_side = nullptr;
+static cudaEvent_t g_ev_a = nullptr, g_ev_p = nullptr;
+
+static int side_resources(cudaStream_t* side) {
+  if (!g_side) {
+    if (cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_ev_a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_ev_p, cudaEventDisableTiming) != cudaSuccess)
+      return RDB_ECUDA;
+  }
+  *side = g_side;
+  return RDB_OK;
+}
+
 int sm_count() {
   setup();
   return g_sms > 0 ? g_sms : 148;
@@ -215,17 +236,41 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   rc = make_ec_map(&cmap, a, n, n, lda, batch > 1 ? stride : n * lda, batch);
   if (rc) return rc;
   if (cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)batch * nt, st) != cudaSuccess) return RDB_ECUDA;
+  // Single matrix: look-ahead. The next panel's column block is updated first
+  // (part 1); the next P1 (one CTA, latency-bound) then runs on a side stream
+  // on one SM while the rest of the update (part 2) uses the other SMs.
+  const bool lookahead = (batch == 1 && nt >= 3);
+  cudaStream_t side = nullptr;
+  if (lookahead) {
+    rc = side_resources(&side);
+    if (rc) return rc;
+  }
+  gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, 0, info, 1);
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
-    gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, p0, info,
-                                                                          k == 0);
-    if (nt > 1) {
-      RowPanelSched rp{a, lda, stride, nt, k, (int)batch};
-      gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES,
-                           st>>>(amap, cmap, rp);
-      UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch};
-      gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), EC::THREADS,
-                         EC::SMEM_BYTES, st>>>(amap, cmap, up);
+    if (k > 0 && !lookahead)
+      gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, p0, info, 0);
+    if (nt == 1) break;
+    RowPanelSched rp{a, lda, stride, nt, k, (int)batch};
+    gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES, st>>>(
+        amap, cmap, rp);
+    if (lookahead && k + 1 < nt) {
+      UpdateSched ua{a, cnt, lda, stride, nt, k, 1, 1};
+      gj_update_kernel<<<persistent_grid(nt - 1), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, ua);
+      cudaEventRecord(g_ev_a, st);
+      cudaStreamWaitEvent(side, g_ev_a, 0);
+      const int p1n = (k + 1) * NB;
+      gj_panel_kernel<<<1, p1::THREADS, p1::SMEM_BYTES, side>>>(a, lda, stride, p1n, p1n, info, 0);
+      cudaEventRecord(g_ev_p, side);
+      UpdateSched ub{a, cnt, lda, stride, nt, k, 1, 2};
+      const int64_t tiles = (int64_t)(nt - 1) * (nt - 1);
+      const unsigned grid = (unsigned)(tiles < sm_count() - 1 ? tiles : sm_count() - 1);
+      gj_update_kernel<<<grid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, ub);
+      cudaStreamWaitEvent(st, g_ev_p, 0);
+    } else {
+      UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch, 0};
+      gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(
+          amap, cmap, up);
     }
   }
   RDB_LAUNCH_CHECK();
