@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=32)
     ap.add_argument("--e2e-chunk", type=int, default=128, help="graphs per pipelined chunk in the e2e engine")
+    ap.add_argument("--single-n", type=int, default=32768,
+                    help="also time one N x N inversion per GPU (config-5 shape); 0 disables")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -276,6 +278,37 @@ def main():
     build_bytes = batch * (N * (N // 8) + 8 * n_pad * n_pad)
     log_bytes = batch * (8 * N * N + 4 * N * N)
 
+    # ---- single large inversion (config-5 shape; BASELINE's "inversion FP64 TFLOP/s"):
+    # M = I - gamma*A, A an ER pattern (p = 0.01) drawn on the device (untimed)
+    single = None
+    if args.single_n > 0:
+        sn = rb._lib.pad_to_nb(args.single_n)
+        warm = torch.eye(2048, dtype=torch.float64, device=dev)  # first single-matrix call sets up side stream
+        wwork = torch.empty(rb._lib.lib().rdb_invert_workspace_bytes(2048, 1), dtype=torch.uint8, device=dev)
+        winfo = rb._lib.pivot_info_tensor(1, dev)
+        rb._lib.check(rb._lib.lib().rdb_invert(warm.data_ptr(), 2048, 2048, wwork.data_ptr(), winfo.data_ptr(), sh),
+                      "rdb_invert")
+        gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+        m1 = (torch.rand((sn, sn), generator=gen, device=dev) < 0.01).to(torch.float64).mul_(-1e-4)
+        m1.diagonal().fill_(1.0)
+        work1 = torch.empty(rb._lib.lib().rdb_invert_workspace_bytes(sn, 1), dtype=torch.uint8, device=dev)
+        info1 = rb._lib.pivot_info_tensor(1, dev)
+        torch.cuda.synchronize(dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        rb._lib.check(rb._lib.lib().rdb_invert(m1.data_ptr(), sn, sn, work1.data_ptr(), info1.data_ptr(), sh),
+                      "rdb_invert")
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
+        t1 = max_over_ranks(ev[0].elapsed_time(ev[1]))
+        rec1 = rb._lib.read_pivot_info(info1)[0]
+        tf1 = 2.0 * sn**3 / (t1 * 1e-3) / 1e12
+        single = {"n": sn, "ms": t1, "tflops_per_gpu": tf1, "frac_of_fp64_peak": tf1 / fp64_peak()[0],
+                  "pivot_flags": rec1.flags, "min_pivot": rec1.min_pivot,
+                  "note": "one N x N M-matrix inverted per GPU (K2 with single-matrix look-ahead)"}
+        del m1, work1
+        torch.cuda.empty_cache()
+
     # ---- e2e: pinned host bits -> engine -> pinned host int32 D
     eng = B.APSPBatchEngine(N, batch, chunk=args.e2e_chunk)
     bits_pin, gam_pin = eng.pin(bits, gammas)
@@ -320,6 +353,7 @@ def main():
         "e2e": {"value": world * batch / e2e_s, "unit": "graphs/s", "h2d_bytes_per_step": int(bits.nbytes + gammas.nbytes),
                 "d2h_bytes_per_step": int(batch * N * N * 4 + batch * 16), "ms_per_step": e2e_s * 1e3},
         "gpu_launches": launches,
+        "single_matrix_inversion": single,
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
