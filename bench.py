@@ -123,10 +123,12 @@ def hbm_peak():
 
 
 def ncu_traffic():
-    p = ROOT / "profiles" / "r01_ncu_summary.json"
+    """DRAM bytes (read + write) of one K2 call over the bench batch, from the
+    committed `ncu --set full` capture of the same workload (profiles/)."""
+    p = ROOT / "profiles" / "r01_ncu_full_cfg2.json"
     try:
         d = json.loads(p.read_text())
-        return d.get("update_kernel_dram_bytes_per_launch")
+        return d.get("k2_dram_bytes_per_call")
     except (OSError, ValueError):
         return None
 
@@ -345,7 +347,8 @@ def main():
         "inversion_tflops": inv_tflops, "inversion_frac_of_fp64_peak": inv_tflops / peak,
         "roofline": {"bound": "tensor", "kernel": "K2 blocked Gauss-Jordan (gj_panel + gj_rowpanel + gj_update, DMMA.8x8x4)",
                      "achieved": inv_tflops, "peak": peak, "unit": "TFLOP/s", "frac": inv_tflops / peak,
-                     "traffic": ncu_traffic(), "peak_source": peak_src,
+                     "traffic": ncu_traffic(), "traffic_unit": "bytes per K2 call (8 GJ steps x 3 kernels, whole batch)",
+                     "traffic_source": "profiles/r01_ncu_full_cfg2.json", "peak_source": peak_src,
                      "work_per_launch": f"2*n^3 = {flops_per_graph:.4g} flop per graph x {batch} graphs"},
         "kernels_ms": {"K1_build_m_bits": t_build, "K2_invert": t_inv, "K3_log_ceil": t_log},
         "hbm_kernels": {"K1_GBps": build_bytes / (t_build * 1e-3) / 1e9, "K3_GBps": log_bytes / (t_log * 1e-3) / 1e9,
