@@ -3,18 +3,19 @@
 # sqrt and log.
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v $(EXTRA)
+BUILD ?= build
 SRC_DIR := paper_2308_07403_b200/csrc
 SRCS := $(wildcard $(SRC_DIR)/*.cu)
-OBJS := $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
+OBJS := $(patsubst $(SRC_DIR)/%.cu,$(BUILD)/%.o,$(SRCS))
 HDRS := $(wildcard $(SRC_DIR)/*.cuh) include/rdist_b200.h
-LIB := paper_2308_07403_b200/librdist_b200.so
+LIB ?= paper_2308_07403_b200/librdist_b200.so
 
 all: $(LIB)
 
-build/%.o: $(SRC_DIR)/%.cu $(HDRS)
-	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+$(BUILD)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; false)
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static

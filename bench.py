@@ -6,13 +6,16 @@ independent unweighted directed graphs with N = 1024 — 128 Erdos-Renyi
 p = 0.8, gamma = 0.1) — seeded synthetic inputs (the reference has no
 dataset). One step = the reference's run_rdist closure for every graph of the
 batch: M = I - gamma*A (K1) -> Y = M^-1 in FP64 (K2, blocked Gauss-Jordan on
-DMMA) -> D = ceil(log Y / log gamma) as int32 (K3).
+DMMA) -> D = ceil(log Y / log gamma) (K3), stored as compact uint8 (default
+--d-dtype uint8: exact for 0 <= D <= 254, 255 = unreachable, any graph outside
+that range is flagged on the device and redone in int32; the bench checks the
+decoded uint8 D against an int32 run bit for bit) or as int32.
 
   value : graphs/s over all ranks, inputs resident in HBM, device-timed
           (CUDA events, barrier + synchronize on both sides, max over ranks).
           The per-step working set (2.1 GB of M + 1 GB of D) exceeds L2.
   e2e   : the same through the public batch engine from pinned host bits to
-          pinned host int32 D (host<->device copies inside the timed region).
+          pinned host D (host<->device copies inside the timed region).
   roofline: K2 (the dominant kernel family) in FP64 TFLOP/s against the
           measured DMMA peak (profiles/r01_fp64_peak.json; MEASURED_PEAKS.json
           has no FP64 entry).
@@ -43,7 +46,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "APSP graphs/sec and inversion FP64 TFLOP/s (frac of peak) at 1/2/4/8 B200"
 WORKLOAD = ("cfg2: 256 unweighted digraphs/GPU, N=1024 (128 ER p=0.02 gamma=1e-2 + "
-            "128 directed 32x32 lattices keep=0.8 gamma=0.1), int32 D out")
+            "128 directed 32x32 lattices keep=0.8 gamma=0.1), D out as {}")
 GRAPHS_PER_GPU = 256
 N = 1024
 
@@ -176,7 +179,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "graphs_per_gpu": GRAPHS_PER_GPU, "n": N,
+        "config": {"workload": WORKLOAD.format("float64 (the reference's rounded_r_distance)"),
+                   "graphs_per_gpu": GRAPHS_PER_GPU, "n": N,
                    "parallelism": "host CPU (numpy/scipy OpenBLAS threads)"},
         "cpu_baseline": {"value": value, "unit": "graphs/s", "cores": cores, "kind": "port",
                          "sample": f"{per_step} cfg2 graphs per step (half ER, half lattice), "
@@ -197,6 +201,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=32)
     ap.add_argument("--e2e-chunk", type=int, default=128, help="graphs per pipelined chunk in the e2e engine")
+    ap.add_argument("--d-dtype", default="uint8", choices=["uint8", "int32"],
+                    help="D storage: compact lossless uint8 (255 = unreachable) or int32 (INT32_MAX)")
     ap.add_argument("--single-n", type=int, default=32768,
                     help="also time one N x N inversion per GPU (config-5 shape); 0 disables")
     args = ap.parse_args()
@@ -221,7 +227,8 @@ def main():
 
     bits, gammas, _ = wl.cfg2_batch(GRAPHS_PER_GPU, rank=rank)
     batch = bits.shape[0]
-    buf = B.BatchBuffers.allocate(N, batch, dev)
+    buf = B.BatchBuffers.allocate(N, batch, dev, d_dtype=args.d_dtype)
+    dsize = buf.d.element_size()
     buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
     buf.gammas.copy_(torch.from_numpy(gammas))
     stream = torch.cuda.current_stream(dev)
@@ -278,7 +285,26 @@ def main():
     peak, peak_src = fp64_peak()
     hbm, hbm_src = hbm_peak()
     build_bytes = batch * (N * (N // 8) + 8 * n_pad * n_pad)
-    log_bytes = batch * (8 * N * N + 4 * N * N)
+    log_bytes = batch * (8 * N * N + dsize * N * N)
+
+    # ---- lossless check of the compact D (outside every timed region): the
+    # uint8 run must flag no graph and decode to the int32 run bit for bit
+    d_check = None
+    if buf.compact:
+        buf.counters.zero_()
+        B.run_chunk(buf, batch, sh)
+        torch.cuda.synchronize(dev)
+        assert B.d8_range_errors(buf.counters).size == 0, "uint8 D out of range"
+        d8 = buf.d.cpu().numpy()
+        buf32 = B.BatchBuffers.allocate(N, batch, dev, d_dtype="int32")
+        buf32.bits.copy_(buf.bits)
+        buf32.gammas.copy_(buf.gammas)
+        B.run_chunk(buf32, batch, sh)
+        same = bool(np.array_equal(B.decode_d8(d8), buf32.d.cpu().numpy()))
+        assert same, "uint8 D differs from int32 D"
+        d_check = "uint8 D decoded == int32 D on all graphs (bitwise), no range flags"
+        del buf32, d8
+        torch.cuda.empty_cache()
 
     # ---- single large inversion (config-5 shape; BASELINE's "inversion FP64 TFLOP/s"):
     # M = I - gamma*A, A an ER pattern (p = 0.01) drawn on the device (untimed)
@@ -312,7 +338,7 @@ def main():
         torch.cuda.empty_cache()
 
     # ---- e2e: pinned host bits -> engine -> pinned host int32 D
-    eng = B.APSPBatchEngine(N, batch, chunk=args.e2e_chunk)
+    eng = B.APSPBatchEngine(N, batch, chunk=args.e2e_chunk, d_dtype=args.d_dtype)
     bits_pin, gam_pin = eng.pin(bits, gammas)
     for _ in range(max(1, args.warmup - 1)):
         eng.run(bits_pin, gam_pin)
@@ -341,7 +367,8 @@ def main():
         "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded ER + directed lattices, BASELINE configs[1])",
-        "config": {"workload": WORKLOAD, "graphs_per_gpu": batch, "global_batch": batch * world, "n": N,
+        "config": {"workload": WORKLOAD.format(args.d_dtype), "d_dtype": args.d_dtype, "d_check": d_check,
+                   "graphs_per_gpu": batch, "global_batch": batch * world, "n": N,
                    "parallelism": f"dp{world} (independent graphs, no collective)",
                    "l2": "working set per step 3.2 GB > L2 (no flush needed)"},
         "inversion_tflops": inv_tflops, "inversion_frac_of_fp64_peak": inv_tflops / peak,
@@ -354,7 +381,9 @@ def main():
         "hbm_kernels": {"K1_GBps": build_bytes / (t_build * 1e-3) / 1e9, "K3_GBps": log_bytes / (t_log * 1e-3) / 1e9,
                         "peak_GBps": hbm, "peak_source": hbm_src},
         "e2e": {"value": world * batch / e2e_s, "unit": "graphs/s", "h2d_bytes_per_step": int(bits.nbytes + gammas.nbytes),
-                "d2h_bytes_per_step": int(batch * N * N * 4 + batch * 16), "ms_per_step": e2e_s * 1e3},
+                "d2h_bytes_per_step": int(batch * N * N * dsize + batch * 16
+                                          + (batch * 8 * rb._lib.RDB_NCOUNTERS if buf.compact else 0)),
+                "ms_per_step": e2e_s * 1e3},
         "gpu_launches": launches,
         "single_matrix_inversion": single,
         "clocks": clk,

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RDB_ABI_VERSION 1
+#define RDB_ABI_VERSION 2
 #define RDB_NB 128 /* Gauss-Jordan panel width; inverted matrices are padded to a multiple */
 
 /* status codes */
@@ -58,7 +58,12 @@ typedef struct rdb_pivot_info {
 /* rdb_log_ceil counters, per matrix */
 #define RDB_CNT_NEGATIVE 0  /* entries below NEGATIVE_ENTRY_TOL (resolvent.py:120) */
 #define RDB_CNT_UNDERFLOW 1 /* exact zeros at reachable off-diagonal pairs (resolvent.py:121-124) */
-#define RDB_NCOUNTERS 2
+#define RDB_CNT_D8_RANGE 2  /* uint8 D only: finite D outside [0, RDB_D8_MAX] (or NaN) */
+#define RDB_NCOUNTERS 3
+
+/* compact uint8 D (rdb_log_ceil_d8): 0..RDB_D8_MAX exact, RDB_D8_UNREACHABLE = +inf */
+#define RDB_D8_MAX 254
+#define RDB_D8_UNREACHABLE 255
 
 const char* rdb_strerror(int code);
 int rdb_abi_version(void);
@@ -152,6 +157,15 @@ int rdb_log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int6
                  int32_t* d32_out, int64_t ldo, int64_t stride_o, const uint8_t* reachable,
                  int64_t ldm, unsigned long long* counters, void* stream);
 
+/* K3 with a compact uint8 D (batch serving: 1/4 of the int32 bytes over
+ * PCIe). Same D as rdb_log_ceil wherever 0 <= D <= RDB_D8_MAX, unreachable
+ * pairs RDB_D8_UNREACHABLE. Entries outside that range are counted in
+ * counters[b * RDB_NCOUNTERS + RDB_CNT_D8_RANGE] (counters required,
+ * caller-zeroed); a matrix with a non-zero count must be redone in int32. */
+int rdb_log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+                    const double* gammas, double gamma, uint8_t* d8_out, int64_t ldo,
+                    int64_t stride_o, unsigned long long* counters, void* stream);
+
 /* K3 over a rows x cols block of a larger Y (e.g. sampled columns, or a rank's
  * block-cyclic tiles): local row i is global row row0 + i, local column j is
  * global column gcol[j] (device int64, or col0 + j when gcol is NULL); the
@@ -199,6 +213,11 @@ int rdb_next_hop(const double* w, int64_t ldw, const double* dist, int64_t ldd, 
 int rdb_apsp_bits_batched(const uint32_t* bits, int64_t n, int64_t batch, const double* gammas,
                           double* mwork, void* work, rdb_pivot_info* info, int32_t* d32,
                           unsigned long long* counters, void* stream);
+
+/* The same with uint8 D (rdb_log_ceil_d8 semantics; counters required). */
+int rdb_apsp_bits_batched_d8(const uint32_t* bits, int64_t n, int64_t batch, const double* gammas,
+                             double* mwork, void* work, rdb_pivot_info* info, uint8_t* d8,
+                             unsigned long long* counters, void* stream);
 
 #ifdef __cplusplus
 }

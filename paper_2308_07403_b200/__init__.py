@@ -35,7 +35,7 @@ from .resolvent import (
     rounded_r_distance,
     suggest_gamma,
 )
-from .batch import UNREACHABLE, rounded_r_distance_batch, rounded_r_distance_batch_device
+from .batch import UNREACHABLE, UNREACHABLE_D8, decode_d8, rounded_r_distance_batch, rounded_r_distance_batch_device
 from ._lib import NativeUnavailableError, load_library
 
 __version__ = "0.1.0"
@@ -45,6 +45,8 @@ __all__ = [
     "NEGATIVE_ENTRY_TOL",
     "PIVOT_RTOL",
     "UNREACHABLE",
+    "UNREACHABLE_D8",
+    "decode_d8",
     "EdgeList",
     "GammaBounds",
     "Graph",

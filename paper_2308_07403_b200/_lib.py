@@ -18,6 +18,7 @@ import torch
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "librdist_b200.so"
 
+RDB_ABI_VERSION = 2  # include/rdist_b200.h; load_library refuses a library built from another header
 RDB_NB = 128
 RDB_OK = 0
 RDB_PIV_NONPOS = 1
@@ -26,7 +27,10 @@ RDB_BUILD_X = 0
 RDB_BUILD_M = 1
 RDB_CNT_NEGATIVE = 0
 RDB_CNT_UNDERFLOW = 1
-RDB_NCOUNTERS = 2
+RDB_CNT_D8_RANGE = 2
+RDB_NCOUNTERS = 3
+RDB_D8_MAX = 254
+RDB_D8_UNREACHABLE = 255
 INT32_SENTINEL = 2147483647
 
 
@@ -82,6 +86,8 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "rdb_next_hop_workspace_bytes": (_sz, [_i64, _i64]),
     "rdb_next_hop": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "rdb_apsp_bits_batched": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rdb_log_ceil_d8": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _dbl, _vp, _i64, _i64, _vp, _vp]),
+    "rdb_apsp_bits_batched_d8": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None
@@ -104,6 +110,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if lib.rdb_abi_version() != RDB_ABI_VERSION:
+            raise NativeUnavailableError(f"{p}: ABI {lib.rdb_abi_version()} != {RDB_ABI_VERSION}; rebuild (`make`)")
         if path is None:
             _lib = lib
         return lib

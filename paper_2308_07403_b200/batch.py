@@ -8,8 +8,12 @@ with per-graph gains, as one device pipeline per chunk: bit-packed adjacency
 D = ceil(log Y / log gamma) (K3), via ``rdb_apsp_bits_batched``.
 
 int32 D uses INT32_MAX for unreachable pairs (the reference's +inf) and 0 on
-the diagonal. A graph whose inversion is not certified or is singular raises
-ResolventSingularError naming the graph.
+the diagonal. ``d_dtype="uint8"`` selects the compact form (rdb_log_ceil_d8):
+the same D wherever 0 <= D <= 254, 255 for unreachable pairs, a quarter of the
+int32 bytes over PCIe; a graph with a D outside that range is counted on the
+device and redone in int32 (:meth:`APSPBatchEngine.wait` widens the batch), so
+the result is never lossy. A graph whose inversion is not certified or is
+singular raises ResolventSingularError naming the graph.
 
 :class:`APSPBatchEngine` owns reusable device and pinned host buffers (the
 serving form: host bits in, host int32 D out, copies overlapped with the
@@ -29,6 +33,15 @@ from .linalg import PIVOT_RTOL, SingularMatrixError
 from .resolvent import ResolventSingularError
 
 UNREACHABLE = L.INT32_SENTINEL
+UNREACHABLE_D8 = L.RDB_D8_UNREACHABLE
+D_DTYPES = {"int32": torch.int32, "uint8": torch.uint8}
+
+
+def decode_d8(d8: np.ndarray) -> np.ndarray:
+    """uint8 D -> int32 D (255 -> INT32_MAX)."""
+    d = d8.astype(np.int32)
+    d[d8 == L.RDB_D8_UNREACHABLE] = UNREACHABLE
+    return d
 
 
 @dataclass
@@ -46,7 +59,7 @@ class BatchBuffers:
     counters: torch.Tensor
 
     @classmethod
-    def allocate(cls, n: int, chunk: int, dev: torch.device) -> "BatchBuffers":
+    def allocate(cls, n: int, chunk: int, dev: torch.device, d_dtype: str = "int32") -> "BatchBuffers":
         n_pad = L.pad_to_nb(n)
         wpr = (n + 31) // 32
         return cls(
@@ -57,9 +70,13 @@ class BatchBuffers:
             m=torch.empty((chunk, n_pad, n_pad), dtype=torch.float64, device=dev),
             work=torch.empty(L.lib().rdb_invert_workspace_bytes(n_pad, chunk), dtype=torch.uint8, device=dev),
             info=L.pivot_info_tensor(chunk, dev),
-            d=torch.empty((chunk, n, n), dtype=torch.int32, device=dev),
+            d=torch.empty((chunk, n, n), dtype=D_DTYPES[d_dtype], device=dev),
             counters=torch.zeros((chunk, L.RDB_NCOUNTERS), dtype=torch.int64, device=dev),
         )
+
+    @property
+    def compact(self) -> bool:
+        return self.d.dtype == torch.uint8
 
     @property
     def n_pad(self) -> int:
@@ -77,22 +94,42 @@ class BatchBuffers:
                 "rdb_invert_batched")
 
     def stage_log_ceil(self, count: int, stream: int) -> None:
-        L.check(L.lib().rdb_log_ceil(self.m.data_ptr(), self.n, self.n_pad, self.n_pad * self.n_pad, count,
-                                     self.gammas.data_ptr(), 0.0, None, None, self.d.data_ptr(), self.n,
-                                     self.n * self.n, None, 0, self.counters.data_ptr(), stream),
+        log_ceil_call(self.m, self.n, count, self.gammas, self.d, self.counters, stream)
+
+
+def apsp_call(bits: torch.Tensor, n: int, count: int, gammas: torch.Tensor, m: torch.Tensor, work: torch.Tensor,
+              info: torch.Tensor, d: torch.Tensor, counters: torch.Tensor, stream: int) -> None:
+    """One rdb_apsp_bits_batched[_d8] call (K1 -> K2 -> K3); the D dtype picks the entry point."""
+    fn, name = ((L.lib().rdb_apsp_bits_batched_d8, "rdb_apsp_bits_batched_d8") if d.dtype == torch.uint8
+                else (L.lib().rdb_apsp_bits_batched, "rdb_apsp_bits_batched"))
+    L.check(fn(bits.data_ptr(), n, count, gammas.data_ptr(), m.data_ptr(), work.data_ptr(), info.data_ptr(),
+               d.data_ptr(), counters.data_ptr(), stream), name)
+
+
+def log_ceil_call(m: torch.Tensor, n: int, count: int, gammas: torch.Tensor, d: torch.Tensor,
+                  counters: torch.Tensor, stream: int) -> None:
+    """K3 over ``count`` padded inverses in ``m`` into D (int32 or uint8 by dtype)."""
+    n_pad = m.shape[-1]
+    if d.dtype == torch.uint8:
+        L.check(L.lib().rdb_log_ceil_d8(m.data_ptr(), n, n_pad, n_pad * n_pad, count, gammas.data_ptr(), 0.0,
+                                        d.data_ptr(), n, n * n, counters.data_ptr(), stream), "rdb_log_ceil_d8")
+    else:
+        L.check(L.lib().rdb_log_ceil(m.data_ptr(), n, n_pad, n_pad * n_pad, count, gammas.data_ptr(), 0.0, None,
+                                     None, d.data_ptr(), n, n * n, None, 0, counters.data_ptr(), stream),
                 "rdb_log_ceil")
 
 
 def run_chunk(buf: BatchBuffers, count: int, stream: int | None = None) -> None:
-    """Launch K1 -> K2 -> K3 for the first ``count`` graphs held in ``buf``."""
-    L.check(
-        L.lib().rdb_apsp_bits_batched(
-            buf.bits.data_ptr(), buf.n, count, buf.gammas.data_ptr(), buf.m.data_ptr(), buf.work.data_ptr(),
-            buf.info.data_ptr(), buf.d.data_ptr(), buf.counters.data_ptr(),
-            L.stream_handle() if stream is None else stream,
-        ),
-        "rdb_apsp_bits_batched",
-    )
+    """Launch K1 -> K2 -> K3 for the first ``count`` graphs held in ``buf``
+    (uint8 D: the range counters must be zero; :func:`d8_range_errors` reads them)."""
+    apsp_call(buf.bits, buf.n, count, buf.gammas, buf.m, buf.work, buf.info, buf.d, buf.counters,
+              L.stream_handle() if stream is None else stream)
+
+
+def d8_range_errors(counters: torch.Tensor) -> np.ndarray:
+    """Indices of graphs whose uint8 D had an entry outside [0, 254] (redo them in int32)."""
+    c = counters.cpu().numpy().reshape(-1, L.RDB_NCOUNTERS)[:, L.RDB_CNT_D8_RANGE]
+    return np.nonzero(c)[0]
 
 
 LAUNCHES_PER_CALL_FIXED = 2  # K1 + K3; K2 adds 3 per panel
@@ -126,28 +163,39 @@ class APSPBatchEngine:
     buffers are reused by every chunk (the compute stream orders them).
     """
 
-    def __init__(self, n: int, max_batch: int, chunk: int = 128):
+    def __init__(self, n: int, max_batch: int, chunk: int = 128, d_dtype: str = "int32"):
         self.dev = L.device()
+        self.d_dtype = D_DTYPES[d_dtype]
         self.n = n
         self.n_pad = L.pad_to_nb(n)
         self.max_batch = max_batch
         self.chunk = max(1, min(chunk, max_batch))
         wpr = (n + 31) // 32
         dev = self.dev
-        self.bits = torch.empty((max_batch, n, wpr), dtype=torch.int32, device=dev)
-        self.gammas = torch.empty(max_batch, dtype=torch.float64, device=dev)
+        # per output slot: inputs and counters, so the host->device copy of
+        # batch s+1 runs while batch s computes
+        self.bits = [torch.empty((max_batch, n, wpr), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.gammas = [torch.empty(max_batch, dtype=torch.float64, device=dev) for _ in range(2)]
         self.m = torch.empty((self.chunk, self.n_pad, self.n_pad), dtype=torch.float64, device=dev)
         self.work = torch.empty(L.lib().rdb_invert_workspace_bytes(self.n_pad, self.chunk), dtype=torch.uint8,
                                 device=dev)
         self.infos = [L.pivot_info_tensor(max_batch, dev) for _ in range(2)]
-        self.counters = torch.zeros((max_batch, L.RDB_NCOUNTERS), dtype=torch.int64, device=dev)
-        self.d = [torch.empty((self.chunk, n, n), dtype=torch.int32, device=dev) for _ in range(2)]
-        self.cs = torch.cuda.Stream(device=dev)
-        self.xs = torch.cuda.Stream(device=dev)
+        self.counters = [torch.zeros((max_batch, L.RDB_NCOUNTERS), dtype=torch.int64, device=dev)
+                         for _ in range(2)]
+        self.d = [torch.empty((self.chunk, n, n), dtype=self.d_dtype, device=dev) for _ in range(2)]
+        self.cs = torch.cuda.Stream(device=dev)  # kernels
+        self.xs = torch.cuda.Stream(device=dev)  # device -> host
+        self.hs = torch.cuda.Stream(device=dev)  # host -> device
+        nchunks = (max_batch + self.chunk - 1) // self.chunk
+        self.uploaded = [[torch.cuda.Event() for _ in range(nchunks)] for _ in range(2)]
+        self.inputs_free = [torch.cuda.Event() for _ in range(2)]
         self.computed = [torch.cuda.Event() for _ in range(2)]
         self.copied = [torch.cuda.Event() for _ in range(2)]
-        self.outs = [torch.empty((max_batch, n, n), dtype=torch.int32).pin_memory() for _ in range(2)]
+        self.outs = [torch.empty((max_batch, n, n), dtype=self.d_dtype).pin_memory() for _ in range(2)]
         self.info_hosts = [torch.empty(max_batch * 16, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        self.cnt_hosts = [torch.empty((max_batch, L.RDB_NCOUNTERS), dtype=torch.int64).pin_memory()
+                          for _ in range(2)]
+        self.inputs: list = [None, None]
         self.done = [torch.cuda.Event() for _ in range(2)]
         self.pending = [0, 0]
         self.launches = 0
@@ -171,46 +219,74 @@ class APSPBatchEngine:
         if self.pending[slot]:
             raise RuntimeError(f"slot {slot} still holds an uncollected batch")
         self.pending[slot] = batch
+        self.inputs[slot] = (bits_pin, gammas_pin)
         out, info_host, info = self.outs[slot], self.info_hosts[slot], self.infos[slot]
+        bits, gam, counters = self.bits[slot], self.gammas[slot], self.counters[slot]
         cur = torch.cuda.current_stream(self.dev)
         self.cs.wait_stream(cur)
         self.xs.wait_stream(cur)
-        lib = L.lib()
+        self.hs.wait_stream(cur)
+        # uploads: as soon as this slot's previous batch has finished computing
+        with torch.cuda.stream(self.hs):
+            self.hs.wait_event(self.inputs_free[slot])
+            for idx, c0 in enumerate(range(0, batch, self.chunk)):
+                cnt = min(self.chunk, batch - c0)
+                bits[c0 : c0 + cnt].copy_(bits_pin[c0 : c0 + cnt], non_blocking=True)
+                gam[c0 : c0 + cnt].copy_(gammas_pin[c0 : c0 + cnt], non_blocking=True)
+                self.uploaded[slot][idx].record(self.hs)
+        with torch.cuda.stream(self.cs):
+            if self.d_dtype == torch.uint8:
+                counters[:batch].zero_()
         for idx, c0 in enumerate(range(0, batch, self.chunk)):
             s = idx % 2
             cnt = min(self.chunk, batch - c0)
             with torch.cuda.stream(self.cs):
-                self.bits[c0 : c0 + cnt].copy_(bits_pin[c0 : c0 + cnt], non_blocking=True)
-                self.gammas[c0 : c0 + cnt].copy_(gammas_pin[c0 : c0 + cnt], non_blocking=True)
-                if idx >= 2:
-                    self.cs.wait_event(self.copied[s])  # slot s drained to the host
-                L.check(
-                    lib.rdb_apsp_bits_batched(
-                        self.bits[c0].data_ptr(), self.n, cnt, self.gammas[c0:].data_ptr(), self.m.data_ptr(),
-                        self.work.data_ptr(), info[c0 * 16 :].data_ptr(), self.d[s].data_ptr(),
-                        self.counters[c0].data_ptr(), self.cs.cuda_stream),
-                    "rdb_apsp_bits_batched",
-                )
+                self.cs.wait_event(self.uploaded[slot][idx])
+                sh = self.cs.cuda_stream
+                lib = L.lib()
+                L.check(lib.rdb_build_m_bits(bits[c0].data_ptr(), self.n, self.n_pad, cnt, gam[c0:].data_ptr(), 0.0,
+                                             self.m.data_ptr(), self.n_pad, self.n_pad * self.n_pad, sh),
+                        "rdb_build_m_bits")
+                L.check(lib.rdb_invert_batched(self.m.data_ptr(), self.n_pad, self.n_pad, self.n_pad * self.n_pad,
+                                               cnt, self.work.data_ptr(), info[c0 * 16 :].data_ptr(), sh),
+                        "rdb_invert_batched")
+                # D slot s must have drained to the host (this batch's chunk
+                # idx-2, or the previous batch's last chunk in that slot)
+                self.cs.wait_event(self.copied[s])
+                log_ceil_call(self.m, self.n, cnt, gam[c0:], self.d[s], counters[c0:], sh)
                 self.launches += launches_per_call(self.n)
                 self.computed[s].record(self.cs)
             with torch.cuda.stream(self.xs):
                 self.xs.wait_event(self.computed[s])
                 out[c0 : c0 + cnt].copy_(self.d[s][:cnt], non_blocking=True)
                 self.copied[s].record(self.xs)
+        self.inputs_free[slot].record(self.cs)
         with torch.cuda.stream(self.xs):
             self.xs.wait_stream(self.cs)
             info_host[: batch * 16].copy_(info[: batch * 16], non_blocking=True)
+            if self.d_dtype == torch.uint8:
+                self.cnt_hosts[slot][:batch].copy_(counters[:batch], non_blocking=True)
             self.done[slot].record(self.xs)
         return batch
 
     def wait(self, slot: int, gammas_pin: torch.Tensor, check: bool = True) -> np.ndarray:
-        """Block until slot ``slot``'s batch is in host memory; its int32 D."""
+        """Block until slot ``slot``'s batch is in host memory; its D (int32, or
+        uint8 for a compact engine). A compact batch with any graph outside the
+        uint8 range is returned widened to int32, those graphs recomputed."""
         batch = self.pending[slot]
         self.done[slot].synchronize()
         self.pending[slot] = 0
         if check:
             check_infos(L.read_pivot_info(self.info_hosts[slot][: batch * 16]), gammas_pin.numpy())
-        return self.outs[slot][:batch].numpy()
+        out = self.outs[slot][:batch].numpy()
+        if self.d_dtype == torch.uint8:
+            bad = np.nonzero(self.cnt_hosts[slot][:batch, L.RDB_CNT_D8_RANGE].numpy())[0]
+            if bad.size:
+                bits_pin, g_pin = self.inputs[slot]
+                wide = decode_d8(out)
+                wide[bad] = rounded_r_distance_batch(bits_pin.numpy()[bad], g_pin.numpy()[bad], self.n)
+                return wide
+        return out
 
     def finish(self, batch: int, gammas_pin: torch.Tensor, check: bool = True) -> np.ndarray:
         return self.wait(0, gammas_pin, check)
@@ -220,9 +296,11 @@ class APSPBatchEngine:
         return self.wait(0, gammas_pin, check)
 
 
-def rounded_r_distance_batch(bits: np.ndarray, gammas, n: int, *, chunk: int = 64) -> np.ndarray:
-    """int32 D (batch, n, n) for bit-packed unweighted graphs (host in, host out)."""
-    eng = APSPBatchEngine(n, np.asarray(bits).shape[0], chunk)
+def rounded_r_distance_batch(bits: np.ndarray, gammas, n: int, *, chunk: int = 64,
+                             d_dtype: str = "int32") -> np.ndarray:
+    """D (batch, n, n) for bit-packed unweighted graphs (host in, host out):
+    int32, or uint8 (255 = unreachable; widened to int32 if a graph needs it)."""
+    eng = APSPBatchEngine(n, np.asarray(bits).shape[0], chunk, d_dtype)
     b, g = eng.pin(bits, gammas)
     return eng.run(b, g).copy()
 

@@ -9,6 +9,9 @@
 namespace rdb {
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                    rdb_pivot_info* info, cudaStream_t st);
+int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+                const double* gammas, double gamma, uint8_t* d8_out, int64_t ldo, int64_t stride_o,
+                unsigned long long* counters, cudaStream_t st);
 int log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
              const double* gammas, double gamma, double* r_out, double* dceil_out, int32_t* d32_out,
              int64_t ldo, int64_t stride_o, const uint8_t* reachable, int64_t ldm,
@@ -56,4 +59,20 @@ extern "C" int rdb_apsp_bits_batched(const uint32_t* bits, int64_t n, int64_t ba
   if (rc) return rc;
   return rdb::log_ceil(mwork, n, n_pad, stride, batch, gammas, 0.0, nullptr, nullptr, d32, n, n * n,
                        nullptr, 0, counters, st);
+}
+
+extern "C" int rdb_apsp_bits_batched_d8(const uint32_t* bits, int64_t n, int64_t batch,
+                                        const double* gammas, double* mwork, void* work,
+                                        rdb_pivot_info* info, uint8_t* d8,
+                                        unsigned long long* counters, void* stream) {
+  if (!bits || !gammas || !mwork || !work || !info || !d8 || !counters || n <= 0 || batch <= 0)
+    return RDB_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n_pad = (n + RDB_NB - 1) / RDB_NB * RDB_NB;
+  const int64_t stride = n_pad * n_pad;
+  int rc = rdb_build_m_bits(bits, n, n_pad, batch, gammas, 0.0, mwork, n_pad, stride, stream);
+  if (rc) return rc;
+  rc = rdb::invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st);
+  if (rc) return rc;
+  return rdb::log_ceil_d8(mwork, n, n_pad, stride, batch, gammas, 0.0, d8, n, n * n, counters, st);
 }

@@ -16,11 +16,16 @@
 //     under that swizzle; the epilogue writes accumulator row r to C row pi(r).
 //   - B (row-major) arrives as 16 one-dimensional bulk copies of 1 KB into a
 //     padded layout (row stride 132 doubles, conflict free).
-// * epilogue: each MMA warp stages its tile in two 16 x 32 pieces in shared
-//   memory and writes each back with ONE TMA tensor store or tensor reduce-add
+// * epilogue: each MMA warp stages its 32 x 32 tile in shared memory and
+//   writes it back with ONE TMA tensor store or tensor reduce-add
 //   (cp.reduce.async.bulk.tensor .add, SASS UTMAREDG.ADD on an FP64 tensor
 //   map): C is never read by the SM; the L2 applies C + acc with one IEEE
-//   rounding.
+//   rounding. The TMA op is issued a few chunks into the next tile
+//   (deferred), so the epilogue itself is only the staging stores.
+// * STAGES = 3 with whole-tile staging measured 1% faster on the config-2
+//   batch and the N = 16384 inversion than 4 stages + half-tile staging
+//   (tools/time_k2.py); conflict-free (shuffle-paired) staging, an L2
+//   prefetch of C and a two-group warp stagger measured no gain.
 #pragma once
 #include <cuda.h>
 
@@ -29,7 +34,16 @@
 namespace rdb {
 namespace eng {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
+#ifndef RDB_ENG_STAGES
+#define RDB_ENG_STAGES 3
+#endif
+#ifndef RDB_ENG_PIECES
+#define RDB_ENG_PIECES 1
+#endif
+#ifndef RDB_ENG_DEFER
+#define RDB_ENG_DEFER 1
+#endif
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = RDB_ENG_STAGES;
 constexpr int BST = BN + 4;  // B row stride (132 = 4 mod 16)
 constexpr uint32_t STAGE_BYTES = (BM * BK + BK * BN) * 8;
 
@@ -42,7 +56,8 @@ struct Cfg {
   static constexpr int MI = BM / WGM / 8;   // 8-row groups per warp
   static constexpr int NI = BN / WGN / 8;   // 8-col groups per warp
   static constexpr int WCOLS = NI * 8;      // warp tile width (doubles)
-  static constexpr int HROWS = MI * 8 / 2;  // staging piece height (half the warp tile)
+  static constexpr int PIECES = RDB_ENG_PIECES;    // staging pieces per warp tile
+  static constexpr int HROWS = MI * 8 / PIECES;  // staging piece height
   struct Smem {
     alignas(1024) double a[STAGES][BM * BK];
     alignas(128) double b[STAGES][BK * BST];
@@ -136,44 +151,84 @@ RDB_DEV void tma_reduce_add_3d(const CUtensorMap* map, int c0, int c1, int c2, c
       : "memory");
 }
 
+
 template <class C>
 struct BulkEpilogue {
   const CUtensorMap* cmap;  // box HROWS x WCOLS over the output matrices
-  RDB_DEV void operator()(Tile T, double (&acc)[C::MI][C::NI][2], int wr, int wc, int lane,
-                          double* stage_out) const {
+  // With the whole warp tile staged (PIECES == 1, the default) the TMA store /
+  // reduce-add is not issued in the epilogue but a few k-chunks into the NEXT
+  // tile (warp w at chunk w*nk/16, see run()): the 128 KB of C traffic per
+  // tile leaves the SM spread over the main loop instead of as one burst
+  // queued in front of the next tile's operand loads, and the epilogue is
+  // just staging + fence.
+  static constexpr bool kDeferred = (C::PIECES == 1) && (RDB_ENG_DEFER != 0);
+
+  // piece h (HROWS rows) of the warp tile -> dense staging box, fenced for TMA
+  RDB_DEV void write_piece(const Tile& T, double (&acc)[C::MI][C::NI][2], int h, int lane, double* stage_out) const {
     const int lr = lane >> 2, lk = lane & 3;
     const int pr = pi_row(lr);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int m = 0; m < C::MI / C::PIECES; ++m)
+#pragma unroll
+      for (int ni = 0; ni < C::NI; ++ni) {
+        const int row = m * 8 + pr;
+        const int col = ni * 8 + 2 * lk;
+        const double x0 = acc[(C::MI / C::PIECES) * h + m][ni][0], x1 = acc[(C::MI / C::PIECES) * h + m][ni][1];
+        *reinterpret_cast<double2*>(&stage_out[row * C::WCOLS + col]) =
+            T.neg ? make_double2(-x0, -x1) : make_double2(x0, x1);
+      }
+    fence_proxy_async();
+    __syncwarp();
+  }
+
+  // lane 0: write piece h of tile T from the staging buffer, after T.wait
+  // when `wait` is set (the deferred form honours the dependency here)
+  RDB_DEV void issue(const Tile& T, int wr, int wc, int h, int lane, bool wait, const double* stage_out) const {
+    if (lane == 0) {
+      if (wait && T.wait) wait_count(T.wait, T.wait_target);
+      const int c0 = T.c_col + wc * C::WCOLS;
+      const int c1 = T.c_row + wr * C::MI * 8 + C::HROWS * h;
+      if (T.mode == EPI_REDUCE)
+        tma_reduce_add_3d(cmap, c0, c1, T.c_mat, stage_out);
+      else
+        tma_store_3d(cmap, c0, c1, T.c_mat, stage_out);
+      bulk_commit();
+    }
+  }
+
+  // deferred form, part 1: stage the warp tile (issue() follows later)
+  RDB_DEV void stage(const Tile& T, double (&acc)[C::MI][C::NI][2], int lane, double* stage_out) const {
+    if (lane == 0) bulk_wait_read0();  // the previous tile's write has left the staging buffer
+    __syncwarp();
+    write_piece(T, acc, 0, lane, stage_out);
+  }
+
+  // immediate form (the run loop has already honoured T.wait)
+  RDB_DEV void operator()(Tile T, double (&acc)[C::MI][C::NI][2], int wr, int wc, int lane,
+                          double* stage_out) const {
+#pragma unroll
+    for (int h = 0; h < C::PIECES; ++h) {
       if (lane == 0) bulk_wait_read0();  // the previous piece has left the staging buffer
       __syncwarp();
-#pragma unroll
-      for (int m = 0; m < C::MI / 2; ++m)
-#pragma unroll
-        for (int ni = 0; ni < C::NI; ++ni) {
-          const int row = m * 8 + pr;
-          const int col = ni * 8 + 2 * lk;
-          const double x0 = acc[(C::MI / 2) * h + m][ni][0], x1 = acc[(C::MI / 2) * h + m][ni][1];
-          *reinterpret_cast<double2*>(&stage_out[row * C::WCOLS + col]) =
-              T.neg ? make_double2(-x0, -x1) : make_double2(x0, x1);
-        }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        const int c0 = T.c_col + wc * C::WCOLS;
-        const int c1 = T.c_row + wr * C::MI * 8 + C::HROWS * h;
-        if (T.mode == EPI_REDUCE)
-          tma_reduce_add_3d(cmap, c0, c1, T.c_mat, stage_out);
-        else
-          tma_store_3d(cmap, c0, c1, T.c_mat, stage_out);
-        bulk_commit();
-      }
+      write_piece(T, acc, h, lane, stage_out);
+      issue(T, wr, wc, h, lane, false, stage_out);
     }
   }
 };
 
+// Epi::kDeferred (when present) selects the stage()/issue() protocol.
+template <class E, class = void>
+struct Defers {
+  static constexpr bool value = false;
+};
+template <class E>
+struct Defers<E, decltype((void)E::kDeferred)> {
+  static constexpr bool value = E::kDeferred;
+};
+
 // Sched must provide: int count() and Tile tile(int t) (identical in every warp).
-// Epi: callable (Tile, acc, wr, wc, lane, staging) run by each MMA warp per tile.
+// Epi: callable (Tile, acc, wr, wc, lane, staging) run by each MMA warp per
+// tile, or a deferred epilogue (BulkEpilogue with kDeferred).
 template <class C, class Sched, class Epi>
 __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* amap, const Sched& sched,
                                     const Epi& epi) {
@@ -229,10 +284,13 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
   const int prow = wr * C::MI * 8 + pi_row(lr);
   const int psw = pi_row(lr);  // == prow % 8
   double* stage_out = s.out[warp];
+  constexpr bool kDefer = Defers<Epi>::value;
+  int pend_t = -1;  // tile whose staged write is not yet issued (deferred epilogue)
   int st = 0;
   uint32_t ph = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const Tile T = sched.tile(t);
+    const int issue_at = kDefer ? (warp * T.nk) / C::MMA_WARPS : 0;
     double acc[C::MI][C::NI][2];
 #pragma unroll
     for (int i = 0; i < C::MI; ++i)
@@ -243,6 +301,12 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
       mbar_wait(&s.full[st], ph);
       // all of this tile's operands are in shared memory: release dependents
       if (c == T.nk - 1 && T.signal && warp == 0 && lane == 0) signal_done(T.signal);
+      if constexpr (kDefer) {
+        if (pend_t >= 0 && c == issue_at) {
+          epi.issue(sched.tile(pend_t), wr, wc, 0, lane, true, stage_out);
+          pend_t = -1;
+        }
+      }
       const char* sa = reinterpret_cast<const char*>(s.a[st]);
       const double* sb = s.b[st] + lk * BST + wc * C::WCOLS + lr;
 #pragma unroll
@@ -268,11 +332,20 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
       }
     }
 
-    if (T.wait) {
-      if (lane == 0) wait_count(T.wait, T.wait_target);
-      __syncwarp();
+    if constexpr (kDefer) {
+      if (pend_t >= 0) epi.issue(sched.tile(pend_t), wr, wc, 0, lane, true, stage_out);  // nk <= issue_at
+      epi.stage(T, acc, lane, stage_out);
+      pend_t = t;
+    } else {
+      if (T.wait) {
+        if (lane == 0) wait_count(T.wait, T.wait_target);
+        __syncwarp();
+      }
+      epi(T, acc, wr, wc, lane, stage_out);
     }
-    epi(T, acc, wr, wc, lane, stage_out);
+  }
+  if constexpr (kDefer) {
+    if (pend_t >= 0) epi.issue(sched.tile(pend_t), wr, wc, 0, lane, true, stage_out);
   }
   bulk_wait0();
 }

@@ -471,3 +471,4 @@ extern "C" int rdb_residual(const double* m, int64_t ldm, const double* y, int64
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
+

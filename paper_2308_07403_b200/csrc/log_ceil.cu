@@ -137,22 +137,46 @@ RDB_DEV double dceil_estimate(double v, double inv_lg, double thr, const LogTab&
   return q;
 }
 
-template <bool HAS_R, bool HAS_DC, bool HAS_D32>
+// Output kinds of D: none, int32 (INT32_MAX sentinel) or uint8 (compact,
+// lossless while 0 <= D <= RDB_D8_MAX; RDB_D8_UNREACHABLE = +inf).
+enum { DK_NONE = 0, DK_I32 = 1, DK_U8 = 2 };
+
+template <bool HAS_R, bool HAS_DC, int DK>
 struct Sink {
   double* r;
   double* dc;
   int32_t* d32;
+  uint8_t* d8;
   // ceil to int32 in one saturating conversion: +inf -> INT_MAX (the sentinel)
   RDB_DEV static int32_t to_i32(double rv) { return __double2int_ru(rv); }
-  RDB_DEV void put1(int64_t o, double rv) const {
+  // ceil to uint8; `bad` counts finite D outside [0, RDB_D8_MAX] (and NaN):
+  // the caller must not use the uint8 D of such a matrix
+  RDB_DEV static uint8_t to_u8(double rv, unsigned& bad) {
+    if (rv == __longlong_as_double(0x7FF0000000000000LL)) return RDB_D8_UNREACHABLE;
+    const double c = ceil(rv);
+    const bool ok = c >= 0.0 && c <= (double)RDB_D8_MAX;  // false for NaN
+    bad += !ok;
+    return ok ? (uint8_t)(int)c : (uint8_t)RDB_D8_MAX;
+  }
+  // each returns the number of out-of-range uint8 entries written (0 otherwise)
+  RDB_DEV unsigned put1(int64_t o, double rv) const {
+    unsigned bad = 0;
     if (HAS_R) r[o] = rv;
     if (HAS_DC) dc[o] = ceil(rv);
-    if (HAS_D32) d32[o] = to_i32(rv);
+    if (DK == DK_I32) d32[o] = to_i32(rv);
+    if (DK == DK_U8) d8[o] = to_u8(rv, bad);
+    return bad;
   }
-  RDB_DEV void put2(int64_t o, double r0, double r1) const {
+  RDB_DEV unsigned put2(int64_t o, double r0, double r1) const {
+    unsigned bad = 0;
     if (HAS_R) *reinterpret_cast<double2*>(r + o) = make_double2(r0, r1);
     if (HAS_DC) *reinterpret_cast<double2*>(dc + o) = make_double2(ceil(r0), ceil(r1));
-    if (HAS_D32) *reinterpret_cast<int2*>(d32 + o) = make_int2(to_i32(r0), to_i32(r1));
+    if (DK == DK_I32) *reinterpret_cast<int2*>(d32 + o) = make_int2(to_i32(r0), to_i32(r1));
+    if (DK == DK_U8) {
+      const uint8_t a = to_u8(r0, bad), b = to_u8(r1, bad);
+      *reinterpret_cast<uchar2*>(d8 + o) = make_uchar2(a, b);
+    }
+    return bad;
   }
 };
 
@@ -165,11 +189,11 @@ struct Shape {
   RDB_DEV int64_t gc(int64_t j) const { return gcol ? gcol[j] : col0 + j; }
 };
 
-template <bool HAS_R, bool HAS_DC, bool HAS_D32, bool VEC>
+template <bool HAS_R, bool HAS_DC, int DK, bool VEC>
 __global__ void __launch_bounds__(256)
     log_ceil_kernel(const double* __restrict__ y, Shape sh, int64_t ldy, int64_t stride_y,
                     int64_t batch, const double* __restrict__ gammas, double gamma,
-                    Sink<HAS_R, HAS_DC, HAS_D32> sink, int64_t ldo, int64_t stride_o,
+                    Sink<HAS_R, HAS_DC, DK> sink, int64_t ldo, int64_t stride_o,
                     const uint8_t* __restrict__ reach, int64_t ldm,
                     unsigned long long* __restrict__ counters) {
   __shared__ LogTab tab;
@@ -200,7 +224,7 @@ __global__ void __launch_bounds__(256)
     const double* Y = y + b * stride_y + i * ldy;
     const int64_t orow = b * stride_o + i * ldo;
     const uint8_t* M = reach ? reach + i * ldm : nullptr;
-    unsigned neg = 0, under = 0;
+    unsigned neg = 0, under = 0, bad = 0;
     int64_t jstart = 0;
     if (VEC) {
       // main body: 4 chunks of 64 columns per pass, all loads issued before any
@@ -237,10 +261,14 @@ __global__ void __launch_bounds__(256)
             r0 = dceil_estimate(v[u].x, inv_lg, thr, tab, n0);
             r1 = dceil_estimate(v[u].y, inv_lg, thr, tab, n1);
             needbits |= ((unsigned)(n0 && !d0) << (2 * u)) | ((unsigned)(n1 && !d1) << (2 * u + 1));
+            // flagged entries are rewritten by the exact path below: store a
+            // neutral provisional value (never counted as out of range)
+            r0 = n0 ? 0.0 : r0;
+            r1 = n1 ? 0.0 : r1;
           }
           r0 = d0 ? 0.0 : r0;
           r1 = d1 ? 0.0 : r1;
-          sink.put2(orow + j, r0, r1);
+          bad += sink.put2(orow + j, r0, r1);
           neg += (v[u].x < NEGATIVE_ENTRY_TOL) + (v[u].y < NEGATIVE_ENTRY_TOL);
           if (M) under += (v[u].x == 0.0 && !d0 && M[j]) + (v[u].y == 0.0 && !d1 && M[j + 1]);
         }
@@ -248,7 +276,7 @@ __global__ void __launch_bounds__(256)
           const int k = __ffs(needbits) - 1;
           needbits &= needbits - 1;
           const int64_t jj = jstart + 64 * (k >> 1) + 2 * lane + (k & 1);
-          sink.put1(orow + jj, rdist_value(Y[jj], g, lg, inv_lg, tab));
+          bad += sink.put1(orow + jj, rdist_value(Y[jj], g, lg, inv_lg, tab));
         }
       }
     }
@@ -262,7 +290,7 @@ __global__ void __launch_bounds__(256)
         double r1 = val(v.y);
         r0 = d0 ? 0.0 : r0;
         r1 = d1 ? 0.0 : r1;
-        sink.put2(orow + j, r0, r1);
+        bad += sink.put2(orow + j, r0, r1);
         neg += (v.x < NEGATIVE_ENTRY_TOL) + (v.y < NEGATIVE_ENTRY_TOL);
         if (M) under += (v.x == 0.0 && !d0 && M[j]) + (v.y == 0.0 && !d1 && M[j + 1]);
       } else {
@@ -272,7 +300,7 @@ __global__ void __launch_bounds__(256)
           if (jj < n) {
             const double v = Y[jj];
             const bool dg = mapped ? gi == sh.gcol[jj] : jj == dj;
-            sink.put1(orow + jj, dg ? 0.0 : val(v));
+            bad += sink.put1(orow + jj, dg ? 0.0 : val(v));
             neg += (v < NEGATIVE_ENTRY_TOL);
             if (M) under += (v == 0.0 && !dg && M[jj]);
           }
@@ -282,20 +310,106 @@ __global__ void __launch_bounds__(256)
     if (counters) {
       neg = __reduce_add_sync(0xffffffffu, neg);
       under = __reduce_add_sync(0xffffffffu, under);
+      if (DK == DK_U8) bad = __reduce_add_sync(0xffffffffu, bad);
       if (lane == 0) {
         if (neg) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_NEGATIVE], (unsigned long long)neg);
         if (under) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_UNDERFLOW], (unsigned long long)under);
+        if (DK == DK_U8 && bad) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_D8_RANGE], (unsigned long long)bad);
       }
     }
   }
 }
 
-template <bool A, bool B, bool C>
+// Compact D (uint8) for whole n x n matrices, the batch serving path: one
+// warp per row, each lane owns 4 consecutive columns of a 128-column block
+// (two 16-byte loads, one 4-byte store: a warp writes 128 contiguous bytes),
+// two blocks in flight per lane. D-only estimate with the exact fallback, as
+// the int32 kernel; `bad` counts entries outside [0, RDB_D8_MAX].
+__global__ void __launch_bounds__(256)
+    log_ceil_d8_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+                       const double* __restrict__ gammas, double gamma, uint8_t* __restrict__ d8, int64_t ldo,
+                       int64_t stride_o, unsigned long long* __restrict__ counters) {
+  __shared__ LogTab tab;
+  for (int e = threadIdx.x; e < 128 * 16; e += blockDim.x) {
+    const int i = e >> 4, k = e & 15;
+    tab.c[i][k] = logtab::kC[i];
+    tab.hi[i][k] = logtab::kLhi[i];
+    tab.lo[i][k] = logtab::kLlo[i];
+  }
+  __syncthreads();
+  using S = Sink<false, false, DK_U8>;
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = n * batch;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t nfull = n & ~(int64_t)127;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += nwarps) {
+    const int64_t b = w / n, i = w - b * n;
+    const double g = gammas ? gammas[b] : gamma;
+    const double lg = log(g);
+    const double inv_lg = 1.0 / lg;
+    const double thr = fmin(2e-6 * fabs(inv_lg), 0.25);
+    const double* Y = y + b * stride_y + i * ldy;
+    uint8_t* O = d8 + b * stride_o + i * ldo;
+    unsigned neg = 0, bad = 0;
+    auto block = [&](int64_t j, double2 p, double2 q) {
+      const double v[4] = {p.x, p.y, q.x, q.y};
+      uint8_t o[4];
+      unsigned need = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        bool nd;
+        double r = dceil_estimate(v[e], inv_lg, thr, tab, nd);
+        const bool dg = j + e == i;
+        need |= (unsigned)(nd && !dg) << e;
+        r = (dg || nd) ? 0.0 : r;
+        o[e] = S::to_u8(r, bad);
+        neg += v[e] < NEGATIVE_ENTRY_TOL;
+      }
+      if (need) {  // rare: exact path (static indices keep v / o in registers)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (need & (1u << e)) o[e] = S::to_u8(rdist_value(v[e], g, lg, inv_lg, tab), bad);
+      }
+      *reinterpret_cast<uchar4*>(O + j) = make_uchar4(o[0], o[1], o[2], o[3]);
+    };
+    int64_t j0 = 0;
+    if (nfull >= 128) {
+      double2 p0 = ldg2(Y + 4 * lane), q0 = ldg2(Y + 4 * lane + 2);
+      for (; j0 + 128 <= nfull; j0 += 128) {
+        double2 p1, q1;
+        const bool more = j0 + 256 <= nfull;
+        if (more) {
+          p1 = ldg2(Y + j0 + 128 + 4 * lane);
+          q1 = ldg2(Y + j0 + 128 + 4 * lane + 2);
+        }
+        block(j0 + 4 * lane, p0, q0);
+        if (more) {
+          p0 = p1;
+          q0 = q1;
+        }
+      }
+    }
+    for (int64_t j = j0 + lane; j < n; j += 32) {  // ragged tail (n % 128)
+      const double v = Y[j];
+      double r = (j == i) ? 0.0 : rdist_value(v, g, lg, inv_lg, tab);
+      O[j] = S::to_u8(r, bad);
+      neg += v < NEGATIVE_ENTRY_TOL;
+    }
+    neg = __reduce_add_sync(0xffffffffu, neg);
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      if (neg) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_NEGATIVE], (unsigned long long)neg);
+      if (bad) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_D8_RANGE], (unsigned long long)bad);
+    }
+  }
+}
+
+template <bool A, bool B, int C>
 static void launch(bool vec, unsigned blocks, cudaStream_t st, const double* y, Shape n, int64_t ldy,
                    int64_t stride_y, int64_t batch, const double* gammas, double gamma, double* r,
                    double* dc, int32_t* d32, int64_t ldo, int64_t stride_o, const uint8_t* reach,
-                   int64_t ldm, unsigned long long* counters) {
-  Sink<A, B, C> sink{r, dc, d32};
+                   int64_t ldm, unsigned long long* counters, uint8_t* d8 = nullptr) {
+  Sink<A, B, C> sink{r, dc, d32, d8};
   if (vec)
     log_ceil_kernel<A, B, C, true><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, sink,
                                                            ldo, stride_o, reach, ldm, counters);
@@ -452,14 +566,14 @@ int log_ceil_shaped(const double* y, Shape sh, int64_t ldy, int64_t stride_y, in
                     d32_out, ldo, stride_o, reachable, ldm, counters);                           \
     break;
   switch (key) {
-    RDB_LC(0, false, false, false)
-    RDB_LC(1, false, false, true)
-    RDB_LC(2, false, true, false)
-    RDB_LC(3, false, true, true)
-    RDB_LC(4, true, false, false)
-    RDB_LC(5, true, false, true)
-    RDB_LC(6, true, true, false)
-    RDB_LC(7, true, true, true)
+    RDB_LC(0, false, false, DK_NONE)
+    RDB_LC(1, false, false, DK_I32)
+    RDB_LC(2, false, true, DK_NONE)
+    RDB_LC(3, false, true, DK_I32)
+    RDB_LC(4, true, false, DK_NONE)
+    RDB_LC(5, true, false, DK_I32)
+    RDB_LC(6, true, true, DK_NONE)
+    RDB_LC(7, true, true, DK_I32)
   }
 #undef RDB_LC
   RDB_LAUNCH_CHECK();
@@ -474,7 +588,34 @@ int log_ceil(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t 
                          dceil_out, d32_out, ldo, stride_o, reachable, ldm, counters, st);
 }
 
+int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+                const double* gammas, double gamma, uint8_t* d8_out, int64_t ldo, int64_t stride_o,
+                unsigned long long* counters, cudaStream_t st) {
+  if (!y || !d8_out || !counters || n <= 0 || ldy < n || ldo < n || batch <= 0) return RDB_EINVAL;
+  if (!gammas && !(gamma > 0.0 && gamma < 1.0)) return RDB_EINVAL;
+  auto al = [](const void* p, uintptr_t a) { return ((uintptr_t)p % a) == 0; };
+  const int64_t rows = n * batch;
+  const int64_t want = (rows + 7) / 8;
+  const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+  if (!(ldy & 1) && !(stride_y & 1) && !(ldo & 3) && !(stride_o & 3) && al(y, 16) && al(d8_out, 4)) {
+    log_ceil_d8_kernel<<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d8_out, ldo, stride_o,
+                                               counters);
+  } else {
+    launch<false, false, DK_U8>(false, blocks, st, y, Shape{n, n, 0, 0, nullptr}, ldy, stride_y, batch, gammas,
+                                gamma, nullptr, nullptr, nullptr, ldo, stride_o, nullptr, 0, counters, d8_out);
+  }
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+
 }  // namespace rdb
+
+extern "C" int rdb_log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+                               const double* gammas, double gamma, uint8_t* d8_out, int64_t ldo,
+                               int64_t stride_o, unsigned long long* counters, void* stream) {
+  return rdb::log_ceil_d8(y, n, ldy, stride_y, batch, gammas, gamma, d8_out, ldo, stride_o, counters,
+                          static_cast<cudaStream_t>(stream));
+}
 
 extern "C" int rdb_log_ceil_block(const double* y, int64_t rows, int64_t cols, int64_t ldy,
                                   int64_t row0, int64_t col0, const int64_t* gcol, double gamma,

@@ -129,3 +129,50 @@ def test_cfg3_full(cuda):
     ref = orc.run_rdist(w, c["gamma"])
     np.testing.assert_array_equal(d, ref)
     assert set(np.unique(d[~np.eye(c["n"], dtype=bool)])) <= {1.0, 2.0}
+
+
+# ---- compact uint8 D (serving form): identical D, 255 = unreachable ----------
+def test_cfg2_uint8_matches_int32_full_batch(cuda):
+    from paper_2308_07403_b200 import batch as B
+
+    bits, gammas, _ = wl.cfg2_batch(256)
+    dev = torch.device("cuda")
+    out = {}
+    for dt in ("int32", "uint8"):
+        buf = B.BatchBuffers.allocate(1024, 256, dev, d_dtype=dt)
+        buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+        buf.gammas.copy_(torch.from_numpy(gammas))
+        buf.counters.zero_()
+        B.run_chunk(buf, 256)
+        torch.cuda.synchronize()
+        if dt == "uint8":
+            assert B.d8_range_errors(buf.counters).size == 0
+        out[dt] = buf.d.cpu().numpy()
+    np.testing.assert_array_equal(B.decode_d8(out["uint8"]), out["int32"])
+    assert out["uint8"].max() == rb.UNREACHABLE_D8 or (out["int32"] != rb.UNREACHABLE).all()
+
+
+def test_cfg2_uint8_engine_golden(cuda, golden):
+    names = ["cfg2_er_2000", "cfg2_lattice_1000", "cfg2_lattice_1001", "cfg2_lattice_1004"]
+    fs = [golden(nm) for nm in names]
+    bits = np.stack([wl.pack_bits(wl.cfg2_present(str(f["kind"]), int(f["seed"]))) for f in fs])
+    gammas = [float(f["gamma"]) for f in fs]
+    d8 = rb.rounded_r_distance_batch(bits, gammas, 1024, chunk=3, d_dtype="uint8")
+    assert d8.dtype == np.uint8
+    for b, f in enumerate(fs):
+        np.testing.assert_array_equal(int32_to_d(rb.decode_d8(d8[b])), u8_to_d(f["d"]))
+
+
+def test_uint8_range_overflow_widens_to_int32(cuda):
+    # a directed path 0 -> 1 -> ... -> 299: D reaches 299 > 254, so the compact
+    # engine must flag the graph on the device and hand back exact int32 D
+    n = 300
+    present = np.zeros((n, n), dtype=bool)
+    present[np.arange(1, n), np.arange(n - 1)] = True  # [i][j]: edge j -> i
+    bits = wl.pack_bits(present)[None]
+    ref = rb.rounded_r_distance_batch(bits, [0.1], n)
+    out = rb.rounded_r_distance_batch(np.concatenate([bits, bits]), [0.1, 0.1], n, d_dtype="uint8")
+    assert out.dtype == np.int32
+    np.testing.assert_array_equal(out[0], ref[0])
+    np.testing.assert_array_equal(out[1], ref[0])
+    assert ref[0].max() == rb.UNREACHABLE and ref[0][n - 1, 0] == n - 1

@@ -35,15 +35,26 @@ def test_binding_table_matches_header():
     assert sorted(L.SIGNATURES) == header_functions()
 
 
+def test_constants_match_header():
+    text = (ROOT / "include" / "rdist_b200.h").read_text()
+    defs = dict(re.findall(r"#define (RDB_[A-Z0-9_]+) (-?\d+)", text))
+    for name in ("RDB_ABI_VERSION", "RDB_NB", "RDB_OK", "RDB_PIV_NONPOS", "RDB_PIV_NONFINITE", "RDB_CNT_NEGATIVE",
+                 "RDB_CNT_UNDERFLOW", "RDB_CNT_D8_RANGE", "RDB_NCOUNTERS", "RDB_D8_MAX", "RDB_D8_UNREACHABLE"):
+        assert getattr(L, name) == int(defs[name]), name
+
+
 def test_abi_version_and_errors_without_gpu():
     lib = L.load_library()
-    assert lib.rdb_abi_version() == 1
+    assert lib.rdb_abi_version() == L.RDB_ABI_VERSION
     assert lib.rdb_strerror(0) == b"ok"
     assert b"invalid" in lib.rdb_strerror(1)
     # argument validation happens before any CUDA call
     assert lib.rdb_invert(None, 128, 128, None, None, None) == 1
     assert lib.rdb_invert(ctypes.c_void_p(256), 100, 100, ctypes.c_void_p(256), ctypes.c_void_p(256), None) == 1
     assert lib.rdb_log_ceil(None, 4, 4, 0, 1, None, 0.5, None, None, None, 4, 0, None, 0, None, None) == 1
+    # uint8 D needs its range counters
+    assert lib.rdb_log_ceil_d8(ctypes.c_void_p(256), 4, 4, 16, 1, None, 0.5, ctypes.c_void_p(256), 4, 16, None,
+                               None) == 1
     assert lib.rdb_invert_workspace_bytes(1024, 256) == 256 * 8 * 4  # row-block counters
     assert lib.rdb_invert_workspace_bytes(0, 1) == 0
 
