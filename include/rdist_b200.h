@@ -191,11 +191,13 @@ int rdb_power_iteration(const double* m, int64_t n, int64_t ldm, int indicator, 
                         int64_t max_iter, void* work, double* result, void* stream);
 
 /* ---- K6: greedy-descent next hop (navigation.py:63-67) -----------------
- * For each target t in `targets` (device int32, n_targets) and every vertex
+ * For each target t = targets[r] (device int32, n_targets) and every vertex
  * j: next[r][j] = the successor k of j (W[k][j] finite, ascending k) that
- * minimises W[k][j] + dist[t][k], first minimum on ties; -1 when j == t,
+ * minimises W[k][j] + dist[r][k], first minimum on ties; -1 when j == t,
  * when j has no successor, or when the best score is not finite (the
- * reference's stop conditions, navigation.py:62-69). W and dist are n x n;
+ * reference's stop conditions, navigation.py:62-69). W is n x n; dist holds
+ * one row per target (row r = the distances to targets[r], ldd), so the
+ * full n x n distance matrix with targets = 0..n-1 is the table case;
  * next is n_targets x n (ldn). work: rdb_next_hop_workspace_bytes(n, nnz)
  * where nnz = number of finite off-diagonal W entries (rdb_count_edges). */
 int rdb_count_edges(const double* w, int64_t n, int64_t ldw, unsigned long long* out_nnz,
@@ -218,6 +220,38 @@ int rdb_apsp_bits_batched(const uint32_t* bits, int64_t n, int64_t batch, const 
 int rdb_apsp_bits_batched_d8(const uint32_t* bits, int64_t n, int64_t batch, const double* gammas,
                              double* mwork, void* work, rdb_pivot_info* info, uint8_t* d8,
                              unsigned long long* counters, void* stream);
+
+/* ---- K8: exact hop distances by all-source BFS (oracles.py:22-41) -------
+ * Unweighted digraph in the rdb_build_m_bits row format (row i, bit j <=>
+ * edge j -> i). dist[i][j] = hops from j to i, 0 on the diagonal,
+ * unreachable INT32_MAX (dist_i32) or +inf (dist_f64): exactly one of the two
+ * outputs is non-NULL. work: rdb_bfs_workspace_bytes(n). Synchronises the
+ * stream once per level (early exit); *levels (host, may be NULL) receives
+ * the deepest level reached. Replaces the reference's dense boolean matrix
+ * products with a sparse-row x bit-matrix product per level. */
+size_t rdb_bfs_workspace_bytes(int64_t n);
+/* bit-packed adjacency pattern of a weight matrix (bit j of row i <=> W[i][j]
+ * finite, i != j; adjacency_indicator, graphs.py:114-116); bits: n x ceil(n/32). */
+int rdb_pattern_bits(const double* w, int64_t n, int64_t ldw, uint32_t* bits, void* stream);
+int rdb_bfs_apsp(const uint32_t* bits, int64_t n, int32_t* dist_i32, double* dist_f64, int64_t ldd,
+                 void* work, int64_t* levels, void* stream);
+
+/* ---- K9: gamma-sweep accuracy counts (navigation.py:77-134) --------------
+ * counts (device, 2 x u64, caller-zeroed, accumulated): {evaluated, hits}.
+ * global: pairs i != j with finite exact; hit when est == exact
+ * (global_accuracy, navigation.py:77-88).
+ * local: (target t = targets[r], node i) with i != t, finite exact[t][i]
+ * and a successor (finite W[k][i], k != i); hit when the estimate's chosen
+ * successor j* = next_est[r][i] (K6 on the zero-weight pattern) has a
+ * finite est[t][j*] and exact[t][j*] <= exact[t][next_exact[r][i]] + atol
+ * (local_accuracy, navigation.py:91-134). est and exact are full n x n
+ * matrices (row = target id); next_* have one row per target. work: n bytes. */
+int rdb_global_accuracy(const double* est, int64_t lde, const double* exact, int64_t ldx, int64_t n,
+                        unsigned long long* counts, void* stream);
+int rdb_local_accuracy(const double* w, int64_t ldw, const int32_t* next_est, const int32_t* next_exact,
+                       int64_t ldn, const double* est, int64_t lde, const double* exact, int64_t ldx,
+                       const int32_t* targets, int64_t n_targets, int64_t n, double atol, void* work,
+                       unsigned long long* counts, void* stream);
 
 #ifdef __cplusplus
 }

@@ -184,6 +184,34 @@ def bfs_apsp(w: np.ndarray) -> np.ndarray:
     return dist
 
 
+def global_accuracy(est: np.ndarray, exact: np.ndarray) -> float:
+    """Share of finite off-diagonal exact pairs the estimate hits exactly (navigation.py:77-88)."""
+    keep = np.isfinite(exact)
+    np.fill_diagonal(keep, False)
+    total = int(keep.sum())
+    return float("nan") if total == 0 else float(np.count_nonzero(est[keep] == exact[keep]) / total)
+
+
+def local_accuracy(w: np.ndarray, est: np.ndarray, exact: np.ndarray, atol: float = 0.0) -> float:
+    """Share of (goal, node) pairs whose first-minimum successor by the estimate
+    is also a closest successor by the exact distances (navigation.py:91-134)."""
+    n = w.shape[0]
+    succ = np.isfinite(w)  # succ[k, i]: edge i -> k
+    has_succ = succ.any(axis=0)
+    total = hits = 0
+    for t in range(n):
+        nodes = np.flatnonzero(np.isfinite(exact[t]) & has_succ & (np.arange(n) != t))
+        if nodes.size == 0:
+            continue
+        e = np.where(succ[:, nodes], est[t][:, None], np.inf)
+        x = np.where(succ[:, nodes], exact[t][:, None], np.inf)
+        pick = e.argmin(axis=0)  # lowest index on ties, first NaN wins (numpy argmin)
+        chosen = e[pick, np.arange(nodes.size)]
+        hits += int(np.count_nonzero(np.isfinite(chosen) & (exact[t, pick] <= x.min(axis=0) + atol)))
+        total += nodes.size
+    return float("nan") if total == 0 else hits / total
+
+
 def sampled_columns_d(m_fortran: np.ndarray, cols: np.ndarray, gamma: float) -> np.ndarray:
     """Config-5 restatement: lu_factor(M) as linalg.py:32,
     then lu_solve on identity columns E_S; returns ceil(R) for those columns

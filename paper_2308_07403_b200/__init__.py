@@ -37,6 +37,8 @@ from .resolvent import (
 )
 from .batch import UNREACHABLE, UNREACHABLE_D8, decode_d8, rounded_r_distance_batch, rounded_r_distance_batch_device
 from ._lib import NativeUnavailableError, load_library
+from .oracles import bfs_apsp, bfs_apsp_device
+from .sweep import SweepRecord, global_accuracy, local_accuracy, sweep_gamma_graph, sweep_point
 
 __version__ = "0.1.0"
 
@@ -46,6 +48,13 @@ __all__ = [
     "PIVOT_RTOL",
     "UNREACHABLE",
     "UNREACHABLE_D8",
+    "bfs_apsp",
+    "bfs_apsp_device",
+    "SweepRecord",
+    "global_accuracy",
+    "local_accuracy",
+    "sweep_gamma_graph",
+    "sweep_point",
     "decode_d8",
     "EdgeList",
     "GammaBounds",

@@ -152,7 +152,9 @@ def resolvent(g, gamma: float, reachable: np.ndarray | None = None, with_residua
         raise ResolventSingularError(gamma) from SingularMatrixError(str(exc))
     counters = torch.zeros(L.RDB_NCOUNTERS, dtype=torch.int64, device=y_pad.device)
     reach_dev = None
-    if reachable is not None:
+    if isinstance(reachable, torch.Tensor):  # device mask (the GPU sweep passes one)
+        reach_dev = reachable.to(device=y_pad.device, dtype=torch.uint8).contiguous()
+    elif reachable is not None:
         r = np.ascontiguousarray(np.asarray(reachable, dtype=bool)).view(np.uint8)
         reach_dev = torch.from_numpy(r).to(y_pad.device)
     _d.log_ceil(y_pad, n, gamma, reachable=reach_dev, counters=counters)

@@ -168,12 +168,100 @@ def main() -> None:
         "paths": np.array(paths, dtype=np.float64),
     }
 
+    out.update(sweep_fixtures())
+    write(out)
+    (HERE / "meta.json").write_text(json.dumps(meta, indent=1) + "\n")
+
+
+def write(out: dict[str, dict[str, np.ndarray]]) -> None:
     for name, arrays in out.items():
         np.savez_compressed(HERE / f"{name}.npz", **arrays)
-    (HERE / "meta.json").write_text(json.dumps(meta, indent=1) + "\n")
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)
 
 
+SWEEPS = (("grid", 64, {}), ("tree", 63, {}), ("hanoi", 81, {}), ("dense", 80, {"p": 0.1, "seed": 3}),
+          ("power_law", 100, {"seed": 1}))
+
+
+def sweep_fixtures() -> dict[str, dict[str, np.ndarray]]:
+    """The reference's gamma sweep (experiments.sweep_gamma, per_decade=3) on
+    five small graph families, the graphs stored as bit-packed patterns (the
+    repo has no copy of the reference's generators), plus the reference's
+    global/local accuracy of fixed estimates (raw R and its ceiling)."""
+    from rdist import experiments as ex
+
+    out = {}
+    for fam, size, kw in SWEEPS:
+        g = ex.build_family(fam, size, **kw)
+        assert g.kind is rdist.GraphKind.UNWEIGHTED
+        present = np.isfinite(g.weights) & ~np.eye(size, dtype=bool)
+        recs = ex.sweep_gamma(fam, [size], per_decade=3, **kw)
+        exact = rdist.bfs_apsp(g)
+        gm = rdist.suggest_gamma(rdist.gamma_bounds(g, max(int(rdist.graph_diameter(exact)), 1)))
+        raw = rdist.r_distance(rdist.resolvent(g, gm))
+        rounded = np.ceil(raw)
+        # per gamma, how many counted items sit on a numerical knife edge of the
+        # reference's own arithmetic (where a different but equally accurate
+        # inverse may legitimately land on the other side):
+        #  global: pairs with |R - round(R)| < 1e-9 (ceil flips);
+        #  local : (goal, node) whose two best successor estimates are within
+        #          1e-9 relative (argmin flips);
+        #  underflow: reachable pairs with 0 <= |y| < 2**-1000 (zero vs tiny).
+        reach = np.isfinite(exact) & ~np.eye(size, dtype=bool)
+        adj = np.isfinite(g.weights)
+        frag = []
+        for r in recs:
+            try:
+                res = rdist.resolvent(g, r.gamma, reachable=reach, with_residual=False)
+            except rdist.ResolventSingularError:
+                frag.append((0, 0, 0))
+                continue
+            rr = rdist.r_distance(res)
+            fin = reach & np.isfinite(rr)
+            fg = int((np.abs(rr[fin] - np.round(rr[fin])) < 1e-9).sum())
+            fl = 0
+            for t in range(size):
+                nodes = np.flatnonzero(np.isfinite(exact[t]) & (np.arange(size) != t) & adj.any(axis=0))
+                if nodes.size == 0:
+                    continue
+                e = np.where(adj[:, nodes], rr[t][:, None], np.inf)
+                e.sort(axis=0)
+                if e.shape[0] > 1:
+                    b0, b1 = e[0], e[1]
+                    close = np.isfinite(b1) & (np.abs(b1 - b0) <= 1e-9 * np.maximum(np.abs(b0), 1e-300))
+                    fl += int(close.sum())
+            fu = int((reach & (np.abs(res.y) < 2.0**-1000)).sum())
+            frag.append((fg, fl, fu))
+        frag = np.array(frag, dtype=np.int64)
+        out[f"sweep_{fam}_{size}"] = {
+            "frag_global": frag[:, 0],
+            "frag_local": frag[:, 1],
+            "frag_underflow": frag[:, 2],
+            "evaluated_global": np.array(int(reach.sum())),
+            "evaluated_local": np.array(int((reach & adj.any(axis=0)[None, :]).sum())),
+            "n": np.array(size),
+            "bits": wl.pack_bits(present),
+            "w_hash": np.array(whash(g.weights)),
+            "gamma": np.array([r.gamma for r in recs]),
+            "global_fraction": np.array([r.global_fraction for r in recs]),
+            "local_fraction": np.array([r.local_fraction for r in recs]),
+            "negative_entries": np.array([r.negative_entries for r in recs]),
+            "underflow_zeros": np.array([r.underflow_zeros for r in recs]),
+            "gamma_over_critical": np.array([r.gamma_over_critical for r in recs]),
+            "precision_floor": np.array([r.precision_floor for r in recs]),
+            "exact": exact,
+            "acc_gamma": np.array(gm),
+            "acc_raw": raw,
+            "acc_global_rounded": np.array(rdist.global_accuracy(rounded, exact)),
+            "acc_local_raw": np.array(rdist.local_accuracy(g, raw, exact)),
+            "acc_local_rounded": np.array(rdist.local_accuracy(g, rounded, exact)),
+        }
+    return out
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["sweep"]:
+        write(sweep_fixtures())
+    else:
+        main()

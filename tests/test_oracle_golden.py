@@ -87,3 +87,22 @@ def test_int32_format():
     d = np.array([[0.0, np.inf], [3.0, 0.0]])
     assert orc.d_to_int32(d).tolist() == [[0, 2147483647], [3, 0]]
     assert math.isinf(u8_to_d(np.array([255], dtype=np.uint8))[0])
+
+
+# ---- gamma-sweep accuracy (navigation.py:77-134) and BFS, pinned to the reference
+SWEEP_FIXTURES = ["sweep_grid_64", "sweep_tree_63", "sweep_hanoi_81", "sweep_dense_80", "sweep_power_law_100"]
+
+
+@pytest.mark.parametrize("name", SWEEP_FIXTURES)
+def test_oracle_accuracy_and_bfs_vs_reference(golden, name):
+    from paper_2308_07403_b200 import workloads as wl
+
+    f = golden(name)
+    n = int(f["n"])
+    w = wl.weights_from_present(wl.unpack_bits(f["bits"], n))
+    assert whash(w) == str(f["w_hash"])  # the stored pattern is the reference's graph
+    np.testing.assert_array_equal(orc.bfs_apsp(w), f["exact"])
+    raw, exact = f["acc_raw"], f["exact"]
+    assert orc.global_accuracy(np.ceil(raw), exact) == float(f["acc_global_rounded"])
+    assert orc.local_accuracy(w, raw, exact) == float(f["acc_local_raw"])
+    assert orc.local_accuracy(w, np.ceil(raw), exact) == float(f["acc_local_rounded"])
