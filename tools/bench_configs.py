@@ -171,7 +171,25 @@ def cfg5(parity: bool, n_cols: int = 4096):
         "min_pivot": rec.min_pivot, "pivot_flags": rec.flags, "sampled_columns": n_cols,
         "D_values": sorted(set(np.unique(dh[np.isfinite(dh)]).tolist()))[:10],
     }
-    del m, ysub
+    del ysub
+    # full D (all 1.07e9 pairs, int32) against the device BFS (K8)
+    d32 = torch.empty((n, n), dtype=torch.int32, device=dev)
+    L.check(L.lib().rdb_log_ceil(m.data_ptr(), n, n, 0, 1, None, gamma, None, None, d32.data_ptr(), n, 0, None, 0,
+                                 None, L.stream_handle()), "log_ceil")
+    del m
+    torch.cuda.empty_cache()
+    from paper_2308_07403_b200 import oracles
+
+    a, b = ev(), ev()
+    a.record()
+    bfs32, levels = oracles.bfs_apsp_bits(bits_d, n, torch.int32)
+    b.record()
+    torch.cuda.synchronize()
+    res["device_ms_bfs_all_sources"] = a.elapsed_time(b)
+    res["bfs_levels"] = levels
+    res["D_equals_device_BFS_all_pairs"] = bool(torch.equal(d32, bfs32))
+    res["pairs_checked"] = n * n
+    del d32, bfs32
     torch.cuda.empty_cache()
     if parity:
         import scipy.sparse
