@@ -320,15 +320,47 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Compact D (uint8) for whole n x n matrices, the batch serving path: one
-// warp per row, each lane owns 4 consecutive columns of a 128-column block
-// (two 16-byte loads, one 4-byte store: a warp writes 128 contiguous bytes),
-// two blocks in flight per lane. D-only estimate with the exact fallback, as
-// the int32 kernel; `bad` counts entries outside [0, RDB_D8_MAX].
+// Lean D-only estimate for the batch kernels: dceil_estimate in 32-bit integer
+// arithmetic (high/low words instead of 64-bit shifts and adds), the table row
+// given by a per-lane base pointer. Same value and same `need` rule.
+struct LeanTab {
+  const double* c;  // &tab.c[0][lane & 15]
+  const double* h;  // &tab.hi[0][lane & 15]
+};
+
+RDB_DEV double dceil_estimate_lean(double v, double inv_lg, double thr, LeanTab T, bool& need) {
+  const int hi = __double2hiint(v), lo = __double2loint(v);
+  const int ex = hi >> 20;  // sign bit set (v <= -0) -> ex < 0 -> need
+  const int idx = (hi >> 13) & 127;
+  const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
+  const int eb = ex - 1023 + (idx >= 53 ? 1 : 0);
+  const double e = __hiloint2double(0x43300000, eb + 0x40000000) - 4503600701112320.0;  // 2^52 + 2^30
+  const double r = fma(m, T.c[idx * 16], -1.0);
+  const double lny = fma(e, 0.6931471805599453, T.h[idx * 16] + fma(-0.5 * r, r, r));
+  const double q = lny * inv_lg;
+  need = (ex <= 0) | (ex >= 2047) | !(fabs(q - rint(q)) > thr);
+  return q;
+}
+
+// D-only K3 for whole n x n matrices, the batch path (no mask, no column map):
+// one warp per row, each lane owns 4 consecutive columns of a 128-column block
+// (two 16-byte loads; a warp stores 128 contiguous bytes of uint8 D or 512 of
+// int32 D), two blocks in flight per lane. uint8 D: `bad` counts entries
+// outside [0, RDB_D8_MAX] (RDB_CNT_D8_RANGE).
+// one block of loads in flight ahead, main loop unrolled twice (measured
+// best of PF 1-3 x unroll 1-4 on the config-2 batch, tools/time_k3.py)
+#ifndef LEAN_PF
+#define LEAN_PF 1
+#endif
+#ifndef LEAN_UNROLL
+#define LEAN_UNROLL 2
+#endif
+constexpr int kLeanUnroll = LEAN_UNROLL;
+template <int DK>
 __global__ void __launch_bounds__(256)
-    log_ceil_d8_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
-                       const double* __restrict__ gammas, double gamma, uint8_t* __restrict__ d8, int64_t ldo,
-                       int64_t stride_o, unsigned long long* __restrict__ counters) {
+    log_ceil_lean_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
+                         const double* __restrict__ gammas, double gamma, void* __restrict__ dout, int64_t ldo,
+                         int64_t stride_o, unsigned long long* __restrict__ counters) {
   __shared__ LogTab tab;
   for (int e = threadIdx.x; e < 128 * 16; e += blockDim.x) {
     const int i = e >> 4, k = e & 15;
@@ -337,69 +369,101 @@ __global__ void __launch_bounds__(256)
     tab.lo[i][k] = logtab::kLlo[i];
   }
   __syncthreads();
-  using S = Sink<false, false, DK_U8>;
   const int lane = threadIdx.x & 31;
+  const LeanTab lt{&tab.c[0][lane & 15], &tab.hi[0][lane & 15]};
   const int64_t rows = n * batch;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t nfull = n & ~(int64_t)127;
+  const int nfull = (int)(n & ~(int64_t)127);
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += nwarps) {
-    const int64_t b = w / n, i = w - b * n;
+    const int64_t b = w / n;
+    const int i = (int)(w - b * n);
     const double g = gammas ? gammas[b] : gamma;
     const double lg = log(g);
     const double inv_lg = 1.0 / lg;
     const double thr = fmin(2e-6 * fabs(inv_lg), 0.25);
-    const double* Y = y + b * stride_y + i * ldy;
-    uint8_t* O = d8 + b * stride_o + i * ldo;
+    const double* Y = y + b * stride_y + (int64_t)i * ldy;
+    const int64_t orow = b * stride_o + (int64_t)i * ldo;
     unsigned neg = 0, bad = 0;
-    auto block = [&](int64_t j, double2 p, double2 q) {
+    auto block = [&](int j, double2 p, double2 q) {
       const double v[4] = {p.x, p.y, q.x, q.y};
-      uint8_t o[4];
+      int d[4];
       unsigned need = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         bool nd;
-        double r = dceil_estimate(v[e], inv_lg, thr, tab, nd);
+        const double r = dceil_estimate_lean(v[e], inv_lg, thr, lt, nd);
         const bool dg = j + e == i;
         need |= (unsigned)(nd && !dg) << e;
-        r = (dg || nd) ? 0.0 : r;
-        o[e] = S::to_u8(r, bad);
+        d[e] = (dg || nd) ? 0 : __double2int_ru(r);
         neg += v[e] < NEGATIVE_ENTRY_TOL;
       }
-      if (need) {  // rare: exact path (static indices keep v / o in registers)
+      if (need) {  // rare: exact path (static indices keep v / d in registers)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (need & (1u << e)) o[e] = S::to_u8(rdist_value(v[e], g, lg, inv_lg, tab), bad);
+          if (need & (1u << e)) {
+            const double r = rdist_value(v[e], g, lg, inv_lg, tab);
+            d[e] = __double2int_ru(r);  // +inf -> INT32_MAX, the int32 sentinel
+            if (DK == DK_U8 && r == __longlong_as_double(0x7FF0000000000000LL)) d[e] = -2;  // unreachable
+            if (DK == DK_U8 && r != r) d[e] = -1;  // NaN: out of range
+          }
       }
-      *reinterpret_cast<uchar4*>(O + j) = make_uchar4(o[0], o[1], o[2], o[3]);
+      if (DK == DK_U8) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool unreachable = d[e] == -2;
+          const bool ok = (unsigned)d[e] <= (unsigned)RDB_D8_MAX;
+          bad += !ok && !unreachable;
+          d[e] = unreachable ? RDB_D8_UNREACHABLE : (ok ? d[e] : RDB_D8_MAX);
+        }
+        *reinterpret_cast<uchar4*>(static_cast<uint8_t*>(dout) + orow + j) =
+            make_uchar4((uint8_t)d[0], (uint8_t)d[1], (uint8_t)d[2], (uint8_t)d[3]);
+      } else {
+        *reinterpret_cast<int4*>(static_cast<int32_t*>(dout) + orow + j) = make_int4(d[0], d[1], d[2], d[3]);
+      }
     };
-    int64_t j0 = 0;
-    if (nfull >= 128) {
-      double2 p0 = ldg2(Y + 4 * lane), q0 = ldg2(Y + 4 * lane + 2);
-      for (; j0 + 128 <= nfull; j0 += 128) {
-        double2 p1, q1;
-        const bool more = j0 + 256 <= nfull;
-        if (more) {
-          p1 = ldg2(Y + j0 + 128 + 4 * lane);
-          q1 = ldg2(Y + j0 + 128 + 4 * lane + 2);
-        }
-        block(j0 + 4 * lane, p0, q0);
-        if (more) {
-          p0 = p1;
-          q0 = q1;
-        }
+    // LEAN_PF blocks of loads in flight ahead of the one being converted
+    constexpr int PF = LEAN_PF;
+    double2 pp[PF], qq[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+      if (128 * (u + 1) <= nfull) {
+        pp[u] = ldg2(Y + 128 * u + 4 * lane);
+        qq[u] = ldg2(Y + 128 * u + 4 * lane + 2);
       }
+    int j0 = 0;
+#pragma unroll kLeanUnroll
+    for (; j0 + 128 <= nfull; j0 += 128) {
+      const double2 p0 = pp[0], q0 = qq[0];
+#pragma unroll
+      for (int u = 0; u + 1 < PF; ++u) {
+        pp[u] = pp[u + 1];
+        qq[u] = qq[u + 1];
+      }
+      if (j0 + 128 * (PF + 1) <= nfull) {
+        pp[PF - 1] = ldg2(Y + j0 + 128 * PF + 4 * lane);
+        qq[PF - 1] = ldg2(Y + j0 + 128 * PF + 4 * lane + 2);
+      }
+      block(j0 + 4 * lane, p0, q0);
     }
-    for (int64_t j = j0 + lane; j < n; j += 32) {  // ragged tail (n % 128)
+    for (int j = j0 + lane; j < n; j += 32) {  // ragged tail (n % 128)
       const double v = Y[j];
-      double r = (j == i) ? 0.0 : rdist_value(v, g, lg, inv_lg, tab);
-      O[j] = S::to_u8(r, bad);
+      const double r = (j == i) ? 0.0 : rdist_value(v, g, lg, inv_lg, tab);
+      if (DK == DK_U8) {
+        unsigned bb = 0;
+        static_cast<uint8_t*>(dout)[orow + j] = Sink<false, false, DK_U8>::to_u8(r, bb);
+        bad += bb;
+      } else {
+        static_cast<int32_t*>(dout)[orow + j] = __double2int_ru(r);
+      }
       neg += v < NEGATIVE_ENTRY_TOL;
     }
-    neg = __reduce_add_sync(0xffffffffu, neg);
-    bad = __reduce_add_sync(0xffffffffu, bad);
-    if (lane == 0) {
-      if (neg) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_NEGATIVE], (unsigned long long)neg);
-      if (bad) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_D8_RANGE], (unsigned long long)bad);
+    if (counters) {
+      neg = __reduce_add_sync(0xffffffffu, neg);
+      if (DK == DK_U8) bad = __reduce_add_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        if (neg) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_NEGATIVE], (unsigned long long)neg);
+        if (DK == DK_U8 && bad) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_D8_RANGE], (unsigned long long)bad);
+      }
     }
   }
 }
@@ -560,6 +624,13 @@ int log_ceil_shaped(const double* y, Shape sh, int64_t ldy, int64_t stride_y, in
   }
   const int64_t want = (rows + 7) / 8;
   const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+  if (key == 1 && vec && !reachable && !sh.gcol && sh.row0 == 0 && sh.col0 == 0 && sh.rows == n &&
+      !(ldo & 3) && !(stride_o & 3) && al(d32_out, 16) && n < (int64_t)1 << 31) {
+    log_ceil_lean_kernel<DK_I32><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d32_out, ldo,
+                                                         stride_o, counters);
+    RDB_LAUNCH_CHECK();
+    return RDB_OK;
+  }
 #define RDB_LC(K, A, B, C)                                                                       \
   case K:                                                                                        \
     launch<A, B, C>(vec, blocks, st, y, sh, ldy, stride_y, batch, gammas, gamma, r_out, dceil_out, \
@@ -597,9 +668,10 @@ int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64
   const int64_t rows = n * batch;
   const int64_t want = (rows + 7) / 8;
   const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
-  if (!(ldy & 1) && !(stride_y & 1) && !(ldo & 3) && !(stride_o & 3) && al(y, 16) && al(d8_out, 4)) {
-    log_ceil_d8_kernel<<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d8_out, ldo, stride_o,
-                                               counters);
+  if (!(ldy & 1) && !(stride_y & 1) && !(ldo & 3) && !(stride_o & 3) && al(y, 16) && al(d8_out, 4) &&
+      n < (int64_t)1 << 31) {
+    log_ceil_lean_kernel<DK_U8><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d8_out, ldo,
+                                                        stride_o, counters);
   } else {
     launch<false, false, DK_U8>(false, blocks, st, y, Shape{n, n, 0, 0, nullptr}, ldy, stride_y, batch, gammas,
                                 gamma, nullptr, nullptr, nullptr, ldo, stride_o, nullptr, 0, counters, d8_out);
