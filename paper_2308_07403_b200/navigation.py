@@ -5,8 +5,9 @@ Mirrors ``greedy_descent`` / ``PathResult`` of pkg/src/rdist/navigation.py
 vertex j minimising W[k][j] + dist[goal][k], lowest index on ties, stopping on
 +inf — is computed on the GPU as a next-hop row (kernel K6) for the goal; the
 walk is then a pointer chase over that row. ``next_hop_table`` evaluates the
-same step for many goals at once (the config-4 table). The accuracy metrics
-of the reference module are outside the hot path.
+same step for many goals at once (the config-4 table; ``next_hop_table_shard``
+gives one rank its block of target rows). The reference module's accuracy
+metrics are in :mod:`.sweep` (K6 + K9 on the device).
 """
 
 from __future__ import annotations
@@ -62,6 +63,33 @@ def next_hop_table(g, dist, targets=None, *, device_out: bool = False):
     tgt = torch.from_numpy(t.astype(np.int32)).to(w.device)
     out = _d.next_hop(w, rows, tgt)
     return out if device_out else out.cpu().numpy()
+
+
+def shard_targets(n: int, rank: int, world: int) -> np.ndarray:
+    """Contiguous block of target rows owned by ``rank`` of ``world`` (config 4
+    sharded by target rows: W and dist replicated, no exchange)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    lo = (n * rank) // world
+    hi = (n * (rank + 1)) // world
+    return np.arange(lo, hi)
+
+
+def next_hop_table_shard(g, dist, rank: int | None = None, world: int | None = None, *, device_out: bool = False):
+    """This rank's rows of the next-hop table (targets ``shard_targets``); rank
+    and world default to the initialised torch.distributed group (one process
+    per GPU), else (0, 1). Returns (targets, table rows)."""
+    if rank is None or world is None:
+        import torch.distributed as dist_mod
+
+        if dist_mod.is_available() and dist_mod.is_initialized():
+            rank, world = dist_mod.get_rank(), dist_mod.get_world_size()
+        else:
+            rank, world = 0, 1
+    t = shard_targets(g.n_vertices, rank, world)
+    if t.size == 0:
+        return t, np.empty((0, g.n_vertices), dtype=np.int32)
+    return t, next_hop_table(g, dist, t, device_out=device_out)
 
 
 def greedy_descent(g, dist: np.ndarray, start: int, goal: int, max_steps: int | None = None) -> PathResult:

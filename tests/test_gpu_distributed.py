@@ -54,3 +54,32 @@ def test_gemm_local_skip_store(cuda):
     exp[128:256] = c0[128:256]
     torch.cuda.synchronize()
     torch.testing.assert_close(c, exp, rtol=1e-13, atol=1e-12)
+
+
+def test_torch_grid_nccl_single_rank(cuda):
+    # the product grid (TorchGrid over a real NCCL process group) on this one
+    # GPU: a 1 x 1 grid, so the collectives (all-reduce of the pivot summary)
+    # run through NCCL; the result must equal the single-GPU inversion bitwise
+    import socket
+
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        n, gamma = 512, 1e-2
+        m = m_on_device(n, gamma, 5)
+        ref = m.clone()
+        rec = _d.invert_padded_nopivot(ref)
+        lay = D.Layout(n, 1, 1)
+        locs = {(0, 0): D.scatter(m, lay, 0, 0)}
+        minp, flags = D.invert_block_cyclic(locs, D.TorchGrid(lay), D.CudaEngine())
+        torch.cuda.synchronize()
+        assert torch.equal(D.gather(locs, lay), ref)
+        assert flags == 0 and minp == rec.min_pivot
+    finally:
+        dist.destroy_process_group()

@@ -176,3 +176,16 @@ def test_uint8_range_overflow_widens_to_int32(cuda):
     np.testing.assert_array_equal(out[0], ref[0])
     np.testing.assert_array_equal(out[1], ref[0])
     assert ref[0].max() == rb.UNREACHABLE and ref[0][n - 1, 0] == n - 1
+
+
+def test_cfg4_table_sharded_by_targets(cuda):
+    # config 4 sharded by target rows: the ranks' row blocks
+    # concatenate to the full table (computed here rank by rank on one GPU)
+    from paper_2308_07403_b200.navigation import next_hop_table_shard
+
+    g = wl.weighted_er_graph(512, 0.1, 1.0, 5.0, 3)
+    r = rb.r_distance(rb.resolvent(g, 1e-3, with_residual=False))
+    full = rb.next_hop_table(g, r)
+    parts = [next_hop_table_shard(g, r, k, 3) for k in range(3)]
+    assert np.array_equal(np.concatenate([p[0] for p in parts]), np.arange(512))
+    np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), full)

@@ -181,3 +181,13 @@ class TestWorkloads:
         fin = np.isfinite(g.weights)
         assert (g.weights[fin] >= 1.0).all() and (g.weights[fin] <= 5.0).all()
         assert g.kind is rb.GraphKind.REAL_WEIGHTED
+
+
+def test_shard_targets_partition():
+    from paper_2308_07403_b200.navigation import shard_targets
+
+    for n, world in ((4096, 8), (4096, 3), (5, 8), (1, 2)):
+        parts = [shard_targets(n, r, world) for r in range(world)]
+        assert np.array_equal(np.concatenate(parts), np.arange(n))
+    with pytest.raises(ValueError):
+        shard_targets(10, 2, 2)
