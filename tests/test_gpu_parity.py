@@ -189,3 +189,20 @@ def test_cfg4_table_sharded_by_targets(cuda):
     parts = [next_hop_table_shard(g, r, k, 3) for k in range(3)]
     assert np.array_equal(np.concatenate([p[0] for p in parts]), np.arange(512))
     np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), full)
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 33, 100, 129, 300])
+@pytest.mark.parametrize("d_dtype", ["int32", "uint8"])
+def test_batch_ragged_sizes_vs_oracle(cuda, n, d_dtype):
+    # sizes off every kernel granule (32-bit words, 128-wide panels, 128-column
+    # K3 blocks), mixed gains, a chunk size that splits the batch unevenly
+    rng = np.random.default_rng(n)
+    present = [(rng.random((n, n)) < min(0.9, 3.0 / max(n, 1))) & ~np.eye(n, dtype=bool) for _ in range(5)]
+    bits = np.stack([wl.pack_bits(p) for p in present])
+    gammas = np.array([0.01, 0.05, 0.1, 0.02, 0.003])
+    d = rb.rounded_r_distance_batch(bits, gammas, n, chunk=2, d_dtype=d_dtype)
+    if d.dtype == np.uint8:
+        d = rb.decode_d8(d)
+    for b in range(5):
+        ref = orc.run_rdist(wl.weights_from_present(present[b]), gammas[b])
+        np.testing.assert_array_equal(int32_to_d(d[b]), ref, err_msg=f"n={n} graph {b}")
