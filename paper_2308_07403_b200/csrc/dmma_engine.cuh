@@ -78,6 +78,7 @@ struct Tile {
   const double* b;          // &B[0][col0]
   int64_t ldb;
   int c_col, c_row, c_mat;  // TMA coordinates of C(row0, col0) in the C tensor map
+  int c_sel = 0;            // 1: write through the epilogue's second C map (cmap2)
   int nk;                   // number of BK chunks
   int mode;                 // EPI_STORE / EPI_REDUCE
   int neg;                  // write -acc instead of acc
@@ -154,7 +155,8 @@ RDB_DEV void tma_reduce_add_3d(const CUtensorMap* map, int c0, int c1, int c2, c
 
 template <class C>
 struct BulkEpilogue {
-  const CUtensorMap* cmap;  // box HROWS x WCOLS over the output matrices
+  const CUtensorMap* cmap;            // box HROWS x WCOLS over the output matrices
+  const CUtensorMap* cmap2 = nullptr;  // optional second output (tiles with c_sel = 1)
   // With the whole warp tile staged (PIECES == 1, the default) the TMA store /
   // reduce-add is not issued in the epilogue but a few k-chunks into the NEXT
   // tile (warp w at chunk w*nk/16, see run()): the 128 KB of C traffic per
@@ -188,10 +190,11 @@ struct BulkEpilogue {
       if (wait && T.wait) wait_count(T.wait, T.wait_target);
       const int c0 = T.c_col + wc * C::WCOLS;
       const int c1 = T.c_row + wr * C::MI * 8 + C::HROWS * h;
+      const CUtensorMap* map = (T.c_sel && cmap2) ? cmap2 : cmap;
       if (T.mode == EPI_REDUCE)
-        tma_reduce_add_3d(cmap, c0, c1, T.c_mat, stage_out);
+        tma_reduce_add_3d(map, c0, c1, T.c_mat, stage_out);
       else
-        tma_store_3d(cmap, c0, c1, T.c_mat, stage_out);
+        tma_store_3d(map, c0, c1, T.c_mat, stage_out);
       bulk_commit();
     }
   }

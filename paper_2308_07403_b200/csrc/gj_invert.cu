@@ -219,8 +219,14 @@ static unsigned persistent_grid(int64_t tiles) {
   return (unsigned)(tiles < sms ? tiles : sms);
 }
 
-int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
-                   rdb_pivot_info* info, cudaStream_t st) {
+static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_info* info, cudaStream_t st);
+static int64_t wide_min_n();
+
+// Blocked Gauss-Jordan with NB = 128 panels. `first` resets the pivot record
+// (step 0); idx_base offsets the reported pivot indices (a diagonal sub-block
+// inverted as part of a larger matrix).
+static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
+                       rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base) {
   if (!a || !work || !info || n <= 0 || batch <= 0) return RDB_EINVAL;
   if (n % NB != 0 || lda < n || (lda & 1) || (batch > 1 && stride < n * lda)) return RDB_EINVAL;
   if (((uintptr_t)a & 15) || ((uintptr_t)work & 15)) return RDB_EINVAL;
@@ -245,11 +251,12 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     rc = side_resources(&side);
     if (rc) return rc;
   }
-  gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, 0, info, 1);
+  gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, idx_base, info, first);
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
     if (k > 0 && !lookahead)
-      gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, p0, info, 0);
+      gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, idx_base + p0,
+                                                                           info, 0);
     if (nt == 1) break;
     RowPanelSched rp{a, lda, stride, nt, k, (int)batch};
     gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES, st>>>(
@@ -260,7 +267,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       cudaEventRecord(g_ev_a, st);
       cudaStreamWaitEvent(side, g_ev_a, 0);
       const int p1n = (k + 1) * NB;
-      gj_panel_kernel<<<1, p1::THREADS, p1::SMEM_BYTES, side>>>(a, lda, stride, p1n, p1n, info, 0);
+      gj_panel_kernel<<<1, p1::THREADS, p1::SMEM_BYTES, side>>>(a, lda, stride, p1n, idx_base + p1n, info, 0);
       cudaEventRecord(g_ev_p, side);
       UpdateSched ub{a, cnt, lda, stride, nt, k, 1, 2};
       const int64_t tiles = (int64_t)(nt - 1) * (nt - 1);
@@ -272,6 +279,173 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(
           amap, cmap, up);
     }
+  }
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+
+int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
+                   rdb_pivot_info* info, cudaStream_t st) {
+  if (batch == 1 && n >= wide_min_n() && n % (2 * NB) == 0 && a && work && info && lda >= n && !(lda & 1) &&
+      !((uintptr_t)a & 15) && !((uintptr_t)work & 15))
+    return invert_wide(a, n, lda, work, info, st);
+  return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0);
+}
+
+// ------------------------------------------------------------------ wide (NB = 256) single matrix
+// One large matrix (config 5; n >= 16384 by default) in 256-wide steps: every rank-256 update
+// tile runs 16 k-chunks per epilogue instead of 8, halving the engine's
+// per-tile cost per flop (tools/tile_overhead.py: 32.0 -> 34.1 TFLOP/s). Step p
+// (band = rows/cols p0 .. p0+255):
+//   1. D = A_pp^-1 in place: the NB = 128 Gauss-Jordan on the 256 x 256 block;
+//   2. R = D A_pJ (J outside the band) into a 256 x n scratch;
+//   3. A_IJ += -(A_Ip R_J) (I, J outside the band, reduce-add) and
+//      C_I = -(A_Ip D) into an n x 256 scratch (I outside the band), in one
+//      launch with two output maps;
+//   4. the scratches are copied into the band rows / columns.
+// The scratches remove every in-kernel dependency (no tile overwrites another
+// tile's operand). Same algebra as the NB = 128 path, different rounding
+// order: the inverse agrees to ~1e-15 relative, D is unchanged (tests).
+constexpr int WB = 2 * NB;
+
+struct WideRowSched {  // R[r][J] = D[r rows] * A_pJ, r in {0, 1}, J outside the band
+  const double* a;
+  int64_t lda;
+  int nt, p0t;  // tiles of 128; band = tiles p0t, p0t + 1
+  RDB_DEV int count() const { return 2 * (nt - 2); }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int r = t / (nt - 2);
+    int J = t - r * (nt - 2);
+    J += (J >= p0t) ? 2 : 0;
+    eng::Tile T;
+    T.a_col = p0t * NB;
+    T.a_row = (p0t + r) * NB;
+    T.a_mat = 0;
+    T.b = a + (int64_t)p0t * NB * lda + (int64_t)J * NB;
+    T.ldb = lda;
+    T.c_col = J * NB;
+    T.c_row = r * NB;
+    T.c_mat = 0;
+    T.nk = WB / eng::BK;
+    T.mode = eng::EPI_STORE;
+    T.neg = 0;
+    T.signal = nullptr;
+    T.wait = nullptr;
+    T.wait_target = 0;
+    return T;
+  }
+};
+
+struct WideUpdateSched {  // rows I outside the band; J outside -> reduce into A, J in band -> column scratch
+  const double* a;
+  const double* rows;  // the 256 x n row scratch R
+  int64_t lda, ldr;
+  int nt, p0t;
+  RDB_DEV int count() const { return (nt - 2) * nt; }
+  RDB_DEV eng::Tile tile(int t) const {
+    int I = t / nt;
+    const int jj = t - I * nt;
+    I += (I >= p0t) ? 2 : 0;
+    // column order: the nt - 2 reduce tiles first, the two band tiles last
+    eng::Tile T;
+    T.a_col = p0t * NB;  // A operand: A_Ip, 128 x 256
+    T.a_row = I * NB;
+    T.a_mat = 0;
+    T.c_row = I * NB;
+    T.c_mat = 0;
+    T.nk = WB / eng::BK;
+    T.neg = 1;
+    T.signal = nullptr;
+    T.wait = nullptr;
+    T.wait_target = 0;
+    if (jj < nt - 2) {
+      const int J = jj + ((jj >= p0t) ? 2 : 0);
+      T.b = rows + (int64_t)J * NB;
+      T.ldb = ldr;
+      T.c_col = J * NB;
+      T.mode = eng::EPI_REDUCE;
+    } else {
+      const int h = jj - (nt - 2);
+      T.b = a + (int64_t)p0t * NB * lda + (int64_t)(p0t + h) * NB;  // D columns
+      T.ldb = lda;
+      T.c_col = h * NB;
+      T.c_sel = 1;
+      T.mode = eng::EPI_STORE;
+    }
+    return T;
+  }
+};
+
+__global__ void __launch_bounds__(EC::THREADS, 1)
+    gj_wide_row_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap rmap,
+                       WideRowSched sched) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&rmap});
+}
+
+__global__ void __launch_bounds__(EC::THREADS, 1)
+    gj_wide_update_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
+                          const __grid_constant__ CUtensorMap smap, WideUpdateSched sched) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap, &smap});
+}
+
+static int64_t wide_min_n() {
+  const char* e = getenv("RDB_GJ_WIDE_MIN");  // tuning / A-B switch (read per call); 0 disables the wide path
+  const int64_t v = e ? atoll(e) : 16384;  // measured: wide wins from 16384 (+2%) to 32768 (+6.6%)
+  return v == 0 ? INT64_MAX : v;
+}
+
+static size_t wide_scratch_bytes(int64_t n) { return (size_t)2 * WB * n * sizeof(double); }
+
+static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_info* info, cudaStream_t st) {
+  int rc = setup();
+  if (rc) return rc;
+  static bool attrs = false;
+  if (!attrs) {
+    if (cudaFuncSetAttribute(gj_wide_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)EC::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(gj_wide_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)EC::SMEM_BYTES) != cudaSuccess)
+      return RDB_ECUDA;
+    attrs = true;
+  }
+  const int nt = (int)(n / NB);
+  // workspace: [counters of the nested 256-block inverse | R (256 x n) | C (n x 256)]
+  char* base = static_cast<char*>(work);
+  int* cnt = reinterpret_cast<int*>(base);
+  double* R = reinterpret_cast<double*>(base + 256);
+  double* Cs = R + (int64_t)WB * n;
+  CUtensorMap amap, cmap, rmap, smap;
+  if ((rc = make_a_map(&amap, a, n, n, lda, n * lda, 1)) || (rc = make_ec_map(&cmap, a, n, n, lda, n * lda, 1)) ||
+      (rc = make_ec_map(&rmap, R, WB, n, n, (int64_t)WB * n, 1)) ||
+      (rc = make_ec_map(&smap, Cs, n, WB, WB, (int64_t)WB * n, 1)))
+    return rc;
+  for (int p = 0; p < nt / 2; ++p) {
+    const int p0t = 2 * p;
+    const int64_t p0 = (int64_t)p0t * NB;
+    // 1. D = A_pp^-1 (NB = 128 Gauss-Jordan on the 256 x 256 block, pivots into the same record)
+    rc = invert_core(a + p0 * lda + p0, WB, lda, 0, 1, cnt, info, st, p == 0 ? 1 : 0, p0);
+    if (rc) return rc;
+    // 2. R = D A_pJ
+    WideRowSched rs{a, lda, nt, p0t};
+    gj_wide_row_kernel<<<persistent_grid(2 * (nt - 2)), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, rmap, rs);
+    // 3. trailing update + new column panel
+    WideUpdateSched us{a, R, lda, n, nt, p0t};
+    gj_wide_update_kernel<<<persistent_grid((int64_t)(nt - 2) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(
+        amap, cmap, smap, us);
+    // 4. scratches -> band rows (R, columns outside the band) and band columns (C, rows outside)
+    const int64_t right = n - p0 - WB;
+    if (p0 > 0 &&
+        (cudaMemcpy2DAsync(a + p0 * lda, lda * 8, R, n * 8, p0 * 8, WB, cudaMemcpyDeviceToDevice, st) ||
+         cudaMemcpy2DAsync(a + p0, lda * 8, Cs, WB * 8, WB * 8, p0, cudaMemcpyDeviceToDevice, st)))
+      return RDB_ECUDA;
+    if (right > 0 &&
+        (cudaMemcpy2DAsync(a + p0 * lda + p0 + WB, lda * 8, R + p0 + WB, n * 8, right * 8, WB,
+                           cudaMemcpyDeviceToDevice, st) ||
+         cudaMemcpy2DAsync(a + (p0 + WB) * lda + p0, lda * 8, Cs + (p0 + WB) * WB, WB * 8, WB * 8, right,
+                           cudaMemcpyDeviceToDevice, st)))
+      return RDB_ECUDA;
   }
   RDB_LAUNCH_CHECK();
   return RDB_OK;
@@ -389,7 +563,10 @@ using namespace rdb;
 extern "C" size_t rdb_invert_workspace_bytes(int64_t n_pad, int64_t batch) {
   if (n_pad <= 0 || batch <= 0) return 0;
   const size_t nt = (size_t)((n_pad + NB - 1) / NB);
-  return ((size_t)batch * nt * sizeof(int) + 255) & ~(size_t)255;
+  const size_t counters = ((size_t)batch * nt * sizeof(int) + 255) & ~(size_t)255;
+  if (batch == 1 && n_pad >= rdb::wide_min_n() && n_pad % rdb::WB == 0)
+    return (counters > 256 ? counters : 256) + rdb::wide_scratch_bytes(n_pad);  // counters | R | C
+  return counters;
 }
 
 extern "C" int rdb_invert_batched(double* a, int64_t n_pad, int64_t lda, int64_t stride,

@@ -376,3 +376,32 @@ class TestGreedyDescent:
         pr = rb.greedy_descent(g, d, 0, 2)
         path, length, reached, steps = orc.greedy_descent(np.asarray(g.weights), d, 0, 2)
         assert (pr.vertices, pr.reached, pr.steps_taken) == (path, reached, steps)
+
+
+def test_wide_inversion_matches_narrow(cuda, monkeypatch):
+    # the NB=256 single-matrix path (default for n >= 16384) against the NB=128
+    # path on the same M-matrix: same pivots, inverse within 1e-13 relative,
+    # identical D
+    import torch
+
+    from paper_2308_07403_b200 import _device as _d
+    from paper_2308_07403_b200 import _lib as L
+    from paper_2308_07403_b200 import workloads as wl
+
+    n, gamma = 4096, 1e-3
+    g = wl.er_graph(n, 0.02, 11)
+    w = _d.graph_weights(g)
+    out = {}
+    for mode, env in (("narrow", "0"), ("wide", "1024")):
+        monkeypatch.setenv("RDB_GJ_WIDE_MIN", env)
+        m = _d.build_m(w, n, gamma, n)
+        rec = _d.invert_padded_nopivot(m)
+        _, d = _d.log_ceil(m, n, gamma, want_dceil=True)
+        out[mode] = (m, rec, d)
+    (a, ra, da), (b, rb_, db) = out["narrow"], out["wide"]
+    assert ra.flags == rb_.flags == 0 and ra.min_index == rb_.min_index
+    assert abs(ra.min_pivot - rb_.min_pivot) <= 1e-15
+    rel = ((a - b).abs() / a.abs().clamp_min(1e-300)).max().item()
+    assert rel < 1e-13, rel
+    assert torch.equal(da, db)
+    assert L.lib().rdb_invert_workspace_bytes(n, 1) > 0

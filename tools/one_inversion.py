@@ -1,0 +1,13 @@
+import os, sys, numpy as np, torch
+sys.path.insert(0, '/root/repo')
+from paper_2308_07403_b200 import _lib as L
+from paper_2308_07403_b200 import workloads as wl
+L.load_library(); dev = torch.device('cuda', 0); n = int(sys.argv[1])
+os.environ['RDB_GJ_WIDE_MIN'] = sys.argv[2]
+bits = torch.from_numpy(wl.er_bits_chunked(n, 0.01, 0, chunk_rows=2048).view(np.int32)).to(dev)
+m = torch.empty((n, n), dtype=torch.float64, device=dev)
+L.check(L.lib().rdb_build_m_bits(bits.data_ptr(), n, n, 1, None, 1e-4, m.data_ptr(), n, n * n, L.stream_handle()), 'b')
+work = torch.empty(L.lib().rdb_invert_workspace_bytes(n, 1), dtype=torch.uint8, device=dev)
+info = L.pivot_info_tensor(1, dev)
+L.check(L.lib().rdb_invert(m.data_ptr(), n, n, work.data_ptr(), info.data_ptr(), L.stream_handle()), 'i')
+torch.cuda.synchronize(); print('ok')
