@@ -293,7 +293,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
 }
 
 // ------------------------------------------------------------------ wide (NB = 256) single matrix
-// One large matrix (config 5; n >= 16384 by default) in 256-wide steps: every rank-256 update
+// One large matrix (configs 3 and 5; n >= 8192 by default) in 256-wide steps: every rank-256 update
 // tile runs 16 k-chunks per epilogue instead of 8, halving the engine's
 // per-tile cost per flop (tools/tile_overhead.py: 32.0 -> 34.1 TFLOP/s). Step p
 // (band = rows/cols p0 .. p0+255):
@@ -341,12 +341,14 @@ struct WideUpdateSched {  // rows I outside the band; J outside -> reduce into A
   const double* rows;  // the 256 x n row scratch R
   int64_t lda, ldr;
   int nt, p0t;
-  RDB_DEV int count() const { return (nt - 2) * nt; }
-  RDB_DEV eng::Tile tile(int t) const {
-    int I = t / nt;
-    const int jj = t - I * nt;
-    I += (I >= p0t) ? 2 : 0;
-    // column order: the nt - 2 reduce tiles first, the two band tiles last
+  // part 0: every tile; 1: only the next band's 2 x 2 diagonal tiles (look-ahead:
+  // the next 256-block inverse can start); 2: every tile except those
+  int part;
+  RDB_DEV int count() const { return part == 1 ? 4 : (nt - 2) * nt - (part == 2 ? 4 : 0); }
+  // (ri, jj): ri-th row tile outside the band, jj-th column in the order
+  // [nt - 2 reduce columns outside the band, then the 2 band columns]
+  RDB_DEV eng::Tile make(int ri, int jj) const {
+    const int I = ri + ((ri >= p0t) ? 2 : 0);
     eng::Tile T;
     T.a_col = p0t * NB;  // A operand: A_Ip, 128 x 256
     T.a_row = I * NB;
@@ -374,6 +376,20 @@ struct WideUpdateSched {  // rows I outside the band; J outside -> reduce into A
     }
     return T;
   }
+  RDB_DEV eng::Tile tile(int t) const {
+    // the next band (tiles p0t + 2, p0t + 3) is row / column index p0t, p0t + 1 here
+    if (part == 1) return make(p0t + (t >> 1), p0t + (t & 1));
+    if (part == 0) return make(t / nt, t - (t / nt) * nt);
+    const int head = p0t * nt;  // rows before the next band: all columns
+    if (t < head) return make(t / nt, t - (t / nt) * nt);
+    t -= head;
+    if (t < 2 * (nt - 2)) {  // the next band's two rows, its two columns skipped
+      const int r = t / (nt - 2), jr = t - r * (nt - 2);
+      return make(p0t + r, jr < p0t ? jr : jr + 2);
+    }
+    t -= 2 * (nt - 2);
+    return make(p0t + 2 + t / nt, t - (t / nt) * nt);
+  }
 };
 
 __global__ void __launch_bounds__(EC::THREADS, 1)
@@ -392,7 +408,7 @@ __global__ void __launch_bounds__(EC::THREADS, 1)
 
 static int64_t wide_min_n() {
   const char* e = getenv("RDB_GJ_WIDE_MIN");  // tuning / A-B switch (read per call); 0 disables the wide path
-  const int64_t v = e ? atoll(e) : 16384;  // measured: wide wins from 16384 (+2%) to 32768 (+6.6%)
+  const int64_t v = e ? atoll(e) : 8192;  // measured (tools/wide_check.py): +8% at 8192, +5.6% at 16384, +6.9% at 32768, even at 4096
   return v == 0 ? INT64_MAX : v;
 }
 
@@ -421,19 +437,39 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
       (rc = make_ec_map(&rmap, R, WB, n, n, (int64_t)WB * n, 1)) ||
       (rc = make_ec_map(&smap, Cs, n, WB, WB, (int64_t)WB * n, 1)))
     return rc;
+  cudaStream_t side = nullptr;
+  if ((rc = side_resources(&side))) return rc;
+  // 1. (step 0) D = A_00^-1: the NB = 128 Gauss-Jordan on the 256 x 256 block
+  rc = invert_core(a, WB, lda, 0, 1, cnt, info, st, 1, 0);
+  if (rc) return rc;
   for (int p = 0; p < nt / 2; ++p) {
     const int p0t = 2 * p;
     const int64_t p0 = (int64_t)p0t * NB;
-    // 1. D = A_pp^-1 (NB = 128 Gauss-Jordan on the 256 x 256 block, pivots into the same record)
-    rc = invert_core(a + p0 * lda + p0, WB, lda, 0, 1, cnt, info, st, p == 0 ? 1 : 0, p0);
-    if (rc) return rc;
+    const bool ahead = p + 1 < nt / 2;
     // 2. R = D A_pJ
     WideRowSched rs{a, lda, nt, p0t};
     gj_wide_row_kernel<<<persistent_grid(2 * (nt - 2)), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, rmap, rs);
-    // 3. trailing update + new column panel
-    WideUpdateSched us{a, R, lda, n, nt, p0t};
-    gj_wide_update_kernel<<<persistent_grid((int64_t)(nt - 2) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(
-        amap, cmap, smap, us);
+    // 3. trailing update + new column panel. Look-ahead: the next band's
+    // diagonal block is updated first and inverted (1.) on a side stream, one
+    // SM, while the rest of the update runs on the other SMs
+    if (ahead) {
+      cudaEventRecord(g_ev_a, st);
+      cudaStreamWaitEvent(side, g_ev_a, 0);
+      WideUpdateSched u1{a, R, lda, n, nt, p0t, 1};
+      gj_wide_update_kernel<<<1, EC::THREADS, EC::SMEM_BYTES, side>>>(amap, cmap, smap, u1);
+      const int64_t q0 = p0 + WB;
+      rc = invert_core(a + q0 * lda + q0, WB, lda, 0, 1, cnt, info, side, 0, q0);
+      if (rc) return rc;
+      cudaEventRecord(g_ev_p, side);
+      WideUpdateSched u2{a, R, lda, n, nt, p0t, 2};
+      const int64_t tiles = (int64_t)(nt - 2) * nt - 4;
+      const unsigned grid = (unsigned)(tiles < sm_count() - 1 ? tiles : sm_count() - 1);
+      gj_wide_update_kernel<<<grid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, smap, u2);
+    } else {
+      WideUpdateSched us{a, R, lda, n, nt, p0t, 0};
+      gj_wide_update_kernel<<<persistent_grid((int64_t)(nt - 2) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(
+          amap, cmap, smap, us);
+    }
     // 4. scratches -> band rows (R, columns outside the band) and band columns (C, rows outside)
     const int64_t right = n - p0 - WB;
     if (p0 > 0 &&
@@ -446,6 +482,7 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
          cudaMemcpy2DAsync(a + (p0 + WB) * lda + p0, lda * 8, Cs + (p0 + WB) * WB, WB * 8, WB * 8, right,
                            cudaMemcpyDeviceToDevice, st)))
       return RDB_ECUDA;
+    if (ahead) cudaStreamWaitEvent(st, g_ev_p, 0);
   }
   RDB_LAUNCH_CHECK();
   return RDB_OK;
