@@ -221,6 +221,13 @@ int rdb_apsp_bits_batched_d8(const uint32_t* bits, int64_t n, int64_t batch, con
                              double* mwork, void* work, rdb_pivot_info* info, uint8_t* d8,
                              unsigned long long* counters, void* stream);
 
+/* Edge list (device int32 from/to, m edges; the caller has checked 0 <= id < n,
+ * no self-loops, no duplicates as graph_from_edge_list does) -> bit-packed
+ * adjacency, bit `from` of row `to` (the rdb_build_m_bits input format).
+ * Zeroes `bits` (n x ceil(n/32) words) first. */
+int rdb_edges_to_bits(const int32_t* src, const int32_t* dst, int64_t m, int64_t n, uint32_t* bits,
+                      void* stream);
+
 /* ---- K8: exact hop distances by all-source BFS (oracles.py:22-41) -------
  * Unweighted digraph in the rdb_build_m_bits row format (row i, bit j <=>
  * edge j -> i). dist[i][j] = hops from j to i, 0 on the diagonal,

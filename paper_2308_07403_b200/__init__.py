@@ -13,7 +13,18 @@ As in the reference (pkg/src/rdist/__init__.py:52-68) the re-exported
 function ``resolvent`` shadows the submodule attribute of the same name.
 """
 
-from .graphs import EdgeList, Graph, GraphKind, adjacency_indicator, graph_from_edge_list
+from .graphs import (
+    EdgeList,
+    Graph,
+    GraphKind,
+    adjacency_indicator,
+    edge_list_from_graph,
+    graph_from_edge_list,
+    infer_kind,
+    read_edge_list,
+    write_distance_csv,
+    write_edge_list,
+)
 from .linalg import PIVOT_RTOL, PowerIterationResult, SingularMatrixError, lu_invert, power_iteration, spectral_radius
 from .navigation import PathResult, greedy_descent, next_hop_table
 from .resolvent import (
@@ -35,7 +46,14 @@ from .resolvent import (
     rounded_r_distance,
     suggest_gamma,
 )
-from .batch import UNREACHABLE, UNREACHABLE_D8, decode_d8, rounded_r_distance_batch, rounded_r_distance_batch_device
+from .batch import (
+    UNREACHABLE,
+    UNREACHABLE_D8,
+    bits_from_edge_list,
+    decode_d8,
+    rounded_r_distance_batch,
+    rounded_r_distance_batch_device,
+)
 from ._lib import NativeUnavailableError, load_library
 from .oracles import bfs_apsp, bfs_apsp_device
 from .sweep import SweepRecord, global_accuracy, local_accuracy, sweep_gamma_graph, sweep_point
@@ -48,6 +66,12 @@ __all__ = [
     "PIVOT_RTOL",
     "UNREACHABLE",
     "UNREACHABLE_D8",
+    "bits_from_edge_list",
+    "edge_list_from_graph",
+    "infer_kind",
+    "read_edge_list",
+    "write_distance_csv",
+    "write_edge_list",
     "bfs_apsp",
     "bfs_apsp_device",
     "SweepRecord",

@@ -88,6 +88,7 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "rdb_apsp_bits_batched": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rdb_log_ceil_d8": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _dbl, _vp, _i64, _i64, _vp, _vp]),
     "rdb_apsp_bits_batched_d8": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rdb_edges_to_bits": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "rdb_bfs_workspace_bytes": (_sz, [_i64]),
     "rdb_pattern_bits": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "rdb_bfs_apsp": (_int, [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp]),

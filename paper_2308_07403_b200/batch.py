@@ -37,6 +37,33 @@ UNREACHABLE_D8 = L.RDB_D8_UNREACHABLE
 D_DTYPES = {"int32": torch.int32, "uint8": torch.uint8}
 
 
+def bits_from_edge_list(edges, device=None) -> torch.Tensor:
+    """Device bit-packed adjacency (n, ceil(n/32)) int32 of an unweighted
+    EdgeList (graphs.py wire format), built on the GPU (rdb_edges_to_bits).
+    Same validation as graph_from_edge_list: range, self-loops, duplicates."""
+    n = int(edges.vertex_count)
+    if n < 1:
+        raise ValueError("vertex_count must be >= 1")
+    e = np.asarray([(s, d) for s, d, _ in edges.edges], dtype=np.int64).reshape(-1, 2)
+    w = np.asarray([w for _, _, w in edges.edges], dtype=np.float64)
+    if e.size:
+        if e.min() < 0 or e.max() >= n:
+            raise ValueError(f"edge out of range for {n} vertices")
+        if (e[:, 0] == e[:, 1]).any():
+            raise ValueError("self-loop in edge list")
+        if np.unique(e[:, 0] * n + e[:, 1]).size != e.shape[0]:
+            raise ValueError("duplicate edge in edge list")
+        if not np.all(w == 1.0):
+            raise ValueError("bits_from_edge_list needs an unweighted edge list (all weights 1)")
+    dev = device or L.device()
+    bits = torch.empty((n, (n + 31) // 32), dtype=torch.int32, device=dev)
+    src = torch.from_numpy(np.ascontiguousarray(e[:, 0], dtype=np.int32)).to(dev)
+    dst = torch.from_numpy(np.ascontiguousarray(e[:, 1], dtype=np.int32)).to(dev)
+    L.check(L.lib().rdb_edges_to_bits(src.data_ptr() if e.size else None, dst.data_ptr() if e.size else None,
+                                      int(e.shape[0]), n, bits.data_ptr(), L.stream_handle()), "rdb_edges_to_bits")
+    return bits
+
+
 def decode_d8(d8: np.ndarray) -> np.ndarray:
     """uint8 D -> int32 D (255 -> INT32_MAX)."""
     d = d8.astype(np.int32)

@@ -182,3 +182,27 @@ extern "C" int rdb_matrix_stats(const double* a, int64_t n, int64_t lda, double*
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
+
+// Edge list (from, to) -> bit-packed adjacency in the rdb_build_m_bits row
+// format (row `to`, bit `from`): the wire format feeding K1 directly
+// (graphs.py:99-111 builds the dense W the same way, w[to, from] = weight).
+__global__ void edges_to_bits_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m,
+                                     int64_t wpr, uint32_t* __restrict__ bits) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = src[e], d = dst[e];
+    atomicOr(&bits[(int64_t)d * wpr + (s >> 5)], 1u << (s & 31));
+  }
+}
+
+extern "C" int rdb_edges_to_bits(const int32_t* src, const int32_t* dst, int64_t m, int64_t n, uint32_t* bits,
+                                 void* stream) {
+  if (!bits || n <= 0 || m < 0 || (m > 0 && (!src || !dst))) return RDB_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t wpr = (n + 31) / 32;
+  if (cudaMemsetAsync(bits, 0, (size_t)(n * wpr) * sizeof(uint32_t), st) != cudaSuccess) return RDB_ECUDA;
+  if (m == 0) return RDB_OK;
+  const int64_t want = (m + 255) / 256;
+  edges_to_bits_kernel<<<(unsigned)(want < 148 * 32 ? want : 148 * 32), 256, 0, st>>>(src, dst, m, wpr, bits);
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}

@@ -16,6 +16,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 from enum import Enum
+from pathlib import Path
 
 import numpy as np
 
@@ -125,3 +126,63 @@ def graph_from_edge_list(edges: EdgeList, kind: GraphKind) -> Graph:
 def adjacency_indicator(g) -> np.ndarray:
     """0/1 float64 matrix of the edge pattern (graphs.py:114-116)."""
     return np.isfinite(np.asarray(g.weights)).astype(np.float64)
+
+
+# ---- wire formats either side of the path (graphs.py:284-329, cli.py:204-210)
+def edge_list_from_graph(g) -> EdgeList:
+    """(from, to, weight) triples of a Graph, sorted (graphs.py:284-290)."""
+    w = np.asarray(g.weights)
+    dst, src = np.nonzero(np.isfinite(w))
+    order = np.lexsort((dst, src))
+    src, dst = src[order], dst[order]
+    return EdgeList(int(g.n_vertices), tuple((int(s), int(d), float(w[d, s])) for s, d in zip(src, dst)))
+
+
+def write_edge_list(edges: EdgeList, path) -> None:
+    """``V <n>`` header, then one ``from to weight`` row per edge, weights with
+    17 significant digits (graphs.py:293-297)."""
+    rows = "".join(f"{s} {d} {w:.17g}\n" for s, d, w in edges.edges)
+    Path(path).write_text(f"V {edges.vertex_count}\n" + rows, encoding="utf-8")
+
+
+def read_edge_list(path) -> EdgeList:
+    """Parse the edge-list format: ``#`` comments and blank lines ignored, the
+    first entry must be ``V <vertex_count>`` (graphs.py:300-319)."""
+    vertex_count = None
+    triples: list[tuple[int, int, float]] = []
+    for lineno, raw in enumerate(Path(path).read_text(encoding="utf-8").splitlines(), 1):
+        line = raw.split("#", 1)[0].strip()
+        if not line:
+            continue
+        parts = line.split()
+        if vertex_count is None:
+            if len(parts) != 2 or parts[0] != "V":
+                raise ValueError(f"{path}:{lineno}: expected header 'V <vertex_count>'")
+            vertex_count = int(parts[1])
+            continue
+        if len(parts) != 3:
+            raise ValueError(f"{path}:{lineno}: expected 'from to weight'")
+        triples.append((int(parts[0]), int(parts[1]), float(parts[2])))
+    if vertex_count is None:
+        raise ValueError(f"{path}: missing 'V <vertex_count>' header")
+    return EdgeList(vertex_count, tuple(triples))
+
+
+def infer_kind(edges: EdgeList) -> GraphKind:
+    """Unweighted if every weight is 1, integer-weighted if all integral, else real (graphs.py:322-329)."""
+    ws = np.array([w for _, _, w in edges.edges], dtype=np.float64)
+    if np.all(ws == 1.0):
+        return GraphKind.UNWEIGHTED
+    if np.all(ws == np.floor(ws)):
+        return GraphKind.INTEGER_WEIGHTED
+    return GraphKind.REAL_WEIGHTED
+
+
+def write_distance_csv(d, path) -> None:
+    """One CSV row per distance row, ``inf`` for unreachable, 12 significant
+    digits (the CLI's distance output, cli.py:204-210)."""
+    d = np.asarray(d, dtype=np.float64)
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        for row in d:
+            fh.write(",".join("inf" if np.isinf(v) else f"{v:.12g}" for v in row))
+            fh.write("\n")

@@ -169,6 +169,7 @@ def main() -> None:
     }
 
     out.update(sweep_fixtures())
+    out.update(wire_fixtures())
     write(out)
     (HERE / "meta.json").write_text(json.dumps(meta, indent=1) + "\n")
 
@@ -260,8 +261,43 @@ def sweep_fixtures() -> dict[str, dict[str, np.ndarray]]:
     return out
 
 
+def wire_fixtures() -> dict[str, dict[str, np.ndarray]]:
+    """The reference's edge-list and distance-CSV formats (graphs.py:284-329,
+    cli.py:204-210) on a small weighted graph and an unweighted one with
+    unreachable pairs."""
+    import tempfile
+
+    from rdist import cli
+    from rdist import graphs as gr
+
+    gw = rdist.gen_weighted_dense(12, 0.3, 1.0, 100.0, 1)
+    el = gr.edge_list_from_graph(gw)
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "g.txt"
+        gr.write_edge_list(el, p)
+        text = p.read_text()
+        back = gr.read_edge_list(p)
+        assert back == el
+        ring = rdist.graph_from_edge_list(rdist.EdgeList(4, ((0, 1, 1.0), (1, 2, 1.0), (2, 0, 1.0))),
+                                          rdist.GraphKind.UNWEIGHTED)
+        d = rdist.rounded_r_distance(rdist.resolvent(ring, 0.1))
+        q = Path(td) / "d.csv"
+        cli._write_distance_csv(d, str(q))
+        csv = q.read_text()
+    return {"wire": {
+        "weights": gw.weights,
+        "edge_text": np.array(text),
+        "edges": np.array(el.edges, dtype=np.float64),
+        "kind": np.array(gr.infer_kind(el).value),
+        "ring_d": d,
+        "ring_csv": np.array(csv),
+    }}
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["sweep"]:
         write(sweep_fixtures())
+    elif sys.argv[1:] == ["wire"]:
+        write(wire_fixtures())
     else:
         main()

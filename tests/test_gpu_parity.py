@@ -206,3 +206,15 @@ def test_batch_ragged_sizes_vs_oracle(cuda, n, d_dtype):
     for b in range(5):
         ref = orc.run_rdist(wl.weights_from_present(present[b]), gammas[b])
         np.testing.assert_array_equal(int32_to_d(d[b]), ref, err_msg=f"n={n} graph {b}")
+
+
+def test_bits_from_edge_list(cuda):
+    # wire format -> device bit-packed adjacency (rdb_edges_to_bits) == host packing
+    present = wl.er_present(300, 0.05, 4)
+    g = rb.Graph(300, wl.weights_from_present(present), rb.GraphKind.UNWEIGHTED)
+    bits = rb.bits_from_edge_list(rb.edge_list_from_graph(g)).cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(bits, wl.pack_bits(present))
+    with pytest.raises(ValueError):
+        rb.bits_from_edge_list(rb.EdgeList(3, ((0, 1, 2.0),)))
+    with pytest.raises(ValueError):
+        rb.bits_from_edge_list(rb.EdgeList(3, ((0, 3, 1.0),)))
