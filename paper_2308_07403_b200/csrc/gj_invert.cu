@@ -77,21 +77,39 @@ struct UpdateSched {
   int* cnt;  // [batch][nt] row-block counters, zeroed before step 0
   int64_t lda, stride;
   int nt, pt, batch;
-  // part 0: every tile; 1: only column block pt+1 (the next panel, look-ahead);
-  // 2: every tile except column block pt+1
+  // part 0: every tile. Single-matrix look-ahead (batch == 1): part 1 is the
+  // next panel's diagonal tile (pt+1, pt+1) alone, part 2 every other tile
   int part;
-  RDB_DEV int cols() const { return part == 0 ? nt : (part == 1 ? 1 : nt - 1); }
-  RDB_DEV int count() const { return batch * (nt - 1) * cols(); }
+  RDB_DEV int count() const { return part == 0 ? batch * (nt - 1) * nt : (part == 1 ? 1 : (nt - 1) * nt - 1); }
   RDB_DEV eng::Tile tile(int t) const {
-    const int nc = cols();
-    const int per = (nt - 1) * nc;
-    const int g = t / per;
-    const int rem = t - g * per;
-    int I = rem / nc;
-    const int jj = rem - I * nc;
-    I += (I >= pt);
-    // column order pt+1, ..., nt-1, 0, ..., pt: the panel column comes last
-    int J = pt + 1 + jj + (part == 2 ? 1 : 0);
+    // (g, row index I' over the rows other than pt, column index jj in the
+    // order pt+1, ..., nt-1, 0, ..., pt: the panel column comes last)
+    int g = 0, Ir, jj;
+    if (part == 0) {
+      const int per = (nt - 1) * nt;
+      g = t / per;
+      const int rem = t - g * per;
+      Ir = rem / nt;
+      jj = rem - Ir * nt;
+    } else if (part == 1) {
+      Ir = pt;  // row pt+1
+      jj = 0;   // column pt+1
+    } else {
+      const int head = pt * nt;
+      if (t < head) {
+        Ir = t / nt;
+        jj = t - Ir * nt;
+      } else if (t - head < nt - 1) {
+        Ir = pt;
+        jj = t - head + 1;  // row pt+1 without its diagonal tile
+      } else {
+        const int r = t - head - (nt - 1);
+        Ir = pt + 1 + r / nt;
+        jj = r - (r / nt) * nt;
+      }
+    }
+    const int I = Ir + (Ir >= pt);
+    int J = pt + 1 + jj;
     if (J >= nt) J -= nt;
     double* A = a + (int64_t)g * stride;
     eng::Tile T;
@@ -196,13 +214,14 @@ static int setup() {
 // Side stream + events of the single-matrix look-ahead (one set per process;
 // the library is used from one device per process).
 static cudaStream_t g_side = nullptr;
-static cudaEvent_t g_ev_a = nullptr, g_ev_p = nullptr;
+static cudaEvent_t g_ev_a = nullptr, g_ev_p = nullptr, g_ev_b = nullptr;
 
 static int side_resources(cudaStream_t* side) {
   if (!g_side) {
     if (cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&g_ev_a, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_ev_p, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&g_ev_p, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_ev_b, cudaEventDisableTiming) != cudaSuccess)
       return RDB_ECUDA;
   }
   *side = g_side;
@@ -262,15 +281,17 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
     gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES, st>>>(
         amap, cmap, rp);
     if (lookahead && k + 1 < nt) {
-      UpdateSched ua{a, cnt, lda, stride, nt, k, 1, 1};
-      gj_update_kernel<<<persistent_grid(nt - 1), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, ua);
+      // side stream, one SM: the next diagonal tile, then its inverse (P1);
+      // main stream, the other SMs: every other tile of this update
       cudaEventRecord(g_ev_a, st);
       cudaStreamWaitEvent(side, g_ev_a, 0);
+      UpdateSched ua{a, cnt, lda, stride, nt, k, 1, 1};
+      gj_update_kernel<<<1, EC::THREADS, EC::SMEM_BYTES, side>>>(amap, cmap, ua);
       const int p1n = (k + 1) * NB;
       gj_panel_kernel<<<1, p1::THREADS, p1::SMEM_BYTES, side>>>(a, lda, stride, p1n, idx_base + p1n, info, 0);
       cudaEventRecord(g_ev_p, side);
       UpdateSched ub{a, cnt, lda, stride, nt, k, 1, 2};
-      const int64_t tiles = (int64_t)(nt - 1) * (nt - 1);
+      const int64_t tiles = (int64_t)(nt - 1) * nt - 1;
       const unsigned grid = (unsigned)(tiles < sm_count() - 1 ? tiles : sm_count() - 1);
       gj_update_kernel<<<grid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, ub);
       cudaStreamWaitEvent(st, g_ev_p, 0);
@@ -412,6 +433,11 @@ static int64_t wide_min_n() {
   return v == 0 ? INT64_MAX : v;
 }
 
+static bool wide_lookahead() {
+  const char* e = getenv("RDB_GJ_WIDE_LA");  // debugging switch: 0 runs the wide steps without look-ahead
+  return !(e && e[0] == '0');
+}
+
 static size_t wide_scratch_bytes(int64_t n) { return (size_t)2 * WB * n * sizeof(double); }
 
 static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_info* info, cudaStream_t st) {
@@ -445,7 +471,7 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
   for (int p = 0; p < nt / 2; ++p) {
     const int p0t = 2 * p;
     const int64_t p0 = (int64_t)p0t * NB;
-    const bool ahead = p + 1 < nt / 2;
+    const bool ahead = p + 1 < nt / 2 && wide_lookahead();
     // 2. R = D A_pJ
     WideRowSched rs{a, lda, nt, p0t};
     gj_wide_row_kernel<<<persistent_grid(2 * (nt - 2)), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, rmap, rs);
@@ -457,6 +483,7 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
       cudaStreamWaitEvent(side, g_ev_a, 0);
       WideUpdateSched u1{a, R, lda, n, nt, p0t, 1};
       gj_wide_update_kernel<<<1, EC::THREADS, EC::SMEM_BYTES, side>>>(amap, cmap, smap, u1);
+      cudaEventRecord(g_ev_b, side);  // u1 has read the old column panel (the copy-back below overwrites it)
       const int64_t q0 = p0 + WB;
       rc = invert_core(a + q0 * lda + q0, WB, lda, 0, 1, cnt, info, side, 0, q0);
       if (rc) return rc;
@@ -471,6 +498,7 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
           amap, cmap, smap, us);
     }
     // 4. scratches -> band rows (R, columns outside the band) and band columns (C, rows outside)
+    if (ahead) cudaStreamWaitEvent(st, g_ev_b, 0);
     const int64_t right = n - p0 - WB;
     if (p0 > 0 &&
         (cudaMemcpy2DAsync(a + p0 * lda, lda * 8, R, n * 8, p0 * 8, WB, cudaMemcpyDeviceToDevice, st) ||
@@ -482,7 +510,13 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
          cudaMemcpy2DAsync(a + (p0 + WB) * lda + p0, lda * 8, Cs + (p0 + WB) * WB, WB * 8, WB * 8, right,
                            cudaMemcpyDeviceToDevice, st)))
       return RDB_ECUDA;
-    if (ahead) cudaStreamWaitEvent(st, g_ev_p, 0);
+    if (ahead) {
+      cudaStreamWaitEvent(st, g_ev_p, 0);
+    } else if (p + 1 < nt / 2) {  // no look-ahead: the next 256-block inverse here
+      const int64_t q0 = p0 + WB;
+      rc = invert_core(a + q0 * lda + q0, WB, lda, 0, 1, cnt, info, st, 0, q0);
+      if (rc) return rc;
+    }
   }
   RDB_LAUNCH_CHECK();
   return RDB_OK;

@@ -378,21 +378,24 @@ class TestGreedyDescent:
         assert (pr.vertices, pr.reached, pr.steps_taken) == (path, reached, steps)
 
 
-def test_wide_inversion_matches_narrow(cuda, monkeypatch):
-    # the NB=256 single-matrix path (default for n >= 16384) against the NB=128
-    # path on the same M-matrix: same pivots, inverse within 1e-13 relative,
-    # identical D
+@pytest.mark.parametrize("n,lookahead", [(1024, "1"), (2048, "1"), (2048, "0"), (4096, "1")])
+def test_wide_inversion_matches_narrow(cuda, monkeypatch, n, lookahead):
+    # the NB=256 single-matrix path (default for n >= 8192), with and without
+    # its look-ahead, against the NB=128 path on the same M-matrix: same
+    # pivots, inverse within 1e-13 relative, identical D. Small n makes the
+    # side stream the longer one (the race a missing event would expose).
     import torch
 
     from paper_2308_07403_b200 import _device as _d
     from paper_2308_07403_b200 import _lib as L
     from paper_2308_07403_b200 import workloads as wl
 
-    n, gamma = 4096, 1e-3
+    gamma = 1e-3
     g = wl.er_graph(n, 0.02, 11)
     w = _d.graph_weights(g)
     out = {}
-    for mode, env in (("narrow", "0"), ("wide", "1024")):
+    monkeypatch.setenv("RDB_GJ_WIDE_LA", lookahead)
+    for mode, env in (("narrow", "0"), ("wide", "256")):
         monkeypatch.setenv("RDB_GJ_WIDE_MIN", env)
         m = _d.build_m(w, n, gamma, n)
         rec = _d.invert_padded_nopivot(m)
