@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RDB_ABI_VERSION 2
+#define RDB_ABI_VERSION 3
 #define RDB_NB 128 /* Gauss-Jordan panel width; inverted matrices are padded to a multiple */
 
 /* status codes */
@@ -198,11 +198,14 @@ int rdb_power_iteration(const double* m, int64_t n, int64_t ldm, int indicator, 
  * reference's stop conditions, navigation.py:62-69). W is n x n; dist holds
  * one row per target (row r = the distances to targets[r], ldd), so the
  * full n x n distance matrix with targets = 0..n-1 is the table case;
- * next is n_targets x n (ldn). work: rdb_next_hop_workspace_bytes(n, nnz)
- * where nnz = number of finite off-diagonal W entries (rdb_count_edges). */
+ * next is n_targets x n (ldn). work: rdb_next_hop_workspace_bytes(n, nnz,
+ * n_targets) where nnz = number of finite off-diagonal W entries
+ * (rdb_count_edges). For n <= 4097 the successors of each column are sorted
+ * by weight and each scan stops once no remaining successor can reach the
+ * best score (exact: see csrc/next_hop.cu); larger n scan every successor. */
 int rdb_count_edges(const double* w, int64_t n, int64_t ldw, unsigned long long* out_nnz,
                     void* stream);
-size_t rdb_next_hop_workspace_bytes(int64_t n, int64_t nnz);
+size_t rdb_next_hop_workspace_bytes(int64_t n, int64_t nnz, int64_t n_targets);
 int rdb_next_hop(const double* w, int64_t ldw, const double* dist, int64_t ldd, int64_t n,
                  int64_t nnz, const int32_t* targets, int64_t n_targets, int32_t* next,
                  int64_t ldn, void* work, void* stream);

@@ -190,7 +190,7 @@ def next_hop(w: torch.Tensor, dist_rows: torch.Tensor, targets: torch.Tensor, nn
         nnz = count_edges(w)
     nt = targets.shape[0]
     out = torch.empty((nt, n), dtype=torch.int32, device=w.device)
-    work = torch.empty(max(1, L.lib().rdb_next_hop_workspace_bytes(n, nnz)), dtype=torch.uint8, device=w.device)
+    work = torch.empty(max(1, L.lib().rdb_next_hop_workspace_bytes(n, nnz, nt)), dtype=torch.uint8, device=w.device)
     L.check(
         L.lib().rdb_next_hop(w.data_ptr(), w.stride(0), dist_rows.data_ptr(), dist_rows.stride(0), n, nnz,
                              targets.data_ptr(), nt, out.data_ptr(), out.stride(0), work.data_ptr(),

@@ -18,7 +18,7 @@ import torch
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "librdist_b200.so"
 
-RDB_ABI_VERSION = 2  # include/rdist_b200.h; load_library refuses a library built from another header
+RDB_ABI_VERSION = 3  # include/rdist_b200.h; load_library refuses a library built from another header
 RDB_NB = 128
 RDB_OK = 0
 RDB_PIV_NONPOS = 1
@@ -83,7 +83,7 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "rdb_power_workspace_bytes": (_sz, [_i64]),
     "rdb_power_iteration": (_int, [_vp, _i64, _i64, _int, _dbl, _i64, _vp, _vp, _vp]),
     "rdb_count_edges": (_int, [_vp, _i64, _i64, _vp, _vp]),
-    "rdb_next_hop_workspace_bytes": (_sz, [_i64, _i64]),
+    "rdb_next_hop_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "rdb_next_hop": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "rdb_apsp_bits_batched": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rdb_log_ceil_d8": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _dbl, _vp, _i64, _i64, _vp, _vp]),

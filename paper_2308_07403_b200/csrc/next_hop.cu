@@ -101,7 +101,8 @@ __global__ void csc_fill_kernel(const double* __restrict__ w, int64_t n, int64_t
 
 // seg[j * (nkb + 1) + q] = first entry of column j with k >= q * NH_KB
 __global__ void csc_seg_kernel(const int64_t* __restrict__ offs, const int32_t* __restrict__ idx,
-                               int64_t n, int64_t nkb, int64_t* __restrict__ seg) {
+                               int64_t n, int64_t nkb, int64_t* __restrict__ seg, const int* __restrict__ only_if) {
+  if (only_if && *only_if == 0) return;  // pruned path: only needed by the NaN-exact kernel
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int64_t beg = offs[j * CSC_SPLIT], end = offs[(j + 1) * CSC_SPLIT];
@@ -358,6 +359,202 @@ __global__ void __launch_bounds__(NP_WARPS * 32)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pruned variant (n <= SORT_MAX + 1, i.e. every column fits the in-smem sort):
+// each column's successors sorted by weight (ties by k). For a target t the
+// remaining candidates of a column score at least w + Rmin[t], where w is the
+// current (smallest remaining) weight and Rmin[t] = min over k != t of
+// dist[t][k]; once fl(w + Rmin[t]) > best[t] for every target of the warp no
+// later candidate can win or tie (rounding is monotonic), so the scan stops.
+// The successor k == t (dist[t][t], outside Rmin) is scored up front. Ties are
+// broken by the lower k, which reproduces the first minimum over ascending k.
+// dist is read transposed (RT[k][r]): one 512-byte coalesced load per entry
+// gives the 64 targets of a warp.
+constexpr int SORT_MAX = 4096;
+
+constexpr int PR_T = 64;      // targets per warp (2 per lane)
+constexpr int PR_WARPS = 8;   // warps per CTA: 8 consecutive columns
+constexpr int PR_COLS = 4;    // columns per warp, one after the other
+constexpr int PR_G = 4;  // entries (RT rows) in flight per step (8 measured slower: later bound checks)
+
+RDB_DEV uint64_t order_key(double w) {  // total order of doubles as unsigned integers
+  const uint64_t b = (uint64_t)__double_as_longlong(w);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+// one CTA per column: bitonic sort of (weight key, k) in shared memory
+__global__ void __launch_bounds__(256) csc_sort_kernel(const int64_t* __restrict__ offs,
+                                                       const int32_t* __restrict__ idx,
+                                                       const double* __restrict__ val, int64_t n,
+                                                       NhEnt* __restrict__ srt) {
+  extern __shared__ unsigned long long sk[];  // [P] keys, then [P] k (as 64-bit for alignment)
+  const int64_t j = blockIdx.x;
+  const int64_t beg = offs[j * CSC_SPLIT], end = offs[(j + 1) * CSC_SPLIT];
+  const int m = (int)(end - beg);
+  if (m == 0) return;
+  int P = 1;
+  while (P < m) P <<= 1;
+  unsigned long long* kk = sk + P;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    if (i < m) {
+      sk[i] = order_key(val[beg + i]);
+      kk[i] = (unsigned long long)idx[beg + i];
+    } else {
+      sk[i] = ~0ULL;
+      kk[i] = ~0ULL;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ stride;
+        if (l > i) {
+          const bool up = (i & size) == 0;
+          const bool gt = sk[i] > sk[l] || (sk[i] == sk[l] && kk[i] > kk[l]);
+          if (gt == up) {
+            const unsigned long long a = sk[i], b = kk[i];
+            sk[i] = sk[l];
+            kk[i] = kk[l];
+            sk[l] = a;
+            kk[l] = b;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const unsigned long long key = sk[i];  // order_key is a bijection: decode the weight exactly
+    const unsigned long long b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFULL) : ~key;
+    srt[beg + i] = NhEnt{__longlong_as_double((long long)b), (int32_t)kk[i], 0};
+  }
+}
+
+// RT[k][r] = dist[r][k] (32 x 32 tiles through shared memory)
+__global__ void transpose_kernel(const double* __restrict__ dist, int64_t ldd, int64_t rows, int64_t cols,
+                                 double* __restrict__ rt) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? dist[r * ldd + c] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) rt[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+// Rmin[r] = min over k != targets[r] of dist[r][k]; any NaN in the row raises *nan_flag
+__global__ void rmin_kernel(const double* __restrict__ dist, int64_t ldd, int64_t n, const int32_t* __restrict__ targets,
+                            int64_t n_targets, double* __restrict__ rmin, int* __restrict__ nan_flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_targets; r += nwarps) {
+    const int64_t t = targets[r];
+    double m = INFINITY;
+    bool nan = false;
+    for (int64_t k = lane; k < n; k += 32) {
+      const double v = dist[r * ldd + k];
+      nan |= (v != v);
+      if (k != t) m = fmin(m, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (__any_sync(0xffffffffu, nan) && lane == 0) atomicOr(nan_flag, 1);
+    if (lane == 0) rmin[r] = m;
+  }
+}
+
+__global__ void __launch_bounds__(PR_WARPS * 32)
+    next_hop_pruned_kernel(const int64_t* __restrict__ offs, const NhEnt* __restrict__ srt,
+                           const double* __restrict__ w, int64_t ldw, const double* __restrict__ rt, int64_t n,
+                           const int32_t* __restrict__ targets, int64_t n_targets, const double* __restrict__ rmin,
+                           int32_t* __restrict__ next, int64_t ldn, const int* __restrict__ nan_flag) {
+  if (*nan_flag) return;  // the exact kernel handles NaN semantics
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.y * PR_T + 2 * lane;  // this lane's two target rows r0, r0 + 1
+  const bool v0 = r0 < n_targets, v1 = r0 + 1 < n_targets;
+  const int64_t t0 = v0 ? targets[r0] : -1, t1 = v1 ? targets[r0 + 1] : -1;
+  const double m0 = v0 ? rmin[r0] : INFINITY, m1 = v1 ? rmin[r0 + 1] : INFINITY;
+  const bool vec = !(n_targets & 1);  // RT rows 16-byte aligned: one double2 per entry
+  for (int c = 0; c < PR_COLS; ++c) {
+    const int64_t j = ((int64_t)blockIdx.x * PR_WARPS + warp) * PR_COLS + c;
+    if (j >= n) break;
+    // the successor k == t (if any) first: W[t][j] + dist[t][t]
+    double b0 = INFINITY, b1 = INFINITY;
+    int32_t k0 = -1, k1 = -1;
+    if (v0 && t0 != j) {
+      const double wt = w[t0 * ldw + j];
+      if (fabs(wt) <= 1.7976931348623157e308) {
+        b0 = wt + rt[t0 * n_targets + r0];
+        k0 = (int32_t)t0;
+      }
+    }
+    if (v1 && t1 != j) {
+      const double wt = w[t1 * ldw + j];
+      if (fabs(wt) <= 1.7976931348623157e308) {
+        b1 = wt + rt[t1 * n_targets + r0 + 1];
+        k1 = (int32_t)t1;
+      }
+    }
+    const int64_t beg = offs[j * CSC_SPLIT], end = offs[(j + 1) * CSC_SPLIT];
+    // entries 32 at a time (one coalesced load), broadcast by shuffles; RT
+    // rows of 4 entries in flight per step; the bound is checked once per 4
+    // (with the smallest weight of the group)
+    bool stop = false;
+    for (int64_t base = beg; base < end && !stop; base += 32) {
+      const int cnt = (int)((end - base) < 32 ? (end - base) : 32);
+      NhEnt mine;
+      mine.w = INFINITY;
+      mine.k = 0;
+      if (lane < cnt) mine = srt[base + lane];
+      for (int i0 = 0; i0 < cnt; i0 += PR_G) {
+        const double wf = __shfl_sync(0xffffffffu, mine.w, i0);
+        const bool done = !(wf + m0 <= b0) && !(wf + m1 <= b1);
+        if (__all_sync(0xffffffffu, done)) {
+          stop = true;
+          break;
+        }
+
+        double we[PR_G];
+        int32_t ke[PR_G];
+        double2 d[PR_G];
+#pragma unroll
+        for (int u = 0; u < PR_G; ++u) {
+          we[u] = __shfl_sync(0xffffffffu, mine.w, i0 + u);
+          ke[u] = __shfl_sync(0xffffffffu, mine.k, i0 + u);
+          const bool live = i0 + u < cnt;
+          const int64_t kr = (int64_t)(live ? ke[u] : 0) * n_targets + r0;
+          if (vec && v1) {
+            d[u] = *reinterpret_cast<const double2*>(rt + kr);
+          } else {
+            d[u].x = v0 ? rt[kr] : INFINITY;
+            d[u].y = v1 ? rt[kr + 1] : INFINITY;
+          }
+          if (!live) we[u] = INFINITY;
+        }
+#pragma unroll
+        for (int u = 0; u < PR_G; ++u) {
+          const int32_t k = ke[u];
+          const double s0 = we[u] + d[u].x, s1 = we[u] + d[u].y;
+          if (k != t0 && (s0 < b0 || (s0 == b0 && k < k0))) {
+            b0 = s0;
+            k0 = k;
+          }
+          if (k != t1 && (s1 < b1 || (s1 == b1 && k < k1))) {
+            b1 = s1;
+            k1 = k;
+          }
+        }
+      }
+    }
+    if (v0) next[r0 * ldn + j] = ((t0 == j) || !(b0 < INFINITY)) ? -1 : k0;
+    if (v1) next[(r0 + 1) * ldn + j] = ((t1 == j) || !(b1 < INFINITY)) ? -1 : k1;
+  }
+}
+
 struct NhWork {
   int64_t* offs;  // n*CSC_SPLIT + 1
   int64_t* seg;   // n*(nkb+1)
@@ -365,11 +562,19 @@ struct NhWork {
   double* val;    // nnz
   NhEnt* pk;      // nnz
   int* nan_flag;  // 1
+  NhEnt* srt;     // nnz, weight-sorted columns (pruned path)
+  double* rt;     // n x n_targets, dist transposed (pruned path)
+  double* rmin;   // n_targets (pruned path)
 };
+
+static bool pruned_path(int64_t n) {
+  const char* e = getenv("RDB_NEXT_HOP_PRUNED");  // A-B switch: 0 selects the unpruned pair kernel
+  return n <= SORT_MAX + 1 && !(e && e[0] == '0');
+}
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static NhWork carve(void* work, int64_t n, int64_t nnz) {
+static NhWork carve(void* work, int64_t n, int64_t nnz, int64_t n_targets) {
   const int64_t nkb = (n + NH_KB - 1) / NH_KB;
   char* p = static_cast<char*>(work);
   NhWork w;
@@ -384,6 +589,17 @@ static NhWork carve(void* work, int64_t n, int64_t nnz) {
   w.pk = reinterpret_cast<NhEnt*>(p);
   p += align256((size_t)(nnz > 0 ? nnz : 1) * sizeof(NhEnt));
   w.nan_flag = reinterpret_cast<int*>(p);
+  p += 256;
+  w.srt = nullptr;
+  w.rt = nullptr;
+  w.rmin = nullptr;
+  if (pruned_path(n)) {
+    w.srt = reinterpret_cast<NhEnt*>(p);
+    p += align256((size_t)(nnz > 0 ? nnz : 1) * sizeof(NhEnt));
+    w.rt = reinterpret_cast<double*>(p);
+    p += align256((size_t)(n * n_targets) * 8);
+    w.rmin = reinterpret_cast<double*>(p);
+  }
   return w;
 }
 
@@ -401,12 +617,16 @@ extern "C" int rdb_count_edges(const double* w, int64_t n, int64_t ldw, unsigned
   return RDB_OK;
 }
 
-extern "C" size_t rdb_next_hop_workspace_bytes(int64_t n, int64_t nnz) {
-  if (n <= 0 || nnz < 0) return 0;
+extern "C" size_t rdb_next_hop_workspace_bytes(int64_t n, int64_t nnz, int64_t n_targets) {
+  if (n <= 0 || nnz < 0 || n_targets < 0) return 0;
   const int64_t nkb = (n + NH_KB - 1) / NH_KB;
-  return align256((size_t)(n * CSC_SPLIT + 1) * 8) + align256((size_t)(n * (nkb + 1)) * 8) +
-         align256((size_t)(nnz > 0 ? nnz : 1) * 8) + align256((size_t)(nnz > 0 ? nnz : 1) * 4) +
-         align256((size_t)(nnz > 0 ? nnz : 1) * sizeof(NhEnt)) + 256;
+  size_t b = align256((size_t)(n * CSC_SPLIT + 1) * 8) + align256((size_t)(n * (nkb + 1)) * 8) +
+             align256((size_t)(nnz > 0 ? nnz : 1) * 8) + align256((size_t)(nnz > 0 ? nnz : 1) * 4) +
+             align256((size_t)(nnz > 0 ? nnz : 1) * sizeof(NhEnt)) + 256;
+  if (pruned_path(n))
+    b += align256((size_t)(nnz > 0 ? nnz : 1) * sizeof(NhEnt)) + align256((size_t)(n * n_targets) * 8) +
+         align256((size_t)(n_targets > 0 ? n_targets : 1) * 8);
+  return b;
 }
 
 extern "C" int rdb_next_hop(const double* w, int64_t ldw, const double* dist, int64_t ldd, int64_t n,
@@ -418,14 +638,35 @@ extern "C" int rdb_next_hop(const double* w, int64_t ldw, const double* dist, in
   if ((n_targets + NH_T - 1) / NH_T > 65535) return RDB_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t nkb = (n + NH_KB - 1) / NH_KB;
-  NhWork wk = carve(work, n, nnz);
+  NhWork wk = carve(work, n, nnz, n_targets);
   const dim3 cg((unsigned)((n + 31) / 32), CSC_SPLIT);
   csc_count_kernel<<<cg, 32, 0, st>>>(w, n, ldw, wk.offs);
   csc_scan_kernel<<<1, 1024, 0, st>>>(wk.offs, n * CSC_SPLIT);
   csc_fill_kernel<<<cg, 32, 0, st>>>(w, n, ldw, wk.offs, wk.idx, wk.val);
-  csc_seg_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(wk.offs, wk.idx, n, nkb, wk.seg);
-  csc_pack_kernel<<<592, 256, 0, st>>>(wk.idx, wk.val, nnz, wk.pk);
   if (cudaMemsetAsync(wk.nan_flag, 0, sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
+  if (wk.srt && n_targets <= 65535LL * PR_T) {
+    // pruned path: weight-sorted columns, dist transposed, per-target lower bounds
+    const int sort_smem = 2 * SORT_MAX * (int)sizeof(unsigned long long);
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(csc_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_smem) !=
+          cudaSuccess)
+        return RDB_ECUDA;
+      attr = true;
+    }
+    csc_sort_kernel<<<(unsigned)n, 256, sort_smem, st>>>(wk.offs, wk.idx, wk.val, n, wk.srt);
+    transpose_kernel<<<dim3((unsigned)((n + 31) / 32), (unsigned)((n_targets + 31) / 32)), dim3(32, 8), 0, st>>>(
+        dist, ldd, n_targets, n, wk.rt);
+    rmin_kernel<<<(unsigned)((n_targets + 7) / 8), 256, 0, st>>>(dist, ldd, n, targets, n_targets, wk.rmin,
+                                                                 wk.nan_flag);
+    next_hop_pruned_kernel<<<dim3((unsigned)((n + PR_WARPS * PR_COLS - 1) / (PR_WARPS * PR_COLS)),
+                                  (unsigned)((n_targets + PR_T - 1) / PR_T)),
+                             PR_WARPS * 32, 0, st>>>(wk.offs, wk.srt, w, ldw, wk.rt, n, targets, n_targets,
+                                                     wk.rmin, next, ldn, wk.nan_flag);
+    csc_seg_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(wk.offs, wk.idx, n, nkb, wk.seg, wk.nan_flag);
+  } else {
+  csc_seg_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(wk.offs, wk.idx, n, nkb, wk.seg, nullptr);
+  csc_pack_kernel<<<592, 256, 0, st>>>(wk.idx, wk.val, nnz, wk.pk);
   const int smem = NH_KB * NP_ST * (int)sizeof(double);
   if (cudaFuncSetAttribute(next_hop_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
       cudaSuccess)
@@ -434,6 +675,7 @@ extern "C" int rdb_next_hop(const double* w, int64_t ldw, const double* dist, in
                               (unsigned)((n_targets + NP_T - 1) / NP_T)),
                          NP_WARPS * 32, smem, st>>>(wk.seg, wk.pk, dist, ldd, n, nkb, targets, n_targets, next,
                                                     ldn, wk.nan_flag);
+  }
   // exact NaN semantics (numpy argmin picks the first NaN and the walk stops):
   // recompute only when a NaN was seen; otherwise every CTA exits at once
   const int smem_exact = NH_KB * NH_T * (int)sizeof(double);

@@ -218,3 +218,28 @@ def test_bits_from_edge_list(cuda):
         rb.bits_from_edge_list(rb.EdgeList(3, ((0, 1, 2.0),)))
     with pytest.raises(ValueError):
         rb.bits_from_edge_list(rb.EdgeList(3, ((0, 3, 1.0),)))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_next_hop_pruned_equals_unpruned_with_ties(cuda, monkeypatch, seed):
+    # integer weights and integer "distances" make exact score ties everywhere:
+    # the weight-sorted, bound-pruned scan must pick the same (lowest-index)
+    # successor as the ascending scan and the oracle restatement
+    from paper_2308_07403_b200 import _device as _d
+
+    n = 700
+    rng = np.random.default_rng(seed)
+    present = (rng.random((n, n)) < 0.05) & ~np.eye(n, dtype=bool)
+    w = np.where(present, rng.integers(1, 4, (n, n)).astype(np.float64), np.inf)
+    dist = rng.integers(0, 6, (n, n)).astype(np.float64)
+    dist[rng.random((n, n)) < 0.05] = np.inf
+    wd = torch.from_numpy(w).cuda()
+    dd = torch.from_numpy(dist).cuda()
+    tg = torch.arange(n, dtype=torch.int32, device="cuda")
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("RDB_NEXT_HOP_PRUNED", mode)
+        out[mode] = _d.next_hop(wd, dd, tg).cpu().numpy()
+    np.testing.assert_array_equal(out["1"], out["0"])
+    ref = orc.next_hop_table(w, dist, np.arange(0, n, 7))
+    np.testing.assert_array_equal(out["1"][::7], ref)
