@@ -463,7 +463,8 @@ def main():
         "config": {"workload": WORKLOAD.format(args.d_dtype), "d_dtype": args.d_dtype, "d_check": d_check,
                    "graphs_per_gpu": batch, "global_batch": batch * world, "n": N,
                    "parallelism": f"dp{world} (independent graphs, no collective)",
-                   "l2": "working set per step 3.2 GB > L2 (no flush needed)"},
+                   "l2": f"working set per step {(buf.m.numel() * 8 + buf.d.numel() * dsize) / 1e9:.1f} GB > 126 MB L2 "
+                         "(inputs larger than L2; no flush needed)"},
         "inversion_tflops": inv_tflops, "inversion_frac_of_fp64_peak": inv_tflops / peak,
         "roofline": {"bound": "tensor", "kernel": "K2 blocked Gauss-Jordan (gj_panel + gj_rowpanel + gj_update, DMMA.8x8x4)",
                      "achieved": inv_tflops, "peak": peak, "unit": "TFLOP/s", "frac": inv_tflops / peak,
