@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(p1::THREADS, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
   p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), a + b * stride + off * lda + off, lda, idx0,
-                    info + b, first, nullptr);
+                    info + b, first);
 }
 
 // ------------------------------------------------------------------ schedulers

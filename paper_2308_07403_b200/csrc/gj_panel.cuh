@@ -1,5 +1,5 @@
 // P1 of the blocked Gauss-Jordan step: D = A_pp^-1 for the NB x NB diagonal
-// block (NB = 128), plus the negated transposed copy of the column panel.
+// block (NB = 128), in place.
 //
 // The block inverse is itself a blocked Gauss-Jordan with 32-wide sub-panels,
 // entirely in shared memory (one CTA of 8 warps per matrix):
@@ -20,7 +20,6 @@ constexpr int THREADS = 256;
 constexpr int SQ = 32;        // sub-panel width
 constexpr int SST = NB + 4;   // S row stride (132 = 4 mod 16: conflict-free fragments)
 constexpr int TST = SQ + 4;   // T row stride (36 = 4 mod 16)
-constexpr int CP_ROWS = 128;  // rows per copy block
 
 struct Smem {
   double S[NB * SST];
@@ -29,8 +28,6 @@ struct Smem {
   double pcol[2][SQ];
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem);
-constexpr int CP_ST = CP_ROWS + 1;
-static_assert((size_t)NB * CP_ST * sizeof(double) <= SMEM_BYTES, "copy staging fits");
 
 RDB_DEV void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
@@ -149,9 +146,9 @@ RDB_DEV void update32(Smem& s, int q0) {
   }
 }
 
-// The whole NB x NB inverse of A (global, row stride lda), in place; D^T -> dt.
+// The whole NB x NB inverse of A (global, row stride lda), in place.
 RDB_DEV void panel_inverse(Smem& s, double* __restrict__ A, int64_t lda, int p0,
-                           rdb_pivot_info* __restrict__ inf, int first, double* __restrict__ dt) {
+                           rdb_pivot_info* __restrict__ inf, int first) {
   const int t = threadIdx.x;
   for (int e = t; e < NB * NB / 2; e += THREADS) {
     const int r = e / (NB / 2), c2 = e % (NB / 2);
@@ -180,12 +177,6 @@ RDB_DEV void panel_inverse(Smem& s, double* __restrict__ A, int64_t lda, int p0,
     const int r = e / (NB / 2), c2 = e % (NB / 2);
     stg2(A + (int64_t)r * lda + 2 * c2, *reinterpret_cast<const double2*>(&s.S[r * SST + 2 * c2]));
   }
-  if (dt) {
-    for (int e = t; e < NB * NB; e += THREADS) {
-      const int r = e / NB, c = e % NB;  // dt[r][c] = D[c][r]; coalesced write
-      dt[e] = s.S[c * SST + r];
-    }
-  }
   if (t == 0) {
     if (first) {
       inf->min_pivot = minp;
@@ -198,23 +189,6 @@ RDB_DEV void panel_inverse(Smem& s, double* __restrict__ A, int64_t lda, int p0,
       }
       inf->flags |= flags;
     }
-  }
-}
-
-// Rows [i0, i0 + CP_ROWS) of the column panel A[:, p0:p0+NB], negated and
-// transposed into cwt (NB x n): cwt[k][i] = -A[i][p0 + k].
-RDB_DEV void panel_copy(double* smem, const double* __restrict__ A, int64_t n, int64_t lda, int p0,
-                        int64_t i0, double* __restrict__ cwt) {
-  for (int e = threadIdx.x; e < CP_ROWS * NB / 2; e += THREADS) {
-    const int il = e / (NB / 2), k2 = e % (NB / 2);
-    const double2 x = ldg2(A + (i0 + il) * lda + p0 + 2 * k2);
-    smem[(2 * k2) * CP_ST + il] = x.x;
-    smem[(2 * k2 + 1) * CP_ST + il] = x.y;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < CP_ROWS * NB; e += THREADS) {
-    const int k = e / CP_ROWS, il = e % CP_ROWS;
-    cwt[(int64_t)k * n + i0 + il] = -smem[k * CP_ST + il];
   }
 }
 

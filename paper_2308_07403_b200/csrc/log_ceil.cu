@@ -103,9 +103,6 @@ RDB_DEV double rdist_value(double v, double g, double lg, double inv_lg, const L
 RDB_DEV double dceil_value(double v, double g, double lg, double inv_lg, double inv_lg2, double thr,
                            const LogTab& T) {
   if (!(v > 0.0)) return INFINITY;
-#ifdef RDB_K3_MEMPROBE
-  return v * inv_lg;  // memory-only probe (not a valid result)
-#endif
   if (!(v < INFINITY)) return -INFINITY;
   const long long b = __double_as_longlong(v);
   const int ex = (int)(b >> 52);
@@ -482,113 +479,6 @@ static void launch(bool vec, unsigned blocks, cudaStream_t st, const double* y, 
                                                             ldo, stride_o, reach, ldm, counters);
 }
 
-// ---------------------------------------------------------------------------
-// TMA-fed variant for the batch hot path (int32 D only, no mask, contiguous
-// rows): a producer warp streams row segments of Y into a 4-stage shared-memory
-// ring with 1-D bulk copies (full/empty mbarriers), so HBM reads stay in
-// flight independently of the 8 compute warps' FP64 work.
-constexpr int TK_STAGES = 4;
-constexpr int TK_SEG = 2048;  // doubles per stage (16 KB)
-constexpr int TK_CWARPS = 8;
-constexpr int TK_THREADS = (TK_CWARPS + 1) * 32;
-
-struct TkSmem {
-  alignas(128) double row[TK_STAGES][TK_SEG];
-  alignas(8) uint64_t full[TK_STAGES];
-  alignas(8) uint64_t empty[TK_STAGES];
-  LogTab tab;
-};
-
-__global__ void __launch_bounds__(TK_THREADS)
-    log_ceil_d32_tma_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y,
-                            int64_t batch, const double* __restrict__ gammas, double gamma,
-                            int32_t* __restrict__ d32, int64_t ldo, int64_t stride_o,
-                            unsigned long long* __restrict__ counters) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  TkSmem& s = *reinterpret_cast<TkSmem*>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < 128 * 16; e += TK_THREADS) {
-    const int i = e >> 4, k = e & 15;
-    s.tab.c[i][k] = logtab::kC[i];
-    s.tab.hi[i][k] = logtab::kLhi[i];
-    s.tab.lo[i][k] = logtab::kLlo[i];
-  }
-  if (tid == 0) {
-    for (int i = 0; i < TK_STAGES; ++i) {
-      mbar_init(&s.full[i], 1);
-      mbar_init(&s.empty[i], TK_CWARPS);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const int64_t nseg = (n + TK_SEG - 1) / TK_SEG;
-  const int64_t items = n * batch * nseg;
-  if (warp == TK_CWARPS) {
-    if (lane == 0) {
-      int st = 0;
-      uint32_t ph = 0;
-      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int64_t w = it / nseg, sg = it - w * nseg;
-        const int64_t b = w / n, i = w - b * n;
-        const int64_t j0 = sg * TK_SEG;
-        const int64_t len = (n - j0) < TK_SEG ? (n - j0) : TK_SEG;
-        mbar_wait(&s.empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&s.full[st], (uint32_t)(len * 8));
-        bulk_g2s(s.row[st], y + b * stride_y + i * ldy + j0, (uint32_t)(len * 8), &s.full[st]);
-        if (++st == TK_STAGES) {
-          st = 0;
-          ph ^= 1;
-        }
-      }
-    }
-    return;
-  }
-  int st = 0;
-  uint32_t ph = 0;
-  int64_t cur_b = -1;
-  double g = 0.0, lg = 0.0, inv_lg = 0.0, thr = 0.0;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const int64_t w = it / nseg, sg = it - w * nseg;
-    const int64_t b = w / n, i = w - b * n;
-    const int64_t j0 = sg * TK_SEG;
-    const int len = (int)((n - j0) < TK_SEG ? (n - j0) : TK_SEG);
-    if (b != cur_b) {  // per-matrix constants (consecutive items mostly share b)
-      cur_b = b;
-      g = gammas ? gammas[b] : gamma;
-      lg = log(g);
-      inv_lg = 1.0 / lg;
-      thr = fmin(2e-6 * fabs(inv_lg), 0.25);
-    }
-    const int dj = (int)(i - j0);  // diagonal column within this segment (may be out of range)
-    int32_t* out = d32 + b * stride_o + i * ldo + j0;
-    unsigned neg = 0;
-    mbar_wait(&s.full[st], ph);
-    const double* row = s.row[st];
-    for (int j = 2 * tid; j < len; j += 2 * 32 * TK_CWARPS) {
-      const double2 v = *reinterpret_cast<const double2*>(row + j);
-      bool n0, n1;
-      double r0 = dceil_estimate(v.x, inv_lg, thr, s.tab, n0);
-      double r1 = dceil_estimate(v.y, inv_lg, thr, s.tab, n1);
-      if (n0 && j != dj) r0 = rdist_value(v.x, g, lg, inv_lg, s.tab);
-      if (n1 && j + 1 != dj) r1 = rdist_value(v.y, g, lg, inv_lg, s.tab);
-      r0 = (j == dj) ? 0.0 : r0;
-      r1 = (j + 1 == dj) ? 0.0 : r1;
-      *reinterpret_cast<int2*>(out + j) = make_int2(__double2int_ru(r0), __double2int_ru(r1));
-      neg += (v.x < NEGATIVE_ENTRY_TOL) + (v.y < NEGATIVE_ENTRY_TOL);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&s.empty[st]);
-    if (++st == TK_STAGES) {
-      st = 0;
-      ph ^= 1;
-    }
-    if (counters) {
-      neg = __reduce_add_sync(0xffffffffu, neg);
-      if (lane == 0 && neg) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_NEGATIVE], (unsigned long long)neg);
-    }
-  }
-}
-
 int log_ceil_shaped(const double* y, Shape sh, int64_t ldy, int64_t stride_y, int64_t batch,
                     const double* gammas, double gamma, double* r_out, double* dceil_out,
                     int32_t* d32_out, int64_t ldo, int64_t stride_o, const uint8_t* reachable,
@@ -603,25 +493,6 @@ int log_ceil_shaped(const double* y, Shape sh, int64_t ldy, int64_t stride_y, in
                    al(r_out, 16) && al(dceil_out, 16) && al(d32_out, 8);
   const int64_t rows = sh.rows * batch;
   const int key = (r_out ? 4 : 0) | (dceil_out ? 2 : 0) | (d32_out ? 1 : 0);
-  // The TMA-fed kernel measured slower than the LDG sweep on cfg2 (per-row
-  // setup amortised over too few elements per thread); kept for reference,
-  // disabled by the `false &&` until it is reworked.
-  if (false && key == 1 && vec && !reachable && !sh.gcol && sh.row0 == 0 && sh.col0 == 0 && sh.rows == n &&
-      (n % 2) == 0) {
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(log_ceil_d32_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(TkSmem)) != cudaSuccess)
-        return RDB_ECUDA;
-      attr = true;
-    }
-    const int64_t items = rows * ((n + TK_SEG - 1) / TK_SEG);
-    const unsigned blocks = (unsigned)(items < 2 * 148 ? items : 2 * 148);
-    log_ceil_d32_tma_kernel<<<blocks, TK_THREADS, sizeof(TkSmem), st>>>(y, n, ldy, stride_y, batch, gammas,
-                                                                       gamma, d32_out, ldo, stride_o, counters);
-    RDB_LAUNCH_CHECK();
-    return RDB_OK;
-  }
   const int64_t want = (rows + 7) / 8;
   const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
   if (key == 1 && vec && !reachable && !sh.gcol && sh.row0 == 0 && sh.col0 == 0 && sh.rows == n &&

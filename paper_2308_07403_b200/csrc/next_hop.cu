@@ -173,72 +173,6 @@ __global__ void __launch_bounds__(NH_THREADS)
   }
 }
 
-// Warp-cooperative variant: a CTA owns 32 targets (one per lane) x 128 source
-// vertices (16 per warp, running minima in registers). Per k-block the 32
-// targets' dist rows are staged transposed in shared memory (dsT[k][lane]), and
-// a warp walks one column's CSC entries with warp-uniform (broadcast) loads of
-// (k, w), every lane scoring its own target: 32 (target, successor) pairs per
-// entry load, conflict-free shared-memory reads.
-constexpr int NW_T = 32;
-constexpr int NW_COLS = 16;  // columns per warp
-constexpr int NW_WARPS = 8;
-constexpr int NW_ST = NW_T + 1;
-
-__global__ void __launch_bounds__(NW_WARPS * 32)
-    next_hop_warp_kernel(const int64_t* __restrict__ seg, const int32_t* __restrict__ idx,
-                         const double* __restrict__ val, const double* __restrict__ dist, int64_t ldd,
-                         int64_t n, int64_t nkb, const int32_t* __restrict__ targets, int64_t n_targets,
-                         int32_t* __restrict__ next, int64_t ldn) {
-  extern __shared__ double dsT[];  // [NH_KB][NW_ST]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t t0 = (int64_t)blockIdx.y * NW_T;
-  const int64_t j0 = (int64_t)blockIdx.x * (NW_COLS * NW_WARPS) + warp * NW_COLS;
-  double best[NW_COLS];
-  int32_t bk[NW_COLS];
-  unsigned nanmask = 0;
-#pragma unroll
-  for (int c = 0; c < NW_COLS; ++c) {
-    best[c] = INFINITY;
-    bk[c] = -1;
-  }
-  for (int64_t kb = 0; kb < nkb; ++kb) {
-    const int64_t k0 = kb * NH_KB;
-    const int kl = (int)((n - k0) < NH_KB ? (n - k0) : NH_KB);
-    __syncthreads();
-    for (int e = threadIdx.x; e < NW_T * NH_KB; e += NW_WARPS * 32) {
-      const int q = e / NH_KB, k = e - (e / NH_KB) * NH_KB;
-      dsT[k * NW_ST + q] = (t0 + q < n_targets && k < kl) ? dist[(t0 + q) * ldd + k0 + k] : INFINITY;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < NW_COLS; ++c) {
-      const int64_t j = j0 + c;
-      if (j >= n) break;
-      const int64_t eb = seg[j * (nkb + 1) + kb], ee = seg[j * (nkb + 1) + kb + 1];
-#pragma unroll 4
-      for (int64_t e = eb; e < ee; ++e) {
-        const int32_t k = __ldg(idx + e);
-        const double s = __ldg(val + e) + dsT[(k - k0) * NW_ST + lane];
-        if (s < best[c]) {
-          best[c] = s;
-          bk[c] = k;
-        }
-        nanmask |= (unsigned)(s != s) << c;
-      }
-    }
-  }
-  const int64_t r = t0 + lane;
-  if (r >= n_targets) return;
-  const int64_t t = targets[r];
-#pragma unroll
-  for (int c = 0; c < NW_COLS; ++c) {
-    const int64_t j = j0 + c;
-    if (j >= n) break;
-    const bool stop = (t == j) || ((nanmask >> c) & 1u) || !(best[c] < INFINITY);
-    next[r * ldn + j] = stop ? -1 : bk[c];
-  }
-}
-
 // Packed CSC entry: one 16-byte (uniform, broadcast) load per entry.
 struct alignas(16) NhEnt {
   double w;
