@@ -64,6 +64,7 @@ struct Cfg {
     alignas(128) double out[MMA_WARPS][HROWS * WCOLS];  // dense HROWS x WCOLS TMA box per warp
     alignas(8) uint64_t full[STAGES];
     alignas(8) uint64_t empty[STAGES];
+    int tile_of[STAGES];  // dynamic scheduling: tile index of the stage's first chunk (-1: done)
   };
   static constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;  // + alignment slack
 };
@@ -219,6 +220,30 @@ struct BulkEpilogue {
   }
 };
 
+// Sched::dyn (when present and non-null): a global tile counter. CTAs then take
+// tiles in arrival order (atomicAdd) instead of the static blockIdx + k*gridDim
+// stride, so a launch that shares the GPU with another stream's kernels
+// balances itself; each CTA still sees increasing tile indices (the in-kernel
+// dependency argument holds). The last grab (value ntiles + gridDim - 1)
+// resets the counter to 0 for the next launch.
+template <class S, class = void>
+struct DynOf {
+  RDB_DEV static int* get(const S&) { return nullptr; }
+};
+template <class S>
+struct DynOf<S, decltype((void)S::dyn)> {
+  RDB_DEV static int* get(const S& s) { return s.dyn; }
+};
+
+RDB_DEV int grab_tile(int* dyn, int ntiles, int lane) {
+  int v = 0;
+  if (lane == 0) {
+    v = atomicAdd(dyn, 1);
+    if (v == ntiles + (int)gridDim.x - 1) atomicExch(dyn, 0);
+  }
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
 // Epi::kDeferred (when present) selects the stage()/issue() protocol.
 template <class E, class = void>
 struct Defers {
@@ -257,12 +282,25 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
     if (lane == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(amap)) : "memory");
     int st = 0;
     uint32_t ph = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int* const dyn = DynOf<Sched>::get(sched);
+    for (int t = dyn ? grab_tile(dyn, ntiles, lane) : (int)blockIdx.x;;
+         t = dyn ? grab_tile(dyn, ntiles, lane) : t + (int)gridDim.x) {
+      if (t >= ntiles) {
+        if (dyn) {  // tell the MMA warps: no more tiles
+          mbar_wait(&s.empty[st], ph ^ 1);
+          if (lane == 0) {
+            s.tile_of[st] = -1;
+            mbar_arrive(&s.full[st]);
+          }
+        }
+        break;
+      }
       const Tile T = sched.tile(t);
       for (int c = 0; c < T.nk; ++c) {
         mbar_wait(&s.empty[st], ph ^ 1);
         const int k0 = c * BK;
         if (lane == 0) {
+          if (c == 0) s.tile_of[st] = t;  // published by the full barrier's completion
           mbar_arrive_expect_tx(&s.full[st], STAGE_BYTES);
           tma_load_3d(s.a[st], amap, T.a_col + k0, T.a_row, T.a_mat, &s.full[st]);
         }
@@ -291,7 +329,15 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
   int pend_t = -1;  // tile whose staged write is not yet issued (deferred epilogue)
   int st = 0;
   uint32_t ph = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const bool dyn = DynOf<Sched>::get(sched) != nullptr;
+  for (int t = blockIdx.x;; t += gridDim.x) {
+    if (dyn) {
+      mbar_wait(&s.full[st], ph);  // the tile's first chunk (or the end marker)
+      t = s.tile_of[st];
+      if (t < 0) break;
+    } else if (t >= ntiles) {
+      break;
+    }
     const Tile T = sched.tile(t);
     const int issue_at = kDefer ? (warp * T.nk) / C::MMA_WARPS : 0;
     double acc[C::MI][C::NI][2];
@@ -301,7 +347,7 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
       for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     for (int c = 0; c < T.nk; ++c) {
-      mbar_wait(&s.full[st], ph);
+      if (!dyn || c > 0) mbar_wait(&s.full[st], ph);
       // all of this tile's operands are in shared memory: release dependents
       if (c == T.nk - 1 && T.signal && warp == 0 && lane == 0) signal_done(T.signal);
       if constexpr (kDefer) {

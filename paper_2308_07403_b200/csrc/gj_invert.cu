@@ -46,6 +46,7 @@ struct RowPanelSched {
   double* a;
   int64_t lda, stride;
   int nt, pt, batch;
+  int* dyn = nullptr;  // dynamic tile counter (batched calls)
   RDB_DEV int count() const { return batch * (nt - 1); }
   RDB_DEV eng::Tile tile(int t) const {
     const int g = t / (nt - 1);
@@ -80,6 +81,7 @@ struct UpdateSched {
   // part 0: every tile. Single-matrix look-ahead (batch == 1): part 1 is the
   // next panel's diagonal tile (pt+1, pt+1) alone, part 2 every other tile
   int part;
+  int* dyn = nullptr;  // dynamic tile counter (batched calls)
   RDB_DEV int count() const { return part == 0 ? batch * (nt - 1) * nt : (part == 1 ? 1 : (nt - 1) * nt - 1); }
   RDB_DEV eng::Tile tile(int t) const {
     // (g, row index I' over the rows other than pt, column index jj in the
@@ -245,7 +247,7 @@ static int64_t wide_min_n();
 // (step 0); idx_base offsets the reported pivot indices (a diagonal sub-block
 // inverted as part of a larger matrix).
 static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
-                       rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base) {
+                       rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base, int* dyn = nullptr) {
   if (!a || !work || !info || n <= 0 || batch <= 0) return RDB_EINVAL;
   if (n % NB != 0 || lda < n || (lda & 1) || (batch > 1 && stride < n * lda)) return RDB_EINVAL;
   if (((uintptr_t)a & 15) || ((uintptr_t)work & 15)) return RDB_EINVAL;
@@ -277,7 +279,7 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
       gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, idx_base + p0,
                                                                            info, 0);
     if (nt == 1) break;
-    RowPanelSched rp{a, lda, stride, nt, k, (int)batch};
+    RowPanelSched rp{a, lda, stride, nt, k, (int)batch, batch > 1 ? dyn : nullptr};
     gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES, st>>>(
         amap, cmap, rp);
     if (lookahead && k + 1 < nt) {
@@ -296,7 +298,7 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
       gj_update_kernel<<<grid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, ub);
       cudaStreamWaitEvent(st, g_ev_p, 0);
     } else {
-      UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch, 0};
+      UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch, 0, batch > 1 && dyn ? dyn + 1 : nullptr};
       gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(
           amap, cmap, up);
     }
@@ -311,6 +313,16 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
 // 18.44 -> 18.03 ms for 256 graphs (tools/two_stream.py).
 static cudaStream_t g_half[2] = {nullptr, nullptr};
 static cudaEvent_t g_fork = nullptr, g_join[2] = {nullptr, nullptr};
+
+static size_t counter_bytes(int64_t n_pad, int64_t batch) {
+  const size_t nt = (size_t)((n_pad + NB - 1) / NB);
+  return ((size_t)batch * nt * sizeof(int) + 255) & ~(size_t)255;
+}
+
+static bool dyn_sched() {
+  const char* e = getenv("RDB_GJ_DYNAMIC");  // A-B switch: 0 keeps the static tile stride
+  return !(e && e[0] == '0');
+}
 
 static int split_min_batch() {
   const char* e = getenv("RDB_GJ_SPLIT_MIN");  // A-B switch; 0 disables the split
@@ -335,13 +347,16 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     int64_t h = (batch / 2 + 3) & ~(int64_t)3;  // keep the second half's counters 16-byte aligned
     if (h >= batch) h = batch / 2;
     if ((h * nt * (int64_t)sizeof(int)) % 16 != 0) return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0);
+    // dynamic tile counters (2 per half) after the row-block counters
+    int* dyn = reinterpret_cast<int*>(static_cast<char*>(work) + counter_bytes(n, batch));
+    if (cudaMemsetAsync(dyn, 0, 4 * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
     cudaEventRecord(g_fork, st);
     int rc = RDB_OK;
     for (int i = 0; i < 2 && rc == RDB_OK; ++i) {
       const int64_t lo = i ? h : 0, cnt = i ? batch - h : h;
       cudaStreamWaitEvent(g_half[i], g_fork, 0);
       rc = invert_core(a + lo * stride, n, lda, stride, cnt, static_cast<char*>(work) + lo * nt * sizeof(int),
-                       info + lo, g_half[i], 1, 0);
+                       info + lo, g_half[i], 1, 0, dyn_sched() ? dyn + 2 * i : nullptr);
       cudaEventRecord(g_join[i], g_half[i]);
     }
     cudaStreamWaitEvent(st, g_join[0], 0);
@@ -671,8 +686,7 @@ using namespace rdb;
 
 extern "C" size_t rdb_invert_workspace_bytes(int64_t n_pad, int64_t batch) {
   if (n_pad <= 0 || batch <= 0) return 0;
-  const size_t nt = (size_t)((n_pad + NB - 1) / NB);
-  const size_t counters = ((size_t)batch * nt * sizeof(int) + 255) & ~(size_t)255;
+  const size_t counters = rdb::counter_bytes(n_pad, batch) + (batch > 1 ? 256 : 0);  // + dynamic tile counters
   if (batch == 1 && n_pad >= rdb::wide_min_n() && n_pad % rdb::WB == 0)
     return (counters > 256 ? counters : 256) + rdb::wide_scratch_bytes(n_pad);  // counters | R | C
   return counters;

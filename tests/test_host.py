@@ -55,7 +55,7 @@ def test_abi_version_and_errors_without_gpu():
     # uint8 D needs its range counters
     assert lib.rdb_log_ceil_d8(ctypes.c_void_p(256), 4, 4, 16, 1, None, 0.5, ctypes.c_void_p(256), 4, 16, None,
                                None) == 1
-    assert lib.rdb_invert_workspace_bytes(1024, 256) == 256 * 8 * 4  # row-block counters
+    assert lib.rdb_invert_workspace_bytes(1024, 256) == 256 * 8 * 4 + 256  # row-block + dynamic tile counters
     assert lib.rdb_invert_workspace_bytes(0, 1) == 0
 
 
