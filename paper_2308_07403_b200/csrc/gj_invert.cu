@@ -307,12 +307,13 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   return RDB_OK;
 }
 
-// Two halves of a large batch on two streams: each half's kernels fill the
-// other's tails (the last partial round of every persistent launch, the
+// Sub-batches of a large batch on their own streams (default two halves):
+// each part's kernels fill the others' tails (the last partial round of every persistent launch, the
 // second wave of the one-CTA-per-matrix panel inverses). Measured on config 2:
 // 18.44 -> 18.03 ms for 256 graphs (tools/two_stream.py).
-static cudaStream_t g_half[2] = {nullptr, nullptr};
-static cudaEvent_t g_fork = nullptr, g_join[2] = {nullptr, nullptr};
+constexpr int MAX_PARTS = 4;
+static cudaStream_t g_part[MAX_PARTS] = {};
+static cudaEvent_t g_fork = nullptr, g_join[MAX_PARTS] = {};
 
 static size_t counter_bytes(int64_t n_pad, int64_t batch) {
   const size_t nt = (size_t)((n_pad + NB - 1) / NB);
@@ -330,37 +331,43 @@ static int split_min_batch() {
   return v <= 0 ? 1 << 30 : v;
 }
 
+static int split_parts() {
+  const char* e = getenv("RDB_GJ_SPLIT_PARTS");  // tuning: sub-batches on their own streams (2..4)
+  const int v = e ? atoi(e) : 2;
+  return v < 2 ? 2 : (v > MAX_PARTS ? MAX_PARTS : v);
+}
+
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                    rdb_pivot_info* info, cudaStream_t st) {
   if (batch == 1 && n >= wide_min_n() && n % (2 * NB) == 0 && a && work && info && lda >= n && !(lda & 1) &&
       !((uintptr_t)a & 15) && !((uintptr_t)work & 15))
     return invert_wide(a, n, lda, work, info, st);
-  if (batch >= split_min_batch() && a && work && info && n % NB == 0 && stride >= n * lda) {
+  const int parts = split_parts();
+  if (batch >= split_min_batch() && batch >= 4 * parts && a && work && info && n % NB == 0 && stride >= n * lda) {
     if (!g_fork) {
-      for (int i = 0; i < 2; ++i)
-        if (cudaStreamCreateWithFlags(&g_half[i], cudaStreamNonBlocking) != cudaSuccess ||
+      for (int i = 0; i < MAX_PARTS; ++i)
+        if (cudaStreamCreateWithFlags(&g_part[i], cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&g_join[i], cudaEventDisableTiming) != cudaSuccess)
           return RDB_ECUDA;
       if (cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess) return RDB_ECUDA;
     }
     const int64_t nt = n / NB;
-    int64_t h = (batch / 2 + 3) & ~(int64_t)3;  // keep the second half's counters 16-byte aligned
-    if (h >= batch) h = batch / 2;
-    if ((h * nt * (int64_t)sizeof(int)) % 16 != 0) return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0);
-    // dynamic tile counters (2 per half) after the row-block counters
+    // sub-batch boundaries at multiples of 4 matrices: every part's counters stay 16-byte aligned
+    int64_t bound[MAX_PARTS + 1];
+    for (int i = 0; i <= parts; ++i) bound[i] = i == parts ? batch : ((batch * i / parts) & ~(int64_t)3);
+    // dynamic tile counters (2 per part) after the row-block counters
     int* dyn = reinterpret_cast<int*>(static_cast<char*>(work) + counter_bytes(n, batch));
-    if (cudaMemsetAsync(dyn, 0, 4 * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
+    if (cudaMemsetAsync(dyn, 0, 2 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
     cudaEventRecord(g_fork, st);
     int rc = RDB_OK;
-    for (int i = 0; i < 2 && rc == RDB_OK; ++i) {
-      const int64_t lo = i ? h : 0, cnt = i ? batch - h : h;
-      cudaStreamWaitEvent(g_half[i], g_fork, 0);
+    for (int i = 0; i < parts && rc == RDB_OK; ++i) {
+      const int64_t lo = bound[i], cnt = bound[i + 1] - bound[i];
+      cudaStreamWaitEvent(g_part[i], g_fork, 0);
       rc = invert_core(a + lo * stride, n, lda, stride, cnt, static_cast<char*>(work) + lo * nt * sizeof(int),
-                       info + lo, g_half[i], 1, 0, dyn_sched() ? dyn + 2 * i : nullptr);
-      cudaEventRecord(g_join[i], g_half[i]);
+                       info + lo, g_part[i], 1, 0, dyn_sched() ? dyn + 2 * i : nullptr);
+      cudaEventRecord(g_join[i], g_part[i]);
     }
-    cudaStreamWaitEvent(st, g_join[0], 0);
-    cudaStreamWaitEvent(st, g_join[1], 0);
+    for (int i = 0; i < parts; ++i) cudaStreamWaitEvent(st, g_join[i], 0);
     return rc;
   }
   return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0);
