@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <mutex>
 
 #include "dmma_engine.cuh"
 #include "gj_panel.cuh"
@@ -337,8 +338,14 @@ static int split_parts() {
   return v < 2 ? 2 : (v > MAX_PARTS ? MAX_PARTS : v);
 }
 
+// The internal streams and events (look-ahead side stream, sub-batch streams)
+// are process-wide: host threads enqueueing inversions concurrently are
+// serialised here (enqueue only; the calls stay asynchronous).
+static std::mutex g_enqueue;
+
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                    rdb_pivot_info* info, cudaStream_t st) {
+  std::lock_guard<std::mutex> guard(g_enqueue);
   if (batch == 1 && n >= wide_min_n() && n % (2 * NB) == 0 && a && work && info && lda >= n && !(lda & 1) &&
       !((uintptr_t)a & 15) && !((uintptr_t)work & 15))
     return invert_wide(a, n, lda, work, info, st);
