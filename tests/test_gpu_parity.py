@@ -243,3 +243,30 @@ def test_next_hop_pruned_equals_unpruned_with_ties(cuda, monkeypatch, seed):
     np.testing.assert_array_equal(out["1"], out["0"])
     ref = orc.next_hop_table(w, dist, np.arange(0, n, 7))
     np.testing.assert_array_equal(out["1"][::7], ref)
+
+
+def test_batch_split_and_dynamic_are_bitwise_neutral(cuda, monkeypatch):
+    # sub-batch streams and dynamic tile scheduling change only which SM does
+    # which tile: every matrix's inverse is bitwise the same
+    from paper_2308_07403_b200 import batch as B
+
+    bits, gammas, _ = wl.cfg2_batch(256)
+    bits, gammas = bits[96:224], gammas[96:224]  # 64 ER + 64 lattice graphs
+    dev = torch.device("cuda")
+    out = {}
+    for name, env in (("default", {}), ("no_split", {"RDB_GJ_SPLIT_MIN": "0"}),
+                      ("static", {"RDB_GJ_DYNAMIC": "0"}), ("four", {"RDB_GJ_SPLIT_PARTS": "4"})):
+        for k in ("RDB_GJ_SPLIT_MIN", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_PARTS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        buf = B.BatchBuffers.allocate(1024, 128, dev)
+        buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+        buf.gammas.copy_(torch.from_numpy(gammas))
+        buf.stage_build(128, torch.cuda.current_stream().cuda_stream)
+        buf.stage_invert(128, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        out[name] = buf.m.clone()
+        del buf
+    for name in ("no_split", "static", "four"):
+        assert torch.equal(out[name], out["default"]), name
