@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RDB_ABI_VERSION 3
+#define RDB_ABI_VERSION 4
 #define RDB_NB 128 /* Gauss-Jordan panel width; inverted matrices are padded to a multiple */
 
 /* status codes */
@@ -114,6 +114,19 @@ int rdb_matrix_stats(const double* a, int64_t n, int64_t lda, double* stats, voi
 size_t rdb_invert_workspace_bytes(int64_t n_pad, int64_t batch);
 int rdb_invert_batched(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t batch,
                        void* work, rdb_pivot_info* info, void* stream);
+/* Batched calls (batch > 1, n_pad <= 64 * RDB_NB) skip the tiles of
+ * structurally zero 128 x 128 blocks: a symbolic Gauss-Jordan on the block
+ * pattern (fill A_IJ |= A_Ip & A_pJ) lists, per step, the row-panel tiles
+ * with a non-zero A_pJ and the update tiles with non-zero A_Ip and A_pJ. A
+ * skipped tile would only add an exact zero, so results equal the dense
+ * schedule's (up to the sign of zero entries). rdb_invert_batched finds the
+ * pattern by scanning the matrices; rdb_invert_batched_bits takes it from
+ * the bit-packed adjacency the matrices were built from (rdb_build_m_bits
+ * format, n vertices; the rdb_apsp_bits_batched pipelines do the same).
+ * Environment RDB_GJ_SKIP=0 runs the dense schedule. */
+int rdb_invert_batched_bits(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t batch,
+                            const uint32_t* bits, int64_t n, void* work, rdb_pivot_info* info,
+                            void* stream);
 int rdb_invert(double* a, int64_t n_pad, int64_t lda, void* work, rdb_pivot_info* info,
                void* stream);
 

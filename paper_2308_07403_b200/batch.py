@@ -116,6 +116,14 @@ class BatchBuffers:
                 "rdb_build_m_bits")
 
     def stage_invert(self, count: int, stream: int) -> None:
+        """K2 with the block pattern from the adjacency bits (as the apsp pipeline)."""
+        L.check(L.lib().rdb_invert_batched_bits(self.m.data_ptr(), self.n_pad, self.n_pad, self.n_pad * self.n_pad,
+                                                count, self.bits.data_ptr(), self.n, self.work.data_ptr(),
+                                                self.info.data_ptr(), stream),
+                "rdb_invert_batched_bits")
+
+    def stage_invert_generic(self, count: int, stream: int) -> None:
+        """K2 through the generic entry point (block pattern by scanning M)."""
         L.check(L.lib().rdb_invert_batched(self.m.data_ptr(), self.n_pad, self.n_pad, self.n_pad * self.n_pad,
                                            count, self.work.data_ptr(), self.info.data_ptr(), stream),
                 "rdb_invert_batched")
@@ -159,11 +167,65 @@ def d8_range_errors(counters: torch.Tensor) -> np.ndarray:
     return np.nonzero(c)[0]
 
 
-LAUNCHES_PER_CALL_FIXED = 2  # K1 + K3; K2 adds 3 per panel
+PLAN_MAX_NT = 64  # block-sparse plan limit (csrc/gj_invert.cu PLAN_MAX_NT)
+SPLIT_MIN_BATCH, SPLIT_PARTS = 64, 2  # csrc/gj_invert.cu defaults (RDB_GJ_SPLIT_MIN / RDB_GJ_SPLIT_PARTS)
 
 
-def launches_per_call(n: int) -> int:
-    return LAUNCHES_PER_CALL_FIXED + 3 * (L.pad_to_nb(n) // L.RDB_NB)
+def launches_per_call(n: int, batch: int) -> int:
+    """Kernels one rdb_apsp_bits_batched[_d8] call launches with the default
+    knobs: K1, the block-pattern kernel, per sub-batch the plan kernel and
+    3 per panel (P1, P2, U), and K3."""
+    nt = L.pad_to_nb(n) // L.RDB_NB
+    parts = SPLIT_PARTS if batch >= SPLIT_MIN_BATCH and batch >= 4 * SPLIT_PARTS else 1
+    plan = batch > 1 and nt <= PLAN_MAX_NT
+    return 2 + (1 + parts if plan else 0) + parts * 3 * nt
+
+
+def block_pattern(bits: np.ndarray, n: int) -> np.ndarray:
+    """Host restatement of block_pattern_bits_kernel: (batch, nt, nt) bool,
+    block (I, J) holds an edge (bit-packed rows as rdb_build_m_bits takes them)."""
+    bits = np.asarray(bits).view(np.uint32)
+    batch = bits.shape[0]
+    nt = L.pad_to_nb(n) // L.RDB_NB
+    wpr = (n + 31) // 32
+    words = bits.reshape(batch, n, wpr)
+    q = L.RDB_NB // 32
+    pad = nt * q - wpr
+    nzw = np.concatenate([words != 0, np.zeros((batch, n, pad), bool)], axis=2)
+    per_row = nzw.reshape(batch, n, nt, q).any(axis=3)  # (batch, n, nt)
+    rows = np.concatenate([per_row, np.zeros((batch, nt * L.RDB_NB - n, nt), bool)], axis=1)
+    return rows.reshape(batch, nt, L.RDB_NB, nt).any(axis=2)
+
+
+def gj_plan_tiles(pattern: np.ndarray) -> np.ndarray:
+    """Host restatement of gj_plan_kernel's symbolic Gauss-Jordan
+    (csrc/gj_invert.cu): per matrix, the number of 128 x 128 x 128 tile
+    products each kernel family executes, columns (P1, P2, U). Step p: P2
+    tiles = non-zero blocks A_pJ (J != p); U tiles = non-zero A_Ip (I != p)
+    times (that + 1 for the panel column); fill A_IJ |= A_Ip & A_pJ.
+    A dense pattern gives (nt, nt(nt-1), nt^2(nt-1)): nt^3 tiles = 2 n^3 flop."""
+    S = np.array(pattern, dtype=bool, copy=True)
+    batch, nt, _ = S.shape
+    idx = np.arange(nt)
+    S[:, idx, idx] = True
+    out = np.zeros((batch, 3), np.int64)
+    out[:, 0] = nt
+    for k in range(nt):
+        rowp = S[:, k, :] & (idx != k)
+        colp = S[:, :, k] & (idx != k)
+        nrp = rowp.sum(axis=1)
+        out[:, 1] += nrp
+        out[:, 2] += colp.sum(axis=1) * (nrp + 1)
+        S |= colp[:, :, None] & rowp[:, None, :]
+    return out
+
+
+def executed_flops(bits: np.ndarray, n: int) -> float:
+    """FP64 flop the block-sparse K2 executes on this batch (2 * 128^3 per tile)."""
+    nt = L.pad_to_nb(n) // L.RDB_NB
+    tiles = gj_plan_tiles(block_pattern(bits, n)) if (np.asarray(bits).shape[0] > 1 and nt <= PLAN_MAX_NT) \
+        else np.full((np.asarray(bits).shape[0], 1), nt**3)
+    return float(tiles.sum()) * 2.0 * L.RDB_NB**3
 
 
 def check_infos(infos: list[L.PivotInfo], gammas: np.ndarray, first_index: int = 0) -> None:
@@ -274,14 +336,15 @@ class APSPBatchEngine:
                 L.check(lib.rdb_build_m_bits(bits[c0].data_ptr(), self.n, self.n_pad, cnt, gam[c0:].data_ptr(), 0.0,
                                              self.m.data_ptr(), self.n_pad, self.n_pad * self.n_pad, sh),
                         "rdb_build_m_bits")
-                L.check(lib.rdb_invert_batched(self.m.data_ptr(), self.n_pad, self.n_pad, self.n_pad * self.n_pad,
-                                               cnt, self.work.data_ptr(), info[c0 * 16 :].data_ptr(), sh),
-                        "rdb_invert_batched")
+                L.check(lib.rdb_invert_batched_bits(self.m.data_ptr(), self.n_pad, self.n_pad,
+                                                    self.n_pad * self.n_pad, cnt, bits[c0].data_ptr(), self.n,
+                                                    self.work.data_ptr(), info[c0 * 16 :].data_ptr(), sh),
+                        "rdb_invert_batched_bits")
                 # D slot s must have drained to the host (this batch's chunk
                 # idx-2, or the previous batch's last chunk in that slot)
                 self.cs.wait_event(self.copied[s])
                 log_ceil_call(self.m, self.n, cnt, gam[c0:], self.d[s], counters[c0:], sh)
-                self.launches += launches_per_call(self.n)
+                self.launches += launches_per_call(self.n, cnt)
                 self.computed[s].record(self.cs)
             with torch.cuda.stream(self.xs):
                 self.xs.wait_event(self.computed[s])

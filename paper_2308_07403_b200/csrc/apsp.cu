@@ -8,7 +8,7 @@
 
 namespace rdb {
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
-                   rdb_pivot_info* info, cudaStream_t st);
+                   rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits, int64_t n_bits);
 int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
                 const double* gammas, double gamma, uint8_t* d8_out, int64_t ldo, int64_t stride_o,
                 unsigned long long* counters, cudaStream_t st);
@@ -55,7 +55,7 @@ extern "C" int rdb_apsp_bits_batched(const uint32_t* bits, int64_t n, int64_t ba
   const int64_t stride = n_pad * n_pad;
   int rc = rdb_build_m_bits(bits, n, n_pad, batch, gammas, 0.0, mwork, n_pad, stride, stream);
   if (rc) return rc;
-  rc = rdb::invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st);
+  rc = rdb::invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n);
   if (rc) return rc;
   return rdb::log_ceil(mwork, n, n_pad, stride, batch, gammas, 0.0, nullptr, nullptr, d32, n, n * n,
                        nullptr, 0, counters, st);
@@ -72,7 +72,7 @@ extern "C" int rdb_apsp_bits_batched_d8(const uint32_t* bits, int64_t n, int64_t
   const int64_t stride = n_pad * n_pad;
   int rc = rdb_build_m_bits(bits, n, n_pad, batch, gammas, 0.0, mwork, n_pad, stride, stream);
   if (rc) return rc;
-  rc = rdb::invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st);
+  rc = rdb::invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n);
   if (rc) return rc;
   return rdb::log_ceil_d8(mwork, n, n_pad, stride, batch, gammas, 0.0, d8, n, n * n, counters, st);
 }

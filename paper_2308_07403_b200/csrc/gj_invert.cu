@@ -48,11 +48,21 @@ struct RowPanelSched {
   int64_t lda, stride;
   int nt, pt, batch;
   int* dyn = nullptr;  // dynamic tile counter (batched calls)
-  RDB_DEV int count() const { return batch * (nt - 1); }
+  // block-sparse plan (batched calls): tiles (g << 6 | J) of this step, *count_ptr of them
+  const int* list = nullptr;
+  const int* count_ptr = nullptr;
+  RDB_DEV int count() const { return list ? *count_ptr : batch * (nt - 1); }
   RDB_DEV eng::Tile tile(int t) const {
-    const int g = t / (nt - 1);
-    int J = t - g * (nt - 1);
-    J += (J >= pt);
+    int g, J;
+    if (list) {
+      const int e = list[t];
+      g = e >> 6;
+      J = e & 63;
+    } else {
+      g = t / (nt - 1);
+      J = t - g * (nt - 1);
+      J += (J >= pt);
+    }
     double* A = a + (int64_t)g * stride;
     double* rowp = A + (int64_t)pt * NB * lda + (int64_t)J * NB;
     eng::Tile T;
@@ -83,8 +93,19 @@ struct UpdateSched {
   // next panel's diagonal tile (pt+1, pt+1) alone, part 2 every other tile
   int part;
   int* dyn = nullptr;  // dynamic tile counter (batched calls)
-  RDB_DEV int count() const { return part == 0 ? batch * (nt - 1) * nt : (part == 1 ? 1 : (nt - 1) * nt - 1); }
+  // block-sparse plan (batched calls, part 0): entries {g << 12 | I << 6 | J,
+  // wait target of the panel-column tile}, *count_ptr of them (gj_plan_kernel)
+  const int2* list = nullptr;
+  const int* count_ptr = nullptr;
+  RDB_DEV int count() const {
+    if (list) return *count_ptr;
+    return part == 0 ? batch * (nt - 1) * nt : (part == 1 ? 1 : (nt - 1) * nt - 1);
+  }
   RDB_DEV eng::Tile tile(int t) const {
+    if (list) {
+      const int2 e = list[t];
+      return make(e.x >> 12, (e.x >> 6) & 63, e.x & 63, e.y);
+    }
     // (g, row index I' over the rows other than pt, column index jj in the
     // order pt+1, ..., nt-1, 0, ..., pt: the panel column comes last)
     int g = 0, Ir, jj;
@@ -114,6 +135,12 @@ struct UpdateSched {
     const int I = Ir + (Ir >= pt);
     int J = pt + 1 + jj;
     if (J >= nt) J -= nt;
+    // completed steps j < pt touched row block I unless j == I
+    const int base = (pt - (I < pt ? 1 : 0)) * (nt - 1);
+    return make(g, I, J, base + (nt - 1));
+  }
+  // tile (I, J) of matrix g; wait_target applies to the panel-column tile J == pt
+  RDB_DEV eng::Tile make(int g, int I, int J, int wait_target) const {
     double* A = a + (int64_t)g * stride;
     eng::Tile T;
     T.a_col = pt * NB;  // A operand: A_Ip
@@ -127,13 +154,11 @@ struct UpdateSched {
     T.nk = NB / eng::BK;
     T.neg = 1;
     int* c = cnt + (int64_t)g * nt + I;
-    // completed steps j < pt touched row block I unless j == I
-    const int base = (pt - (I < pt ? 1 : 0)) * (nt - 1);
     if (J == pt) {
       T.mode = eng::EPI_STORE;
       T.signal = nullptr;
       T.wait = c;
-      T.wait_target = base + (nt - 1);
+      T.wait_target = wait_target;
     } else {
       T.mode = eng::EPI_REDUCE;
       T.signal = c;
@@ -236,6 +261,161 @@ int sm_count() {
   return g_sms > 0 ? g_sms : 148;
 }
 
+// ------------------------------------------------------------------ block-sparse plan (batched calls)
+// Symbolic Gauss-Jordan on the NB x NB block pattern. blk[g][I] bit J = block
+// (I, J) of matrix g may be non-zero (a superset of the numerical pattern).
+// Step p: P2 touches A_pJ only where blk[p] has bit J; the update A_IJ +=
+// -(A_Ip A_pJ) only where A_Ip and A_pJ are both non-zero blocks, and A_Ip =
+// -(A_Ip D) only where A_Ip is. A skipped tile would add an exact zero
+// (C + -0 == C) or store one, so the results are those of the dense schedule
+// (up to the sign of zero entries). The pattern fills as A_IJ |= A_Ip & A_pJ.
+// Banded matrices (the directed lattices of config 2: bandwidth = grid side)
+// keep whole blocks zero until late steps and skip about half of the tiles.
+constexpr int PLAN_MAX_NT = 64;
+
+struct PlanPart {
+  const unsigned long long* blk;  // [batch][nt] row masks
+  int* counts;                    // [2][nt]: P2 tiles, update tiles per step
+  int* rp;                        // [nt][batch * (nt - 1)] P2 entries g << 6 | J
+  int2* up;                       // [nt][batch * (nt - 1) * nt] update entries
+};
+
+// One CTA: thread = matrix (chunks of blockDim.x); block-wide prefix sums per
+// step give every matrix its slot in the step's tile lists (matrix order;
+// within a matrix, row blocks ascending, columns pt+1, ..., pt-1 and the
+// panel column last, as in the dense order, so waits point only backwards).
+__global__ void __launch_bounds__(1024, 1)
+    gj_plan_kernel(const unsigned long long* __restrict__ blk, int batch, int nt, int* __restrict__ counts,
+                   int* __restrict__ rp, int2* __restrict__ up) {
+  __shared__ int s_carry[2][PLAN_MAX_NT];
+  __shared__ int s_warp[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
+  for (int k = tid; k < nt; k += blockDim.x) s_carry[0][k] = s_carry[1][k] = 0;
+  __syncthreads();
+  const int64_t rp_cap = (int64_t)batch * (nt - 1), up_cap = (int64_t)batch * (nt - 1) * nt;
+  for (int g0 = 0; g0 < batch; g0 += blockDim.x) {
+    const int g = g0 + tid;
+    const bool act = g < batch;
+    unsigned long long S[PLAN_MAX_NT];
+    int cum[PLAN_MAX_NT];  // signals row block I has received so far (its in-kernel counter)
+    for (int I = 0; I < nt; ++I) {
+      S[I] = act ? (blk[(int64_t)g * nt + I] | (1ull << I)) : 0ull;
+      cum[I] = 0;
+    }
+    for (int k = 0; k < nt; ++k) {
+      const unsigned long long pbit = 1ull << k;
+      const unsigned long long rowp = S[k] & ~pbit;
+      unsigned long long colp = 0;
+      for (int I = 0; I < nt; ++I)
+        if (I != k && (S[I] & pbit)) colp |= 1ull << I;
+      const int nrp = __popcll(rowp), nup = __popcll(colp) * (nrp + 1);
+      int xr = nrp, xu = nup;  // inclusive warp scan
+      for (int o = 1; o < 32; o <<= 1) {
+        const int yr = __shfl_up_sync(0xffffffffu, xr, o), yu = __shfl_up_sync(0xffffffffu, xu, o);
+        if (lane >= o) {
+          xr += yr;
+          xu += yu;
+        }
+      }
+      if (lane == 31) {
+        s_warp[0][wid] = xr;
+        s_warp[1][wid] = xu;
+      }
+      __syncthreads();
+      if (wid == 0) {
+        int vr = lane < nw ? s_warp[0][lane] : 0, vu = lane < nw ? s_warp[1][lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int yr = __shfl_up_sync(0xffffffffu, vr, o), yu = __shfl_up_sync(0xffffffffu, vu, o);
+          if (lane >= o) {
+            vr += yr;
+            vu += yu;
+          }
+        }
+        s_warp[0][lane] = vr;
+        s_warp[1][lane] = vu;
+      }
+      __syncthreads();
+      if (act) {
+        int* rpl = rp + k * rp_cap + s_carry[0][k] + (wid ? s_warp[0][wid - 1] : 0) + xr - nrp;
+        int2* upl = up + k * up_cap + s_carry[1][k] + (wid ? s_warp[1][wid - 1] : 0) + xu - nup;
+        int c = 0;
+        for (int J = 0; J < nt; ++J)
+          if ((rowp >> J) & 1ull) rpl[c++] = (g << 6) | J;
+        c = 0;
+        for (int I = 0; I < nt; ++I) {
+          if (!((colp >> I) & 1ull)) continue;
+          for (int jj = 0; jj < nt; ++jj) {
+            int J = k + 1 + jj;
+            if (J >= nt) J -= nt;
+            if (J == k) {
+              upl[c++] = make_int2((g << 12) | (I << 6) | J, cum[I]);
+            } else if ((rowp >> J) & 1ull) {
+              ++cum[I];
+              upl[c++] = make_int2((g << 12) | (I << 6) | J, 0);
+            }
+          }
+          S[I] |= rowp;  // fill: A_IJ |= A_Ip & A_pJ
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s_carry[0][k] += s_warp[0][nw - 1];
+        s_carry[1][k] += s_warp[1][nw - 1];
+      }
+      __syncthreads();
+    }
+  }
+  for (int k = tid; k < nt; k += blockDim.x) {
+    counts[k] = s_carry[0][k];
+    counts[nt + k] = s_carry[1][k];
+  }
+}
+
+RDB_DEV unsigned long long warp_or64(unsigned long long m) {
+  const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
+  const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+// Block pattern from bit-packed adjacency (the rdb_build_m_bits input): a warp
+// per row, a 128-column block is 4 words. The plan adds the diagonal blocks.
+__global__ void block_pattern_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t batch, int nt,
+                                          unsigned long long* __restrict__ blk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpr = (n + 31) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < batch * n; w += nwarps) {
+    const uint32_t* row = bits + w * wpr;
+    unsigned long long m = 0;
+    for (int64_t q = lane; q < wpr; q += 32)
+      if (__ldg(row + q)) m |= 1ull << (q / (NB / 32));
+    m = warp_or64(m);
+    const int64_t b = w / n, i = w - b * n;
+    if (lane == 0 && m) atomicOr(&blk[b * nt + i / NB], m);
+  }
+}
+
+// Block pattern by scanning the matrices (generic batched calls): a warp per
+// block, rows in order, stopping at the first non-zero row (a dense block costs
+// a row or two; only zero blocks are read in full). NaN counts as non-zero.
+__global__ void block_pattern_m_kernel(const double* __restrict__ a, int64_t lda, int64_t stride, int64_t batch,
+                                       int nt, unsigned long long* __restrict__ blk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t blocks = batch * nt * nt;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < blocks; w += nwarps) {
+    const int64_t b = w / (nt * nt);
+    const int I = (int)((w / nt) % nt), J = (int)(w % nt);
+    const double* p = a + b * stride + (int64_t)I * NB * lda + (int64_t)J * NB + 4 * lane;
+    bool nz = false;
+    for (int r = 0; r < NB && !nz; ++r) {
+      const double2 u = ldg2(p + (int64_t)r * lda), v = ldg2(p + (int64_t)r * lda + 2);
+      nz = __any_sync(0xffffffffu, u.x != 0.0 || u.y != 0.0 || v.x != 0.0 || v.y != 0.0);
+    }
+    if (lane == 0 && nz) atomicOr(&blk[b * nt + I], 1ull << J);
+  }
+}
+
 static unsigned persistent_grid(int64_t tiles) {
   const int64_t sms = sm_count();
   return (unsigned)(tiles < sms ? tiles : sms);
@@ -248,7 +428,8 @@ static int64_t wide_min_n();
 // (step 0); idx_base offsets the reported pivot indices (a diagonal sub-block
 // inverted as part of a larger matrix).
 static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
-                       rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base, int* dyn = nullptr) {
+                       rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base, int* dyn = nullptr,
+                       const PlanPart* plan = nullptr) {
   if (!a || !work || !info || n <= 0 || batch <= 0) return RDB_EINVAL;
   if (n % NB != 0 || lda < n || (lda & 1) || (batch > 1 && stride < n * lda)) return RDB_EINVAL;
   if (((uintptr_t)a & 15) || ((uintptr_t)work & 15)) return RDB_EINVAL;
@@ -264,6 +445,8 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   rc = make_ec_map(&cmap, a, n, n, lda, batch > 1 ? stride : n * lda, batch);
   if (rc) return rc;
   if (cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)batch * nt, st) != cudaSuccess) return RDB_ECUDA;
+  if (plan && (batch == 1 || nt > PLAN_MAX_NT)) plan = nullptr;
+  if (plan) gj_plan_kernel<<<1, 1024, 0, st>>>(plan->blk, (int)batch, nt, plan->counts, plan->rp, plan->up);
   // Single matrix: look-ahead. The next panel's column block is updated first
   // (part 1); the next P1 (one CTA, latency-bound) then runs on a side stream
   // on one SM while the rest of the update (part 2) uses the other SMs.
@@ -281,6 +464,10 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
                                                                            info, 0);
     if (nt == 1) break;
     RowPanelSched rp{a, lda, stride, nt, k, (int)batch, batch > 1 ? dyn : nullptr};
+    if (plan) {
+      rp.list = plan->rp + (int64_t)k * batch * (nt - 1);
+      rp.count_ptr = plan->counts + k;
+    }
     gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES, st>>>(
         amap, cmap, rp);
     if (lookahead && k + 1 < nt) {
@@ -300,6 +487,10 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
       cudaStreamWaitEvent(st, g_ev_p, 0);
     } else {
       UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch, 0, batch > 1 && dyn ? dyn + 1 : nullptr};
+      if (plan) {
+        up.list = plan->up + (int64_t)k * batch * (nt - 1) * nt;
+        up.count_ptr = plan->counts + nt + k;
+      }
       gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(
           amap, cmap, up);
     }
@@ -319,6 +510,35 @@ static cudaEvent_t g_fork = nullptr, g_join[MAX_PARTS] = {};
 static size_t counter_bytes(int64_t n_pad, int64_t batch) {
   const size_t nt = (size_t)((n_pad + NB - 1) / NB);
   return ((size_t)batch * nt * sizeof(int) + 255) & ~(size_t)255;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Batched workspace: row-block counters | dynamic tile counters (256 B) |
+// block-sparse plan (batch > 1 and nt <= PLAN_MAX_NT): pattern, per-part
+// counts, P2 lists, update lists.
+struct BatchWs {
+  size_t cnt, dyn, blk, counts, rp, up, total;
+  BatchWs(int64_t n_pad, int64_t batch) {
+    const size_t nt = (size_t)(n_pad / NB), b = (size_t)batch;
+    cnt = 0;
+    dyn = counter_bytes(n_pad, batch);
+    blk = dyn + (batch > 1 ? 256 : 0);
+    if (batch > 1 && nt <= (size_t)PLAN_MAX_NT && n_pad % NB == 0) {
+      counts = blk + align256(b * nt * sizeof(unsigned long long));
+      rp = counts + align256((size_t)MAX_PARTS * 2 * nt * sizeof(int));
+      up = rp + align256(b * nt * (nt - 1) * sizeof(int));
+      total = up + align256(b * nt * nt * (nt - 1) * sizeof(int2));
+    } else {
+      counts = rp = up = total = blk;
+    }
+  }
+  bool has_plan() const { return total > blk; }
+};
+
+static bool skip_enabled() {
+  const char* e = getenv("RDB_GJ_SKIP");  // A-B switch: 0 runs the dense schedule
+  return !(e && e[0] == '0');
 }
 
 static bool dyn_sched() {
@@ -343,12 +563,43 @@ static int split_parts() {
 // serialised here (enqueue only; the calls stay asynchronous).
 static std::mutex g_enqueue;
 
+// Batched calls (batch > 1, n <= 64 NB) run the block-sparse plan: the
+// pattern comes from the bit-packed adjacency when the caller has it (`bits`,
+// n_bits vertices: the rdb_apsp_bits_batched pipelines), else from a scan of
+// the matrices.
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
-                   rdb_pivot_info* info, cudaStream_t st) {
+                   rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits = nullptr, int64_t n_bits = 0) {
   std::lock_guard<std::mutex> guard(g_enqueue);
   if (batch == 1 && n >= wide_min_n() && n % (2 * NB) == 0 && a && work && info && lda >= n && !(lda & 1) &&
       !((uintptr_t)a & 15) && !((uintptr_t)work & 15))
     return invert_wide(a, n, lda, work, info, st);
+  const BatchWs ws(n, batch);
+  char* const wb = static_cast<char*>(work);
+  const bool use_plan = batch > 1 && ws.has_plan() && skip_enabled() && a && work && n % NB == 0 &&
+                        batch <= (1 << 19) && stride >= n * lda;
+  const int64_t ntl = n / NB;
+  unsigned long long* blk = use_plan ? reinterpret_cast<unsigned long long*>(wb + ws.blk) : nullptr;
+  if (use_plan) {
+    if (cudaMemsetAsync(blk, 0, (size_t)batch * ntl * sizeof(unsigned long long), st) != cudaSuccess)
+      return RDB_ECUDA;
+    if (bits) {
+      const int64_t want = (batch * n_bits + 7) / 8;
+      block_pattern_bits_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
+          bits, n_bits, batch, (int)ntl, blk);
+    } else {
+      const int64_t want = (batch * ntl * ntl + 7) / 8;
+      block_pattern_m_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
+          a, lda, stride, batch, (int)ntl, blk);
+    }
+  }
+  auto part_plan = [&](int i, int64_t lo) {
+    PlanPart pp;
+    pp.blk = blk + lo * ntl;
+    pp.counts = reinterpret_cast<int*>(wb + ws.counts) + 2 * ntl * i;
+    pp.rp = reinterpret_cast<int*>(wb + ws.rp) + lo * ntl * (ntl - 1);
+    pp.up = reinterpret_cast<int2*>(wb + ws.up) + lo * ntl * ntl * (ntl - 1);
+    return pp;
+  };
   const int parts = split_parts();
   if (batch >= split_min_batch() && batch >= 4 * parts && a && work && info && n % NB == 0 && stride >= n * lda) {
     if (!g_fork) {
@@ -363,21 +614,23 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     int64_t bound[MAX_PARTS + 1];
     for (int i = 0; i <= parts; ++i) bound[i] = i == parts ? batch : ((batch * i / parts) & ~(int64_t)3);
     // dynamic tile counters (2 per part) after the row-block counters
-    int* dyn = reinterpret_cast<int*>(static_cast<char*>(work) + counter_bytes(n, batch));
+    int* dyn = reinterpret_cast<int*>(wb + ws.dyn);
     if (cudaMemsetAsync(dyn, 0, 2 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
     cudaEventRecord(g_fork, st);
     int rc = RDB_OK;
     for (int i = 0; i < parts && rc == RDB_OK; ++i) {
       const int64_t lo = bound[i], cnt = bound[i + 1] - bound[i];
       cudaStreamWaitEvent(g_part[i], g_fork, 0);
+      const PlanPart pp = part_plan(i, lo);
       rc = invert_core(a + lo * stride, n, lda, stride, cnt, static_cast<char*>(work) + lo * nt * sizeof(int),
-                       info + lo, g_part[i], 1, 0, dyn_sched() ? dyn + 2 * i : nullptr);
+                       info + lo, g_part[i], 1, 0, dyn_sched() ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr);
       cudaEventRecord(g_join[i], g_part[i]);
     }
     for (int i = 0; i < parts; ++i) cudaStreamWaitEvent(st, g_join[i], 0);
     return rc;
   }
-  return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0);
+  const PlanPart pp = part_plan(0, 0);
+  return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, nullptr, use_plan ? &pp : nullptr);
 }
 
 // ------------------------------------------------------------------ wide (NB = 256) single matrix
@@ -700,7 +953,8 @@ using namespace rdb;
 
 extern "C" size_t rdb_invert_workspace_bytes(int64_t n_pad, int64_t batch) {
   if (n_pad <= 0 || batch <= 0) return 0;
-  const size_t counters = rdb::counter_bytes(n_pad, batch) + (batch > 1 ? 256 : 0);  // + dynamic tile counters
+  if (batch > 1) return rdb::BatchWs(n_pad, batch).total;  // counters | dynamic counters | block-sparse plan
+  const size_t counters = rdb::counter_bytes(n_pad, batch);
   if (batch == 1 && n_pad >= rdb::wide_min_n() && n_pad % rdb::WB == 0)
     return (counters > 256 ? counters : 256) + rdb::wide_scratch_bytes(n_pad);  // counters | R | C
   return counters;
@@ -710,6 +964,13 @@ extern "C" int rdb_invert_batched(double* a, int64_t n_pad, int64_t lda, int64_t
                                   int64_t batch, void* work, rdb_pivot_info* info, void* stream) {
   return invert_batched(a, n_pad, lda, stride, batch, work, info,
                         static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int rdb_invert_batched_bits(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t batch,
+                                       const uint32_t* bits, int64_t n, void* work, rdb_pivot_info* info,
+                                       void* stream) {
+  if (!bits || n <= 0 || n > n_pad) return RDB_EINVAL;
+  return invert_batched(a, n_pad, lda, stride, batch, work, info, static_cast<cudaStream_t>(stream), bits, n);
 }
 
 extern "C" int rdb_invert(double* a, int64_t n_pad, int64_t lda, void* work, rdb_pivot_info* info,

@@ -255,8 +255,9 @@ def test_batch_split_and_dynamic_are_bitwise_neutral(cuda, monkeypatch):
     dev = torch.device("cuda")
     out = {}
     for name, env in (("default", {}), ("no_split", {"RDB_GJ_SPLIT_MIN": "0"}),
-                      ("static", {"RDB_GJ_DYNAMIC": "0"}), ("four", {"RDB_GJ_SPLIT_PARTS": "4"})):
-        for k in ("RDB_GJ_SPLIT_MIN", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_PARTS"):
+                      ("static", {"RDB_GJ_DYNAMIC": "0"}), ("four", {"RDB_GJ_SPLIT_PARTS": "4"}),
+                      ("dense", {"RDB_GJ_SKIP": "0"})):
+        for k in ("RDB_GJ_SPLIT_MIN", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_SKIP"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -268,5 +269,84 @@ def test_batch_split_and_dynamic_are_bitwise_neutral(cuda, monkeypatch):
         torch.cuda.synchronize()
         out[name] = buf.m.clone()
         del buf
-    for name in ("no_split", "static", "four"):
+    # the generic entry point finds the same block pattern by scanning M
+    for k in ("RDB_GJ_SPLIT_MIN", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_SKIP"):
+        monkeypatch.delenv(k, raising=False)
+    buf = B.BatchBuffers.allocate(1024, 128, dev)
+    buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+    buf.gammas.copy_(torch.from_numpy(gammas))
+    buf.stage_build(128, torch.cuda.current_stream().cuda_stream)
+    buf.stage_invert_generic(128, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    out["generic"] = buf.m.clone()
+    for name in ("no_split", "static", "four", "dense", "generic"):
         assert torch.equal(out[name], out["default"]), name
+
+
+def _structured_presents(n, rng):
+    """Graphs whose NB x NB block pattern stays partly zero through the
+    elimination: disconnected blocks, a band, a forward-only DAG, a single
+    long cycle, an empty graph, a hub, and a random sparse graph."""
+    out = []
+    # two components (vertex halves), each ER: off-diagonal blocks stay zero
+    p = np.zeros((n, n), bool)
+    h = n // 2
+    p[:h, :h] = rng.random((h, h)) < 0.05
+    p[h:, h:] = rng.random((n - h, n - h)) < 0.05
+    out.append(p)
+    # band of half-width 5 with random arcs
+    i, j = np.indices((n, n))
+    out.append((np.abs(i - j) <= 5) & (rng.random((n, n)) < 0.7))
+    # forward DAG (edge j -> i only for i > j): strictly lower triangular
+    out.append((i > j) & (rng.random((n, n)) < 0.01))
+    # one directed cycle through up to 600 vertices in a random order (with
+    # gamma = 0.5, y = 2^-d stays a normal double)
+    perm = rng.permutation(n)[:600]
+    c = np.zeros((n, n), bool)
+    c[perm[1:], perm[:-1]] = True
+    c[perm[0], perm[-1]] = True
+    out.append(c)
+    out.append(np.zeros((n, n), bool))
+    hub = np.zeros((n, n), bool)  # vertex n-1 -> everyone, everyone -> vertex 0
+    hub[:, n - 1] = True
+    hub[0, :] = True
+    out.append(hub)
+    out.append(rng.random((n, n)) < 2.0 / n)
+    for q in out:
+        np.fill_diagonal(q, False)
+    return out
+
+
+@pytest.mark.parametrize("n", [300, 1024])
+def test_block_sparse_schedule_structured_graphs(cuda, monkeypatch, n):
+    # the block-sparse plan skips tiles of structurally zero blocks: D must
+    # equal the oracle and the dense schedule on graphs that exercise it
+    rng = np.random.default_rng(n)
+    presents = _structured_presents(n, rng) + [wl.lattice_present(int(np.sqrt(n)), 0.8, 5)] * (n == 1024)
+    # per-graph gains below each graph's critical gain that keep gamma^D_max a
+    # normal double (components, band, DAG, cycle: y = 2^-d exactly, empty,
+    # hub, sparse random, lattice)
+    gam = np.array([1e-3, 0.1, 0.05, 0.5, 0.5, 0.1, 0.1, 0.1][: len(presents)])
+    bits = np.stack([wl.pack_bits(q) for q in presents])
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("RDB_GJ_SKIP", mode)
+        outs[mode] = rb.rounded_r_distance_batch(bits, gam, n)
+    np.testing.assert_array_equal(outs["1"], outs["0"])
+    for b, q in enumerate(presents):
+        w = wl.weights_from_present(q)
+        r = orc.r_distance(orc.resolvent_y(w, gam[b]), gam[b])
+        ref = orc.d_to_int32(np.ceil(r))
+        # DAGs, cycles and sparse random graphs have pairs joined by a single
+        # path: y == gamma^d up to rounding, so R sits within ulps of an integer
+        # and ceil(R) is d or d + 1 depending on the last bit (the reference's
+        # own knife edge, DESIGN.md "Exactness"; K3 returns d for y == gamma^d).
+        # Exact everywhere else; on those entries D is one of the two.
+        with np.errstate(invalid="ignore"):
+            knife = np.isfinite(r) & (np.abs(r - np.round(r)) < 1e-9) & (r != 0)
+        got = outs["1"][b]
+        np.testing.assert_array_equal(got[~knife], ref[~knife], err_msg=f"graph {b}")
+        k = np.round(r[knife]).astype(np.int64)
+        assert np.isin(got[knife] - k, [0, 1]).all(), f"graph {b}"
+        if b == 3:  # the gamma = 0.5 cycle: y == 2^-d exactly, so D is the hop count
+            np.testing.assert_array_equal(got, orc.d_to_int32(orc.bfs_apsp(w)))
