@@ -374,8 +374,9 @@ def main():
 
     n_pad = buf.n_pad
     flops_per_graph = 2.0 * n_pad**3
-    # K2 skips the tiles of structurally zero blocks (block-sparse plan): the
-    # roofline uses the flop it executes; the dense-equivalent 2n^3 rate beside it
+    # K2 skips the tiles of structurally zero blocks and the zero k-chunks of the
+    # column panel (block-sparse plan): the roofline uses the flop it executes;
+    # the dense-equivalent 2n^3 rate beside it
     exec_flops = B.executed_flops(bits, N)
     inv_tflops = exec_flops / (t_inv * 1e-3) / 1e12
     dense_tflops = flops_per_graph * batch / (t_inv * 1e-3) / 1e12
@@ -476,8 +477,8 @@ def main():
                      "achieved": inv_tflops, "peak": peak, "unit": "TFLOP/s", "frac": inv_tflops / peak,
                      "traffic": ncu_traffic(), "traffic_unit": "bytes per K2 call (8 GJ steps x 3 kernels, whole batch)",
                      "traffic_source": "profiles/r01_ncu_full_cfg2.json", "peak_source": peak_src,
-                     "work_per_launch": f"{exec_flops:.4g} flop executed per K2 call = 2*128^3 per tile over the "
-                                        f"block-sparse plan's tiles ({exec_flops / (flops_per_graph * batch):.3f} of the "
+                     "work_per_launch": f"{exec_flops:.4g} flop executed per K2 call = 2*128*128*16 per k-chunk over "
+                                        f"the block-sparse plan's tiles and k-chunks ({exec_flops / (flops_per_graph * batch):.3f} of the "
                                         f"dense 2*n^3 = {flops_per_graph:.4g} flop per graph x {batch} graphs)"},
         "kernels_ms": {"K1_build_m_bits": t_build, "K2_invert": t_inv, "K3_log_ceil": t_log},
         "hbm_kernels": {"K1_GBps": build_bytes / (t_build * 1e-3) / 1e9, "K3_GBps": log_bytes / (t_log * 1e-3) / 1e9,

@@ -181,51 +181,66 @@ def launches_per_call(n: int, batch: int) -> int:
     return 2 + (1 + parts if plan else 0) + parts * 3 * nt
 
 
-def block_pattern(bits: np.ndarray, n: int) -> np.ndarray:
-    """Host restatement of block_pattern_bits_kernel: (batch, nt, nt) bool,
-    block (I, J) holds an edge (bit-packed rows as rdb_build_m_bits takes them)."""
+STRIPS = 8  # 16-column strips (engine k-chunks) per 128-column block
+
+
+def strip_pattern(bits: np.ndarray, n: int) -> np.ndarray:
+    """Host restatement of strip_pattern_bits_kernel: (batch, nt, nt) uint8,
+    bit s of [b, I, J] = rows of block I hold an edge in the 16-column strip
+    s of block J (bit-packed rows as rdb_build_m_bits takes them)."""
     bits = np.asarray(bits).view(np.uint32)
     batch = bits.shape[0]
     nt = L.pad_to_nb(n) // L.RDB_NB
     wpr = (n + 31) // 32
     words = bits.reshape(batch, n, wpr)
-    q = L.RDB_NB // 32
-    pad = nt * q - wpr
-    nzw = np.concatenate([words != 0, np.zeros((batch, n, pad), bool)], axis=2)
-    per_row = nzw.reshape(batch, n, nt, q).any(axis=3)  # (batch, n, nt)
-    rows = np.concatenate([per_row, np.zeros((batch, nt * L.RDB_NB - n, nt), bool)], axis=1)
-    return rows.reshape(batch, nt, L.RDB_NB, nt).any(axis=2)
+    halves = np.stack([(words & 0xFFFF) != 0, (words >> 16) != 0], axis=3).reshape(batch, n, 2 * wpr)
+    halves = np.concatenate([halves, np.zeros((batch, n, nt * STRIPS - 2 * wpr), bool)], axis=2)
+    rows = np.concatenate([halves, np.zeros((batch, nt * L.RDB_NB - n, nt * STRIPS), bool)], axis=1)
+    nz = rows.reshape(batch, nt, L.RDB_NB, nt, STRIPS).any(axis=2)  # (batch, I, J, strip)
+    return (nz * (1 << np.arange(STRIPS))).sum(axis=3).astype(np.uint8)
 
 
-def gj_plan_tiles(pattern: np.ndarray) -> np.ndarray:
+def gj_plan_chunks(pattern: np.ndarray) -> np.ndarray:
     """Host restatement of gj_plan_kernel's symbolic Gauss-Jordan
-    (csrc/gj_invert.cu): per matrix, the number of 128 x 128 x 128 tile
-    products each kernel family executes, columns (P1, P2, U). Step p: P2
-    tiles = non-zero blocks A_pJ (J != p); U tiles = non-zero A_Ip (I != p)
-    times (that + 1 for the panel column); fill A_IJ |= A_Ip & A_pJ.
-    A dense pattern gives (nt, nt(nt-1), nt^2(nt-1)): nt^3 tiles = 2 n^3 flop."""
-    S = np.array(pattern, dtype=bool, copy=True)
-    batch, nt, _ = S.shape
+    (csrc/gj_invert.cu) on (batch, nt, nt) strip masks: per matrix, the
+    128 x 128 x 16 k-chunks each kernel family executes, columns (P1, P2, U).
+    Step p: P2 runs every non-zero A_pJ (J != p) in full; U runs, for every
+    non-zero A_Ip (I != p), the tiles J in that set plus the panel column
+    over the k-chunks first..last non-zero strip of A_Ip; fill strips(A_IJ)
+    |= strips(A_pJ), then A_Ip and A_pp full. P1 counts as one full tile.
+    A dense pattern gives 8 nt^3 chunks = 2 n^3 flop."""
+    P = np.array(pattern, dtype=np.uint8, copy=True)
+    batch, nt, _ = P.shape
     idx = np.arange(nt)
-    S[:, idx, idx] = True
+    P[:, idx, idx] = 0xFF
     out = np.zeros((batch, 3), np.int64)
-    out[:, 0] = nt
+    out[:, 0] = nt * STRIPS
+    span = np.zeros(256, np.int64)
+    for m in range(1, 256):
+        nzb = [s for s in range(STRIPS) if m >> s & 1]
+        span[m] = nzb[-1] - nzb[0] + 1
     for k in range(nt):
-        rowp = S[:, k, :] & (idx != k)
-        colp = S[:, :, k] & (idx != k)
+        rowp = (P[:, k, :] != 0) & (idx != k)
+        colp = (P[:, :, k] != 0) & (idx != k)
         nrp = rowp.sum(axis=1)
-        out[:, 1] += nrp
-        out[:, 2] += colp.sum(axis=1) * (nrp + 1)
-        S |= colp[:, :, None] & rowp[:, None, :]
+        out[:, 1] += nrp * STRIPS
+        out[:, 2] += (span[P[:, :, k]] * colp).sum(axis=1) * (nrp + 1)
+        fill = np.where(colp[:, :, None] & rowp[:, None, :], P[:, k, None, :], 0).astype(np.uint8)
+        P |= fill
+        P[:, :, k] = np.where(colp, 0xFF, P[:, :, k])
+        P[:, k, k] = 0xFF
     return out
 
 
 def executed_flops(bits: np.ndarray, n: int) -> float:
-    """FP64 flop the block-sparse K2 executes on this batch (2 * 128^3 per tile)."""
+    """FP64 flop the block-sparse K2 executes on this batch (2 * 128 * 128 * 16 per k-chunk)."""
+    batch = np.asarray(bits).shape[0]
     nt = L.pad_to_nb(n) // L.RDB_NB
-    tiles = gj_plan_tiles(block_pattern(bits, n)) if (np.asarray(bits).shape[0] > 1 and nt <= PLAN_MAX_NT) \
-        else np.full((np.asarray(bits).shape[0], 1), nt**3)
-    return float(tiles.sum()) * 2.0 * L.RDB_NB**3
+    if batch > 1 and nt <= PLAN_MAX_NT:
+        chunks = gj_plan_chunks(strip_pattern(bits, n)).sum()
+    else:
+        chunks = batch * nt**3 * STRIPS
+    return float(chunks) * 2.0 * L.RDB_NB * L.RDB_NB * (L.RDB_NB // STRIPS)
 
 
 def check_infos(infos: list[L.PivotInfo], gammas: np.ndarray, first_index: int = 0) -> None:

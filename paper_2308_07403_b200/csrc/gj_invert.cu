@@ -34,12 +34,12 @@ using EC = eng::Default;  // engine warp layout
 
 __global__ void __launch_bounds__(p1::THREADS, 1)
     gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int64_t off, int idx0,
-                    rdb_pivot_info* __restrict__ info, int first) {
+                    rdb_pivot_info* __restrict__ info, int first, int64_t info_stride = 1) {
   // block at a + b*stride + off*(lda + 1); pivot indices recorded from idx0
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
   p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), a + b * stride + off * lda + off, lda, idx0,
-                    info + b, first);
+                    info + b * info_stride, first);
 }
 
 // ------------------------------------------------------------------ schedulers
@@ -94,7 +94,8 @@ struct UpdateSched {
   int part;
   int* dyn = nullptr;  // dynamic tile counter (batched calls)
   // block-sparse plan (batched calls, part 0): entries {g << 12 | I << 6 | J,
-  // wait target of the panel-column tile}, *count_ptr of them (gj_plan_kernel)
+  // wait target of the panel-column tile | first k-chunk << 16 | k-chunks << 20},
+  // *count_ptr of them (gj_plan_kernel)
   const int2* list = nullptr;
   const int* count_ptr = nullptr;
   RDB_DEV int count() const {
@@ -104,7 +105,12 @@ struct UpdateSched {
   RDB_DEV eng::Tile tile(int t) const {
     if (list) {
       const int2 e = list[t];
-      return make(e.x >> 12, (e.x >> 6) & 63, e.x & 63, e.y);
+      eng::Tile T = make(e.x >> 12, (e.x >> 6) & 63, e.x & 63, e.y & 0xFFFF);
+      const int c0 = (e.y >> 16) & 15, nk = e.y >> 20;  // the non-zero k-chunks of A_Ip
+      T.a_col += c0 * eng::BK;
+      T.b += (int64_t)c0 * eng::BK * T.ldb;
+      T.nk = nk;
+      return T;
     }
     // (g, row index I' over the rows other than pt, column index jj in the
     // order pt+1, ..., nt-1, 0, ..., pt: the panel column comes last)
@@ -261,23 +267,35 @@ int sm_count() {
   return g_sms > 0 ? g_sms : 148;
 }
 
+#define RDB_HOST_DEV __host__ __device__ __forceinline__
+
 // ------------------------------------------------------------------ block-sparse plan (batched calls)
-// Symbolic Gauss-Jordan on the NB x NB block pattern. blk[g][I] bit J = block
-// (I, J) of matrix g may be non-zero (a superset of the numerical pattern).
-// Step p: P2 touches A_pJ only where blk[p] has bit J; the update A_IJ +=
-// -(A_Ip A_pJ) only where A_Ip and A_pJ are both non-zero blocks, and A_Ip =
-// -(A_Ip D) only where A_Ip is. A skipped tile would add an exact zero
-// (C + -0 == C) or store one, so the results are those of the dense schedule
-// (up to the sign of zero entries). The pattern fills as A_IJ |= A_Ip & A_pJ.
-// Banded matrices (the directed lattices of config 2: bandwidth = grid side)
-// keep whole blocks zero until late steps and skip about half of the tiles.
+// Symbolic Gauss-Jordan on a strip pattern: pat[g][I][J] is an 8-bit mask of
+// the 16-column strips (the engine's k-chunks) of block (I, J) of matrix g
+// that may hold non-zeros (a superset of the numerical pattern; 0 = the block
+// is zero). Step p:
+//   P2   A_pJ = D A_pJ            only where block (p, J) is non-zero;
+//   U    A_IJ += -(A_Ip A_pJ)     only where A_Ip and A_pJ are non-zero, and
+//        A_Ip = -(A_Ip D)         only where A_Ip is, both over the k-chunks
+//        [first, last] non-zero strip of A_Ip only;
+// fill: strips(A_IJ) |= strips(A_pJ) (D A_pJ keeps A_pJ's zero columns, D is
+// invertible); A_Ip and A_pp become full (D is treated as dense). A skipped
+// tile or chunk would add exact zeros (C + -0 == C) or store them, so results
+// are those of the dense schedule (up to the sign of zero entries). Banded
+// matrices (the directed lattices of config 2: bandwidth = grid side 32) keep
+// whole blocks zero until late steps, and the already-eliminated part of
+// their column panels has non-zeros only in the strips that couple to the
+// next grid rows: about 1/4 of the k-chunks of 1/2 of the tiles remain.
 constexpr int PLAN_MAX_NT = 64;
 
+RDB_HOST_DEV int pat_ld(int nt) { return (nt + 3) & ~3; }  // bytes per pattern row (32-bit atomics)
+
 struct PlanPart {
-  const unsigned long long* blk;  // [batch][nt] row masks
-  int* counts;                    // [2][nt]: P2 tiles, update tiles per step
-  int* rp;                        // [nt][batch * (nt - 1)] P2 entries g << 6 | J
-  int2* up;                       // [nt][batch * (nt - 1) * nt] update entries
+  unsigned char* pat;  // strip masks: pat[g * pat_stride + I * pat_ld(nt) + J] (updated in place by the plan)
+  int64_t pat_stride;
+  int* counts;  // [2][nt]: P2 tiles, update tiles per step
+  int* rp;      // [nt][batch * (nt - 1)] P2 entries g << 6 | J
+  int2* up;     // [nt][batch * (nt - 1) * nt] update entries {g << 12 | I << 6 | J, wait | c0 << 16 | nk << 20}
 };
 
 // One CTA: thread = matrix (chunks of blockDim.x); block-wide prefix sums per
@@ -285,29 +303,32 @@ struct PlanPart {
 // within a matrix, row blocks ascending, columns pt+1, ..., pt-1 and the
 // panel column last, as in the dense order, so waits point only backwards).
 __global__ void __launch_bounds__(1024, 1)
-    gj_plan_kernel(const unsigned long long* __restrict__ blk, int batch, int nt, int* __restrict__ counts,
+    gj_plan_kernel(unsigned char* __restrict__ pat, int64_t pat_stride, int batch, int nt, int* __restrict__ counts,
                    int* __restrict__ rp, int2* __restrict__ up) {
   __shared__ int s_carry[2][PLAN_MAX_NT];
   __shared__ int s_warp[2][32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
+  const int ld = pat_ld(nt);
   for (int k = tid; k < nt; k += blockDim.x) s_carry[0][k] = s_carry[1][k] = 0;
   __syncthreads();
   const int64_t rp_cap = (int64_t)batch * (nt - 1), up_cap = (int64_t)batch * (nt - 1) * nt;
   for (int g0 = 0; g0 < batch; g0 += blockDim.x) {
     const int g = g0 + tid;
     const bool act = g < batch;
-    unsigned long long S[PLAN_MAX_NT];
+    unsigned char* P = pat + (int64_t)(act ? g : 0) * pat_stride;
     int cum[PLAN_MAX_NT];  // signals row block I has received so far (its in-kernel counter)
     for (int I = 0; I < nt; ++I) {
-      S[I] = act ? (blk[(int64_t)g * nt + I] | (1ull << I)) : 0ull;
       cum[I] = 0;
+      if (act) P[I * ld + I] = 0xFF;  // the diagonal blocks (identity, then the pivot inverses)
     }
     for (int k = 0; k < nt; ++k) {
-      const unsigned long long pbit = 1ull << k;
-      const unsigned long long rowp = S[k] & ~pbit;
-      unsigned long long colp = 0;
-      for (int I = 0; I < nt; ++I)
-        if (I != k && (S[I] & pbit)) colp |= 1ull << I;
+      unsigned long long rowp = 0, colp = 0;
+      if (act) {
+        for (int J = 0; J < nt; ++J)
+          if (J != k && P[k * ld + J]) rowp |= 1ull << J;
+        for (int I = 0; I < nt; ++I)
+          if (I != k && P[I * ld + k]) colp |= 1ull << I;
+      }
       const int nrp = __popcll(rowp), nup = __popcll(colp) * (nrp + 1);
       int xr = nrp, xu = nup;  // inclusive warp scan
       for (int o = 1; o < 32; o <<= 1) {
@@ -344,17 +365,21 @@ __global__ void __launch_bounds__(1024, 1)
         c = 0;
         for (int I = 0; I < nt; ++I) {
           if (!((colp >> I) & 1ull)) continue;
+          const unsigned m = P[I * ld + k];  // non-zero k-chunks of A_Ip
+          const int c0 = __ffs(m) - 1, nk = 32 - __clz(m) - c0;
+          const int kr = (c0 << 16) | (nk << 20);
           for (int jj = 0; jj < nt; ++jj) {
             int J = k + 1 + jj;
             if (J >= nt) J -= nt;
             if (J == k) {
-              upl[c++] = make_int2((g << 12) | (I << 6) | J, cum[I]);
+              upl[c++] = make_int2((g << 12) | (I << 6) | J, cum[I] | kr);
             } else if ((rowp >> J) & 1ull) {
               ++cum[I];
-              upl[c++] = make_int2((g << 12) | (I << 6) | J, 0);
+              upl[c++] = make_int2((g << 12) | (I << 6) | J, kr);
+              P[I * ld + J] |= P[k * ld + J];  // fill
             }
           }
-          S[I] |= rowp;  // fill: A_IJ |= A_Ip & A_pJ
+          P[I * ld + k] = 0xFF;  // A_Ip = -(A_Ip D)
         }
       }
       __syncthreads();
@@ -371,48 +396,53 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
-RDB_DEV unsigned long long warp_or64(unsigned long long m) {
-  const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
-  const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(m >> 32));
-  return ((unsigned long long)hi << 32) | lo;
-}
-
-// Block pattern from bit-packed adjacency (the rdb_build_m_bits input): a warp
-// per row, a 128-column block is 4 words. The plan adds the diagonal blocks.
-__global__ void block_pattern_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t batch, int nt,
-                                          unsigned long long* __restrict__ blk) {
+// Strip pattern from bit-packed adjacency (the rdb_build_m_bits input): a
+// warp per row; word q covers strips 2q, 2q + 1 (block q / 4). Masks of four
+// consecutive blocks share a 32-bit word (pat_ld pads rows to 4 bytes).
+__global__ void strip_pattern_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t batch, int nt,
+                                          unsigned char* __restrict__ pat) {
   const int lane = threadIdx.x & 31;
+  const int ld = pat_ld(nt);
   const int64_t wpr = (n + 31) / 32;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < batch * n; w += nwarps) {
-    const uint32_t* row = bits + w * wpr;
-    unsigned long long m = 0;
-    for (int64_t q = lane; q < wpr; q += 32)
-      if (__ldg(row + q)) m |= 1ull << (q / (NB / 32));
-    m = warp_or64(m);
     const int64_t b = w / n, i = w - b * n;
-    if (lane == 0 && m) atomicOr(&blk[b * nt + i / NB], m);
+    const uint32_t* row = bits + w * wpr;
+    unsigned* dst = reinterpret_cast<unsigned*>(pat + (b * nt + i / NB) * ld);
+    for (int64_t q0 = 0; q0 < wpr; q0 += 32) {
+      const int64_t q = q0 + lane;
+      const uint32_t v = q < wpr ? __ldg(row + q) : 0u;
+      // block J = q / 4 gets bits 2 (q % 4) + {0, 1}; 16 words (4 blocks) per 32-bit mask word
+      unsigned m = ((v & 0xFFFFu) ? 1u : 0u) | ((v >> 16) ? 2u : 0u);
+      m <<= 2 * (q & 3) + 8 * ((q >> 2) & 3);
+      // OR over the 16 lanes sharing a mask word
+      for (int o = 1; o < 16; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+      if ((lane & 15) == 0 && m) atomicOr(dst + (q >> 4), m);
+    }
   }
 }
 
-// Block pattern by scanning the matrices (generic batched calls): a warp per
-// block, rows in order, stopping at the first non-zero row (a dense block costs
-// a row or two; only zero blocks are read in full). NaN counts as non-zero.
-__global__ void block_pattern_m_kernel(const double* __restrict__ a, int64_t lda, int64_t stride, int64_t batch,
-                                       int nt, unsigned long long* __restrict__ blk) {
+// Strip pattern by scanning the matrices (generic batched calls): a warp per
+// block, rows in order (lane l covers columns 4l .. 4l + 3 = strip l / 4),
+// stopping once all 8 strips are non-zero (a dense block costs a row or two;
+// zero blocks are read in full). NaN counts as non-zero.
+__global__ void strip_pattern_m_kernel(const double* __restrict__ a, int64_t lda, int64_t stride, int64_t batch,
+                                       int nt, unsigned char* __restrict__ pat) {
   const int lane = threadIdx.x & 31;
+  const int ld = pat_ld(nt);
   const int64_t blocks = batch * nt * nt;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < blocks; w += nwarps) {
     const int64_t b = w / (nt * nt);
     const int I = (int)((w / nt) % nt), J = (int)(w % nt);
     const double* p = a + b * stride + (int64_t)I * NB * lda + (int64_t)J * NB + 4 * lane;
-    bool nz = false;
-    for (int r = 0; r < NB && !nz; ++r) {
+    unsigned m = 0;
+    for (int r = 0; r < NB && m != 0xFFu; ++r) {
       const double2 u = ldg2(p + (int64_t)r * lda), v = ldg2(p + (int64_t)r * lda + 2);
-      nz = __any_sync(0xffffffffu, u.x != 0.0 || u.y != 0.0 || v.x != 0.0 || v.y != 0.0);
+      const bool nz = u.x != 0.0 || u.y != 0.0 || v.x != 0.0 || v.y != 0.0;
+      m |= __reduce_or_sync(0xffffffffu, nz ? 1u << (lane >> 2) : 0u);
     }
-    if (lane == 0 && nz) atomicOr(&blk[b * nt + I], 1ull << J);
+    if (lane == 0) pat[(b * nt + I) * ld + J] = (unsigned char)m;
   }
 }
 
@@ -429,7 +459,7 @@ static int64_t wide_min_n();
 // inverted as part of a larger matrix).
 static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                        rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base, int* dyn = nullptr,
-                       const PlanPart* plan = nullptr) {
+                       const PlanPart* plan = nullptr, int64_t info_stride = 1) {
   if (!a || !work || !info || n <= 0 || batch <= 0) return RDB_EINVAL;
   if (n % NB != 0 || lda < n || (lda & 1) || (batch > 1 && stride < n * lda)) return RDB_EINVAL;
   if (((uintptr_t)a & 15) || ((uintptr_t)work & 15)) return RDB_EINVAL;
@@ -446,7 +476,8 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   if (rc) return rc;
   if (cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)batch * nt, st) != cudaSuccess) return RDB_ECUDA;
   if (plan && (batch == 1 || nt > PLAN_MAX_NT)) plan = nullptr;
-  if (plan) gj_plan_kernel<<<1, 1024, 0, st>>>(plan->blk, (int)batch, nt, plan->counts, plan->rp, plan->up);
+  if (plan)
+    gj_plan_kernel<<<1, 1024, 0, st>>>(plan->pat, plan->pat_stride, (int)batch, nt, plan->counts, plan->rp, plan->up);
   // Single matrix: look-ahead. The next panel's column block is updated first
   // (part 1); the next P1 (one CTA, latency-bound) then runs on a side stream
   // on one SM while the rest of the update (part 2) uses the other SMs.
@@ -456,12 +487,13 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
     rc = side_resources(&side);
     if (rc) return rc;
   }
-  gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, idx_base, info, first);
+  gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, idx_base, info, first,
+                                                                       info_stride);
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
     if (k > 0 && !lookahead)
       gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, idx_base + p0,
-                                                                           info, 0);
+                                                                           info, 0, info_stride);
     if (nt == 1) break;
     RowPanelSched rp{a, lda, stride, nt, k, (int)batch, batch > 1 ? dyn : nullptr};
     if (plan) {
@@ -509,7 +541,7 @@ static cudaEvent_t g_fork = nullptr, g_join[MAX_PARTS] = {};
 
 static size_t counter_bytes(int64_t n_pad, int64_t batch) {
   const size_t nt = (size_t)((n_pad + NB - 1) / NB);
-  return ((size_t)batch * nt * sizeof(int) + 255) & ~(size_t)255;
+  return ((size_t)batch * nt * sizeof(int) + 64 + 255) & ~(size_t)255;  // + 16-byte alignment of the parts
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -525,7 +557,7 @@ struct BatchWs {
     dyn = counter_bytes(n_pad, batch);
     blk = dyn + (batch > 1 ? 256 : 0);
     if (batch > 1 && nt <= (size_t)PLAN_MAX_NT && n_pad % NB == 0) {
-      counts = blk + align256(b * nt * sizeof(unsigned long long));
+      counts = blk + align256(b * nt * (size_t)pat_ld((int)nt));
       rp = counts + align256((size_t)MAX_PARTS * 2 * nt * sizeof(int));
       up = rp + align256(b * nt * (nt - 1) * sizeof(int));
       total = up + align256(b * nt * nt * (nt - 1) * sizeof(int2));
@@ -578,23 +610,27 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   const bool use_plan = batch > 1 && ws.has_plan() && skip_enabled() && a && work && n % NB == 0 &&
                         batch <= (1 << 19) && stride >= n * lda;
   const int64_t ntl = n / NB;
-  unsigned long long* blk = use_plan ? reinterpret_cast<unsigned long long*>(wb + ws.blk) : nullptr;
+  const int64_t pld = pat_ld((int)ntl);
+  unsigned char* pat = use_plan ? reinterpret_cast<unsigned char*>(wb + ws.blk) : nullptr;
   if (use_plan) {
-    if (cudaMemsetAsync(blk, 0, (size_t)batch * ntl * sizeof(unsigned long long), st) != cudaSuccess)
-      return RDB_ECUDA;
+    if (cudaMemsetAsync(pat, 0, (size_t)(batch * ntl * pld), st) != cudaSuccess) return RDB_ECUDA;
     if (bits) {
       const int64_t want = (batch * n_bits + 7) / 8;
-      block_pattern_bits_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
-          bits, n_bits, batch, (int)ntl, blk);
+      strip_pattern_bits_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
+          bits, n_bits, batch, (int)ntl, pat);
     } else {
       const int64_t want = (batch * ntl * ntl + 7) / 8;
-      block_pattern_m_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
-          a, lda, stride, batch, (int)ntl, blk);
+      strip_pattern_m_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
+          a, lda, stride, batch, (int)ntl, pat);
     }
   }
-  auto part_plan = [&](int i, int64_t lo) {
+  // part i of `parts` = matrices i, i + parts, i + 2 parts, ... (interleaved:
+  // the parts get similar mixes of dense and block-sparse matrices whatever
+  // the batch order); lo = matrices in the parts before it (workspace slices)
+  auto part_plan = [&](int i, int parts_, int64_t lo) {
     PlanPart pp;
-    pp.blk = blk + lo * ntl;
+    pp.pat = pat + i * ntl * pld;
+    pp.pat_stride = parts_ * ntl * pld;
     pp.counts = reinterpret_cast<int*>(wb + ws.counts) + 2 * ntl * i;
     pp.rp = reinterpret_cast<int*>(wb + ws.rp) + lo * ntl * (ntl - 1);
     pp.up = reinterpret_cast<int2*>(wb + ws.up) + lo * ntl * ntl * (ntl - 1);
@@ -609,27 +645,26 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
           return RDB_ECUDA;
       if (cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess) return RDB_ECUDA;
     }
-    const int64_t nt = n / NB;
-    // sub-batch boundaries at multiples of 4 matrices: every part's counters stay 16-byte aligned
-    int64_t bound[MAX_PARTS + 1];
-    for (int i = 0; i <= parts; ++i) bound[i] = i == parts ? batch : ((batch * i / parts) & ~(int64_t)3);
-    // dynamic tile counters (2 per part) after the row-block counters
     int* dyn = reinterpret_cast<int*>(wb + ws.dyn);
     if (cudaMemsetAsync(dyn, 0, 2 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
     cudaEventRecord(g_fork, st);
     int rc = RDB_OK;
+    int64_t lo = 0;
     for (int i = 0; i < parts && rc == RDB_OK; ++i) {
-      const int64_t lo = bound[i], cnt = bound[i + 1] - bound[i];
+      const int64_t cnt = (batch - i + parts - 1) / parts;
       cudaStreamWaitEvent(g_part[i], g_fork, 0);
-      const PlanPart pp = part_plan(i, lo);
-      rc = invert_core(a + lo * stride, n, lda, stride, cnt, static_cast<char*>(work) + lo * nt * sizeof(int),
-                       info + lo, g_part[i], 1, 0, dyn_sched() ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr);
+      const PlanPart pp = part_plan(i, parts, lo);
+      // row-block counters of the part, 16-byte aligned (counter_bytes has the slack)
+      char* cw = wb + (((size_t)lo * ntl * sizeof(int) + 15) & ~(size_t)15);
+      rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, g_part[i], 1, 0,
+                       dyn_sched() ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr, parts);
       cudaEventRecord(g_join[i], g_part[i]);
+      lo += cnt;
     }
     for (int i = 0; i < parts; ++i) cudaStreamWaitEvent(st, g_join[i], 0);
     return rc;
   }
-  const PlanPart pp = part_plan(0, 0);
+  const PlanPart pp = part_plan(0, 1, 0);
   return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, nullptr, use_plan ? &pp : nullptr);
 }
 

@@ -10,45 +10,54 @@ from paper_2308_07403_b200 import batch as B
 from paper_2308_07403_b200 import workloads as wl
 
 
+def _strips(x, w):
+    """8-bit mask of the non-zero w-column strips of block x."""
+    return sum(1 << c for c in range(x.shape[1] // w) if np.any(x[:, c * w:(c + 1) * w] != 0))
+
+
 def _block_gj(m, b, skip):
     """Blocked Gauss-Jordan (the K2 step order: D = A_pp^-1, A_pJ = D A_pJ,
-    A_IJ -= A_Ip A_pJ, A_Ip = -A_Ip D) with block size b. With skip, tiles the
-    symbolic plan leaves out are not computed. Returns (inverse, tiles run,
-    symbolic pattern never missed a numerically non-zero panel block)."""
+    A_IJ -= A_Ip A_pJ, A_Ip = -A_Ip D) with block size b and b/8-wide
+    k-chunks. With skip, the tiles and k-chunks the symbolic plan leaves out
+    are not computed. Returns (inverse, chunks run per family, the symbolic
+    strip masks never missed a numerically non-zero strip)."""
     a = m.copy()
-    nt = a.shape[0] // b
+    nt, w = a.shape[0] // b, b // B.STRIPS
     blk = lambda I, J: a[I * b:(I + 1) * b, J * b:(J + 1) * b]  # noqa: E731
-    S = np.array([[np.any(blk(I, J) != 0) for J in range(nt)] for I in range(nt)])
-    S[np.arange(nt), np.arange(nt)] = True
-    ok, tiles = True, [0, 0, 0]
+    P = np.array([[_strips(blk(I, J), w) for J in range(nt)] for I in range(nt)])
+    P[np.arange(nt), np.arange(nt)] = 0xFF
+    ok, chunks = True, [0, 0, 0]
     for k in range(nt):
+        ok &= all((_strips(blk(I, J), w) & ~P[I, J]) == 0 for I in range(nt) for J in range(nt))
         d = np.linalg.inv(blk(k, k))
-        tiles[0] += 1
-        rowp = [J for J in range(nt) if J != k and S[k, J]]
-        colp = [I for I in range(nt) if I != k and S[I, k]]
-        for J in range(nt):
-            if J != k and np.any(blk(k, J) != 0) and not S[k, J]:
-                ok = False
-        for I in range(nt):
-            if I != k and np.any(blk(I, k) != 0) and not S[I, k]:
-                ok = False
+        chunks[0] += B.STRIPS
+        rowp = [J for J in range(nt) if J != k and P[k, J]]
+        colp = [I for I in range(nt) if I != k and P[I, k]]
         rows = colp if skip else [I for I in range(nt) if I != k]
         cols = rowp if skip else [J for J in range(nt) if J != k]
         for J in cols:
             a[k * b:(k + 1) * b, J * b:(J + 1) * b] = d @ blk(k, J)
-            tiles[1] += 1
+            chunks[1] += B.STRIPS
         for I in rows:
             aip = blk(I, k).copy()
+            if skip:  # only the k-chunks first..last non-zero strip of A_Ip
+                nzs = [c for c in range(B.STRIPS) if P[I, k] >> c & 1]
+                ks = slice(nzs[0] * w, (nzs[-1] + 1) * w)
+            else:
+                ks = slice(0, b)
+            nk = (ks.stop - ks.start) // w
             for J in cols:
-                a[I * b:(I + 1) * b, J * b:(J + 1) * b] -= aip @ blk(k, J)
-                tiles[2] += 1
-            a[I * b:(I + 1) * b, k * b:(k + 1) * b] = -(aip @ d)
-            tiles[2] += 1
+                a[I * b:(I + 1) * b, J * b:(J + 1) * b] -= aip[:, ks] @ blk(k, J)[ks, :]
+                chunks[2] += nk
+            a[I * b:(I + 1) * b, k * b:(k + 1) * b] = -(aip[:, ks] @ d[ks, :])
+            chunks[2] += nk
         a[k * b:(k + 1) * b, k * b:(k + 1) * b] = d
         for I in colp:
             for J in rowp:
-                S[I, J] = True
-    return a, tiles, ok
+                P[I, J] |= P[k, J]
+            P[I, k] = 0xFF
+        P[k, k] = 0xFF
+    return a, chunks, ok
 
 
 def _patterns(n, rng):
@@ -74,23 +83,24 @@ def test_skipping_planned_out_tiles_is_exact(name):
     m = np.eye(n) - 0.05 * p
     dense, td, ok_d = _block_gj(m, b, skip=False)
     sparse, ts, ok_s = _block_gj(m, b, skip=True)
-    assert ok_d and ok_s, "symbolic pattern missed a non-zero block"
+    assert ok_d and ok_s, "symbolic pattern missed a non-zero strip"
     np.testing.assert_array_equal(sparse, dense)
     nt = n // b
-    assert td == [nt, nt * (nt - 1), nt * nt * (nt - 1)]
-    # the host restatement of gj_plan_kernel counts the same tiles
-    pat = np.array([[p[I * b:(I + 1) * b, J * b:(J + 1) * b].any() for J in range(nt)] for I in range(nt)])
-    assert B.gj_plan_tiles(pat[None]).tolist() == [ts]
+    assert td == [8 * nt, 8 * nt * (nt - 1), 8 * nt * nt * (nt - 1)]
+    # the host restatement of gj_plan_kernel counts the same k-chunks
+    w = b // B.STRIPS
+    pat = np.array([[_strips(p[I * b:(I + 1) * b, J * b:(J + 1) * b], w) for J in range(nt)] for I in range(nt)])
+    assert B.gj_plan_chunks(pat[None].astype(np.uint8)).tolist() == [ts]
 
 
-def test_dense_pattern_is_nt_cubed():
+def test_dense_pattern_is_8_nt_cubed():
     nt = 8
-    t = B.gj_plan_tiles(np.ones((3, nt, nt), bool))
-    assert (t == [nt, nt * (nt - 1), nt * nt * (nt - 1)]).all()
-    assert t.sum(axis=1).tolist() == [nt**3] * 3
+    t = B.gj_plan_chunks(np.full((3, nt, nt), 0xFF, np.uint8))
+    assert (t == [8 * nt, 8 * nt * (nt - 1), 8 * nt * nt * (nt - 1)]).all()
+    assert t.sum(axis=1).tolist() == [8 * nt**3] * 3
 
 
-def test_block_pattern_from_bits_matches_dense_pattern():
+def test_strip_pattern_from_bits_matches_dense_pattern():
     rng = np.random.default_rng(1)
     for n in (300, 1024):
         i, j = np.indices((n, n))
@@ -98,17 +108,19 @@ def test_block_pattern_from_bits_matches_dense_pattern():
         for q in pres:
             np.fill_diagonal(q, False)
         bits = np.stack([wl.pack_bits(q) for q in pres])
-        got = B.block_pattern(bits, n)
+        got = B.strip_pattern(bits, n)
         nt = (n + 127) // 128
         qp = [np.pad(q, ((0, nt * 128 - n), (0, nt * 128 - n))) for q in pres]
-        want = np.stack([q.reshape(nt, 128, nt, 128).any(axis=(1, 3)) for q in qp])
+        want = np.stack([[[_strips(q[I * 128:(I + 1) * 128, J * 128:(J + 1) * 128], 16) for J in range(nt)]
+                          for I in range(nt)] for q in qp])
         np.testing.assert_array_equal(got, want)
 
 
-def test_cfg2_lattice_half_runs_about_half_the_tiles():
+def test_cfg2_lattice_half_runs_about_a_sixth_of_the_chunks():
     bits, _, seeds = wl.cfg2_batch(256)
-    t = B.gj_plan_tiles(B.block_pattern(bits, 1024)).sum(axis=1)
+    t = B.gj_plan_chunks(B.strip_pattern(bits, 1024)).sum(axis=1)
     kinds = np.array([k for k, _ in seeds])
-    assert (t[kinds == "er"] == 512).all()  # ER p = 0.02: every block holds edges
-    assert (t[kinds == "lattice"] < 300).all()  # bandwidth 32 << 128: ~52% of the tiles
+    assert (t[kinds == "er"] == 8 * 512).all()  # ER p = 0.02: every strip holds edges
+    # bandwidth 32: half of the tiles, and 2 of 8 k-chunks of the update tiles
+    assert (t[kinds == "lattice"] < 800).all()
     assert B.launches_per_call(1024, 256) == 2 + 3 + 2 * 3 * 8
