@@ -184,35 +184,51 @@ def launches_per_call(n: int, batch: int) -> int:
 STRIPS = 8  # 16-column strips (engine k-chunks) per 128-column block
 
 
+def _masks(nz: np.ndarray) -> np.ndarray:
+    return (nz * (1 << np.arange(STRIPS))).sum(axis=-1).astype(np.uint8)
+
+
 def strip_pattern(bits: np.ndarray, n: int) -> np.ndarray:
-    """Host restatement of strip_pattern_bits_kernel: (batch, nt, nt) uint8,
-    bit s of [b, I, J] = rows of block I hold an edge in the 16-column strip
-    s of block J (bit-packed rows as rdb_build_m_bits takes them)."""
+    """Host restatement of strip_pattern_bits_kernel: (batch, 2, nt, nt)
+    uint8; [b, 0, I, J] bit s = block (I, J) holds an edge in its 16-column
+    strip s, [b, 1, I, J] bit s = in its 16-row strip s (bit-packed rows as
+    rdb_build_m_bits takes them)."""
     bits = np.asarray(bits).view(np.uint32)
     batch = bits.shape[0]
     nt = L.pad_to_nb(n) // L.RDB_NB
+    nb = L.RDB_NB
     wpr = (n + 31) // 32
     words = bits.reshape(batch, n, wpr)
     halves = np.stack([(words & 0xFFFF) != 0, (words >> 16) != 0], axis=3).reshape(batch, n, 2 * wpr)
     halves = np.concatenate([halves, np.zeros((batch, n, nt * STRIPS - 2 * wpr), bool)], axis=2)
-    rows = np.concatenate([halves, np.zeros((batch, nt * L.RDB_NB - n, nt * STRIPS), bool)], axis=1)
-    nz = rows.reshape(batch, nt, L.RDB_NB, nt, STRIPS).any(axis=2)  # (batch, I, J, strip)
-    return (nz * (1 << np.arange(STRIPS))).sum(axis=3).astype(np.uint8)
+    rows = np.concatenate([halves, np.zeros((batch, nt * nb - n, nt * STRIPS), bool)], axis=1)
+    r5 = rows.reshape(batch, nt, STRIPS, nb // STRIPS, nt, STRIPS)  # (b, I, row strip, row, J, col strip)
+    col = _masks(r5.any(axis=(2, 3)))                               # (b, I, J)
+    row = _masks(r5.any(axis=(3, 5)).transpose(0, 1, 3, 2))        # (b, I, J)
+    return np.stack([col, row], axis=1)
 
 
 def gj_plan_chunks(pattern: np.ndarray) -> np.ndarray:
     """Host restatement of gj_plan_kernel's symbolic Gauss-Jordan
-    (csrc/gj_invert.cu) on (batch, nt, nt) strip masks: per matrix, the
-    128 x 128 x 16 k-chunks each kernel family executes, columns (P1, P2, U).
-    Step p: P2 runs every non-zero A_pJ (J != p) in full; U runs, for every
-    non-zero A_Ip (I != p), the tiles J in that set plus the panel column
-    over the k-chunks first..last non-zero strip of A_Ip; fill strips(A_IJ)
-    |= strips(A_pJ), then A_Ip and A_pp full. P1 counts as one full tile.
+    (csrc/gj_invert.cu): per matrix, the 128 x 128 x 16 k-chunks each kernel
+    family executes, columns (P1, P2, U). ``pattern``: (batch, 2, nt, nt)
+    column / row strip masks, or (batch, nt, nt) column masks (row masks then
+    full on every non-zero block, as strip_pattern_m_kernel). Step p: P2 runs
+    every non-zero A_pJ (J != p) over the k-chunks first..last non-zero row
+    strip of A_pJ; U runs, for every non-zero A_Ip (I != p), the tiles J of
+    P2 plus the panel column over the k-chunks first..last non-zero column
+    strip of A_Ip; fill C(A_IJ) |= C(A_pJ), R(A_IJ) |= R(A_Ip); then D A_pJ
+    has full rows, A_Ip D full columns, A_pp full. P1 counts as a full tile.
     A dense pattern gives 8 nt^3 chunks = 2 n^3 flop."""
-    P = np.array(pattern, dtype=np.uint8, copy=True)
-    batch, nt, _ = P.shape
+    pattern = np.asarray(pattern, dtype=np.uint8)
+    if pattern.ndim == 3:
+        pattern = np.stack([pattern, np.where(pattern != 0, 0xFF, 0).astype(np.uint8)], axis=1)
+    C = pattern[:, 0].copy()
+    R = pattern[:, 1].copy()
+    batch, nt, _ = C.shape
     idx = np.arange(nt)
-    P[:, idx, idx] = 0xFF
+    C[:, idx, idx] = 0xFF
+    R[:, idx, idx] = 0xFF
     out = np.zeros((batch, 3), np.int64)
     out[:, 0] = nt * STRIPS
     span = np.zeros(256, np.int64)
@@ -220,15 +236,17 @@ def gj_plan_chunks(pattern: np.ndarray) -> np.ndarray:
         nzb = [s for s in range(STRIPS) if m >> s & 1]
         span[m] = nzb[-1] - nzb[0] + 1
     for k in range(nt):
-        rowp = (P[:, k, :] != 0) & (idx != k)
-        colp = (P[:, :, k] != 0) & (idx != k)
+        rowp = (C[:, k, :] != 0) & (idx != k)
+        colp = (C[:, :, k] != 0) & (idx != k)
         nrp = rowp.sum(axis=1)
-        out[:, 1] += nrp * STRIPS
-        out[:, 2] += (span[P[:, :, k]] * colp).sum(axis=1) * (nrp + 1)
-        fill = np.where(colp[:, :, None] & rowp[:, None, :], P[:, k, None, :], 0).astype(np.uint8)
-        P |= fill
-        P[:, :, k] = np.where(colp, 0xFF, P[:, :, k])
-        P[:, k, k] = 0xFF
+        out[:, 1] += (span[R[:, k, :]] * rowp).sum(axis=1)
+        out[:, 2] += (span[C[:, :, k]] * colp).sum(axis=1) * (nrp + 1)
+        R[:, k, :] = np.where(rowp, 0xFF, R[:, k, :])
+        both = colp[:, :, None] & rowp[:, None, :]
+        C |= np.where(both, C[:, k, None, :], 0).astype(np.uint8)
+        R |= np.where(both, R[:, :, k, None], 0).astype(np.uint8)
+        C[:, :, k] = np.where(colp, 0xFF, C[:, :, k])
+        C[:, k, k] = R[:, k, k] = 0xFF
     return out
 
 

@@ -48,15 +48,19 @@ struct RowPanelSched {
   int64_t lda, stride;
   int nt, pt, batch;
   int* dyn = nullptr;  // dynamic tile counter (batched calls)
-  // block-sparse plan (batched calls): tiles (g << 6 | J) of this step, *count_ptr of them
+  // block-sparse plan (batched calls): tiles (g << 13 | first k-chunk << 10 |
+  // k-chunks << 6 | J) of this step, *count_ptr of them
   const int* list = nullptr;
   const int* count_ptr = nullptr;
   RDB_DEV int count() const { return list ? *count_ptr : batch * (nt - 1); }
   RDB_DEV eng::Tile tile(int t) const {
     int g, J;
+    int c0 = 0, nk = NB / eng::BK;
     if (list) {
       const int e = list[t];
-      g = e >> 6;
+      g = e >> 13;
+      c0 = (e >> 10) & 7;
+      nk = (e >> 6) & 15;
       J = e & 63;
     } else {
       g = t / (nt - 1);
@@ -66,15 +70,15 @@ struct RowPanelSched {
     double* A = a + (int64_t)g * stride;
     double* rowp = A + (int64_t)pt * NB * lda + (int64_t)J * NB;
     eng::Tile T;
-    T.a_col = pt * NB;  // A operand: D = A_pp
+    T.a_col = pt * NB + c0 * eng::BK;  // A operand: D = A_pp (columns of the k-chunks)
     T.a_row = pt * NB;
     T.a_mat = g;
-    T.b = rowp;
+    T.b = rowp + (int64_t)c0 * eng::BK * lda;  // the non-zero row strips of A_pJ
     T.ldb = lda;
     T.c_col = J * NB;
     T.c_row = pt * NB;
     T.c_mat = g;
-    T.nk = NB / eng::BK;
+    T.nk = nk;
     T.mode = eng::EPI_STORE;
     T.neg = 0;
     T.signal = nullptr;
@@ -270,16 +274,18 @@ int sm_count() {
 #define RDB_HOST_DEV __host__ __device__ __forceinline__
 
 // ------------------------------------------------------------------ block-sparse plan (batched calls)
-// Symbolic Gauss-Jordan on a strip pattern: pat[g][I][J] is an 8-bit mask of
+// Symbolic Gauss-Jordan on strip patterns: C[g][I][J] is an 8-bit mask of
 // the 16-column strips (the engine's k-chunks) of block (I, J) of matrix g
-// that may hold non-zeros (a superset of the numerical pattern; 0 = the block
-// is zero). Step p:
-//   P2   A_pJ = D A_pJ            only where block (p, J) is non-zero;
+// that may hold non-zeros, R[g][I][J] the same for its 16-row strips
+// (supersets of the numerical patterns; 0 = the block is zero). Step p:
+//   P2   A_pJ = D A_pJ            only where block (p, J) is non-zero, over
+//        the k-chunks first..last non-zero row strip of A_pJ;
 //   U    A_IJ += -(A_Ip A_pJ)     only where A_Ip and A_pJ are non-zero, and
 //        A_Ip = -(A_Ip D)         only where A_Ip is, both over the k-chunks
 //        [first, last] non-zero strip of A_Ip only;
-// fill: strips(A_IJ) |= strips(A_pJ) (D A_pJ keeps A_pJ's zero columns, D is
-// invertible); A_Ip and A_pp become full (D is treated as dense). A skipped
+// fill: C(A_IJ) |= C(A_pJ), R(A_IJ) |= R(A_Ip) (D A_pJ keeps A_pJ's zero
+// columns and A_Ip D A_Ip's zero rows, D is invertible); D A_pJ has full rows,
+// A_Ip D full columns and A_pp = D is full (D is treated as dense). A skipped
 // tile or chunk would add exact zeros (C + -0 == C) or store them, so results
 // are those of the dense schedule (up to the sign of zero entries). Banded
 // matrices (the directed lattices of config 2: bandwidth = grid side 32) keep
@@ -291,10 +297,12 @@ constexpr int PLAN_MAX_NT = 64;
 RDB_HOST_DEV int pat_ld(int nt) { return (nt + 3) & ~3; }  // bytes per pattern row (32-bit atomics)
 
 struct PlanPart {
-  unsigned char* pat;  // strip masks: pat[g * pat_stride + I * pat_ld(nt) + J] (updated in place by the plan)
+  // strip masks of matrix g: C at pat + g * pat_stride + I * pat_ld(nt) + J, R
+  // nt * pat_ld(nt) bytes after C (updated in place by the plan)
+  unsigned char* pat;
   int64_t pat_stride;
   int* counts;  // [2][nt]: P2 tiles, update tiles per step
-  int* rp;      // [nt][batch * (nt - 1)] P2 entries g << 6 | J
+  int* rp;      // [nt][batch * (nt - 1)] P2 entries g << 13 | c0 << 10 | nk << 6 | J
   int2* up;     // [nt][batch * (nt - 1) * nt] update entries {g << 12 | I << 6 | J, wait | c0 << 16 | nk << 20}
 };
 
@@ -315,11 +323,12 @@ __global__ void __launch_bounds__(1024, 1)
   for (int g0 = 0; g0 < batch; g0 += blockDim.x) {
     const int g = g0 + tid;
     const bool act = g < batch;
-    unsigned char* P = pat + (int64_t)(act ? g : 0) * pat_stride;
+    unsigned char* P = pat + (int64_t)(act ? g : 0) * pat_stride;  // column strips
+    unsigned char* Rs = P + nt * ld;                                 // row strips
     int cum[PLAN_MAX_NT];  // signals row block I has received so far (its in-kernel counter)
     for (int I = 0; I < nt; ++I) {
       cum[I] = 0;
-      if (act) P[I * ld + I] = 0xFF;  // the diagonal blocks (identity, then the pivot inverses)
+      if (act) P[I * ld + I] = Rs[I * ld + I] = 0xFF;  // the diagonal blocks (identity, then the pivot inverses)
     }
     for (int k = 0; k < nt; ++k) {
       unsigned long long rowp = 0, colp = 0;
@@ -361,7 +370,12 @@ __global__ void __launch_bounds__(1024, 1)
         int2* upl = up + k * up_cap + s_carry[1][k] + (wid ? s_warp[1][wid - 1] : 0) + xu - nup;
         int c = 0;
         for (int J = 0; J < nt; ++J)
-          if ((rowp >> J) & 1ull) rpl[c++] = (g << 6) | J;
+          if ((rowp >> J) & 1ull) {
+            const unsigned m = Rs[k * ld + J];  // non-zero k-chunks (row strips) of A_pJ
+            const int c0 = __ffs(m) - 1, nk = 32 - __clz(m) - c0;
+            rpl[c++] = (g << 13) | (c0 << 10) | (nk << 6) | J;
+            Rs[k * ld + J] = 0xFF;  // D A_pJ
+          }
         c = 0;
         for (int I = 0; I < nt; ++I) {
           if (!((colp >> I) & 1ull)) continue;
@@ -377,6 +391,7 @@ __global__ void __launch_bounds__(1024, 1)
               ++cum[I];
               upl[c++] = make_int2((g << 12) | (I << 6) | J, kr);
               P[I * ld + J] |= P[k * ld + J];  // fill
+              Rs[I * ld + J] |= Rs[I * ld + k];
             }
           }
           P[I * ld + k] = 0xFF;  // A_Ip = -(A_Ip D)
@@ -396,9 +411,10 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
-// Strip pattern from bit-packed adjacency (the rdb_build_m_bits input): a
-// warp per row; word q covers strips 2q, 2q + 1 (block q / 4). Masks of four
-// consecutive blocks share a 32-bit word (pat_ld pads rows to 4 bytes).
+// Strip patterns from bit-packed adjacency (the rdb_build_m_bits input): a
+// warp per row. Column strips: word q covers strips 2q, 2q + 1 of block q / 4;
+// masks of four consecutive blocks share a 32-bit word (pat_ld pads rows to 4
+// bytes). Row strips: bit (i % NB) / 16 in every block the row touches.
 __global__ void strip_pattern_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t batch, int nt,
                                           unsigned char* __restrict__ pat) {
   const int lane = threadIdx.x & 31;
@@ -408,7 +424,10 @@ __global__ void strip_pattern_bits_kernel(const uint32_t* __restrict__ bits, int
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < batch * n; w += nwarps) {
     const int64_t b = w / n, i = w - b * n;
     const uint32_t* row = bits + w * wpr;
-    unsigned* dst = reinterpret_cast<unsigned*>(pat + (b * nt + i / NB) * ld);
+    unsigned char* Pc = pat + b * 2 * nt * ld;
+    unsigned* dst = reinterpret_cast<unsigned*>(Pc + (i / NB) * ld);
+    unsigned* rdst = reinterpret_cast<unsigned*>(Pc + (nt + i / NB) * ld);
+    const unsigned rbit = 1u << ((i % NB) / 16);
     for (int64_t q0 = 0; q0 < wpr; q0 += 32) {
       const int64_t q = q0 + lane;
       const uint32_t v = q < wpr ? __ldg(row + q) : 0u;
@@ -417,15 +436,22 @@ __global__ void strip_pattern_bits_kernel(const uint32_t* __restrict__ bits, int
       m <<= 2 * (q & 3) + 8 * ((q >> 2) & 3);
       // OR over the 16 lanes sharing a mask word
       for (int o = 1; o < 16; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
-      if ((lane & 15) == 0 && m) atomicOr(dst + (q >> 4), m);
+      if ((lane & 15) == 0 && m) {
+        atomicOr(dst + (q >> 4), m);
+        unsigned r = 0;  // the row strip in each of the (up to 4) blocks this word touches
+        for (int j = 0; j < 4; ++j)
+          if ((m >> (8 * j)) & 0xFFu) r |= rbit << (8 * j);
+        atomicOr(rdst + (q >> 4), r);
+      }
     }
   }
 }
 
-// Strip pattern by scanning the matrices (generic batched calls): a warp per
+// Strip patterns by scanning the matrices (generic batched calls): a warp per
 // block, rows in order (lane l covers columns 4l .. 4l + 3 = strip l / 4),
-// stopping once all 8 strips are non-zero (a dense block costs a row or two;
-// zero blocks are read in full). NaN counts as non-zero.
+// stopping once all 8 column strips are non-zero (a dense block costs a row
+// or two; zero blocks are read in full). Row strips are not resolved: a
+// non-zero block gets all 8. NaN counts as non-zero.
 __global__ void strip_pattern_m_kernel(const double* __restrict__ a, int64_t lda, int64_t stride, int64_t batch,
                                        int nt, unsigned char* __restrict__ pat) {
   const int lane = threadIdx.x & 31;
@@ -442,7 +468,10 @@ __global__ void strip_pattern_m_kernel(const double* __restrict__ a, int64_t lda
       const bool nz = u.x != 0.0 || u.y != 0.0 || v.x != 0.0 || v.y != 0.0;
       m |= __reduce_or_sync(0xffffffffu, nz ? 1u << (lane >> 2) : 0u);
     }
-    if (lane == 0) pat[(b * nt + I) * ld + J] = (unsigned char)m;
+    if (lane == 0) {
+      pat[(b * 2 * nt + I) * ld + J] = (unsigned char)m;
+      pat[(b * 2 * nt + nt + I) * ld + J] = m ? 0xFF : 0;
+    }
   }
 }
 
@@ -557,7 +586,7 @@ struct BatchWs {
     dyn = counter_bytes(n_pad, batch);
     blk = dyn + (batch > 1 ? 256 : 0);
     if (batch > 1 && nt <= (size_t)PLAN_MAX_NT && n_pad % NB == 0) {
-      counts = blk + align256(b * nt * (size_t)pat_ld((int)nt));
+      counts = blk + align256(b * 2 * nt * (size_t)pat_ld((int)nt));  // column + row strip masks
       rp = counts + align256((size_t)MAX_PARTS * 2 * nt * sizeof(int));
       up = rp + align256(b * nt * (nt - 1) * sizeof(int));
       total = up + align256(b * nt * nt * (nt - 1) * sizeof(int2));
@@ -613,7 +642,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   const int64_t pld = pat_ld((int)ntl);
   unsigned char* pat = use_plan ? reinterpret_cast<unsigned char*>(wb + ws.blk) : nullptr;
   if (use_plan) {
-    if (cudaMemsetAsync(pat, 0, (size_t)(batch * ntl * pld), st) != cudaSuccess) return RDB_ECUDA;
+    if (cudaMemsetAsync(pat, 0, (size_t)(batch * 2 * ntl * pld), st) != cudaSuccess) return RDB_ECUDA;
     if (bits) {
       const int64_t want = (batch * n_bits + 7) / 8;
       strip_pattern_bits_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
@@ -629,8 +658,8 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   // the batch order); lo = matrices in the parts before it (workspace slices)
   auto part_plan = [&](int i, int parts_, int64_t lo) {
     PlanPart pp;
-    pp.pat = pat + i * ntl * pld;
-    pp.pat_stride = parts_ * ntl * pld;
+    pp.pat = pat + i * 2 * ntl * pld;
+    pp.pat_stride = parts_ * 2 * ntl * pld;
     pp.counts = reinterpret_cast<int*>(wb + ws.counts) + 2 * ntl * i;
     pp.rp = reinterpret_cast<int*>(wb + ws.rp) + lo * ntl * (ntl - 1);
     pp.up = reinterpret_cast<int2*>(wb + ws.up) + lo * ntl * ntl * (ntl - 1);

@@ -25,10 +25,13 @@ def _block_gj(m, b, skip):
     nt, w = a.shape[0] // b, b // B.STRIPS
     blk = lambda I, J: a[I * b:(I + 1) * b, J * b:(J + 1) * b]  # noqa: E731
     P = np.array([[_strips(blk(I, J), w) for J in range(nt)] for I in range(nt)])
+    R = np.array([[_strips(blk(I, J).T, w) for J in range(nt)] for I in range(nt)])
     P[np.arange(nt), np.arange(nt)] = 0xFF
+    R[np.arange(nt), np.arange(nt)] = 0xFF
     ok, chunks = True, [0, 0, 0]
     for k in range(nt):
         ok &= all((_strips(blk(I, J), w) & ~P[I, J]) == 0 for I in range(nt) for J in range(nt))
+        ok &= all((_strips(blk(I, J).T, w) & ~R[I, J]) == 0 for I in range(nt) for J in range(nt))
         d = np.linalg.inv(blk(k, k))
         chunks[0] += B.STRIPS
         rowp = [J for J in range(nt) if J != k and P[k, J]]
@@ -36,8 +39,14 @@ def _block_gj(m, b, skip):
         rows = colp if skip else [I for I in range(nt) if I != k]
         cols = rowp if skip else [J for J in range(nt) if J != k]
         for J in cols:
-            a[k * b:(k + 1) * b, J * b:(J + 1) * b] = d @ blk(k, J)
-            chunks[1] += B.STRIPS
+            if skip:  # only the k-chunks first..last non-zero row strip of A_pJ
+                nzs = [c for c in range(B.STRIPS) if R[k, J] >> c & 1]
+                ks = slice(nzs[0] * w, (nzs[-1] + 1) * w)
+            else:
+                ks = slice(0, b)
+            a[k * b:(k + 1) * b, J * b:(J + 1) * b] = d[:, ks] @ blk(k, J)[ks, :]
+            chunks[1] += (ks.stop - ks.start) // w
+            R[k, J] = 0xFF
         for I in rows:
             aip = blk(I, k).copy()
             if skip:  # only the k-chunks first..last non-zero strip of A_Ip
@@ -55,8 +64,9 @@ def _block_gj(m, b, skip):
         for I in colp:
             for J in rowp:
                 P[I, J] |= P[k, J]
+                R[I, J] |= R[I, k]
             P[I, k] = 0xFF
-        P[k, k] = 0xFF
+        P[k, k] = R[k, k] = 0xFF
     return a, chunks, ok
 
 
@@ -89,7 +99,8 @@ def test_skipping_planned_out_tiles_is_exact(name):
     assert td == [8 * nt, 8 * nt * (nt - 1), 8 * nt * nt * (nt - 1)]
     # the host restatement of gj_plan_kernel counts the same k-chunks
     w = b // B.STRIPS
-    pat = np.array([[_strips(p[I * b:(I + 1) * b, J * b:(J + 1) * b], w) for J in range(nt)] for I in range(nt)])
+    pat = np.array([[[_strips(p[I * b:(I + 1) * b, J * b:(J + 1) * b].T if r else p[I * b:(I + 1) * b, J * b:(J + 1) * b], w)
+                      for J in range(nt)] for I in range(nt)] for r in (0, 1)])
     assert B.gj_plan_chunks(pat[None].astype(np.uint8)).tolist() == [ts]
 
 
@@ -111,8 +122,9 @@ def test_strip_pattern_from_bits_matches_dense_pattern():
         got = B.strip_pattern(bits, n)
         nt = (n + 127) // 128
         qp = [np.pad(q, ((0, nt * 128 - n), (0, nt * 128 - n))) for q in pres]
-        want = np.stack([[[_strips(q[I * 128:(I + 1) * 128, J * 128:(J + 1) * 128], 16) for J in range(nt)]
-                          for I in range(nt)] for q in qp])
+        blkq = lambda q, I, J: q[I * 128:(I + 1) * 128, J * 128:(J + 1) * 128]  # noqa: E731
+        want = np.stack([[[[_strips(blkq(q, I, J).T if r else blkq(q, I, J), 16) for J in range(nt)]
+                           for I in range(nt)] for r in (0, 1)] for q in qp])
         np.testing.assert_array_equal(got, want)
 
 
