@@ -99,7 +99,7 @@ struct UpdateSched {
   int* dyn = nullptr;  // dynamic tile counter (batched calls)
   // block-sparse plan (batched calls, part 0): entries {g << 12 | I << 6 | J,
   // wait target of the panel-column tile | first k-chunk << 16 | k-chunks << 20},
-  // *count_ptr of them (gj_plan_kernel)
+  // *count_ptr of them (gj_plan_walk)
   const int2* list = nullptr;
   const int* count_ptr = nullptr;
   RDB_DEV int count() const {
@@ -298,143 +298,183 @@ RDB_HOST_DEV int pat_ld(int nt) { return (nt + 3) & ~3; }  // bytes per pattern 
 
 struct PlanPart {
   // strip masks of matrix g: C at pat + g * pat_stride + I * pat_ld(nt) + J, R
-  // nt * pat_ld(nt) bytes after C (updated in place by the plan)
+  // nt * pat_ld(nt) bytes after C
   unsigned char* pat;
   int64_t pat_stride;
   int* counts;  // [2][nt]: P2 tiles, update tiles per step
+  int* offs;    // [2][nt][batch]: per-matrix tile counts, then list offsets
   int* rp;      // [nt][batch * (nt - 1)] P2 entries g << 13 | c0 << 10 | nk << 6 | J
   int2* up;     // [nt][batch * (nt - 1) * nt] update entries {g << 12 | I << 6 | J, wait | c0 << 16 | nk << 20}
 };
 
-// One CTA: thread = matrix (chunks of blockDim.x); block-wide prefix sums per
-// step give every matrix its slot in the step's tile lists (matrix order;
-// within a matrix, row blocks ascending, columns pt+1, ..., pt-1 and the
-// panel column last, as in the dense order, so waits point only backwards).
-__global__ void __launch_bounds__(1024, 1)
-    gj_plan_kernel(unsigned char* __restrict__ pat, int64_t pat_stride, int batch, int nt, int* __restrict__ counts,
-                   int* __restrict__ rp, int2* __restrict__ up) {
-  __shared__ int s_carry[2][PLAN_MAX_NT];
-  __shared__ int s_warp[2][32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
+// The plan in three launches, all parallel over matrices: gj_plan_walk<false>
+// (a warp per matrix, lane = row block I and I + 32, the matrix's masks in
+// shared memory) counts each step's P2 and update tiles per matrix;
+// gj_plan_scan turns the counts into list offsets (matrix order) and totals;
+// gj_plan_walk<true> repeats the walk and writes the entries (within a
+// matrix: row blocks ascending, columns pt+1, ..., pt-1 and the panel column
+// last, as in the dense order, so waits point only backwards).
+RDB_DEV unsigned long long ballot64(bool lo, bool hi) {
+  return (unsigned long long)__ballot_sync(0xffffffffu, lo) | ((unsigned long long)__ballot_sync(0xffffffffu, hi) << 32);
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(1024)
+    gj_plan_walk(const unsigned char* __restrict__ pat, int64_t pat_stride, int batch, int nt,
+                 int* __restrict__ offs, int* __restrict__ rp, int2* __restrict__ up) {
+  // offs: [2][nt][batch] per-matrix counts (WRITE = false) / exclusive offsets (WRITE = true)
+  extern __shared__ __align__(16) unsigned char s_pat[];  // per warp: C then R, nt rows of ld bytes each
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (g >= batch) return;  // warp-uniform
   const int ld = pat_ld(nt);
-  for (int k = tid; k < nt; k += blockDim.x) s_carry[0][k] = s_carry[1][k] = 0;
-  __syncthreads();
+  const int gbytes = 2 * nt * ld;
+  unsigned char* C = s_pat + wid * gbytes;
+  unsigned char* R = C + nt * ld;
+  const unsigned char* src = pat + (int64_t)g * pat_stride;
+  for (int q = lane; q < gbytes / 4; q += 32)
+    reinterpret_cast<unsigned*>(C)[q] = reinterpret_cast<const unsigned*>(src)[q];
+  __syncwarp();
+  const int I0 = lane, I1 = lane + 32;
+  if (I0 < nt) C[I0 * ld + I0] = R[I0 * ld + I0] = 0xFF;  // the diagonal blocks
+  if (I1 < nt) C[I1 * ld + I1] = R[I1 * ld + I1] = 0xFF;
   const int64_t rp_cap = (int64_t)batch * (nt - 1), up_cap = (int64_t)batch * (nt - 1) * nt;
-  for (int g0 = 0; g0 < batch; g0 += blockDim.x) {
-    const int g = g0 + tid;
-    const bool act = g < batch;
-    unsigned char* P = pat + (int64_t)(act ? g : 0) * pat_stride;  // column strips
-    unsigned char* Rs = P + nt * ld;                                 // row strips
-    int cum[PLAN_MAX_NT];  // signals row block I has received so far (its in-kernel counter)
-    for (int I = 0; I < nt; ++I) {
-      cum[I] = 0;
-      if (act) P[I * ld + I] = Rs[I * ld + I] = 0xFF;  // the diagonal blocks (identity, then the pivot inverses)
-    }
-    for (int k = 0; k < nt; ++k) {
-      unsigned long long rowp = 0, colp = 0;
-      if (act) {
-        for (int J = 0; J < nt; ++J)
-          if (J != k && P[k * ld + J]) rowp |= 1ull << J;
-        for (int I = 0; I < nt; ++I)
-          if (I != k && P[I * ld + k]) colp |= 1ull << I;
+  int cum0 = 0, cum1 = 0;  // signals row blocks I0, I1 have received (their in-kernel counters)
+  for (int k = 0; k < nt; ++k) {
+    __syncwarp();
+    const unsigned long long rowp =
+        ballot64(I0 < nt && I0 != k && C[k * ld + I0], I1 < nt && I1 != k && C[k * ld + I1]);
+    const unsigned long long colp =
+        ballot64(I0 < nt && I0 != k && C[I0 * ld + k], I1 < nt && I1 != k && C[I1 * ld + k]);
+    const int nrp = __popcll(rowp);
+    if (!WRITE) {
+      if (lane == 0) {
+        offs[(int64_t)k * batch + g] = nrp;
+        offs[((int64_t)nt + k) * batch + g] = __popcll(colp) * (nrp + 1);
       }
-      const int nrp = __popcll(rowp), nup = __popcll(colp) * (nrp + 1);
-      int xr = nrp, xu = nup;  // inclusive warp scan
-      for (int o = 1; o < 32; o <<= 1) {
-        const int yr = __shfl_up_sync(0xffffffffu, xr, o), yu = __shfl_up_sync(0xffffffffu, xu, o);
-        if (lane >= o) {
-          xr += yr;
-          xu += yu;
+    } else {
+      // P2 tiles: lane J (J in rowp) over A_pJ's non-zero row strips
+      const int rbase = offs[(int64_t)k * batch + g];
+      const int ubase = offs[((int64_t)nt + k) * batch + g];
+      for (int h = 0; h < 2; ++h) {
+        const int J = h ? I1 : I0;
+        if (J < nt && ((rowp >> J) & 1ull)) {
+          const unsigned m = R[k * ld + J];
+          const int c0 = __ffs(m) - 1, nk = 32 - __clz(m) - c0;
+          rp[k * rp_cap + rbase + __popcll(rowp & ((1ull << J) - 1))] = (g << 13) | (c0 << 10) | (nk << 6) | J;
         }
       }
-      if (lane == 31) {
-        s_warp[0][wid] = xr;
-        s_warp[1][wid] = xu;
-      }
-      __syncthreads();
-      if (wid == 0) {
-        int vr = lane < nw ? s_warp[0][lane] : 0, vu = lane < nw ? s_warp[1][lane] : 0;
-        for (int o = 1; o < 32; o <<= 1) {
-          const int yr = __shfl_up_sync(0xffffffffu, vr, o), yu = __shfl_up_sync(0xffffffffu, vu, o);
-          if (lane >= o) {
-            vr += yr;
-            vu += yu;
-          }
-        }
-        s_warp[0][lane] = vr;
-        s_warp[1][lane] = vu;
-      }
-      __syncthreads();
-      if (act) {
-        int* rpl = rp + k * rp_cap + s_carry[0][k] + (wid ? s_warp[0][wid - 1] : 0) + xr - nrp;
-        int2* upl = up + k * up_cap + s_carry[1][k] + (wid ? s_warp[1][wid - 1] : 0) + xu - nup;
-        int c = 0;
-        for (int J = 0; J < nt; ++J)
-          if ((rowp >> J) & 1ull) {
-            const unsigned m = Rs[k * ld + J];  // non-zero k-chunks (row strips) of A_pJ
-            const int c0 = __ffs(m) - 1, nk = 32 - __clz(m) - c0;
-            rpl[c++] = (g << 13) | (c0 << 10) | (nk << 6) | J;
-            Rs[k * ld + J] = 0xFF;  // D A_pJ
-          }
-        c = 0;
-        for (int I = 0; I < nt; ++I) {
-          if (!((colp >> I) & 1ull)) continue;
-          const unsigned m = P[I * ld + k];  // non-zero k-chunks of A_Ip
+      // update tiles: lane I (I in colp) writes its row's nrp + 1 entries
+      for (int h = 0; h < 2; ++h) {
+        const int I = h ? I1 : I0;
+        if (I < nt && ((colp >> I) & 1ull)) {
+          int2* upl = up + k * up_cap + ubase + __popcll(colp & ((1ull << I) - 1)) * (nrp + 1);
+          const unsigned m = C[I * ld + k];  // non-zero k-chunks of A_Ip
           const int c0 = __ffs(m) - 1, nk = 32 - __clz(m) - c0;
           const int kr = (c0 << 16) | (nk << 20);
+          int& cum = h ? cum1 : cum0;
+          int c = 0;
           for (int jj = 0; jj < nt; ++jj) {
             int J = k + 1 + jj;
             if (J >= nt) J -= nt;
             if (J == k) {
-              upl[c++] = make_int2((g << 12) | (I << 6) | J, cum[I] | kr);
+              upl[c++] = make_int2((g << 12) | (I << 6) | J, cum | kr);
             } else if ((rowp >> J) & 1ull) {
-              ++cum[I];
+              ++cum;
               upl[c++] = make_int2((g << 12) | (I << 6) | J, kr);
-              P[I * ld + J] |= P[k * ld + J];  // fill
-              Rs[I * ld + J] |= Rs[I * ld + k];
             }
           }
-          P[I * ld + k] = 0xFF;  // A_Ip = -(A_Ip D)
         }
       }
-      __syncthreads();
-      if (tid == 0) {
-        s_carry[0][k] += s_warp[0][nw - 1];
-        s_carry[1][k] += s_warp[1][nw - 1];
-      }
-      __syncthreads();
     }
-  }
-  for (int k = tid; k < nt; k += blockDim.x) {
-    counts[k] = s_carry[0][k];
-    counts[nt + k] = s_carry[1][k];
+    __syncwarp();
+    // fill (rows I != k read only row k's C and their own R[I][k])
+    for (int h = 0; h < 2; ++h) {
+      const int I = h ? I1 : I0;
+      if (I < nt && ((colp >> I) & 1ull)) {
+        const unsigned char rik = R[I * ld + k];
+        for (int J = 0; J < nt; ++J)
+          if ((rowp >> J) & 1ull) {
+            C[I * ld + J] |= C[k * ld + J];
+            R[I * ld + J] |= rik;
+          }
+        C[I * ld + k] = 0xFF;  // A_Ip = -(A_Ip D)
+      }
+    }
+    __syncwarp();
+    for (int h = 0; h < 2; ++h) {  // D A_pJ
+      const int J = h ? I1 : I0;
+      if (J < nt && ((rowp >> J) & 1ull)) R[k * ld + J] = 0xFF;
+    }
   }
 }
 
+// One CTA: exclusive prefix sums of the 2 nt per-matrix count rows in place
+// (a warp per row); the totals go to counts[0 .. 2 nt).
+__global__ void __launch_bounds__(1024)
+    gj_plan_scan(int* __restrict__ offs, int batch, int nt, int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  for (int row = wid; row < 2 * nt; row += nw) {
+    int* v = offs + (int64_t)row * batch;
+    int carry = 0;
+    for (int g0 = 0; g0 < batch; g0 += 32) {
+      const int g = g0 + lane;
+      const int x = g < batch ? v[g] : 0;
+      int y = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      if (g < batch) v[g] = carry + y - x;
+      carry += __shfl_sync(0xffffffffu, y, 31);
+    }
+    if (lane == 0) counts[row] = carry;
+  }
+}
+
+// Host: warps per CTA of gj_plan_walk (shared memory holds one matrix's masks per warp).
+static int plan_warps(int nt) {
+  const int bytes = 2 * nt * pat_ld(nt);
+  int w = (48 * 1024) / bytes;
+  return w < 1 ? 1 : (w > 8 ? 8 : w);
+}
+
+static void launch_plan(const PlanPart& pp, int batch, int nt, cudaStream_t st) {
+  const int w = plan_warps(nt);
+  const unsigned grid = (unsigned)((batch + w - 1) / w);
+  const size_t smem = (size_t)w * 2 * nt * pat_ld(nt);
+  gj_plan_walk<false><<<grid, 32 * w, smem, st>>>(pp.pat, pp.pat_stride, batch, nt, pp.offs, pp.rp, pp.up);
+  gj_plan_scan<<<1, 32 * (2 * nt < 32 ? 2 * nt : 32), 0, st>>>(pp.offs, batch, nt, pp.counts);
+  gj_plan_walk<true><<<grid, 32 * w, smem, st>>>(pp.pat, pp.pat_stride, batch, nt, pp.offs, pp.rp, pp.up);
+}
+
 // Strip patterns from bit-packed adjacency (the rdb_build_m_bits input): a
-// warp per row. Column strips: word q covers strips 2q, 2q + 1 of block q / 4;
-// masks of four consecutive blocks share a 32-bit word (pat_ld pads rows to 4
-// bytes). Row strips: bit (i % NB) / 16 in every block the row touches.
+// warp per 16-row strip (ORed in registers, then one atomic per mask word).
+// Column strips: word q covers strips 2q, 2q + 1 of block q / 4; masks of four
+// consecutive blocks share a 32-bit word (pat_ld pads rows to 4 bytes). Row
+// strips: bit (i % NB) / 16 in every block the strip's rows touch.
 __global__ void strip_pattern_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t batch, int nt,
                                           unsigned char* __restrict__ pat) {
   const int lane = threadIdx.x & 31;
   const int ld = pat_ld(nt);
   const int64_t wpr = (n + 31) / 32;
+  const int64_t strips = (n + 15) / 16;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < batch * n; w += nwarps) {
-    const int64_t b = w / n, i = w - b * n;
-    const uint32_t* row = bits + w * wpr;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < batch * strips; w += nwarps) {
+    const int64_t b = w / strips, s16 = w - b * strips;
+    const int64_t i0 = s16 * 16, i1 = i0 + 16 < n ? i0 + 16 : n;
     unsigned char* Pc = pat + b * 2 * nt * ld;
-    unsigned* dst = reinterpret_cast<unsigned*>(Pc + (i / NB) * ld);
-    unsigned* rdst = reinterpret_cast<unsigned*>(Pc + (nt + i / NB) * ld);
-    const unsigned rbit = 1u << ((i % NB) / 16);
+    unsigned* dst = reinterpret_cast<unsigned*>(Pc + (i0 / NB) * ld);
+    unsigned* rdst = reinterpret_cast<unsigned*>(Pc + (nt + i0 / NB) * ld);
+    const unsigned rbit = 1u << ((i0 % NB) / 16);
     for (int64_t q0 = 0; q0 < wpr; q0 += 32) {
       const int64_t q = q0 + lane;
-      const uint32_t v = q < wpr ? __ldg(row + q) : 0u;
+      uint32_t v = 0;
+      if (q < wpr)
+        for (int64_t i = i0; i < i1; ++i) v |= __ldg(bits + (b * n + i) * wpr + q);
       // block J = q / 4 gets bits 2 (q % 4) + {0, 1}; 16 words (4 blocks) per 32-bit mask word
       unsigned m = ((v & 0xFFFFu) ? 1u : 0u) | ((v >> 16) ? 2u : 0u);
       m <<= 2 * (q & 3) + 8 * ((q >> 2) & 3);
-      // OR over the 16 lanes sharing a mask word
       for (int o = 1; o < 16; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
       if ((lane & 15) == 0 && m) {
         atomicOr(dst + (q >> 4), m);
@@ -506,7 +546,7 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   if (cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)batch * nt, st) != cudaSuccess) return RDB_ECUDA;
   if (plan && (batch == 1 || nt > PLAN_MAX_NT)) plan = nullptr;
   if (plan)
-    gj_plan_kernel<<<1, 1024, 0, st>>>(plan->pat, plan->pat_stride, (int)batch, nt, plan->counts, plan->rp, plan->up);
+    launch_plan(*plan, (int)batch, nt, st);
   // Single matrix: look-ahead. The next panel's column block is updated first
   // (part 1); the next P1 (one CTA, latency-bound) then runs on a side stream
   // on one SM while the rest of the update (part 2) uses the other SMs.
@@ -579,7 +619,7 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // block-sparse plan (batch > 1 and nt <= PLAN_MAX_NT): pattern, per-part
 // counts, P2 lists, update lists.
 struct BatchWs {
-  size_t cnt, dyn, blk, counts, rp, up, total;
+  size_t cnt, dyn, blk, counts, rp, up, offs, total;
   BatchWs(int64_t n_pad, int64_t batch) {
     const size_t nt = (size_t)(n_pad / NB), b = (size_t)batch;
     cnt = 0;
@@ -589,9 +629,10 @@ struct BatchWs {
       counts = blk + align256(b * 2 * nt * (size_t)pat_ld((int)nt));  // column + row strip masks
       rp = counts + align256((size_t)MAX_PARTS * 2 * nt * sizeof(int));
       up = rp + align256(b * nt * (nt - 1) * sizeof(int));
-      total = up + align256(b * nt * nt * (nt - 1) * sizeof(int2));
+      offs = up + align256(b * nt * nt * (nt - 1) * sizeof(int2));
+      total = offs + align256(b * 2 * nt * sizeof(int));
     } else {
-      counts = rp = up = total = blk;
+      counts = rp = up = offs = total = blk;
     }
   }
   bool has_plan() const { return total > blk; }
@@ -644,7 +685,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   if (use_plan) {
     if (cudaMemsetAsync(pat, 0, (size_t)(batch * 2 * ntl * pld), st) != cudaSuccess) return RDB_ECUDA;
     if (bits) {
-      const int64_t want = (batch * n_bits + 7) / 8;
+      const int64_t want = (batch * ((n_bits + 15) / 16) + 7) / 8;
       strip_pattern_bits_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
           bits, n_bits, batch, (int)ntl, pat);
     } else {
@@ -663,6 +704,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     pp.counts = reinterpret_cast<int*>(wb + ws.counts) + 2 * ntl * i;
     pp.rp = reinterpret_cast<int*>(wb + ws.rp) + lo * ntl * (ntl - 1);
     pp.up = reinterpret_cast<int2*>(wb + ws.up) + lo * ntl * ntl * (ntl - 1);
+    pp.offs = reinterpret_cast<int*>(wb + ws.offs) + lo * 2 * ntl;
     return pp;
   };
   const int parts = split_parts();

@@ -59,7 +59,7 @@ def test_abi_version_and_errors_without_gpu():
     # per-part counts, row-panel and update tile lists; 256-byte aligned parts)
     al = lambda x: (x + 255) // 256 * 256  # noqa: E731
     assert lib.rdb_invert_workspace_bytes(1024, 256) == (al(256 * 8 * 4 + 64) + 256 + al(256 * 2 * 8 * 8) + al(4 * 2 * 8 * 4)
-                                                         + al(256 * 8 * 7 * 4) + al(256 * 8 * 8 * 7 * 8))
+                                                         + al(256 * 8 * 7 * 4) + al(256 * 8 * 8 * 7 * 8) + al(256 * 2 * 8 * 4))
     assert lib.rdb_invert_batched_bits(None, 128, 128, 128 * 128, 2, None, 100, None, None, None) == 1
     assert lib.rdb_invert_workspace_bytes(0, 1) == 0
 

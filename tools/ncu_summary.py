@@ -61,6 +61,27 @@ def summarise(path):
     return out
 
 
+def families(launches):
+    """Per kernel family: launches, total / average duration, DRAM bytes,
+    duration-weighted DMMA pipe activity, and the K2 bytes of the capture
+    (every gj_* / pattern / plan launch: one call when the capture is one call)."""
+    fam = {}
+    for r in launches:
+        k = r["kernel"].split("(")[0].replace("void ", "").split("<")[0].replace("rdb::", "")
+        f = fam.setdefault(k, {"launches": 0, "total_ns": 0.0, "dram_bytes": 0.0, "_dmma": 0.0})
+        f["launches"] += 1
+        f["total_ns"] += r.get("duration_ns", 0.0)
+        f["dram_bytes"] += r.get("dram_bytes", 0.0)
+        f["_dmma"] += r.get("dmma_pipe_active_pct", 0.0) * r.get("duration_ns", 0.0)
+    tot = sum(f["total_ns"] for f in fam.values()) or 1.0
+    for f in fam.values():
+        f["avg_ns"] = f["total_ns"] / f["launches"]
+        f["share"] = f["total_ns"] / tot
+        f["dmma_pipe_active_pct"] = f.pop("_dmma") / max(f["total_ns"], 1.0)
+    k2 = sum(f["dram_bytes"] for k, f in fam.items() if k.startswith("gj_") or "pattern" in k)
+    return fam, k2
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
@@ -68,6 +89,7 @@ if __name__ == "__main__":
     ap.add_argument("--note", default="")
     a = ap.parse_args()
     res = {"report": a.report, "note": a.note, "launches": summarise(a.report)}
+    res["families"], res["k2_dram_bytes_per_call"] = families(res["launches"])
     txt = json.dumps(res, indent=1)
     if a.out:
         open(a.out, "w").write(txt + "\n")
