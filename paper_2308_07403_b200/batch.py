@@ -173,12 +173,12 @@ SPLIT_MIN_BATCH, SPLIT_PARTS = 64, 2  # csrc/gj_invert.cu defaults (RDB_GJ_SPLIT
 
 def launches_per_call(n: int, batch: int) -> int:
     """Kernels one rdb_apsp_bits_batched[_d8] call launches with the default
-    knobs: K1, the block-pattern kernel, per sub-batch the plan kernel and
-    3 per panel (P1, P2, U), and K3."""
+    knobs: K1, the strip-pattern kernel, per sub-batch the plan (count walk,
+    scan, write walk) and 3 per panel (P1, P2, U), and K3."""
     nt = L.pad_to_nb(n) // L.RDB_NB
     parts = SPLIT_PARTS if batch >= SPLIT_MIN_BATCH and batch >= 4 * SPLIT_PARTS else 1
     plan = batch > 1 and nt <= PLAN_MAX_NT
-    return 2 + (1 + parts if plan else 0) + parts * 3 * nt
+    return 2 + (1 + 3 * parts if plan else 0) + parts * 3 * nt
 
 
 STRIPS = 8  # 16-column strips (engine k-chunks) per 128-column block

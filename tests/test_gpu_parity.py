@@ -255,7 +255,7 @@ def test_batch_split_and_dynamic_are_bitwise_neutral(cuda, monkeypatch):
     dev = torch.device("cuda")
     out = {}
     for name, env in (("default", {}), ("no_split", {"RDB_GJ_SPLIT_MIN": "0"}),
-                      ("static", {"RDB_GJ_DYNAMIC": "0"}), ("four", {"RDB_GJ_SPLIT_PARTS": "4"}),
+                      ("dynamic", {"RDB_GJ_DYNAMIC": "1"}), ("four", {"RDB_GJ_SPLIT_PARTS": "4"}),
                       ("dense", {"RDB_GJ_SKIP": "0"})):
         for k in ("RDB_GJ_SPLIT_MIN", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_SKIP"):
             monkeypatch.delenv(k, raising=False)
@@ -279,7 +279,7 @@ def test_batch_split_and_dynamic_are_bitwise_neutral(cuda, monkeypatch):
     buf.stage_invert_generic(128, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     out["generic"] = buf.m.clone()
-    for name in ("no_split", "static", "four", "dense", "generic"):
+    for name in ("no_split", "dynamic", "four", "dense", "generic"):
         assert torch.equal(out[name], out["default"]), name
 
 
