@@ -381,6 +381,7 @@ def main():
     # column panel (block-sparse plan): the roofline uses the flop it executes;
     # the dense-equivalent 2n^3 rate beside it
     exec_flops = B.executed_flops(bits, N)
+    n_gj = int((~B.banded(bits, N)).sum())
     inv_tflops = exec_flops / (t_inv * 1e-3) / 1e12
     dense_tflops = flops_per_graph * batch / (t_inv * 1e-3) / 1e12
     peak, peak_src = fp64_peak()
@@ -477,12 +478,15 @@ def main():
         "inversion_tflops": inv_tflops, "inversion_frac_of_fp64_peak": inv_tflops / peak,
         "inversion_dense_equivalent_tflops": dense_tflops,
         "executed_flop_fraction": exec_flops / (flops_per_graph * batch),
-        "roofline": {"bound": "tensor", "kernel": "K2 blocked Gauss-Jordan (gj_panel + gj_rowpanel + gj_update, DMMA.8x8x4)",
+        "roofline": {"bound": "tensor", "kernel": "K2 blocked Gauss-Jordan (gj_panel + gj_rowpanel + gj_update, DMMA.8x8x4) "
+                                                  "+ banded inverse of the block-tridiagonal graphs (band_factor + band_chain)",
                      "achieved": inv_tflops, "peak": peak, "unit": "TFLOP/s", "frac": inv_tflops / peak,
                      "traffic": ncu_traffic(), "traffic_unit": "bytes per K2 call (8 GJ steps x 3 kernels, whole batch)",
                      "traffic_source": "profiles/r01_ncu_full_cfg2.json", "peak_source": peak_src,
                      "work_per_launch": f"{exec_flops:.4g} flop executed per K2 call = 2*128*128*16 per k-chunk over "
-                                        f"the block-sparse plan's tiles and k-chunks ({exec_flops / (flops_per_graph * batch):.3f} of the "
+                                        f"the block-sparse plan's tiles and k-chunks for the {n_gj} Gauss-Jordan graphs + "
+                                        f"{B.band_flops(N):.4g} per banded graph x {batch - n_gj} "
+                                        f"({exec_flops / (flops_per_graph * batch):.3f} of the "
                                         f"dense 2*n^3 = {flops_per_graph:.4g} flop per graph x {batch} graphs)"},
         "kernels_ms": {"K1_build_m_bits": t_build, "K2_invert": t_inv, "K3_log_ceil": t_log},
         "hbm_kernels": {"K1_GBps": build_bytes / (t_build * 1e-3) / 1e9, "K3_GBps": log_bytes / (t_log * 1e-3) / 1e9,

@@ -178,7 +178,8 @@ def launches_per_call(n: int, batch: int) -> int:
     nt = L.pad_to_nb(n) // L.RDB_NB
     parts = SPLIT_PARTS if batch >= SPLIT_MIN_BATCH and batch >= 4 * SPLIT_PARTS else 1
     plan = batch > 1 and nt <= PLAN_MAX_NT
-    return 2 + (1 + 3 * parts if plan else 0) + parts * 3 * nt
+    # with the plan: + band detection, band factor and band chain (gj_band.cu)
+    return 2 + (1 + 3 * parts + 3 if plan else 0) + parts * 3 * nt
 
 
 STRIPS = 8  # 16-column strips (engine k-chunks) per 128-column block
@@ -250,15 +251,43 @@ def gj_plan_chunks(pattern: np.ndarray) -> np.ndarray:
     return out
 
 
+BAND = 32  # block size of the banded path (csrc/gj_band.cu)
+
+
+def banded(bits: np.ndarray, n: int) -> np.ndarray:
+    """Host restatement of band_detect_bits_kernel: (batch,) bool, True when
+    every edge j -> i of the graph has |i // 32 - j // 32| <= 1."""
+    bits = np.asarray(bits).view(np.uint32)
+    batch = bits.shape[0]
+    wpr = (n + 31) // 32
+    words = bits.reshape(batch, n, wpr)
+    q = np.arange(wpr)[None, :]
+    outside = np.abs(q - (np.arange(n) // BAND)[:, None]) > 1
+    return ~((words != 0) & outside[None]).any(axis=(1, 2))
+
+
+def band_flops(n: int) -> float:
+    """FP64 flop of the banded inverse of one matrix (csrc/gj_band.cu): 2 * 32^3
+    per block product or block inverse; (nb - 1)(nb + 5) products (sweeps,
+    diagonal, chains) and 3 nb inverses, nb = n_pad / 32."""
+    nb = L.pad_to_nb(n) // BAND
+    return float((nb - 1) * (nb + 5) + 3 * nb) * 2.0 * BAND**3
+
+
 def executed_flops(bits: np.ndarray, n: int) -> float:
-    """FP64 flop the block-sparse K2 executes on this batch (2 * 128 * 128 * 16 per k-chunk)."""
+    """FP64 flop K2 executes on this batch with the default knobs: the banded
+    path for block-tridiagonal graphs, the block-sparse Gauss-Jordan plan
+    (2 * 128 * 128 * 16 per k-chunk) for the others."""
     batch = np.asarray(bits).shape[0]
     nt = L.pad_to_nb(n) // L.RDB_NB
     if batch > 1 and nt <= PLAN_MAX_NT:
-        chunks = gj_plan_chunks(strip_pattern(bits, n)).sum()
+        band = banded(bits, n)
+        chunks = gj_plan_chunks(strip_pattern(np.asarray(bits)[~band], n)).sum() if (~band).any() else 0
+        extra = band.sum() * band_flops(n)
     else:
         chunks = batch * nt**3 * STRIPS
-    return float(chunks) * 2.0 * L.RDB_NB * L.RDB_NB * (L.RDB_NB // STRIPS)
+        extra = 0.0
+    return float(chunks) * 2.0 * L.RDB_NB * L.RDB_NB * (L.RDB_NB // STRIPS) + extra
 
 
 def check_infos(infos: list[L.PivotInfo], gammas: np.ndarray, first_index: int = 0) -> None:

@@ -34,10 +34,13 @@ using EC = eng::Default;  // engine warp layout
 
 __global__ void __launch_bounds__(p1::THREADS, 1)
     gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int64_t off, int idx0,
-                    rdb_pivot_info* __restrict__ info, int first, int64_t info_stride = 1) {
-  // block at a + b*stride + off*(lda + 1); pivot indices recorded from idx0
+                    rdb_pivot_info* __restrict__ info, int first, int64_t info_stride = 1,
+                    const int* __restrict__ nonband = nullptr) {
+  // block at a + b*stride + off*(lda + 1); pivot indices recorded from idx0.
+  // Matrices the banded path inverts (nonband[b * info_stride] == 0) are skipped.
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
+  if (nonband && !nonband[b * info_stride]) return;
   p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), a + b * stride + off * lda + off, lda, idx0,
                     info + b * info_stride, first);
 }
@@ -454,7 +457,7 @@ static void launch_plan(const PlanPart& pp, int batch, int nt, cudaStream_t st) 
 // consecutive blocks share a 32-bit word (pat_ld pads rows to 4 bytes). Row
 // strips: bit (i % NB) / 16 in every block the strip's rows touch.
 __global__ void strip_pattern_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t batch, int nt,
-                                          unsigned char* __restrict__ pat) {
+                                          unsigned char* __restrict__ pat, const int* __restrict__ nonband) {
   const int lane = threadIdx.x & 31;
   const int ld = pat_ld(nt);
   const int64_t wpr = (n + 31) / 32;
@@ -462,6 +465,7 @@ __global__ void strip_pattern_bits_kernel(const uint32_t* __restrict__ bits, int
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < batch * strips; w += nwarps) {
     const int64_t b = w / strips, s16 = w - b * strips;
+    if (nonband && !nonband[b]) continue;  // banded path: the pattern stays zero, no GJ tiles
     const int64_t i0 = s16 * 16, i1 = i0 + 16 < n ? i0 + 16 : n;
     unsigned char* Pc = pat + b * 2 * nt * ld;
     unsigned* dst = reinterpret_cast<unsigned*>(Pc + (i0 / NB) * ld);
@@ -528,7 +532,7 @@ static int64_t wide_min_n();
 // inverted as part of a larger matrix).
 static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                        rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base, int* dyn = nullptr,
-                       const PlanPart* plan = nullptr, int64_t info_stride = 1) {
+                       const PlanPart* plan = nullptr, int64_t info_stride = 1, const int* nonband = nullptr) {
   if (!a || !work || !info || n <= 0 || batch <= 0) return RDB_EINVAL;
   if (n % NB != 0 || lda < n || (lda & 1) || (batch > 1 && stride < n * lda)) return RDB_EINVAL;
   if (((uintptr_t)a & 15) || ((uintptr_t)work & 15)) return RDB_EINVAL;
@@ -557,12 +561,12 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
     if (rc) return rc;
   }
   gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, idx_base, info, first,
-                                                                       info_stride);
+                                                                       info_stride, nonband);
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
     if (k > 0 && !lookahead)
       gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, idx_base + p0,
-                                                                           info, 0, info_stride);
+                                                                           info, 0, info_stride, nonband);
     if (nt == 1) break;
     RowPanelSched rp{a, lda, stride, nt, k, (int)batch, batch > 1 ? dyn : nullptr};
     if (plan) {
@@ -617,9 +621,17 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Batched workspace: row-block counters | dynamic tile counters (256 B) |
 // block-sparse plan (batch > 1 and nt <= PLAN_MAX_NT): pattern, per-part
-// counts, P2 lists, update lists.
+// counts, P2 lists, update lists | banded path: per-matrix flags, G/H/D blocks
+// (gj_band.cu).
+namespace band {
+size_t ws_doubles(int64_t n_pad);
+}
+int band_detect(const uint32_t* bits, int64_t n, int64_t batch, int* nonband, cudaStream_t st);
+int band_invert(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t batch, const int* nonband,
+                double* ws, rdb_pivot_info* info, cudaStream_t st);
+
 struct BatchWs {
-  size_t cnt, dyn, blk, counts, rp, up, offs, total;
+  size_t cnt, dyn, blk, counts, rp, up, offs, band, band_ws, total;
   BatchWs(int64_t n_pad, int64_t batch) {
     const size_t nt = (size_t)(n_pad / NB), b = (size_t)batch;
     cnt = 0;
@@ -630,9 +642,11 @@ struct BatchWs {
       rp = counts + align256((size_t)MAX_PARTS * 2 * nt * sizeof(int));
       up = rp + align256(b * nt * (nt - 1) * sizeof(int));
       offs = up + align256(b * nt * nt * (nt - 1) * sizeof(int2));
-      total = offs + align256(b * 2 * nt * sizeof(int));
+      band = offs + align256(b * 2 * nt * sizeof(int));
+      band_ws = band + align256(b * sizeof(int));
+      total = band_ws + align256(b * band::ws_doubles(n_pad) * sizeof(double));
     } else {
-      counts = rp = up = offs = total = blk;
+      counts = rp = up = offs = band = band_ws = total = blk;
     }
   }
   bool has_plan() const { return total > blk; }
@@ -646,6 +660,13 @@ static bool skip_enabled() {
 // Dynamic tile grabbing (a global atomic per tile) balanced the two dense
 // sub-batch streams best; with the block-sparse plan's many short tiles the
 // static stride measured faster (config 2: 10.98 -> 10.83 ms per K2 call).
+// Block-tridiagonal matrices (every edge within the 32-block band, from the
+// adjacency bits) skip Gauss-Jordan and run the banded inverse (gj_band.cu).
+static bool band_enabled() {
+  const char* e = getenv("RDB_GJ_BAND");  // A-B switch: 0 sends every matrix through Gauss-Jordan
+  return !(e && e[0] == '0');
+}
+
 static bool dyn_sched() {
   const char* e = getenv("RDB_GJ_DYNAMIC");  // A-B switch: 1 grabs tiles dynamically
   return e && e[0] == '1';
@@ -685,12 +706,19 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   const int64_t ntl = n / NB;
   const int64_t pld = pat_ld((int)ntl);
   unsigned char* pat = use_plan ? reinterpret_cast<unsigned char*>(wb + ws.blk) : nullptr;
+  const bool use_band = use_plan && bits && band_enabled() && info && lda >= n;
+  int* nonband = use_band ? reinterpret_cast<int*>(wb + ws.band) : nullptr;
+  double* band_ws = use_band ? reinterpret_cast<double*>(wb + ws.band_ws) : nullptr;
   if (use_plan) {
     if (cudaMemsetAsync(pat, 0, (size_t)(batch * 2 * ntl * pld), st) != cudaSuccess) return RDB_ECUDA;
+    if (use_band) {
+      const int rc = band_detect(bits, n_bits, batch, nonband, st);
+      if (rc) return rc;
+    }
     if (bits) {
       const int64_t want = (batch * ((n_bits + 15) / 16) + 7) / 8;
       strip_pattern_bits_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
-          bits, n_bits, batch, (int)ntl, pat);
+          bits, n_bits, batch, (int)ntl, pat, nonband);
     } else {
       const int64_t want = (batch * ntl * ntl + 7) / 8;
       strip_pattern_m_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(
@@ -722,7 +750,8 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     int* dyn = reinterpret_cast<int*>(wb + ws.dyn);
     if (cudaMemsetAsync(dyn, 0, 2 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
     cudaEventRecord(g_fork, st);
-    int rc = RDB_OK;
+    // the banded matrices on this stream, concurrently with the sub-batches
+    int rc = use_band ? band_invert(a, n, lda, stride, batch, nonband, band_ws, info, st) : RDB_OK;
     int64_t lo = 0;
     for (int i = 0; i < parts && rc == RDB_OK; ++i) {
       const int64_t cnt = (batch - i + parts - 1) / parts;
@@ -731,7 +760,8 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       // row-block counters of the part, 16-byte aligned (counter_bytes has the slack)
       char* cw = wb + (((size_t)lo * ntl * sizeof(int) + 15) & ~(size_t)15);
       rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, g_part[i], 1, 0,
-                       dyn_sched() ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr, parts);
+                       dyn_sched() ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr, parts,
+                       nonband ? nonband + i : nullptr);
       cudaEventRecord(g_join[i], g_part[i]);
       lo += cnt;
     }
@@ -739,7 +769,12 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     return rc;
   }
   const PlanPart pp = part_plan(0, 1, 0);
-  return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, nullptr, use_plan ? &pp : nullptr);
+  if (use_band) {
+    const int rc = band_invert(a, n, lda, stride, batch, nonband, band_ws, info, st);
+    if (rc) return rc;
+  }
+  return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, nullptr, use_plan ? &pp : nullptr, 1,
+                     nonband);
 }
 
 // ------------------------------------------------------------------ wide (NB = 256) single matrix

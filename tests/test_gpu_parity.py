@@ -254,6 +254,9 @@ def test_batch_split_and_dynamic_are_bitwise_neutral(cuda, monkeypatch):
     bits, gammas = bits[96:224], gammas[96:224]  # 64 ER + 64 lattice graphs
     dev = torch.device("cuda")
     out = {}
+    # (the banded path for the lattices has its own rounding order: off here,
+    # compared separately in test_banded_path_matches_gauss_jordan)
+    monkeypatch.setenv("RDB_GJ_BAND", "0")
     for name, env in (("default", {}), ("no_split", {"RDB_GJ_SPLIT_MIN": "0"}),
                       ("dynamic", {"RDB_GJ_DYNAMIC": "1"}), ("four", {"RDB_GJ_SPLIT_PARTS": "4"}),
                       ("dense", {"RDB_GJ_SKIP": "0"})):
@@ -329,10 +332,15 @@ def test_block_sparse_schedule_structured_graphs(cuda, monkeypatch, n):
     gam = np.array([1e-3, 0.1, 0.05, 0.5, 0.5, 0.1, 0.1, 0.1][: len(presents)])
     bits = np.stack([wl.pack_bits(q) for q in presents])
     outs = {}
+    monkeypatch.setenv("RDB_GJ_BAND", "0")
     for mode in ("1", "0"):
         monkeypatch.setenv("RDB_GJ_SKIP", mode)
         outs[mode] = rb.rounded_r_distance_batch(bits, gam, n)
     np.testing.assert_array_equal(outs["1"], outs["0"])
+    # the banded path (band, empty graph and lattice are block tridiagonal)
+    monkeypatch.setenv("RDB_GJ_SKIP", "1")
+    monkeypatch.setenv("RDB_GJ_BAND", "1")
+    outs["band"] = rb.rounded_r_distance_batch(bits, gam, n)
     for b, q in enumerate(presents):
         w = wl.weights_from_present(q)
         r = orc.r_distance(orc.resolvent_y(w, gam[b]), gam[b])
@@ -344,9 +352,84 @@ def test_block_sparse_schedule_structured_graphs(cuda, monkeypatch, n):
         # Exact everywhere else; on those entries D is one of the two.
         with np.errstate(invalid="ignore"):
             knife = np.isfinite(r) & (np.abs(r - np.round(r)) < 1e-9) & (r != 0)
-        got = outs["1"][b]
-        np.testing.assert_array_equal(got[~knife], ref[~knife], err_msg=f"graph {b}")
         k = np.round(r[knife]).astype(np.int64)
-        assert np.isin(got[knife] - k, [0, 1]).all(), f"graph {b}"
+        for mode in ("1", "band"):
+            got = outs[mode][b]
+            np.testing.assert_array_equal(got[~knife], ref[~knife], err_msg=f"graph {b} {mode}")
+            assert np.isin(got[knife] - k, [0, 1]).all(), f"graph {b} {mode}"
+        got = outs["1"][b]
         if b == 3:  # the gamma = 0.5 cycle: y == 2^-d exactly, so D is the hop count
             np.testing.assert_array_equal(got, orc.d_to_int32(orc.bfs_apsp(w)))
+
+
+def _banded_presents(n, rng):
+    """Block-tridiagonal patterns (every edge within |i/32 - j/32| <= 1) and
+    near misses: a directed lattice of side 32 (n = 1024), a random band of
+    half-width 32, the widest edges the band allows (i = 32q + 31 <-> j =
+    32(q + 1) + 31), a path, and one graph with a single edge outside the band."""
+    i, j = np.indices((n, n))
+    out = []
+    if n == 1024:
+        out.append(wl.lattice_present(32, 0.8, 17))
+    out.append((np.abs(i - j) <= 32) & (np.abs(i // 32 - j // 32) <= 1) & (rng.random((n, n)) < 0.2))
+    wide = (np.abs(i // 32 - j // 32) <= 1) & (rng.random((n, n)) < 0.05)
+    wide[31::32, :] |= (np.abs(i[31::32] // 32 - j[31::32] // 32) == 1) & (j[31::32] % 32 == 0)
+    out.append(wide)
+    path = np.zeros((n, n), bool)
+    path[np.arange(1, n), np.arange(n - 1)] = True
+    out.append(path)
+    miss = (np.abs(i - j) <= 3) & (rng.random((n, n)) < 0.5)
+    miss[n - 1, 0] = True  # one edge outside the band: Gauss-Jordan
+    out.append(miss)
+    for q in out:
+        np.fill_diagonal(q, False)
+    return out
+
+
+@pytest.mark.parametrize("n", [300, 1024])
+def test_banded_path_matches_gauss_jordan(cuda, monkeypatch, n):
+    # K2b (gj_band.cu) against Gauss-Jordan on the same matrices: inverse
+    # within 1e-12 componentwise, identical D, pivot records agree, and D
+    # equal to the oracle away from the reference's own knife edges
+    from paper_2308_07403_b200 import batch as B
+    from paper_2308_07403_b200 import _lib as L
+
+    rng = np.random.default_rng(n + 1)
+    presents = _banded_presents(n, rng)
+    gam = np.array([0.1, 0.02, 0.05, 0.6, 0.1][-len(presents):])  # 0.6^1023 stays a normal double
+    bits = np.stack([wl.pack_bits(q) for q in presents])
+    cnt = len(presents)
+    dev = torch.device("cuda")
+    ys, infos = {}, {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("RDB_GJ_BAND", mode)
+        buf = B.BatchBuffers.allocate(n, cnt, dev)
+        buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+        buf.gammas.copy_(torch.from_numpy(gam))
+        sh = torch.cuda.current_stream().cuda_stream
+        buf.stage_build(cnt, sh)
+        buf.stage_invert(cnt, sh)
+        torch.cuda.synchronize()
+        ys[mode] = buf.m.cpu().numpy()[:, :n, :n]
+        infos[mode] = L.read_pivot_info(buf.info)
+        del buf
+    for b in range(cnt):
+        ya, yb = ys["0"][b], ys["1"][b]
+        assert np.array_equal(ya == 0, yb == 0), b
+        nz = ya != 0
+        assert np.max(np.abs(yb[nz] - ya[nz]) / np.abs(ya[nz])) < 1e-12, b
+        ia, ib = infos["0"][b], infos["1"][b]
+        assert ia.flags == ib.flags == 0, b
+        assert abs(ia.min_pivot - ib.min_pivot) <= 1e-14 * ia.min_pivot, b
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("RDB_GJ_BAND", mode)
+        outs[mode] = rb.rounded_r_distance_batch(bits, gam, n)
+    for b, q in enumerate(presents):
+        w = wl.weights_from_present(q)
+        r = orc.r_distance(orc.resolvent_y(w, gam[b]), gam[b])
+        ref = orc.d_to_int32(np.ceil(r))
+        with np.errstate(invalid="ignore"):
+            knife = np.isfinite(r) & (np.abs(r - np.round(r)) < 1e-9) & (r != 0)
+        for mode in ("0", "1"):
+            np.testing.assert_array_equal(outs[mode][b][~knife], ref[~knife], err_msg=f"graph {b} band={mode}")

@@ -135,4 +135,23 @@ def test_cfg2_lattice_half_runs_about_a_sixth_of_the_chunks():
     assert (t[kinds == "er"] == 8 * 512).all()  # ER p = 0.02: every strip holds edges
     # bandwidth 32: half of the tiles, and 2 of 8 k-chunks of the update tiles
     assert (t[kinds == "lattice"] < 800).all()
-    assert B.launches_per_call(1024, 256) == 2 + 1 + 2 * 3 + 2 * 3 * 8
+    assert B.launches_per_call(1024, 256) == 2 + 1 + 2 * 3 + 3 + 2 * 3 * 8
+
+
+def test_band_detection_restatement():
+    # every cfg2 lattice (row-major 32 x 32 grid) is block tridiagonal in
+    # 32-blocks, no cfg2 ER graph is; one edge just outside the band flips it
+    bits, _, seeds = wl.cfg2_batch(16)
+    kinds = np.array([k for k, _ in seeds])
+    np.testing.assert_array_equal(B.banded(bits, 1024), kinds == "lattice")
+    n = 300
+    i, j = np.indices((n, n))
+    inside = (np.abs(i // 32 - j // 32) <= 1) & (i != j)
+    q = inside.copy()
+    q[64, 0] = True  # block 2 <- block 0
+    assert B.banded(np.stack([wl.pack_bits(inside), wl.pack_bits(q)]), n).tolist() == [True, False]
+    # (nb - 1)(nb + 5) block products + 3 nb block inverses of 2 * 32^3 flop
+    assert B.band_flops(1024) == (31 * 37 + 96) * 2 * 32**3
+    fl = B.executed_flops(bits, 1024)
+    er = B.gj_plan_chunks(B.strip_pattern(bits[kinds == "er"], 1024)).sum() * 2 * 128 * 128 * 16
+    assert fl == er + (kinds == "lattice").sum() * B.band_flops(1024)
