@@ -9,11 +9,12 @@
 // two block-Schur sweeps instead of Gauss-Jordan on the whole matrix:
 //   forward   D_0 = T_0,       D_r = T_r + L_r G_{r-1},  G_r = -D_r^-1 U_r
 //   backward  S_last = T_last,  S_r = T_r + U_r H_{r+1},  H_r = -S_r^-1 L_r
-//   diagonal  Y_rr = (D_r + U_r H_{r+1})^-1
+//   diagonal  Y_rr = (D_r + K_r)^-1,  K_r = U_r H_{r+1}
 //   chains    Y_ij = G_i Y_{i+1,j} (i < j),   Y_ij = H_i Y_{i-1,j} (i > j)
 // (block row i of M Y = I for i < j reads L_i Y_{i-1,j} + T_i Y_ij + U_i
 // Y_{i+1,j} = 0; eliminating downwards gives D_i Y_ij = -U_i Y_{i+1,j}.)
-// 2 (nb^2 + 7 nb) 32^3 flop against GJ's 2 n^3 (n = 1024: 8.1e7 vs 2.1e9).
+// 2 32^3 ((nb - 1)(nb + 5) + 3 nb) flop against GJ's 2 n^3 (n = 1024: 8.1e7
+// vs 2.1e9).
 //
 // Numerics: for a nonsingular M-matrix every D_r, S_r and diagonal Schur
 // complement is again an M-matrix (inverse >= 0), G_r, H_r >= 0 and every
@@ -25,11 +26,12 @@
 // inversions sets RDB_PIV_NONPOS (the caller then runs the pivoted kernel).
 //
 // Kernels: band_detect_bits_kernel (flag per matrix from the adjacency bits),
-// band_factor_kernel (one CTA per matrix: the two sweeps on two 4-warp groups
-// concurrently, then the diagonal blocks), band_chain_kernel (a warp per
-// block column j: nb - 1 chained 32 x 32 x 32 DMMA products, the operator
-// G_i / H_i prefetched into registers one step ahead, the running block in
-// shared memory, every product stored to its place in M).
+// band_factor_kernel (two matrices per CTA, a 4-warp group per sweep, all
+// four sweeps concurrent; the backward sweep also keeps K_r = U_r H_{r+1}),
+// band_chain_kernel (a warp per block column j: Y_jj = (D_j + K_j)^-1 by a
+// register-resident warp Gauss-Jordan, then nb - 1 chained 32 x 32 x 32 DMMA
+// products, the operator G_i / H_i prefetched into registers one step ahead,
+// the running block in shared memory, every block stored to its place in M).
 #include "common.cuh"
 
 namespace rdb {
@@ -41,8 +43,10 @@ constexpr int BLK = S * S;     // doubles per block in the workspace
 constexpr int SBUF = S * LD;   // doubles per shared-memory block
 constexpr int CW = 4;          // warps (block columns) per chain CTA
 
-// Workspace per matrix: G[nb] and H[nb] in A-fragment order, then D[nb] row-major.
-size_t ws_doubles(int64_t n_pad) { return (size_t)3 * (size_t)(n_pad / S) * BLK; }
+// Workspace per matrix: G[nb] and H[nb] in A-fragment order, D[nb] and K[nb] row-major.
+size_t ws_doubles(int64_t n_pad) { return (size_t)4 * (size_t)(n_pad / S) * BLK; }
+constexpr int GPC = 2;         // matrices per factor CTA
+constexpr size_t CHAIN_SMEM = (size_t)CW * 2 * SBUF * sizeof(double);
 
 RDB_DEV void gbar(int id) { asm volatile("bar.sync %0, 128;\n" ::"r"(id) : "memory"); }
 
@@ -61,8 +65,8 @@ struct Group {  // one 4-warp group's shared memory
   double prow[2][S], pcol[2][S];
 };
 struct FactorSmem {
-  Group g[2];
-  int flags[2];
+  Group g[2 * GPC];
+  int flags[2 * GPC];
 };
 
 // 128 threads: global row-major block (ld) <-> shared block
@@ -167,6 +171,28 @@ RDB_DEV void inverse(Group& g, double* X, int id, int t, bool rec, int base, dou
   gbar(id);
 }
 
+// Warp-level Gauss-Jordan inverse without pivoting, lane j holding column j
+// in v (the same operations as inverse(): the pivot column's entries reach
+// the other lanes by shuffles).
+RDB_DEV void warp_inverse(double (&v)[S], int lane, int& flags) {
+#pragma unroll
+  for (int kk = 0; kk < S; ++kk) {
+    const double p = __shfl_sync(0xffffffffu, v[kk], kk);
+    const double pinv = rcp_nr(p);
+    if (!(fabs(p) < INFINITY)) flags |= RDB_PIV_NONFINITE;
+    if (!(p > 0.0)) flags |= RDB_PIV_NONPOS;
+    const bool piv = (lane == kk);
+    const double u = piv ? pinv : v[kk] * pinv;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      if (i == kk) continue;
+      const double f = __shfl_sync(0xffffffffu, v[i], kk);
+      v[i] = fma(-f, u, piv ? 0.0 : v[i]);
+    }
+    v[kk] = u;
+  }
+}
+
 }  // namespace band
 
 using namespace band;
@@ -189,118 +215,125 @@ __global__ void band_detect_bits_kernel(const uint32_t* __restrict__ bits, int64
   }
 }
 
-// Both block-Schur sweeps and the diagonal blocks of one banded matrix per CTA
-// (256 threads: group 0 forward, group 1 backward, then alternate diagonal
-// blocks). Writes Y_rr into the diagonal blocks of M and the pivot record.
-__global__ void __launch_bounds__(256, 1)
-    band_factor_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int nb, const int* __restrict__ nonband,
-                       int64_t nb_stride, double* __restrict__ ws, rdb_pivot_info* __restrict__ info,
-                       int64_t info_stride) {
-  const int64_t m = blockIdx.x;
-  if (nonband[m * nb_stride]) return;
+// Both block-Schur sweeps of GPC matrices per CTA (a 4-warp group per sweep,
+// 128 * 2 * GPC threads). Writes G, H, D, K to the workspace and the pivot
+// record (forward pivots = LAPACK's diag(U); flags from every inverse).
+__global__ void __launch_bounds__(256 * GPC, 1)
+    band_factor_kernel(const double* __restrict__ a, int64_t lda, int64_t stride, int nb, int64_t batch,
+                       const int* __restrict__ nonband, double* __restrict__ ws, rdb_pivot_info* __restrict__ info) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FactorSmem& s = *reinterpret_cast<FactorSmem*>(smem_raw);
-  double* A = a + m * stride;
-  double* G = ws + m * 3 * (int64_t)nb * BLK;
-  double* H = G + (int64_t)nb * BLK;
-  double* Dl = H + (int64_t)nb * BLK;
   const int grp = threadIdx.x >> 7, t = threadIdx.x & 127, id = 1 + grp;
-  Group& g = s.g[grp];
-  auto blk = [&](int r, int c) { return A + (int64_t)(S * r) * lda + S * c; };
+  const int64_t m = (int64_t)blockIdx.x * GPC + (grp >> 1);
+  const bool active = m < batch && !nonband[m];  // uniform per group (named barriers are per group)
   double minp = INFINITY;
   int mini = -1, flags = 0;
-  if (grp == 0) {
-    for (int r = 0; r < nb; ++r) {  // D_r = T_r + L_r G_{r-1}; G_r = -D_r^-1 U_r
-      load_block(g.X, blk(r, r), lda, t);
-      if (r > 0) {
-        load_block(g.A, blk(r, r - 1), lda, t);
-        gbar(id);
-        gemm(g.X, g.X, g.A, g.P, false, t, id);
-      } else {
-        gbar(id);
+  if (active) {
+    const double* A = a + m * stride;
+    double* G = ws + m * 4 * (int64_t)nb * BLK;
+    double* H = G + (int64_t)nb * BLK;
+    double* Dl = H + (int64_t)nb * BLK;
+    double* K = Dl + (int64_t)nb * BLK;
+    Group& g = s.g[grp];
+    auto blk = [&](int r, int c) { return A + (int64_t)(S * r) * lda + S * c; };
+    if ((grp & 1) == 0) {
+      for (int r = 0; r < nb; ++r) {  // D_r = T_r + L_r G_{r-1}; G_r = -D_r^-1 U_r
+        load_block(g.X, blk(r, r), lda, t);
+        if (r > 0) {
+          load_block(g.A, blk(r, r - 1), lda, t);
+          gbar(id);
+          gemm(g.X, g.X, g.A, g.P, false, t, id);
+        } else {
+          gbar(id);
+        }
+        store_block(Dl + (int64_t)r * BLK, S, g.X, t);
+        inverse(g, g.X, id, t, true, S * r, minp, mini, flags);
+        if (r < nb - 1) {
+          load_block(g.A, blk(r, r + 1), lda, t);
+          gbar(id);
+          gemm(g.P, nullptr, g.X, g.A, true, t, id);
+          store_frag(G + (int64_t)r * BLK, g.P, t);
+        }
       }
-      store_block(Dl + (int64_t)r * BLK, S, g.X, t);
-      inverse(g, g.X, id, t, true, S * r, minp, mini, flags);
-      if (r < nb - 1) {
-        load_block(g.A, blk(r, r + 1), lda, t);
-        gbar(id);
-        gemm(g.P, nullptr, g.X, g.A, true, t, id);
-        store_frag(G + (int64_t)r * BLK, g.P, t);
-      }
-    }
-  } else {
-    for (int r = nb - 1; r >= 0; --r) {  // S_r = T_r + U_r H_{r+1}; H_r = -S_r^-1 L_r
-      load_block(g.X, blk(r, r), lda, t);
-      if (r < nb - 1) {
-        load_block(g.A, blk(r, r + 1), lda, t);
-        gbar(id);
-        gemm(g.X, g.X, g.A, g.P, false, t, id);
-      } else {
-        gbar(id);
-      }
-      inverse(g, g.X, id, t, false, 0, minp, mini, flags);
-      if (r > 0) {
-        load_block(g.A, blk(r, r - 1), lda, t);
-        gbar(id);
-        gemm(g.P, nullptr, g.X, g.A, true, t, id);
-        store_frag(H + (int64_t)r * BLK, g.P, t);
-      }
-    }
-  }
-  __syncthreads();
-  for (int r = grp; r < nb; r += 2) {  // Y_rr = (D_r + U_r H_{r+1})^-1 (no longer reads T_r)
-    load_block(g.X, Dl + (int64_t)r * BLK, S, t);
-    if (r < nb - 1) {
-      load_block(g.A, blk(r, r + 1), lda, t);
-      load_frag(g.P, H + (int64_t)(r + 1) * BLK, t);
-      gbar(id);
-      gemm(g.X, g.X, g.A, g.P, false, t, id);
     } else {
-      gbar(id);
+      for (int r = nb - 1; r >= 0; --r) {  // K_r = U_r H_{r+1}; S_r = T_r + K_r; H_r = -S_r^-1 L_r
+        load_block(g.X, blk(r, r), lda, t);
+        if (r < nb - 1) {
+          load_block(g.A, blk(r, r + 1), lda, t);
+          gbar(id);
+          gemm(g.A, nullptr, g.A, g.P, false, t, id);
+          store_block(K + (int64_t)r * BLK, S, g.A, t);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int e = t + 128 * q, rr = e >> 5, cc = e & 31;
+            g.X[rr * LD + cc] += g.A[rr * LD + cc];
+          }
+        } else {
+          const int e0 = t;
+          for (int e = e0; e < BLK; e += 128) K[(int64_t)r * BLK + e] = 0.0;
+        }
+        gbar(id);
+        inverse(g, g.X, id, t, false, 0, minp, mini, flags);
+        if (r > 0) {
+          load_block(g.A, blk(r, r - 1), lda, t);
+          gbar(id);
+          gemm(g.P, nullptr, g.X, g.A, true, t, id);
+          store_frag(H + (int64_t)r * BLK, g.P, t);
+        }
+      }
     }
-    inverse(g, g.X, id, t, false, 0, minp, mini, flags);
-    store_block(blk(r, r), lda, g.X, t);
-    gbar(id);
   }
   if (t == 0) s.flags[grp] = flags;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    rdb_pivot_info* inf = info + m * info_stride;
+  if (active && (grp & 1) == 0 && t == 0) {
+    rdb_pivot_info* inf = info + m;
     inf->min_pivot = minp;
     inf->min_index = mini;
-    inf->flags = s.flags[0] | s.flags[1];
+    inf->flags = flags | s.flags[grp + 1];
   }
 }
 
-// Off-diagonal blocks: warp j of the grid row owns block column j: up the
-// column (Y_ij = G_i Y_{i+1,j}, i = j-1 .. 0), then down (Y_ij = H_i
-// Y_{i-1,j}, i = j+1 .. nb-1), nb - 1 products per warp.
+// Block column j per warp: Y_jj = (D_j + K_j)^-1 (warp Gauss-Jordan, flags
+// ORed into the pivot record), then up the column (Y_ij = G_i Y_{i+1,j},
+// i = j-1 .. 0) and down (Y_ij = H_i Y_{i-1,j}, i = j+1 .. nb-1): nb - 1
+// products per warp. Reads only the workspace, writes every block of M.
 __global__ void __launch_bounds__(CW * 32, 2)
     band_chain_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int nb, const int* __restrict__ nonband,
-                      const double* __restrict__ ws) {
+                      const double* __restrict__ ws, rdb_pivot_info* __restrict__ info) {
   const int64_t m = blockIdx.y;
   if (nonband[m]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * CW + warp;
   if (j >= nb) return;  // warp-uniform; only warp-level synchronisation below
-  __shared__ __align__(16) double sb[CW][SBUF];
-  double* B = sb[warp];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* B = reinterpret_cast<double*>(smem_raw) + warp * 2 * SBUF;  // the running block (B operand)
+  double* Yd = B + SBUF;                                              // Y_jj, the start of both chains
   double* A = a + m * stride;
-  const double* G = ws + m * 3 * (int64_t)nb * BLK;
+  const double* G = ws + m * 4 * (int64_t)nb * BLK;
   const double* H = G + (int64_t)nb * BLK;
+  const double* Dl = H + (int64_t)nb * BLK + (int64_t)j * BLK;
+  const double* K = Dl + (int64_t)nb * BLK;
   const int lr = lane >> 2, lk = lane & 3;
-  auto load_diag = [&]() {
+  {
+    double v[S];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int e = lane + 32 * q, r = e >> 4, c2 = e & 15;
-      *reinterpret_cast<double2*>(B + r * LD + 2 * c2) = ldg2(A + (int64_t)(S * j + r) * lda + S * j + 2 * c2);
+    for (int i = 0; i < S; ++i) v[i] = Dl[i * S + lane] + K[i * S + lane];
+    int flags = 0;
+    warp_inverse(v, lane, flags);
+    double* out = A + (int64_t)(S * j) * lda + S * j;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      B[i * LD + lane] = v[i];
+      Yd[i * LD + lane] = v[i];
+      out[(int64_t)i * lda + lane] = v[i];
     }
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (flags && lane == 0) atomicOr(&info[m].flags, flags);
     __syncwarp();
-  };
+  }
   auto op_of = [&](int st) -> const double2* {
     return reinterpret_cast<const double2*>(st < j ? G + (int64_t)(j - 1 - st) * BLK : H + (int64_t)(st + 1) * BLK);
   };
-  load_diag();
   const int steps = nb - 1;
   double2 cur[16], nxt[16];
   {
@@ -314,7 +347,14 @@ __global__ void __launch_bounds__(CW * 32, 2)
 #pragma unroll
       for (int q = 0; q < 16; ++q) nxt[q] = o[q * 32 + lane];
     }
-    if (st == j && j > 0) load_diag();  // the downward chain starts again from Y_jj
+    if (st == j && j > 0) {  // the downward chain starts again from Y_jj
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int e = lane + 32 * q, r = e >> 4, c2 = e & 15;
+        *reinterpret_cast<double2*>(B + r * LD + 2 * c2) = *reinterpret_cast<const double2*>(Yd + r * LD + 2 * c2);
+      }
+      __syncwarp();
+    }
     const int i = st < j ? j - 1 - st : st + 1;
     double acc[4][4][2];
 #pragma unroll
@@ -366,14 +406,17 @@ int band_invert(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t b
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(band_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(FactorSmem)) != cudaSuccess)
+                             (int)sizeof(FactorSmem)) != cudaSuccess ||
+        cudaFuncSetAttribute(band_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM) !=
+            cudaSuccess)
       return RDB_ECUDA;
     attr = true;
   }
   const int nb = (int)(n_pad / S);
-  band_factor_kernel<<<(unsigned)batch, 256, sizeof(FactorSmem), st>>>(a, lda, stride, nb, nonband, 1, ws, info, 1);
-  band_chain_kernel<<<dim3((unsigned)((nb + CW - 1) / CW), (unsigned)batch), CW * 32, 0, st>>>(a, lda, stride, nb,
-                                                                                            nonband, ws);
+  band_factor_kernel<<<(unsigned)((batch + GPC - 1) / GPC), 256 * GPC, sizeof(FactorSmem), st>>>(
+      a, lda, stride, nb, batch, nonband, ws, info);
+  band_chain_kernel<<<dim3((unsigned)((nb + CW - 1) / CW), (unsigned)batch), CW * 32, CHAIN_SMEM, st>>>(a, lda, stride, nb,
+                                                                                            nonband, ws, info);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }

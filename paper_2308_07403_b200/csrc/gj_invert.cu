@@ -41,6 +41,9 @@ __global__ void __launch_bounds__(p1::THREADS, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
   if (nonband && !nonband[b * info_stride]) return;
+#ifdef RDB_EXP_NO_P1
+  return;  // timing experiment only (tools/k2_split.py on a variant library): wrong results
+#endif
   p1::panel_inverse(*reinterpret_cast<p1::Smem*>(smem_raw), a + b * stride + off * lda + off, lda, idx0,
                     info + b * info_stride, first);
 }

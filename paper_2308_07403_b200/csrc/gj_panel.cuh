@@ -159,7 +159,9 @@ RDB_DEV void panel_inverse(Smem& s, double* __restrict__ A, int64_t lda, int p0,
   int mini = -1, flags = 0;
   for (int q0 = 0; q0 < NB; q0 += SQ) {
     if (t < 128) {
+#ifndef RDB_EXP_P1_NOINV
       inverse32(s, q0, minp, mini, flags);
+#endif
     } else {
       // copy the old S_rq (rows outside q) to T: the A operand of (iii)
       for (int e = t - 128; e < NB * SQ; e += THREADS - 128) {
@@ -170,7 +172,9 @@ RDB_DEV void panel_inverse(Smem& s, double* __restrict__ A, int64_t lda, int p0,
     __syncthreads();
     rowpanel32(s, q0);
     __syncthreads();
+#ifndef RDB_EXP_P1_NOUPD
     update32(s, q0);
+#endif
     __syncthreads();
   }
   for (int e = t; e < NB * NB / 2; e += THREADS) {

@@ -46,6 +46,9 @@ def time_case(name, bits, gammas, reps=5):
 
 
 def main():
+    if len(sys.argv) > 1:  # a variant library (make BUILD=... LIB=tools/_var/x.so EXTRA=-D...)
+        from paper_2308_07403_b200 import _lib as L
+        L._lib = L.load_library(sys.argv[1])
     bits, gammas, _ = wl.cfg2_batch(256)
     er = np.concatenate([bits[:128], bits[:128]])
     lat = np.concatenate([bits[128:], bits[128:]])
