@@ -8,7 +8,26 @@
 
 namespace rdb {
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
-                   rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits, int64_t n_bits);
+                   rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits, int64_t n_bits, bool band_ready);
+int* band_flags(void* work, int64_t n, int64_t batch);
+int band_detect(const uint32_t* bits, int64_t n, int64_t batch, int* nonband, cudaStream_t st);
+int build_m_bits_banded(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch, const double* gammas,
+                        double* out, int64_t stride_o, const int* nonband, cudaStream_t st);
+
+// K1 and K2 of the pipelines: banded matrices are detected first, so K1
+// writes only their band (the banded inverse overwrites the rest).
+static int build_and_invert(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch, const double* gammas,
+                            double* mwork, void* work, rdb_pivot_info* info, cudaStream_t st) {
+  const int64_t stride = n_pad * n_pad;
+  int* nonband = band_flags(work, n_pad, batch);
+  if (nonband) {
+    const int rc = band_detect(bits, n, batch, nonband, st);
+    if (rc) return rc;
+  }
+  int rc = build_m_bits_banded(bits, n, n_pad, batch, gammas, mwork, stride, nonband, st);
+  if (rc) return rc;
+  return invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, nonband != nullptr);
+}
 int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
                 const double* gammas, double gamma, uint8_t* d8_out, int64_t ldo, int64_t stride_o,
                 unsigned long long* counters, cudaStream_t st);
@@ -53,9 +72,7 @@ extern "C" int rdb_apsp_bits_batched(const uint32_t* bits, int64_t n, int64_t ba
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n_pad = (n + RDB_NB - 1) / RDB_NB * RDB_NB;
   const int64_t stride = n_pad * n_pad;
-  int rc = rdb_build_m_bits(bits, n, n_pad, batch, gammas, 0.0, mwork, n_pad, stride, stream);
-  if (rc) return rc;
-  rc = rdb::invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n);
+  const int rc = rdb::build_and_invert(bits, n, n_pad, batch, gammas, mwork, work, info, st);
   if (rc) return rc;
   return rdb::log_ceil(mwork, n, n_pad, stride, batch, gammas, 0.0, nullptr, nullptr, d32, n, n * n,
                        nullptr, 0, counters, st);
@@ -70,9 +87,7 @@ extern "C" int rdb_apsp_bits_batched_d8(const uint32_t* bits, int64_t n, int64_t
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n_pad = (n + RDB_NB - 1) / RDB_NB * RDB_NB;
   const int64_t stride = n_pad * n_pad;
-  int rc = rdb_build_m_bits(bits, n, n_pad, batch, gammas, 0.0, mwork, n_pad, stride, stream);
-  if (rc) return rc;
-  rc = rdb::invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n);
+  const int rc = rdb::build_and_invert(bits, n, n_pad, batch, gammas, mwork, work, info, st);
   if (rc) return rc;
   return rdb::log_ceil_d8(mwork, n, n_pad, stride, batch, gammas, 0.0, d8, n, n * n, counters, st);
 }

@@ -44,9 +44,13 @@ __global__ void build_m_kernel(const double* __restrict__ w, int64_t ldw, int64_
 // Bit-packed adjacency -> M. Thread handles 2 adjacent columns (double2 store).
 __global__ void build_m_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t n_pad,
                                     int64_t batch, const double* __restrict__ gammas, double gamma,
-                                    double* __restrict__ out, int64_t ldo, int64_t stride_o) {
+                                    double* __restrict__ out, int64_t ldo, int64_t stride_o,
+                                    const int* __restrict__ nonband) {
   // one warp per output row (grid-stride over batch * n_pad rows); lane l
   // writes columns 2l, 2l+1 of every 64-column chunk: 512 B per store wave.
+  // nonband (APSP pipelines): a matrix the banded inverse takes (nonband[b] ==
+  // 0) gets only the 64-column chunks covering its 32-block tridiagonal band,
+  // the blocks band_factor_kernel reads (the inverse overwrites the rest).
   const int lane = threadIdx.x & 31;
   const int64_t wpr = (n + 31) / 32;
   const int64_t rows = n_pad * batch;
@@ -56,7 +60,13 @@ __global__ void build_m_bits_kernel(const uint32_t* __restrict__ bits, int64_t n
     const double ng = -(gammas ? gammas[b] : gamma);
     const uint32_t* row = bits + (b * n + i) * wpr;
     double* O = out + b * stride_o + i * ldo;
-    for (int64_t j0 = 0; j0 < n_pad; j0 += 64) {
+    int64_t jb = 0, je = n_pad;
+    if (nonband && !nonband[b]) {
+      const int64_t bi = i / 32;
+      jb = bi > 0 ? ((32 * (bi - 1)) & ~(int64_t)63) : 0;
+      je = ((32 * (bi + 2) + 63) & ~(int64_t)63) < n_pad ? ((32 * (bi + 2) + 63) & ~(int64_t)63) : n_pad;
+    }
+    for (int64_t j0 = jb; j0 < je; j0 += 64) {
       const int64_t j = j0 + 2 * lane;
       const int64_t wi = j0 >> 5;  // two words cover this 64-column chunk
       uint32_t w0 = 0, w1 = 0;
@@ -158,10 +168,28 @@ extern "C" int rdb_build_m_bits(const uint32_t* bits, int64_t n, int64_t n_pad, 
   const int64_t rows = n_pad * batch;
   const int64_t blocks = (rows + 7) / 8 < 148 * 32 ? (rows + 7) / 8 : 148 * 32;
   build_m_bits_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      bits, n, n_pad, batch, gammas, gamma, out, ldo, stride_o);
+      bits, n, n_pad, batch, gammas, gamma, out, ldo, stride_o, nullptr);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
+
+namespace rdb {
+// The APSP pipelines' K1 (apsp.cu): as rdb_build_m_bits (same checks), band
+// rows only for the matrices the banded inverse takes.
+int build_m_bits_banded(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch, const double* gammas,
+                        double* out, int64_t stride_o, const int* nonband, cudaStream_t st) {
+  if (!nonband) return rdb_build_m_bits(bits, n, n_pad, batch, gammas, 0.0, out, n_pad, stride_o, st);
+  if (!bits || !out || !gammas || n <= 0 || n_pad < n || n_pad % 64 || batch <= 0 || batch > 65535 ||
+      ((uintptr_t)out & 15))
+    return RDB_EINVAL;
+  const int64_t rows = n_pad * batch;
+  const int64_t blocks = (rows + 7) / 8 < 148 * 32 ? (rows + 7) / 8 : 148 * 32;
+  build_m_bits_kernel<<<(unsigned)blocks, 256, 0, st>>>(bits, n, n_pad, batch, gammas, 0.0, out, n_pad, stride_o,
+                                                        nonband);
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+}  // namespace rdb
 
 extern "C" int rdb_pad_identity(double* a, int64_t n, int64_t n_pad, int64_t lda, int64_t stride,
                                 int64_t batch, void* stream) {

@@ -696,8 +696,18 @@ static std::mutex g_enqueue;
 // pattern comes from the bit-packed adjacency when the caller has it (`bits`,
 // n_bits vertices: the rdb_apsp_bits_batched pipelines), else from a scan of
 // the matrices.
+// The banded path's per-matrix flags in a batched workspace, or nullptr when
+// invert_batched will not use the banded path for (n, batch). The APSP
+// pipelines fill them before K1 (band_detect) and pass band_ready.
+int* band_flags(void* work, int64_t n, int64_t batch) {
+  const BatchWs ws(n, batch);
+  if (!work || batch <= 1 || n % NB || !ws.has_plan() || !skip_enabled() || !band_enabled()) return nullptr;
+  return reinterpret_cast<int*>(static_cast<char*>(work) + ws.band);
+}
+
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
-                   rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits = nullptr, int64_t n_bits = 0) {
+                   rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits = nullptr, int64_t n_bits = 0,
+                   bool band_ready = false) {
   std::lock_guard<std::mutex> guard(g_enqueue);
   if (batch == 1 && n >= wide_min_n() && n % (2 * NB) == 0 && a && work && info && lda >= n && !(lda & 1) &&
       !((uintptr_t)a & 15) && !((uintptr_t)work & 15))
@@ -709,12 +719,13 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   const int64_t ntl = n / NB;
   const int64_t pld = pat_ld((int)ntl);
   unsigned char* pat = use_plan ? reinterpret_cast<unsigned char*>(wb + ws.blk) : nullptr;
-  const bool use_band = use_plan && bits && band_enabled() && info && lda >= n;
+  const bool use_band = use_plan && bits && (band_ready || band_enabled()) && info && lda >= n;
+  if (band_ready && !use_band) return RDB_EINVAL;  // K1 has skipped the off-band blocks: must not run GJ on them
   int* nonband = use_band ? reinterpret_cast<int*>(wb + ws.band) : nullptr;
   double* band_ws = use_band ? reinterpret_cast<double*>(wb + ws.band_ws) : nullptr;
   if (use_plan) {
     if (cudaMemsetAsync(pat, 0, (size_t)(batch * 2 * ntl * pld), st) != cudaSuccess) return RDB_ECUDA;
-    if (use_band) {
+    if (use_band && !band_ready) {
       const int rc = band_detect(bits, n_bits, batch, nonband, st);
       if (rc) return rc;
     }
