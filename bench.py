@@ -293,7 +293,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=32)
-    ap.add_argument("--e2e-chunk", type=int, default=128, help="graphs per pipelined chunk in the e2e engine")
+    ap.add_argument("--e2e-chunk", type=int, default=256, help="graphs per pipelined chunk in the e2e engine")
     ap.add_argument("--e2e-steps", type=int, default=16,
                     help="steps of the streaming e2e measurement (at least --steps): the pipeline's fill and drain "
                          "(first upload, last download) are paid once per run, so short runs understate throughput")

@@ -307,7 +307,8 @@ def check_infos(infos: list[L.PivotInfo], gammas: np.ndarray, first_index: int =
 class APSPBatchEngine:
     """Reusable pipeline: pinned host bits -> device -> int32 D -> pinned host.
 
-    All kernels run back to back on one compute stream, chunk by chunk; a copy
+    All kernels run back to back on one compute stream, chunk by chunk (one
+    rdb_apsp_bits_batched[_d8] pipeline call per chunk); a copy
     stream moves each chunk's int32 D to pinned host memory as soon as its K3
     finishes (CUDA events), so the device->host transfer of chunk i overlaps
     the kernels of chunks i+1, i+2, ... Two D slots ping-pong; the M / work
@@ -349,6 +350,7 @@ class APSPBatchEngine:
         self.inputs: list = [None, None]
         self.done = [torch.cuda.Event() for _ in range(2)]
         self.pending = [0, 0]
+        self.dslot = 0
         self.launches = 0
 
     def pin(self, bits: np.ndarray, gammas) -> tuple[torch.Tensor, torch.Tensor]:
@@ -389,23 +391,18 @@ class APSPBatchEngine:
             if self.d_dtype == torch.uint8:
                 counters[:batch].zero_()
         for idx, c0 in enumerate(range(0, batch, self.chunk)):
-            s = idx % 2
+            s = self.dslot  # D slots alternate over every chunk ever submitted
+            self.dslot ^= 1
             cnt = min(self.chunk, batch - c0)
             with torch.cuda.stream(self.cs):
                 self.cs.wait_event(self.uploaded[slot][idx])
-                sh = self.cs.cuda_stream
-                lib = L.lib()
-                L.check(lib.rdb_build_m_bits(bits[c0].data_ptr(), self.n, self.n_pad, cnt, gam[c0:].data_ptr(), 0.0,
-                                             self.m.data_ptr(), self.n_pad, self.n_pad * self.n_pad, sh),
-                        "rdb_build_m_bits")
-                L.check(lib.rdb_invert_batched_bits(self.m.data_ptr(), self.n_pad, self.n_pad,
-                                                    self.n_pad * self.n_pad, cnt, bits[c0].data_ptr(), self.n,
-                                                    self.work.data_ptr(), info[c0 * 16 :].data_ptr(), sh),
-                        "rdb_invert_batched_bits")
-                # D slot s must have drained to the host (this batch's chunk
-                # idx-2, or the previous batch's last chunk in that slot)
+                # D slot s must have drained to the host (the chunk submitted
+                # two chunks earlier, in this batch or the previous one)
                 self.cs.wait_event(self.copied[s])
-                log_ceil_call(self.m, self.n, cnt, gam[c0:], self.d[s], counters[c0:], sh)
+                # K1 -> K2 -> K3 in one pipeline call (banded graphs detected
+                # before K1, which then writes only their band)
+                apsp_call(bits[c0:], self.n, cnt, gam[c0:], self.m, self.work, info[c0 * 16 :], self.d[s],
+                          counters[c0:], self.cs.cuda_stream)
                 self.launches += launches_per_call(self.n, cnt)
                 self.computed[s].record(self.cs)
             with torch.cuda.stream(self.xs):
