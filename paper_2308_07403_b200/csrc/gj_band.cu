@@ -46,7 +46,6 @@ constexpr int CW = 4;          // warps (block columns) per chain CTA
 // Workspace per matrix: G[nb] and H[nb] in A-fragment order, D[nb] and K[nb] row-major.
 size_t ws_doubles(int64_t n_pad) { return (size_t)4 * (size_t)(n_pad / S) * BLK; }
 constexpr int GPC = 2;         // matrices per factor CTA
-constexpr size_t CHAIN_SMEM = (size_t)CW * 2 * SBUF * sizeof(double);
 
 RDB_DEV void gbar(int id) { asm volatile("bar.sync %0, 128;\n" ::"r"(id) : "memory"); }
 
@@ -198,20 +197,39 @@ RDB_DEV void warp_inverse(double (&v)[S], int lane, int& flags) {
 using namespace band;
 
 // nonband[b] = 1 unless every edge of graph b lies in the 32-block tridiagonal
-// band (word q of row i non-zero only for |q - i / 32| <= 1). Warp per row;
-// the caller zeroes nonband first.
+// band (word q of row i non-zero only for |q - i / 32| <= 1). A thread per
+// 16-byte group of words (coalesced over the whole batch); the caller zeroes
+// nonband first. Rows whose word count is not a multiple of 4 take the
+// word-by-word loop.
 __global__ void band_detect_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t batch,
                                         int* __restrict__ nonband) {
-  const int lane = threadIdx.x & 31;
   const int64_t wpr = (n + 31) / 32;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < batch * n; w += nwarps) {
-    const int64_t b = w / n, i = w - b * n, bi = i / 32;
-    if (*(volatile int*)(nonband + b)) continue;  // warp-uniform
-    bool bad = false;
-    for (int64_t q = lane; q < wpr; q += 32)
-      if ((q < bi - 1 || q > bi + 1) && __ldg(bits + (b * n + i) * wpr + q)) bad = true;
-    if (__any_sync(0xffffffffu, bad) && lane == 0) nonband[b] = 1;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((wpr & 3) == 0 && !((uintptr_t)bits & 15)) {
+    const int64_t q4r = wpr / 4;  // uint4 per row
+    const uint4* b4 = reinterpret_cast<const uint4*>(bits);
+    for (int64_t e = t0; e < batch * n * q4r; e += nthreads) {
+      const int64_t row = e / q4r, q0 = 4 * (e - row * q4r);
+      const int64_t b = row / n, bi = (row - b * n) / 32;
+      if (q0 + 3 >= bi - 1 && q0 <= bi + 1) {  // the group touches the band: check its outside words
+        const uint4 v = __ldg(b4 + e);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bad |= (q0 + k < bi - 1 || q0 + k > bi + 1) && w[k];
+        if (bad) nonband[b] = 1;
+      } else {
+        const uint4 v = __ldg(b4 + e);
+        if (v.x | v.y | v.z | v.w) nonband[b] = 1;
+      }
+    }
+  } else {
+    for (int64_t e = t0; e < batch * n * wpr; e += nthreads) {
+      const int64_t row = e / wpr, q = e - row * wpr;
+      const int64_t b = row / n, bi = (row - b * n) / 32;
+      if ((q < bi - 1 || q > bi + 1) && __ldg(bits + e)) nonband[b] = 1;
+    }
   }
 }
 
@@ -296,7 +314,18 @@ __global__ void __launch_bounds__(256 * GPC, 1)
 // Block column j per warp: Y_jj = (D_j + K_j)^-1 (warp Gauss-Jordan, flags
 // ORed into the pivot record), then up the column (Y_ij = G_i Y_{i+1,j},
 // i = j-1 .. 0) and down (Y_ij = H_i Y_{i-1,j}, i = j+1 .. nb-1): nb - 1
-// products per warp. Reads only the workspace, writes every block of M.
+// products per warp. The operator G_i / H_i of the next product streams into
+// a second shared-memory buffer (cp.async, each lane copies the 16-byte
+// fragment pairs it reads itself) while the current one multiplies. Reads only
+// the workspace (and its own Y_jj), writes every block of M.
+constexpr size_t CHAIN_SMEM = (size_t)CW * (SBUF + 2 * BLK) * sizeof(double);
+
+RDB_DEV void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+RDB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+RDB_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
 __global__ void __launch_bounds__(CW * 32, 2)
     band_chain_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int nb, const int* __restrict__ nonband,
                       const double* __restrict__ ws, rdb_pivot_info* __restrict__ info) {
@@ -306,55 +335,55 @@ __global__ void __launch_bounds__(CW * 32, 2)
   const int j = blockIdx.x * CW + warp;
   if (j >= nb) return;  // warp-uniform; only warp-level synchronisation below
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* B = reinterpret_cast<double*>(smem_raw) + warp * 2 * SBUF;  // the running block (B operand)
-  double* Yd = B + SBUF;                                              // Y_jj, the start of both chains
+  double* B = reinterpret_cast<double*>(smem_raw) + warp * (SBUF + 2 * BLK);  // the running block (B operand)
+  double2* Abuf = reinterpret_cast<double2*>(B + SBUF);                      // 2 x BLK: operators, fragment order
   double* A = a + m * stride;
   const double* G = ws + m * 4 * (int64_t)nb * BLK;
   const double* H = G + (int64_t)nb * BLK;
   const double* Dl = H + (int64_t)nb * BLK + (int64_t)j * BLK;
   const double* K = Dl + (int64_t)nb * BLK;
+  double* diag = A + (int64_t)(S * j) * lda + S * j;
   const int lr = lane >> 2, lk = lane & 3;
+  auto op_of = [&](int st) -> const double2* {
+    return reinterpret_cast<const double2*>(st < j ? G + (int64_t)(j - 1 - st) * BLK : H + (int64_t)(st + 1) * BLK);
+  };
+  auto fetch = [&](int st) {  // this lane's 16 fragment pairs of operator st into buffer st & 1
+    const double2* src = op_of(st);
+    double2* dst = Abuf + (st & 1) * (BLK / 2);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) cp_async16(dst + q * 32 + lane, src + q * 32 + lane);
+    cp_async_commit();
+  };
+  const int steps = nb - 1;
+  fetch(0);
   {
     double v[S];
 #pragma unroll
     for (int i = 0; i < S; ++i) v[i] = Dl[i * S + lane] + K[i * S + lane];
     int flags = 0;
     warp_inverse(v, lane, flags);
-    double* out = A + (int64_t)(S * j) * lda + S * j;
 #pragma unroll
     for (int i = 0; i < S; ++i) {
       B[i * LD + lane] = v[i];
-      Yd[i * LD + lane] = v[i];
-      out[(int64_t)i * lda + lane] = v[i];
+      diag[(int64_t)i * lda + lane] = v[i];
     }
     flags = __reduce_or_sync(0xffffffffu, flags);
     if (flags && lane == 0) atomicOr(&info[m].flags, flags);
     __syncwarp();
   }
-  auto op_of = [&](int st) -> const double2* {
-    return reinterpret_cast<const double2*>(st < j ? G + (int64_t)(j - 1 - st) * BLK : H + (int64_t)(st + 1) * BLK);
-  };
-  const int steps = nb - 1;
-  double2 cur[16], nxt[16];
-  {
-    const double2* o = op_of(0);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) cur[q] = o[q * 32 + lane];
-  }
   for (int st = 0; st < steps; ++st) {
-    if (st + 1 < steps) {
-      const double2* o = op_of(st + 1);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) nxt[q] = o[q * 32 + lane];
-    }
-    if (st == j && j > 0) {  // the downward chain starts again from Y_jj
+    if (st + 1 < steps) fetch(st + 1);
+    else cp_async_commit();  // empty group: wait_group 1 below still retires operator st
+    if (st == j && j > 0) {  // the downward chain starts again from Y_jj (written above by this warp)
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int e = lane + 32 * q, r = e >> 4, c2 = e & 15;
-        *reinterpret_cast<double2*>(B + r * LD + 2 * c2) = *reinterpret_cast<const double2*>(Yd + r * LD + 2 * c2);
+        *reinterpret_cast<double2*>(B + r * LD + 2 * c2) = *reinterpret_cast<const double2*>(diag + (int64_t)r * lda + 2 * c2);
       }
       __syncwarp();
     }
+    cp_async_wait1();
+    const double2* As = Abuf + (st & 1) * (BLK / 2);
     const int i = st < j ? j - 1 - st : st + 1;
     double acc[4][4][2];
 #pragma unroll
@@ -366,12 +395,12 @@ __global__ void __launch_bounds__(CW * 32, 2)
       double bf[4];
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) bf[ni] = B[(4 * ks + lk) * LD + 8 * ni + lr];
+      const double2 a01 = As[(2 * ks) * 32 + lane], a23 = As[(2 * ks + 1) * 32 + lane];
+      const double af[4] = {a01.x, a01.y, a23.x, a23.y};
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const double af = (mi & 1) ? cur[2 * ks + (mi >> 1)].y : cur[2 * ks + (mi >> 1)].x;
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
-      }
+        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
     }
     __syncwarp();
     double* out = A + (int64_t)(S * i) * lda + S * j;
@@ -385,8 +414,6 @@ __global__ void __launch_bounds__(CW * 32, 2)
         stg2(out + (int64_t)row * lda + col, v);
       }
     __syncwarp();
-#pragma unroll
-    for (int q = 0; q < 16; ++q) cur[q] = nxt[q];
   }
 }
 
@@ -394,8 +421,9 @@ __global__ void __launch_bounds__(CW * 32, 2)
 // ws_doubles(n_pad) per matrix; nonband (batch ints) filled by band_detect().
 int band_detect(const uint32_t* bits, int64_t n, int64_t batch, int* nonband, cudaStream_t st) {
   if (cudaMemsetAsync(nonband, 0, sizeof(int) * (size_t)batch, st) != cudaSuccess) return RDB_ECUDA;
-  const int64_t want = (batch * n + 7) / 8;
-  band_detect_bits_kernel<<<(unsigned)(want < 148 * 16 ? want : 148 * 16), 256, 0, st>>>(bits, n, batch, nonband);
+  const int64_t want = (batch * n * ((n + 31) / 32) / 4 + 255) / 256;
+  band_detect_bits_kernel<<<(unsigned)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8), 256, 0, st>>>(bits, n, batch,
+                                                                                                    nonband);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
