@@ -339,6 +339,20 @@ RDB_DEV double dceil_estimate_lean(double v, double inv_lg, double thr, LeanTab 
   return q;
 }
 
+// The same estimate with the mantissa's log2 from MUFU.LG2 on its leading 23
+// bits (dceil_value's estimate: absolute error < 4e-7 in log2 y, so the
+// quotient's error is < 4e-7 / |log2 gamma| = thr / 10 with thr as below): no
+// table lookups. need as dceil_estimate_lean (non-positive, subnormal,
+// non-finite, or within thr of an integer).
+RDB_DEV double dceil_estimate_mufu(double v, double inv_lg2, double thr, bool& need) {
+  const int hi = __double2hiint(v), lo = __double2loint(v);
+  const int ex = hi >> 20;  // sign bit set (v <= -0) -> ex < 0 -> need
+  const float mf = __int_as_float(((hi & 0x000FFFFF) << 3) | ((unsigned)lo >> 29) | 0x3F800000);
+  const double q = ((double)(ex - 1023) + (double)__log2f(mf)) * inv_lg2;
+  need = ((unsigned)(ex - 1) >= 2046u) | !(fabs(q - rint(q)) > thr);
+  return q;
+}
+
 // D-only K3 for whole n x n matrices, the batch path (no mask, no column map):
 // one warp per row, each lane owns 4 consecutive columns of a 128-column block
 // (two 16-byte loads; a warp stores 128 contiguous bytes of uint8 D or 512 of
@@ -346,6 +360,9 @@ RDB_DEV double dceil_estimate_lean(double v, double inv_lg, double thr, LeanTab 
 // outside [0, RDB_D8_MAX] (RDB_CNT_D8_RANGE).
 // one block of loads in flight ahead, main loop unrolled twice (measured
 // best of PF 1-3 x unroll 1-4 on the config-2 batch, tools/time_k3.py)
+#ifndef RDB_K3_MUFU
+#define RDB_K3_MUFU 1
+#endif
 #ifndef LEAN_PF
 #define LEAN_PF 1
 #endif
@@ -381,6 +398,12 @@ __global__ void __launch_bounds__(256)
     const double* Y = y + b * stride_y + (int64_t)i * ldy;
     const int64_t orow = b * stride_o + (int64_t)i * ldo;
     unsigned neg = 0, bad = 0;
+#if RDB_K3_MUFU
+    const double inv_lg2 = 0.6931471805599453 * inv_lg;  // 1 / log2(gamma)
+    // common path: the estimate, diagonal 0; D > RDB_D8_MAX or < 0 (u8) are
+    // tracked by an unsigned max and counted below only when it exceeds the range
+    unsigned dmax = 0;
+#endif
     auto block = [&](int j, double2 p, double2 q) {
       const double v[4] = {p.x, p.y, q.x, q.y};
       int d[4];
@@ -388,11 +411,17 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         bool nd;
+#if RDB_K3_MUFU
+        const double r = dceil_estimate_mufu(v[e], inv_lg2, thr, nd);
+#else
         const double r = dceil_estimate_lean(v[e], inv_lg, thr, lt, nd);
+#endif
         const bool dg = j + e == i;
         need |= (unsigned)(nd && !dg) << e;
         d[e] = (dg || nd) ? 0 : __double2int_ru(r);
+#if !RDB_K3_MUFU
         neg += v[e] < NEGATIVE_ENTRY_TOL;
+#endif
       }
       if (need) {  // rare: exact path (static indices keep v / d in registers)
 #pragma unroll
@@ -402,8 +431,26 @@ __global__ void __launch_bounds__(256)
             d[e] = __double2int_ru(r);  // +inf -> INT32_MAX, the int32 sentinel
             if (DK == DK_U8 && r == __longlong_as_double(0x7FF0000000000000LL)) d[e] = -2;  // unreachable
             if (DK == DK_U8 && r != r) d[e] = -1;  // NaN: out of range
+#if RDB_K3_MUFU
+            neg += v[e] < NEGATIVE_ENTRY_TOL;  // a negative entry always takes this path (sign bit -> need)
+            if (DK == DK_U8) {  // resolve here: the common path below sees only 0 .. 254 or a range error
+              const bool unreachable = d[e] == -2;
+              const bool ok = (unsigned)d[e] <= (unsigned)RDB_D8_MAX;
+              bad += !ok && !unreachable;
+              d[e] = unreachable ? RDB_D8_UNREACHABLE : (ok ? d[e] : RDB_D8_MAX);
+            }
+#endif
           }
       }
+#if RDB_K3_MUFU
+      if (DK == DK_U8) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const unsigned u = (need >> e) & 1u ? 0u : (unsigned)d[e];  // exact-path values already resolved
+          dmax = max(dmax, u);
+          d[e] = (need >> e) & 1u ? d[e] : (int)min(u, (unsigned)RDB_D8_MAX);
+        }
+#else
       if (DK == DK_U8) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -412,6 +459,7 @@ __global__ void __launch_bounds__(256)
           bad += !ok && !unreachable;
           d[e] = unreachable ? RDB_D8_UNREACHABLE : (ok ? d[e] : RDB_D8_MAX);
         }
+#endif
         *reinterpret_cast<uchar4*>(static_cast<uint8_t*>(dout) + orow + j) =
             make_uchar4((uint8_t)d[0], (uint8_t)d[1], (uint8_t)d[2], (uint8_t)d[3]);
       } else {
@@ -454,6 +502,18 @@ __global__ void __launch_bounds__(256)
       }
       neg += v < NEGATIVE_ENTRY_TOL;
     }
+#if RDB_K3_MUFU
+    if (lane == 0 && i < nfull) neg += Y[i] < NEGATIVE_ENTRY_TOL;  // the diagonal (skips the exact path)
+    if (DK == DK_U8 && __any_sync(0xffffffffu, dmax > (unsigned)RDB_D8_MAX)) {
+      // rare: some common-path D left 0 .. 254; count them (the stored value is
+      // already the clamp): re-derive the row's common-path D's
+      for (int j = lane; j < nfull; j += 32) {
+        bool nd;
+        const double r = dceil_estimate_mufu(Y[j], inv_lg2, thr, nd);
+        if (!nd && j != i) bad += (unsigned)__double2int_ru(r) > (unsigned)RDB_D8_MAX;
+      }
+    }
+#endif
     if (counters) {
       neg = __reduce_add_sync(0xffffffffu, neg);
       if (DK == DK_U8) bad = __reduce_add_sync(0xffffffffu, bad);

@@ -14,6 +14,7 @@ from paper_2308_07403_b200 import workloads as wl  # noqa: E402
 
 bits, gammas, _ = wl.cfg2_batch(256)
 dev = torch.device("cuda", 0)
+first = {}
 for path in sys.argv[1:]:
     L._lib = L.load_library(path)
     res = {"lib": path}
@@ -32,6 +33,8 @@ for path in sys.argv[1:]:
         torch.cuda.synchronize()
         t = ev[0].elapsed_time(ev[1]) / 10
         byt = 256 * 1024 * 1024 * (8 + buf.d.element_size())
-        res[dt] = {"ms": t, "GBps": byt / t / 1e6}
+        d = buf.d.cpu()
+        first.setdefault(dt, d)
+        res[dt] = {"ms": t, "GBps": byt / t / 1e6, "same_d_as_first_lib": bool(torch.equal(d, first[dt]))}
         del buf
     print(json.dumps(res), flush=True)
