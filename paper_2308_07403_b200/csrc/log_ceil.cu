@@ -58,7 +58,17 @@ struct LogTab {
   RDB_DEV double L(int i) const { return lo[i][threadIdx.x & 15]; }
 };
 
-RDB_DEV double fast_log(double y, const LogTab& T) {
+// The same table read straight from constant memory: for kernels whose common
+// path needs no table (the MUFU estimate), so the rare exact path costs no
+// shared memory (full occupancy) and no per-block staging.
+struct ConstTab {
+  RDB_DEV double C(int i) const { return logtab::kC[i]; }
+  RDB_DEV double H(int i) const { return logtab::kLhi[i]; }
+  RDB_DEV double L(int i) const { return logtab::kLlo[i]; }
+};
+
+template <class Tab>
+RDB_DEV double fast_log(double y, const Tab& T) {
   long long b = __double_as_longlong(y);
   int ex = (int)(b >> 52);
   int esub = 0;
@@ -86,7 +96,8 @@ RDB_DEV double fast_log(double y, const LogTab& T) {
   return s + (t + fma(e, logtab::LN2_LO, T.L(idx)) + p);
 }
 
-RDB_DEV double rdist_value(double v, double g, double lg, double inv_lg, const LogTab& T) {
+template <class Tab>
+RDB_DEV double rdist_value(double v, double g, double lg, double inv_lg, const Tab& T) {
   if (!(v > 0.0)) return INFINITY;
   if (!(v < INFINITY)) return -INFINITY;  // log(inf) / log(gamma), as numpy
   const double r = fast_log(v, T) * inv_lg;
@@ -358,8 +369,10 @@ RDB_DEV double dceil_estimate_mufu(double v, double inv_lg2, double thr, bool& n
 // (two 16-byte loads; a warp stores 128 contiguous bytes of uint8 D or 512 of
 // int32 D), two blocks in flight per lane. uint8 D: `bad` counts entries
 // outside [0, RDB_D8_MAX] (RDB_CNT_D8_RANGE).
-// one block of loads in flight ahead, main loop unrolled twice (measured
-// best of PF 1-3 x unroll 1-4 on the config-2 batch, tools/time_k3.py)
+// one block of loads in flight ahead, main loop not unrolled, registers capped
+// at 64 (4 blocks per SM; the common path needs no shared table): measured
+// best of PF 1-2 x unroll 1-2 x 1/4/5/6 blocks per SM on the config-2 batch
+// (tools/time_k3.py: uint8 D 0.56 -> 0.48 ms, int32 D 0.61 -> 0.53 ms)
 #ifndef RDB_K3_MUFU
 #define RDB_K3_MUFU 1
 #endif
@@ -367,14 +380,24 @@ RDB_DEV double dceil_estimate_mufu(double v, double inv_lg2, double thr, bool& n
 #define LEAN_PF 1
 #endif
 #ifndef LEAN_UNROLL
-#define LEAN_UNROLL 2
+#define LEAN_UNROLL 1
+#endif
+#ifndef LEAN_MINB
+#define LEAN_MINB 4
+#endif
+#ifndef LEAN_GRID_PER_SM
+#define LEAN_GRID_PER_SM 16
 #endif
 constexpr int kLeanUnroll = LEAN_UNROLL;
 template <int DK>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, LEAN_MINB)
     log_ceil_lean_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
                          const double* __restrict__ gammas, double gamma, void* __restrict__ dout, int64_t ldo,
                          int64_t stride_o, unsigned long long* __restrict__ counters) {
+#if RDB_K3_MUFU
+  const ConstTab tab;  // exact path only
+  const int lane = threadIdx.x & 31;
+#else
   __shared__ LogTab tab;
   for (int e = threadIdx.x; e < 128 * 16; e += blockDim.x) {
     const int i = e >> 4, k = e & 15;
@@ -385,6 +408,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const LeanTab lt{&tab.c[0][lane & 15], &tab.hi[0][lane & 15]};
+#endif
   const int64_t rows = n * batch;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int nfull = (int)(n & ~(int64_t)127);
@@ -598,7 +622,7 @@ int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64
   auto al = [](const void* p, uintptr_t a) { return ((uintptr_t)p % a) == 0; };
   const int64_t rows = n * batch;
   const int64_t want = (rows + 7) / 8;
-  const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+  const unsigned blocks = (unsigned)(want < 148 * LEAN_GRID_PER_SM ? want : 148 * LEAN_GRID_PER_SM);
   if (!(ldy & 1) && !(stride_y & 1) && !(ldo & 3) && !(stride_o & 3) && al(y, 16) && al(d8_out, 4) &&
       n < (int64_t)1 << 31) {
     log_ceil_lean_kernel<DK_U8><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d8_out, ldo,

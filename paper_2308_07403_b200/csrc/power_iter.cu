@@ -21,7 +21,12 @@ namespace rdb {
 
 constexpr int PI_THREADS = 512;
 
-__global__ void __launch_bounds__(PI_THREADS)
+// matrix element as the GEMV reads it: the value, or isfinite(a) as 0/1
+RDB_DEV double elem(double a, int indicator) {
+  return indicator ? ((fabs(a) <= 1.7976931348623157e308) ? 1.0 : 0.0) : a;
+}
+
+__global__ void __launch_bounds__(PI_THREADS, 2)
     power_kernel(const double* __restrict__ m, int64_t n, int64_t ldm, int indicator, double tol,
                  int64_t max_iter, double* __restrict__ v, double* __restrict__ w,
                  double* __restrict__ partial, double* __restrict__ result) {
@@ -33,6 +38,9 @@ __global__ void __launch_bounds__(PI_THREADS)
   const int64_t gtid = (int64_t)blockIdx.x * PI_THREADS + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * PI_THREADS;
 
+  // 16-byte row loads when every row start is 16-byte aligned (v is: workspace start)
+  const bool vec = !(ldm & 1) && !((uintptr_t)m & 15);
+  const int64_t n2 = n & ~(int64_t)1;
   const double v0 = 1.0 / sqrt((double)n);
   for (int64_t i = gtid; i < n; i += nthreads) v[i] = v0;
   grid.sync();
@@ -44,10 +52,30 @@ __global__ void __launch_bounds__(PI_THREADS)
     for (int64_t i = gwarp; i < n; i += nwarps) {
       const double* row = m + i * ldm;
       double s = 0.0;
-      for (int64_t j = lane; j < n; j += 32) {
-        const double a = row[j];
-        const double x = indicator ? ((fabs(a) <= 1.7976931348623157e308) ? 1.0 : 0.0) : a;
-        s = fma(x, v[j], s);
+      if (vec) {
+        // lane owns columns 2 lane + 64 k (16-byte loads), four loads in flight
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int64_t j = 2 * lane;
+        for (; j + 192 < n2; j += 256) {
+          double2 a[4], x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a[u] = __ldcs(reinterpret_cast<const double2*>(row + j + 64 * u));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = *reinterpret_cast<const double2*>(v + j + 64 * u);
+          s = fma(elem(a[0].x, indicator), x[0].x, fma(elem(a[0].y, indicator), x[0].y, s));
+          s1 = fma(elem(a[1].x, indicator), x[1].x, fma(elem(a[1].y, indicator), x[1].y, s1));
+          s2 = fma(elem(a[2].x, indicator), x[2].x, fma(elem(a[2].y, indicator), x[2].y, s2));
+          s3 = fma(elem(a[3].x, indicator), x[3].x, fma(elem(a[3].y, indicator), x[3].y, s3));
+        }
+        for (; j < n2; j += 64) {
+          const double2 a = __ldcs(reinterpret_cast<const double2*>(row + j));
+          const double2 x = *reinterpret_cast<const double2*>(v + j);
+          s = fma(elem(a.x, indicator), x.x, fma(elem(a.y, indicator), x.y, s));
+        }
+        s = (s + s1) + (s2 + s3);
+        if (lane == 0 && n2 < n) s = fma(elem(row[n2], indicator), v[n2], s);
+      } else {
+        for (int64_t j = lane; j < n; j += 32) s = fma(elem(row[j], indicator), v[j], s);
       }
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) {

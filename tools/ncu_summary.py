@@ -64,7 +64,7 @@ def summarise(path):
 def families(launches):
     """Per kernel family: launches, total / average duration, DRAM bytes,
     duration-weighted DMMA pipe activity, and the K2 bytes of the capture
-    (every gj_* / pattern / plan launch: one call when the capture is one call)."""
+    (every gj_* / band_* / pattern / plan launch: one call when the capture is one call)."""
     fam = {}
     for r in launches:
         k = r["kernel"].split("(")[0].replace("void ", "").split("<")[0].replace("rdb::", "")
@@ -78,7 +78,8 @@ def families(launches):
         f["avg_ns"] = f["total_ns"] / f["launches"]
         f["share"] = f["total_ns"] / tot
         f["dmma_pipe_active_pct"] = f.pop("_dmma") / max(f["total_ns"], 1.0)
-    k2 = sum(f["dram_bytes"] for k, f in fam.items() if k.startswith("gj_") or "pattern" in k)
+    k2 = sum(f["dram_bytes"] for k, f in fam.items()
+             if k.startswith(("gj_", "band_")) or "pattern" in k)
     return fam, k2
 
 
