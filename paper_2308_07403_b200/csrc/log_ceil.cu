@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256)
     const double lg = log(g);
     const double inv_lg = 1.0 / lg;
     const double inv_lg2 = 0.6931471805599453 * inv_lg;  // 1 / log2(gamma)
+    const float inv_lg2f = (float)inv_lg2, thr0 = (float)(1e-6 * fabs(inv_lg2));
     const double thr = fmin(2e-6 * fabs(inv_lg), 0.25);  // 10x the estimate's error bound
     auto val = [&](double v) -> double {
       return HAS_R ? rdist_value(v, g, lg, inv_lg, tab) : dceil_value(v, g, lg, inv_lg, inv_lg2, thr, tab);
@@ -364,6 +365,24 @@ RDB_DEV double dceil_estimate_mufu(double v, double inv_lg2, double thr, bool& n
   return q;
 }
 
+// The same decision in FP32 (the FP32 pipe issues twice the FP64 rate and the
+// ceil is one F2I): s = (ex - 1023) + lg2(mantissa, 23 bits) rounded to float,
+// q = s * (1 / log2 gamma) in float. Error of q against the true quotient:
+// mantissa truncation + MUFU.LG2 < 4e-7 in log2 y (as above), the float
+// rounding of s < 6e-8 |s|, of 1/log2 gamma and of the product < 6e-8 |q|
+// each, so |err| < 4e-7 |1/log2 gamma| + 1.8e-7 |q|. need unless q is more than
+// thr0 + 4e-7 |q| (thr0 = 1e-6 |1/log2 gamma|) from an integer, i.e. more than
+// twice the bound; the reference's own fp64 quotient is within ~1e-15 of the
+// true one, so then both ceilings agree. q - rint(q) is exact in float.
+RDB_DEV int dceil_estimate_f32(double v, float inv_lg2f, float thr0, bool& need) {
+  const int hi = __double2hiint(v), lo = __double2loint(v);
+  const int ex = hi >> 20;  // sign bit set (v <= -0) -> ex < 0 -> need
+  const float mf = __int_as_float(((hi & 0x000FFFFF) << 3) | ((unsigned)lo >> 29) | 0x3F800000);
+  const float q = ((float)(ex - 1023) + __log2f(mf)) * inv_lg2f;
+  need = ((unsigned)(ex - 1) >= 2046u) | !(fabsf(q - rintf(q)) > fmaf(4e-7f, fabsf(q), thr0));
+  return __float2int_ru(q);
+}
+
 // D-only K3 for whole n x n matrices, the batch path (no mask, no column map):
 // one warp per row, each lane owns 4 consecutive columns of a 128-column block
 // (two 16-byte loads; a warp stores 128 contiguous bytes of uint8 D or 512 of
@@ -375,6 +394,9 @@ RDB_DEV double dceil_estimate_mufu(double v, double inv_lg2, double thr, bool& n
 // (tools/time_k3.py: uint8 D 0.56 -> 0.48 ms, int32 D 0.61 -> 0.53 ms)
 #ifndef RDB_K3_MUFU
 #define RDB_K3_MUFU 1
+#endif
+#ifndef RDB_K3_F32
+#define RDB_K3_F32 1  // the MUFU estimate in FP32 (dceil_estimate_f32)
 #endif
 #ifndef LEAN_PF
 #define LEAN_PF 1
@@ -424,6 +446,7 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
     unsigned neg = 0, bad = 0;
 #if RDB_K3_MUFU
     const double inv_lg2 = 0.6931471805599453 * inv_lg;  // 1 / log2(gamma)
+    const float inv_lg2f = (float)inv_lg2, thr0 = (float)(1e-6 * fabs(inv_lg2));
     // common path: the estimate, diagonal 0; D > RDB_D8_MAX or < 0 (u8) are
     // tracked by an unsigned max and counted below only when it exceeds the range
     unsigned dmax = 0;
@@ -435,14 +458,20 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         bool nd;
+        const bool dg = j + e == i;
+#if RDB_K3_MUFU && RDB_K3_F32
+        const int de = dceil_estimate_f32(v[e], inv_lg2f, thr0, nd);
+        need |= (unsigned)(nd && !dg) << e;
+        d[e] = (dg || nd) ? 0 : de;
+#else
 #if RDB_K3_MUFU
         const double r = dceil_estimate_mufu(v[e], inv_lg2, thr, nd);
 #else
         const double r = dceil_estimate_lean(v[e], inv_lg, thr, lt, nd);
 #endif
-        const bool dg = j + e == i;
         need |= (unsigned)(nd && !dg) << e;
         d[e] = (dg || nd) ? 0 : __double2int_ru(r);
+#endif
 #if !RDB_K3_MUFU
         neg += v[e] < NEGATIVE_ENTRY_TOL;
 #endif
@@ -533,8 +562,12 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
       // already the clamp): re-derive the row's common-path D's
       for (int j = lane; j < nfull; j += 32) {
         bool nd;
-        const double r = dceil_estimate_mufu(Y[j], inv_lg2, thr, nd);
-        if (!nd && j != i) bad += (unsigned)__double2int_ru(r) > (unsigned)RDB_D8_MAX;
+#if RDB_K3_F32
+        const int de = dceil_estimate_f32(Y[j], inv_lg2f, thr0, nd);
+#else
+        const int de = __double2int_ru(dceil_estimate_mufu(Y[j], inv_lg2, thr, nd));
+#endif
+        if (!nd && j != i) bad += (unsigned)de > (unsigned)RDB_D8_MAX;
       }
     }
 #endif

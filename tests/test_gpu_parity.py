@@ -433,3 +433,61 @@ def test_banded_path_matches_gauss_jordan(cuda, monkeypatch, n):
             knife = np.isfinite(r) & (np.abs(r - np.round(r)) < 1e-9) & (r != 0)
         for mode in ("0", "1"):
             np.testing.assert_array_equal(outs[mode][b][~knife], ref[~knife], err_msg=f"graph {b} band={mode}")
+
+
+@pytest.mark.parametrize("d_dtype", ["uint8", "int32"])
+def test_lean_k3_adversarial_values(cuda, d_dtype):
+    """The batch K3 (lean kernel: FP32 MUFU estimate, exact FP64 path within its
+    error bound of an integer) on values placed around every gamma^k: relative
+    offsets from 1e-16 to 1e-3 either side (the estimate's threshold lies in
+    that range for every gamma below), log-uniform values, zeros, negatives and
+    subnormals. D must equal ceil(np.log(y) / log(gamma)) (resolvent.py:140-153)
+    except at the reference's own knife edge (|R - k| < 1e-9, DESIGN.md
+    "Exactness"), where k or k + 1 is accepted."""
+    from paper_2308_07403_b200 import _lib as L
+    from paper_2308_07403_b200 import batch as B
+
+    n = 256
+    gammas = np.array([1e-2, 0.1, 1e-5, 0.5, 0.9, 1e-3])
+    rng = np.random.default_rng(5)
+    deltas = np.array([0.0, 1e-16, 3e-16, 1e-13, 1e-10, 1e-8, 3e-8, 1e-7, 2e-7, 4e-7, 1e-6, 2e-6, 5e-6, 1e-5,
+                       3e-5, 1e-4, 1e-3])
+    deltas = np.concatenate([deltas, -deltas[1:]])
+    ys = []
+    for g in gammas:
+        kmax = int(min(200, np.floor(np.log(1e-300) / np.log(g))))
+        ks = np.arange(1, kmax + 1)
+        base = np.power(g, ks.astype(np.float64))
+        near = (base[:, None] * (1.0 + deltas[None, :])).ravel()
+        near = near[(near > 0) & (near < 1)]
+        lo = np.log(max(g ** min(kmax, 150), 1e-300))
+        rnd = np.exp(rng.uniform(lo, 0.0, n * n))
+        special = [0.0, -1e-13, -0.5] + ([1e-310, 4.9e-324] if g < 0.05 else [])  # D <= 254 for uint8
+        y = np.concatenate([near, special, rnd])[: n * n]
+        y = rng.permutation(np.resize(y, n * n)) if y.size < n * n else rng.permutation(y)
+        ys.append(y.reshape(n, n))
+    Y = np.stack(ys)
+    m = torch.from_numpy(Y).to(cuda)
+    gam = torch.from_numpy(gammas).to(cuda)
+    dt = torch.uint8 if d_dtype == "uint8" else torch.int32
+    d = torch.empty((len(gammas), n, n), dtype=dt, device=cuda)
+    counters = torch.zeros((len(gammas), L.RDB_NCOUNTERS), dtype=torch.int64, device=cuda)
+    B.log_ceil_call(m, n, len(gammas), gam, d, counters, L.stream_handle())
+    got = d.cpu().numpy()
+    got = B.decode_d8(got) if d_dtype == "uint8" else got
+    cnt = counters.cpu().numpy()
+    for b, g in enumerate(gammas):
+        y = Y[b]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            r = np.where(y > 0, np.log(np.where(y > 0, y, 1.0)) / np.log(g), np.inf)
+        np.fill_diagonal(r, 0.0)
+        ref = orc.d_to_int32(np.ceil(r))
+        rf = np.where(np.isfinite(r), r, 0.0)
+        knife = np.isfinite(r) & (np.abs(rf - np.round(rf)) < 1e-9) & (r != 0)
+        assert knife.sum() < 0.05 * n * n
+        np.testing.assert_array_equal(got[b][~knife], ref[~knife], err_msg=f"gamma {g}")
+        k = np.round(r[knife]).astype(np.int64)
+        assert np.isin(got[b][knife] - k, [0, 1]).all(), f"gamma {g}"
+        assert cnt[b, L.RDB_CNT_NEGATIVE] == int((y < -1e-12).sum())
+        if d_dtype == "uint8":
+            assert cnt[b, L.RDB_CNT_D8_RANGE] == 0
