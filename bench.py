@@ -481,7 +481,7 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "K2 blocked Gauss-Jordan (gj_panel + gj_rowpanel + gj_update, DMMA.8x8x4) "
                                                   "+ banded inverse of the block-tridiagonal graphs (band_factor + band_chain)",
                      "achieved": inv_tflops, "peak": peak, "unit": "TFLOP/s", "frac": inv_tflops / peak,
-                     "traffic": ncu_traffic(), "traffic_unit": "bytes per K2 call (8 GJ steps x 3 kernels, whole batch)",
+                     "traffic": ncu_traffic(), "traffic_unit": "bytes per K2 call (8 GJ steps x 3 kernels x 2 sub-batches + plan + banded factor and chain, whole batch)",
                      "traffic_source": "profiles/r01_ncu_full_cfg2.json", "peak_source": peak_src,
                      "work_per_launch": f"{exec_flops:.4g} flop executed per K2 call = 2*128*128*16 per k-chunk over "
                                         f"the block-sparse plan's tiles and k-chunks for the {n_gj} Gauss-Jordan graphs + "

@@ -16,11 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--iters", type=int, default=1)
 ap.add_argument("--n", type=int, default=1024)
+ap.add_argument("--d-dtype", default="uint8", choices=["uint8", "int32"])
 args = ap.parse_args()
 
 bits, gammas, _ = wl.cfg2_batch(args.batch)
 dev = torch.device("cuda", 0)
-buf = B.BatchBuffers.allocate(1024, args.batch, dev)
+buf = B.BatchBuffers.allocate(1024, args.batch, dev, d_dtype=args.d_dtype)
 buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
 buf.gammas.copy_(torch.from_numpy(gammas))
 B.run_chunk(buf, args.batch)
