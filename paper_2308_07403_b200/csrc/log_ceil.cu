@@ -383,6 +383,20 @@ RDB_DEV int dceil_estimate_f32(double v, float inv_lg2f, float thr0, bool& need)
   return __float2int_ru(q);
 }
 
+// The lean kernel's exact path (rare): out of line by default, so its
+// registers do not count against the streaming loop's.
+#ifndef RDB_K3_NOINLINE
+#define RDB_K3_NOINLINE 0
+#endif
+#if RDB_K3_NOINLINE
+__device__ __noinline__
+#else
+RDB_DEV
+#endif
+double exact_value(double v, double g, double lg, double inv_lg) {
+  return rdist_value(v, g, lg, inv_lg, ConstTab{});
+}
+
 // D-only K3 for whole n x n matrices, the batch path (no mask, no column map):
 // one warp per row, each lane owns 4 consecutive columns of a 128-column block
 // (two 16-byte loads; a warp stores 128 contiguous bytes of uint8 D or 512 of
@@ -480,7 +494,7 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           if (need & (1u << e)) {
-            const double r = rdist_value(v[e], g, lg, inv_lg, tab);
+            const double r = exact_value(v[e], g, lg, inv_lg);
             d[e] = __double2int_ru(r);  // +inf -> INT32_MAX, the int32 sentinel
             if (DK == DK_U8 && r == __longlong_as_double(0x7FF0000000000000LL)) d[e] = -2;  // unreachable
             if (DK == DK_U8 && r != r) d[e] = -1;  // NaN: out of range
