@@ -119,7 +119,8 @@ def invert(a: torch.Tensor, scale: float, z_matrix: bool, pivot_rtol: float) -> 
 
     Z-matrices go through the no-pivot DMMA kernel; its pivots certify the
     result (all positive => nonsingular M-matrix, where partial pivoting is
-    unnecessary). Without that certificate the partial-pivoting kernel runs.
+    unnecessary). Without that certificate, or when a no-pivot pivot falls
+    below the tolerance, the partial-pivoting kernel runs and its pivots decide.
     Raises InversionFailure on the reference's rule min|pivot| < rtol*scale
     (linalg.py:33-38).
     """
@@ -131,9 +132,7 @@ def invert(a: torch.Tensor, scale: float, z_matrix: bool, pivot_rtol: float) -> 
         n_pad = L.pad_to_nb(n)
         y = pad_copy(a, n_pad)
         rec = invert_padded_nopivot(y)
-        if not (rec.flags & (L.RDB_PIV_NONPOS | L.RDB_PIV_NONFINITE)):
-            if not (rec.min_pivot >= tol):
-                raise InversionFailure(rec.min_pivot, scale)
+        if not (rec.flags & (L.RDB_PIV_NONPOS | L.RDB_PIV_NONFINITE)) and rec.min_pivot >= tol:
             return y[:n, :n] if n_pad != n else y
     y = a.clone()
     rec = invert_pivoted(y)

@@ -12,8 +12,10 @@ the diagonal. ``d_dtype="uint8"`` selects the compact form (rdb_log_ceil_d8):
 the same D wherever 0 <= D <= 254, 255 for unreachable pairs, a quarter of the
 int32 bytes over PCIe; a graph with a D outside that range is counted on the
 device and redone in int32 (:meth:`APSPBatchEngine.wait` widens the batch), so
-the result is never lossy. A graph whose inversion is not certified or is
-singular raises ResolventSingularError naming the graph.
+the result is never lossy. A graph whose no-pivot inverse is not certified
+(gamma past the critical gain, or a pivot below tolerance) is recomputed
+through the partial-pivoting path, which raises ResolventSingularError
+(naming the graph) exactly where the reference's LAPACK path would.
 
 :class:`APSPBatchEngine` owns reusable device and pinned host buffers (the
 serving form: host bits in, host int32 D out, copies overlapped with the
@@ -290,18 +292,55 @@ def executed_flops(bits: np.ndarray, n: int) -> float:
     return float(chunks) * 2.0 * L.RDB_NB * L.RDB_NB * (L.RDB_NB // STRIPS) + extra
 
 
+def _certified(rec: L.PivotInfo) -> bool:
+    """No-pivot pivots all positive (nonsingular M-matrix) and above the
+    reference's tolerance (linalg.py:33-38; scale = max|M| = 1 for
+    M = I - gamma*A with 0 < gamma < 1)."""
+    return not (rec.flags & (L.RDB_PIV_NONPOS | L.RDB_PIV_NONFINITE)) and rec.min_pivot >= PIVOT_RTOL * 1.0
+
+
+def uncertified(infos: list[L.PivotInfo]) -> np.ndarray:
+    """Indices of graphs whose no-pivot inverse is not certified: gamma past the
+    critical gain (a non-positive pivot) or a pivot below tolerance. Their D is
+    recomputed by :func:`redo_pivoted`."""
+    return np.array([k for k, rec in enumerate(infos) if not _certified(rec)], dtype=np.int64)
+
+
 def check_infos(infos: list[L.PivotInfo], gammas: np.ndarray, first_index: int = 0) -> None:
-    """The reference's singularity rule per graph (linalg.py:33-38; scale = max|M| = 1
-    for M = I - gamma*A with 0 < gamma < 1)."""
+    """Strict form: raise ResolventSingularError for the first graph whose
+    no-pivot inverse is not certified (bench.py asserts none is)."""
     for k, rec in enumerate(infos):
-        bad_cert = rec.flags & (L.RDB_PIV_NONPOS | L.RDB_PIV_NONFINITE)
-        if bad_cert or not (rec.min_pivot >= PIVOT_RTOL * 1.0):
-            g = float(gammas[k])
-            err = ResolventSingularError(g)
+        if not _certified(rec):
+            err = ResolventSingularError(float(gammas[k]))
             err.graph_index = first_index + k
             raise err from SingularMatrixError(
                 f"graph {first_index + k}: min pivot {rec.min_pivot:.3e} (flags {rec.flags})"
             )
+
+
+def redo_pivoted(bits: np.ndarray, gammas: np.ndarray, n: int, idx: np.ndarray) -> np.ndarray:
+    """int32 D of the graphs ``idx`` through the drop-in single-graph path:
+    the no-pivot kernel's certificate failed, so M is inverted by the
+    partial-pivoting kernel, which raises ResolventSingularError exactly when
+    the reference's LAPACK path does (linalg.py:32-38, resolvent.py:116-119).
+    The error carries ``graph_index``."""
+    from .graphs import Graph, GraphKind
+    from .resolvent import resolvent, rounded_r_distance
+    from .workloads import unpack_bits
+
+    out = np.empty((len(idx), n, n), dtype=np.int32)
+    for r, k in enumerate(idx):
+        present = unpack_bits(np.asarray(bits)[k].view(np.uint32), n)
+        g = Graph(n, np.where(present, 1.0, np.inf), GraphKind.UNWEIGHTED)
+        try:
+            d = rounded_r_distance(resolvent(g, float(gammas[k]), with_residual=False))
+        except ResolventSingularError as err:
+            err.graph_index = int(k)
+            raise
+        fin = np.isfinite(d)
+        out[r] = np.where(fin, d, 0).astype(np.int32)
+        out[r][~fin] = UNREACHABLE
+    return out
 
 
 class APSPBatchEngine:
@@ -425,16 +464,19 @@ class APSPBatchEngine:
         batch = self.pending[slot]
         self.done[slot].synchronize()
         self.pending[slot] = 0
-        if check:
-            check_infos(L.read_pivot_info(self.info_hosts[slot][: batch * 16]), gammas_pin.numpy())
         out = self.outs[slot][:batch].numpy()
+        bits_pin, g_pin = self.inputs[slot]
+        redo = uncertified(L.read_pivot_info(self.info_hosts[slot][: batch * 16])) if check else np.zeros(0, np.int64)
         if self.d_dtype == torch.uint8:
             bad = np.nonzero(self.cnt_hosts[slot][:batch, L.RDB_CNT_D8_RANGE].numpy())[0]
-            if bad.size:
-                bits_pin, g_pin = self.inputs[slot]
-                wide = decode_d8(out)
-                wide[bad] = rounded_r_distance_batch(bits_pin.numpy()[bad], g_pin.numpy()[bad], self.n)
-                return wide
+            bad = np.setdiff1d(bad, redo)
+            if bad.size or redo.size:
+                out = decode_d8(out)
+                if bad.size:
+                    out[bad] = rounded_r_distance_batch(bits_pin.numpy()[bad], g_pin.numpy()[bad], self.n)
+        if redo.size:
+            out = out.copy() if out.base is not None else out
+            out[redo] = redo_pivoted(bits_pin.numpy(), g_pin.numpy(), self.n, redo)
         return out
 
     def finish(self, batch: int, gammas_pin: torch.Tensor, check: bool = True) -> np.ndarray:

@@ -535,7 +535,8 @@ static int64_t wide_min_n();
 // inverted as part of a larger matrix).
 static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                        rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base, int* dyn = nullptr,
-                       const PlanPart* plan = nullptr, int64_t info_stride = 1, const int* nonband = nullptr) {
+                       const PlanPart* plan = nullptr, int64_t info_stride = 1, const int* nonband = nullptr,
+                       int grid_cap = 0) {
   if (!a || !work || !info || n <= 0 || batch <= 0) return RDB_EINVAL;
   if (n % NB != 0 || lda < n || (lda & 1) || (batch > 1 && stride < n * lda)) return RDB_EINVAL;
   if (((uintptr_t)a & 15) || ((uintptr_t)work & 15)) return RDB_EINVAL;
@@ -588,19 +589,20 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
       const int p1n = (k + 1) * NB;
       gj_panel_kernel<<<1, p1::THREADS, p1::SMEM_BYTES, side>>>(a, lda, stride, p1n, idx_base + p1n, info, 0);
       cudaEventRecord(g_ev_p, side);
-      UpdateSched ub{a, cnt, lda, stride, nt, k, 1, 2};
+      UpdateSched ub{a, cnt, lda, stride, nt, k, 1, 2, dyn ? dyn + 1 : nullptr};
       const int64_t tiles = (int64_t)(nt - 1) * nt - 1;
       const unsigned grid = (unsigned)(tiles < sm_count() - 1 ? tiles : sm_count() - 1);
       gj_update_kernel<<<grid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, ub);
       cudaStreamWaitEvent(st, g_ev_p, 0);
     } else {
-      UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch, 0, batch > 1 && dyn ? dyn + 1 : nullptr};
+      UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch, 0, dyn ? dyn + 1 : nullptr};
       if (plan) {
         up.list = plan->up + (int64_t)k * batch * (nt - 1) * nt;
         up.count_ptr = plan->counts + nt + k;
       }
-      gj_update_kernel<<<persistent_grid((int64_t)batch * (nt - 1) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(
-          amap, cmap, up);
+      unsigned grid = persistent_grid((int64_t)batch * (nt - 1) * nt);
+      if (grid_cap > 0 && grid > (unsigned)grid_cap) grid = (unsigned)grid_cap;
+      gj_update_kernel<<<grid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, up);
     }
   }
   RDB_LAUNCH_CHECK();
@@ -639,7 +641,7 @@ struct BatchWs {
     const size_t nt = (size_t)(n_pad / NB), b = (size_t)batch;
     cnt = 0;
     dyn = counter_bytes(n_pad, batch);
-    blk = dyn + (batch > 1 ? 256 : 0);
+    blk = dyn + 256;  // dynamic tile counters (2 per sub-batch part)
     if (batch > 1 && nt <= (size_t)PLAN_MAX_NT && n_pad % NB == 0) {
       counts = blk + align256(b * 2 * nt * (size_t)pat_ld((int)nt));  // column + row strip masks
       rp = counts + align256((size_t)MAX_PARTS * 2 * nt * sizeof(int));
@@ -660,9 +662,11 @@ static bool skip_enabled() {
   return !(e && e[0] == '0');
 }
 
-// Dynamic tile grabbing (a global atomic per tile) balanced the two dense
-// sub-batch streams best; with the block-sparse plan's many short tiles the
-// static stride measured faster (config 2: 10.98 -> 10.83 ms per K2 call).
+// Update tiles are taken by atomic ticket (a global counter per launch) by
+// default: the forward-progress argument for the in-kernel waits then needs
+// no co-residency (every tile a waiting tile depends on was grabbed earlier by
+// a running CTA), whatever else shares the GPU. Measured equal to the static
+// stride on config 2 (9.498 vs 9.497 ms per K2 call, profiles/r02_k2_modes.json).
 // Block-tridiagonal matrices (every edge within the 32-block band, from the
 // adjacency bits) skip Gauss-Jordan and run the banded inverse (gj_band.cu).
 static bool band_enabled() {
@@ -671,8 +675,23 @@ static bool band_enabled() {
 }
 
 static bool dyn_sched() {
-  const char* e = getenv("RDB_GJ_DYNAMIC");  // A-B switch: 1 grabs tiles dynamically
-  return e && e[0] == '1';
+  const char* e = getenv("RDB_GJ_DYNAMIC");  // A-B switch: 0 takes tiles by static stride
+  return !(e && e[0] == '0');
+}
+
+// Forward progress of the update kernel's in-kernel waits (the panel-column
+// tile of a row block waits for that row's other tiles, which have smaller
+// indices): with the static tile stride a waiting CTA needs every CTA of its
+// own grid resident. When the sub-batches' update kernels run concurrently on
+// their own streams, that holds if their grids together fit one CTA per SM
+// (every other kernel in flight — panel inverses, row panels, the banded
+// path — never waits, so it frees its SM): each part's update grid is capped
+// at sm_count / parts when the static stride is selected (RDB_GJ_DYNAMIC=0);
+// RDB_GJ_COSCHED=0 lifts that cap (A-B timing only). The default ticket order
+// is sound without it.
+static bool cosched_cap() {
+  const char* e = getenv("RDB_GJ_COSCHED");
+  return !(e && e[0] == '0');
 }
 
 static int split_min_batch() {
@@ -773,9 +792,10 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       const PlanPart pp = part_plan(i, parts, lo);
       // row-block counters of the part, 16-byte aligned (counter_bytes has the slack)
       char* cw = wb + (((size_t)lo * ntl * sizeof(int) + 15) & ~(size_t)15);
+      const bool dyn_on = dyn_sched();
       rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, g_part[i], 1, 0,
-                       dyn_sched() ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr, parts,
-                       nonband ? nonband + i : nullptr);
+                       dyn_on ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr, parts,
+                       nonband ? nonband + i : nullptr, (!dyn_on && cosched_cap()) ? sm_count() / parts : 0);
       cudaEventRecord(g_join[i], g_part[i]);
       lo += cnt;
     }
@@ -787,7 +807,14 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     const int rc = band_invert(a, n, lda, stride, batch, nonband, band_ws, info, st);
     if (rc) return rc;
   }
-  return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, nullptr, use_plan ? &pp : nullptr, 1,
+  if (!a || !work || !info || n <= 0 || n % NB != 0 || lda < n || batch <= 0 || ((uintptr_t)work & 15))
+    return RDB_EINVAL;  // (validated before the first CUDA call)
+  int* dyn = nullptr;
+  if (dyn_sched()) {
+    dyn = reinterpret_cast<int*>(wb + ws.dyn);
+    if (cudaMemsetAsync(dyn, 0, 2 * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
+  }
+  return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, dyn, use_plan ? &pp : nullptr, 1,
                      nonband);
 }
 
@@ -1111,11 +1138,10 @@ using namespace rdb;
 
 extern "C" size_t rdb_invert_workspace_bytes(int64_t n_pad, int64_t batch) {
   if (n_pad <= 0 || batch <= 0) return 0;
-  if (batch > 1) return rdb::BatchWs(n_pad, batch).total;  // counters | dynamic counters | block-sparse plan
   const size_t counters = rdb::counter_bytes(n_pad, batch);
   if (batch == 1 && n_pad >= rdb::wide_min_n() && n_pad % rdb::WB == 0)
     return (counters > 256 ? counters : 256) + rdb::wide_scratch_bytes(n_pad);  // counters | R | C
-  return counters;
+  return rdb::BatchWs(n_pad, batch).total;  // counters | dynamic tile counters | block-sparse plan
 }
 
 extern "C" int rdb_invert_batched(double* a, int64_t n_pad, int64_t lda, int64_t stride,

@@ -107,8 +107,9 @@ RDB_DEV double rdist_value(double v, double g, double lg, double inv_lg, const T
 }
 
 // D-only path: a value whose ceil equals ceil(rdist_value(v)). log2 y is first
-// estimated as exponent + __log2f(mantissa) (absolute error < 4e-7, so the
-// quotient's error is < 4e-7 / |log2 gamma| = thr / 10); only when the estimate
+// estimated as exponent + __log2f(mantissa) (absolute error < 4.1e-7: __log2f
+// 2^-22 on [1, 2) plus 2^-23 / ln 2 for the 23-bit truncation, so the
+// quotient's error is < 4.1e-7 / |log2 gamma| < thr / 7); only when the estimate
 // lies within thr of an integer does the element take the full FP64 log and
 // refinement. For the config-2 gains that is a tiny fraction of the entries.
 RDB_DEV double dceil_value(double v, double g, double lg, double inv_lg, double inv_lg2, double thr,
@@ -226,7 +227,10 @@ __global__ void __launch_bounds__(256)
     const double inv_lg = 1.0 / lg;
     const double inv_lg2 = 0.6931471805599453 * inv_lg;  // 1 / log2(gamma)
     const float inv_lg2f = (float)inv_lg2, thr0 = (float)(1e-6 * fabs(inv_lg2));
-    const double thr = fmin(2e-6 * fabs(inv_lg), 0.25);  // 10x the estimate's error bound
+    // 7x the MUFU estimate's error bound (4.1e-7 |1/log2 gamma| = 2.85e-7 |1/log gamma|)
+    // and 12x the table estimate's (1.6e-7 |1/log gamma|). No cap: for gamma
+    // near 1 the bound exceeds 1/2 and every element takes the exact path.
+    const double thr = 2e-6 * fabs(inv_lg);
     auto val = [&](double v) -> double {
       return HAS_R ? rdist_value(v, g, lg, inv_lg, tab) : dceil_value(v, g, lg, inv_lg, inv_lg2, thr, tab);
     };
@@ -352,8 +356,8 @@ RDB_DEV double dceil_estimate_lean(double v, double inv_lg, double thr, LeanTab 
 }
 
 // The same estimate with the mantissa's log2 from MUFU.LG2 on its leading 23
-// bits (dceil_value's estimate: absolute error < 4e-7 in log2 y, so the
-// quotient's error is < 4e-7 / |log2 gamma| = thr / 10 with thr as below): no
+// bits (dceil_value's estimate: absolute error < 4.1e-7 in log2 y, so the
+// quotient's error is < 4.1e-7 / |log2 gamma| < thr / 7 with thr as below): no
 // table lookups. need as dceil_estimate_lean (non-positive, subnormal,
 // non-finite, or within thr of an integer).
 RDB_DEV double dceil_estimate_mufu(double v, double inv_lg2, double thr, bool& need) {
@@ -368,11 +372,12 @@ RDB_DEV double dceil_estimate_mufu(double v, double inv_lg2, double thr, bool& n
 // The same decision in FP32 (the FP32 pipe issues twice the FP64 rate and the
 // ceil is one F2I): s = (ex - 1023) + lg2(mantissa, 23 bits) rounded to float,
 // q = s * (1 / log2 gamma) in float. Error of q against the true quotient:
-// mantissa truncation + MUFU.LG2 < 4e-7 in log2 y (as above), the float
-// rounding of s < 6e-8 |s|, of 1/log2 gamma and of the product < 6e-8 |q|
-// each, so |err| < 4e-7 |1/log2 gamma| + 1.8e-7 |q|. need unless q is more than
-// thr0 + 4e-7 |q| (thr0 = 1e-6 |1/log2 gamma|) from an integer, i.e. more than
-// twice the bound; the reference's own fp64 quotient is within ~1e-15 of the
+// mantissa truncation (2^-23 / ln 2 = 1.72e-7) + MUFU.LG2 (2^-22 = 2.38e-7)
+// < 4.1e-7 in log2 y, the float rounding of s < 6e-8 |s|, of 1/log2 gamma and
+// of the product < 6e-8 |q| each, so |err| < 4.1e-7 |1/log2 gamma| +
+// 1.8e-7 |q|. need unless q is more than thr0 + 4e-7 |q| (thr0 = 1e-6
+// |1/log2 gamma|) from an integer, i.e. more than twice the bound (2.4x and
+// 2.2x per term); the reference's own fp64 quotient is within ~1e-15 of the
 // true one, so then both ceilings agree. q - rint(q) is exact in float.
 RDB_DEV int dceil_estimate_f32(double v, float inv_lg2f, float thr0, bool& need) {
   const int hi = __double2hiint(v), lo = __double2loint(v);
@@ -454,7 +459,7 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
     const double g = gammas ? gammas[b] : gamma;
     const double lg = log(g);
     const double inv_lg = 1.0 / lg;
-    const double thr = fmin(2e-6 * fabs(inv_lg), 0.25);
+    const double thr = 2e-6 * fabs(inv_lg);  // as log_ceil_kernel's (no cap)
     const double* Y = y + b * stride_y + (int64_t)i * ldy;
     const int64_t orow = b * stride_o + (int64_t)i * ldo;
     unsigned neg = 0, bad = 0;

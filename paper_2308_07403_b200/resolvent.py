@@ -15,7 +15,7 @@ suggest_gamma) are host arithmetic, as in the reference.
 from __future__ import annotations
 
 import math
-from dataclasses import FrozenInstanceError, dataclass
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -55,49 +55,56 @@ class HealthFlags:
     inversion_residual: float
 
 
+class _HostY:
+    """Data descriptor behind ``ResolventResult.y``: the host array, copied
+    from the device matrix on first access when the result came from
+    :func:`resolvent` (which keeps Y on the GPU). Raising AttributeError on
+    class access tells ``dataclass`` the field has no default."""
+
+    def __get__(self, obj, owner=None):
+        if obj is None:
+            raise AttributeError("y")
+        d = obj.__dict__
+        if d.get("_y_host") is None and d.get("_y_dev") is not None:
+            n = d["_n"]
+            d["_y_host"] = d["_y_dev"][:n, :n].cpu().numpy().copy(order="C")
+        return d.get("_y_host")
+
+    def __set__(self, obj, value):  # reached only through object.__setattr__ (frozen)
+        obj.__dict__["_y_host"] = value
+        if value is not None:
+            obj.__dict__["_n"] = np.asarray(value).shape[0]
+
+
+@dataclass(frozen=True)
 class ResolventResult:
-    """(y, gamma, health) as in resolvent.py:60-64, with Y kept on the device.
+    """(y, gamma, health) as the reference's frozen dataclass (resolvent.py:60-64):
+    same fields, so ``dataclasses.fields/replace/asdict`` work for drop-in
+    callers. A result made by :func:`resolvent` also holds Y on the device
+    (``device_y()``); ``y`` is then copied to the host on first access."""
 
-    Constructed either by users with a host ``y`` (as the reference's tests
-    do) or by :func:`resolvent` with a device matrix; ``y`` is the host array
-    either way (copied from the device on first access).
-    """
+    y: np.ndarray = _HostY()
+    gamma: float
+    health: HealthFlags
 
-    __slots__ = ("_y_host", "_y_dev", "_n", "gamma", "health")
-
-    def __init__(self, y, gamma: float, health: HealthFlags, *, _device_y: torch.Tensor | None = None,
-                 _n: int | None = None):
-        object.__setattr__(self, "_y_host", None if y is None else np.asarray(y))
-        object.__setattr__(self, "_y_dev", _device_y)
-        if y is not None:
-            n = np.asarray(y).shape[0]
-        else:
-            n = _device_y.shape[0] if _n is None else _n
-        object.__setattr__(self, "_n", n)
-        object.__setattr__(self, "gamma", gamma)
-        object.__setattr__(self, "health", health)
-
-    def __setattr__(self, name, value):
-        raise FrozenInstanceError(f"cannot assign to field {name!r}")
-
-    @property
-    def y(self) -> np.ndarray:
-        if self._y_host is None:
-            n = self._n
-            host = self._y_dev[:n, :n].cpu().numpy().copy(order="C")
-            object.__setattr__(self, "_y_host", host)
-        return self._y_host
+    @classmethod
+    def _on_device(cls, y_dev: torch.Tensor, n: int, gamma: float, health: HealthFlags) -> "ResolventResult":
+        res = cls(None, gamma, health)
+        object.__setattr__(res, "_y_dev", y_dev)
+        object.__setattr__(res, "_n", n)
+        return res
 
     def device_y(self) -> torch.Tensor:
         """Y on the CUDA device (an n x n view, possibly of a padded buffer)."""
-        if self._y_dev is None:
-            dev = L.device()
-            t = torch.from_numpy(np.ascontiguousarray(self._y_host, dtype=np.float64)).to(dev)
+        d = self.__dict__
+        if d.get("_y_dev") is None:
+            t = torch.from_numpy(np.ascontiguousarray(d["_y_host"], dtype=np.float64)).to(L.device())
             object.__setattr__(self, "_y_dev", t)
-        return self._y_dev[: self._n, : self._n]
+        n = d["_n"]
+        return d["_y_dev"][:n, :n]
 
     def __repr__(self) -> str:
-        return f"ResolventResult(n={self._n}, gamma={self.gamma!r}, health={self.health!r})"
+        return f"ResolventResult(n={self.__dict__.get('_n')}, gamma={self.gamma!r}, health={self.health!r})"
 
 
 @dataclass(frozen=True)
@@ -164,20 +171,20 @@ def resolvent(g, gamma: float, reachable: np.ndarray | None = None, with_residua
     residual = math.nan
     if with_residual:
         residual = _d.residual(m_keep, y_pad)
-    return ResolventResult(None, gamma, HealthFlags(negative, underflow, residual), _device_y=y_pad, _n=n)
+    return ResolventResult._on_device(y_pad, n, gamma, HealthFlags(negative, underflow, residual))
 
 
 def _invert_m(m_pad: torch.Tensor, n: int, scale: float, z_matrix: bool, rebuild) -> torch.Tensor:
     """Inverse of the padded M: in place by the no-pivot DMMA kernel when its
-    pivots certify a nonsingular M-matrix, else (on a rebuilt M) pivoted."""
+    pivots certify a nonsingular M-matrix and pass the reference's rule, else
+    (on a rebuilt M) by the partial-pivoting kernel, whose pivots then decide
+    singularity exactly as LAPACK's getrf pivots do in linalg.py:32-38."""
     tol = PIVOT_RTOL * scale
     if scale == 0.0:
         raise _d.InversionFailure(0.0, scale)
     if z_matrix:
         rec = _d.invert_padded_nopivot(m_pad)
-        if not (rec.flags & (L.RDB_PIV_NONPOS | L.RDB_PIV_NONFINITE)):
-            if not (rec.min_pivot >= tol):
-                raise _d.InversionFailure(rec.min_pivot, scale)
+        if not (rec.flags & (L.RDB_PIV_NONPOS | L.RDB_PIV_NONFINITE)) and rec.min_pivot >= tol:
             return m_pad
         m_pad = rebuild()
     y = _d.invert(m_pad[:n, :n].contiguous(), scale, False, PIVOT_RTOL)

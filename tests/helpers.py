@@ -65,3 +65,27 @@ def u8_to_d(u8):
     d = u8.astype(np.float64)
     d[u8 == 255] = np.inf
     return d
+
+
+def d_digest(d_u8) -> bytes:
+    """Digest of a D in the compact byte form (uint8, 255 = +inf), as
+    tests/golden/make_golden_full.py stores the reference's."""
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(d_u8, dtype=np.uint8).tobytes()).digest()[:16]
+
+
+def int32_to_u8(d32):
+    """int32 D (INT32_MAX = unreachable, all finite D <= 254) -> uint8 form."""
+    fin = d32 != np.iinfo(np.int32).max
+    assert (d32[fin] >= 0).all() and (d32[fin] <= 254).all()
+    out = np.full(d32.shape, 255, np.uint8)
+    out[fin] = d32[fin]
+    return out
+
+
+def f64_to_u8(d):
+    fin = np.isfinite(d)
+    out = np.full(d.shape, 255, np.uint8)
+    out[fin] = d[fin].astype(np.uint8)
+    return out

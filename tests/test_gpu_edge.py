@@ -1,0 +1,98 @@
+"""Edge cases of the batch and K3 paths (round-2 review items).
+
+- A batched graph whose no-pivot inverse is not certified (gamma past the
+  critical gain, or exactly singular) goes through the partial-pivoting path,
+  as the reference's LAPACK lu_invert does (linalg.py:32-38): a nonsingular
+  M gives the reference's D, a singular one raises ResolventSingularError
+  naming the graph (resolvent.py:116-119).
+- K3 with gamma close to 1 (1 - 1e-7): the near-integer threshold grows
+  without a cap, so every element takes the exact path and D equals
+  ceil(log y / log gamma) (resolvent.py:140-153) on log-uniform y.
+- ResolventResult is the reference's frozen dataclass (resolvent.py:60-64).
+"""
+
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2308_07403_b200 as rb
+import rdist_oracle as orc
+from paper_2308_07403_b200 import _lib as L
+from paper_2308_07403_b200 import batch as B
+from paper_2308_07403_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+
+def _complete(n):
+    p = np.ones((n, n), bool)
+    np.fill_diagonal(p, False)
+    return p
+
+
+@pytest.mark.parametrize("d_dtype", ["int32", "uint8"])
+def test_batch_past_critical_gain_matches_reference(cuda, d_dtype):
+    n = 64  # complete digraph: rho = 63, critical gain 1/63
+    presents = [_complete(n), wl.er_present(n, 0.1, 3), _complete(n), wl.er_present(n, 0.2, 4)]
+    gammas = np.array([0.05, 1e-2, 0.2, 0.3])  # graphs 0, 2 (and maybe 3) past the critical gain
+    bits = np.stack([wl.pack_bits(p) for p in presents])
+    d = rb.rounded_r_distance_batch(bits, gammas, n, d_dtype=d_dtype)
+    assert d.dtype == np.int32  # uncertified graphs widen a compact batch
+    for b, (p, g) in enumerate(zip(presents, gammas)):
+        ref = orc.d_to_int32(orc.run_rdist(wl.weights_from_present(p), g))
+        np.testing.assert_array_equal(d[b], ref, err_msg=f"graph {b}")
+    # negative entries past the critical gain: those pairs are unreachable (+inf)
+    assert (d[0][~np.eye(n, dtype=bool)] == rb.UNREACHABLE).any()
+
+
+def test_batch_singular_graph_raises_with_index(cuda):
+    n = 64
+    presents = [wl.er_present(n, 0.1, 3), _complete(n)]
+    gammas = np.array([1e-2, 1.0 / 63.0])  # M = I - A/63 is singular (A 1 = 63 * 1)
+    bits = np.stack([wl.pack_bits(p) for p in presents])
+    with pytest.raises(rb.ResolventSingularError) as exc:
+        rb.rounded_r_distance_batch(bits, gammas, n)
+    assert exc.value.graph_index == 1
+    assert exc.value.gamma == pytest.approx(1.0 / 63.0)
+    # the reference raises on the same graph
+    with pytest.raises(Exception):
+        orc.run_rdist(wl.weights_from_present(presents[1]), gammas[1])
+
+
+@pytest.mark.parametrize("n", [255, 256])
+@pytest.mark.parametrize("gamma", [1 - 1e-7, 1 - 2e-7, 1 - 1e-6, 0.999])
+def test_k3_gamma_near_one(cuda, n, gamma):
+    rng = np.random.default_rng(n)
+    y = np.exp(rng.uniform(math.log(1e-6), 0.0, (n, n)))
+    y[: n // 4] = np.exp(rng.uniform(math.log(0.9995), 0.0, (n // 4, n)))  # R < ~5000: the refined range
+    res = rb.ResolventResult(y, gamma, rb.HealthFlags(False, None, 0.0))
+    with np.errstate(divide="ignore"):
+        r = np.log(y) / math.log(gamma)
+    np.fill_diagonal(r, 0.0)
+    ref = np.ceil(r)
+    np.testing.assert_array_equal(rb.rounded_r_distance(res), ref)  # fp64 D (drop-in)
+    # the int32 batch K3 (n % 4 != 0 takes the generic kernel, n == 256 the lean one)
+    m = torch.from_numpy(y[None]).to(cuda)
+    d = torch.empty((1, n, n), dtype=torch.int32, device=cuda)
+    cnt = torch.zeros((1, L.RDB_NCOUNTERS), dtype=torch.int64, device=cuda)
+    gam = torch.tensor([gamma], dtype=torch.float64, device=cuda)
+    B.log_ceil_call(m, n, 1, gam, d, cnt, L.stream_handle())
+    big = ref > np.iinfo(np.int32).max
+    got = d.cpu().numpy()[0]
+    np.testing.assert_array_equal(got[~big], ref[~big].astype(np.int64))
+
+
+def test_resolvent_result_is_the_reference_dataclass(cuda):
+    g = wl.er_graph(40, 0.2, 1)
+    res = rb.resolvent(g, 1e-2)
+    assert [f.name for f in dataclasses.fields(res)] == ["y", "gamma", "health"]
+    with pytest.raises(dataclasses.FrozenInstanceError):
+        res.gamma = 0.5
+    y = res.y  # host copy of the device inverse
+    assert y.shape == (40, 40) and np.allclose(y @ (np.eye(40) - orc.build_x(np.asarray(g.weights), 1e-2)), np.eye(40))
+    res2 = dataclasses.replace(res, gamma=1e-2)
+    np.testing.assert_array_equal(rb.rounded_r_distance(res2), rb.rounded_r_distance(res))
+    assert dataclasses.asdict(res)["health"]["inversion_residual"] == res.health.inversion_residual
