@@ -15,23 +15,34 @@ decoded uint8 D against an int32 run bit for bit) or as int32.
           (CUDA events, barrier + synchronize on both sides, max over ranks).
           The per-step working set (2.1 GB of M + 1 GB of D) exceeds L2.
   e2e   : the same through the public batch engine from pinned host bits to
-          pinned host D (host<->device copies inside the timed region).
+          pinned host D (host<->device copies inside the timed region); an
+          int32-D e2e beside it (e2e_int32).
   roofline: K2 (the dominant kernel family) in FP64 TFLOP/s against the
           measured DMMA peak (profiles/r01_fp64_peak.json; MEASURED_PEAKS.json
-          has no FP64 entry).
-  cpu_baseline: the reference pipeline restated in oracle/ (numpy + scipy
-          LAPACK, all host threads) on a bounded sample of the same graphs.
+          has no FP64 entry): on the flop it executes (frac), on the dense
+          2 n^3 (frac_dense_2n3), the graphs/s roofline, and the ER-only K2.
+  inversion_cfg5: the config-5 inversion (N = 32768, BASELINE's seed):
+          one GPU, or the 2D block-cyclic grid over all ranks (1x2, 2x2, 2x4)
+          with NCCL panel broadcasts and look-ahead; FP64 TFLOP/s = 2 n^3 / t
+          (max over ranks) and D on the 4096 seeded sample columns compared
+          with digests of the reference's own LAPACK columns.
+  cpu_baseline: the reference's own CPU pipeline (its stock rdist package,
+          installed into baseline/_ref) on a bounded sample of the same
+          graphs, one single-threaded process per host core.
 
 --impl reference times that CPU pipeline alone (rank 0; other ranks exit).
-Multi-GPU: launched by torch.distributed.run, one rank per GPU; each rank
-owns its own 256 graphs (weak scaling, no collective on the data path).
+Multi-GPU: `--gpus N` (N > 1) without a torch.distributed environment
+re-launches itself under torch.distributed.run with N ranks; each rank owns
+its own 256 graphs (weak scaling, no collective on the cfg2 data path).
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -49,6 +60,9 @@ WORKLOAD = ("cfg2: 256 unweighted digraphs/GPU, N=1024 (128 ER p=0.02 gamma=1e-2
             "128 directed 32x32 lattices keep=0.8 gamma=0.1), D out as {}")
 GRAPHS_PER_GPU = 256
 N = 1024
+REF_DIR = ROOT / "baseline" / "_ref"
+CFG5_FIXTURE = ROOT / "tests" / "golden" / "cfg5_cols.npz"
+GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
 
 
 def env_int(name, default):
@@ -72,7 +86,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except (OSError, FileNotFoundError):
@@ -128,44 +142,38 @@ def hbm_peak():
 def ncu_traffic():
     """DRAM bytes (read + write) of one K2 call over the bench batch, from the
     committed `ncu --set full` capture of the same workload (profiles/)."""
-    p = ROOT / "profiles" / "r01_ncu_full_cfg2.json"
-    try:
-        d = json.loads(p.read_text())
-        return d.get("k2_dram_bytes_per_call")
-    except (OSError, ValueError):
-        return None
+    for name in ("r02_ncu_full_cfg2.json", "r01_ncu_full_cfg2.json"):
+        p = ROOT / "profiles" / name
+        try:
+            d = json.loads(p.read_text())
+            return d.get("k2_dram_bytes_per_call"), f"profiles/{name}"
+        except (OSError, ValueError):
+            continue
+    return None, None
 
 
-# ---------------------------------------------------------------- CPU side
-def cpu_sample_graphs(count: int):
-    from paper_2308_07403_b200 import workloads as wl
-
-    seeds = wl.cfg2_seeds(GRAPHS_PER_GPU)
-    half = count // 2
-    pick = seeds[:half] + seeds[GRAPHS_PER_GPU // 2: GRAPHS_PER_GPU // 2 + count - half]
-    return [(wl.weights_from_present(wl.cfg2_present(k, s)), wl.cfg2_gamma(k)) for k, s in pick]
-
-
-def cpu_run(graphs):
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import rdist_oracle as orc
-
-    for w, g in graphs:
-        orc.run_rdist(w, g)
-
-
-# Process-parallel CPU pipeline: one single-threaded BLAS process per host core,
-# each running the reference's per-graph closure (run_rdist) on whole graphs —
-# the fastest way to spend the host's cores on this workload (one graph per
-# core beats one multi-threaded LAPACK call per graph at N=1024).
+# ---------------------------------------------------------------- CPU side (the reference's own pipeline)
 _GRAPH_CACHE: dict = {}
 _LIMITS = None
+_RDIST = None
 
 
-def _pool_init():
-    global _LIMITS
+def reference_kind() -> str:
+    """'reference' when the stock reference package is installed in baseline/_ref
+    (pip install --no-deps --target baseline/_ref /root/reference/pkg), else
+    'port' (the oracle restatement, oracle/rdist_oracle.py)."""
+    return "reference" if (REF_DIR / "rdist" / "__init__.py").exists() else "port"
+
+
+def _pool_init(kind):
+    global _LIMITS, _RDIST
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "oracle"))
+    if kind == "reference":
+        sys.path.insert(0, str(REF_DIR))
+        import rdist
+
+        _RDIST = rdist
     import rdist_oracle  # noqa: F401  (loads numpy's and scipy's BLAS before limiting them)
     import scipy.linalg  # noqa: F401
     from threadpoolctl import threadpool_limits
@@ -173,32 +181,44 @@ def _pool_init():
     _LIMITS = threadpool_limits(1)
 
 
-def _pool_task(item):
+def _run_one(w, gamma):
+    """The reference's timed closure run_rdist (experiments.py:305-310):
+    resolvent(g, gamma, with_residual=False) -> r_distance -> ceil."""
+    if _RDIST is not None:
+        rd = _RDIST
+        g = rd.Graph(w.shape[0], w, rd.GraphKind.UNWEIGHTED)
+        return np.ceil(rd.r_distance(rd.resolvent(g, gamma, with_residual=False)))
     import rdist_oracle as orc
 
+    return orc.run_rdist(w, gamma)
+
+
+def _pool_task(item):
     from paper_2308_07403_b200 import workloads as wl
 
     if item not in _GRAPH_CACHE:
         k, s = item
         _GRAPH_CACHE[item] = (wl.weights_from_present(wl.cfg2_present(k, s)), wl.cfg2_gamma(k))
     w, g = _GRAPH_CACHE[item]
-    orc.run_rdist(w, g)
+    _run_one(w, g)
     return 0
 
 
 class CpuPool:
-    """nproc single-threaded workers; ``run(items)`` is one timed batch."""
+    """nproc single-threaded workers running the reference's closure; ``run()``
+    is one timed sample (``per_core`` graphs per worker, half ER, half lattice)."""
 
     def __init__(self, per_core: int = 2):
         import multiprocessing as mp
 
         from paper_2308_07403_b200 import workloads as wl
 
+        self.kind = reference_kind()
         self.procs = os.cpu_count() or 1
         saved = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
         os.environ.update({k: "1" for k in saved})  # inherited by the spawned workers only
         try:
-            self.pool = mp.get_context("spawn").Pool(self.procs, initializer=_pool_init)
+            self.pool = mp.get_context("spawn").Pool(self.procs, initializer=_pool_init, initargs=(self.kind,))
         finally:
             for k, v in saved.items():
                 if v is None:
@@ -215,17 +235,26 @@ class CpuPool:
         self.pool.map(_pool_task, self.items, chunksize=1)
         return time.perf_counter() - t0
 
+    def sample(self) -> str:
+        what = ("the stock reference package from baseline/_ref (rdist.resolvent(with_residual=False) -> "
+                "rdist.r_distance -> np.ceil, experiments.py:305-310)" if self.kind == "reference" else
+                "oracle/rdist_oracle.run_rdist (the reference's run_rdist restated, scipy LAPACK)")
+        return (f"{len(self.items)} cfg2 graphs per sample (half ER, half lattice), 2 per core, "
+                f"{self.procs} single-threaded processes, through {what}")
+
     def close(self):
         self.pool.close()
         self.pool.join()
 
 
-def cpu_host_info(graphs) -> dict:
+def cpu_host_info() -> dict:
     """Host facts the baseline is quoted with: CPU model, core
     count, library versions, BLAS threads, and the 1-thread time per graph."""
     import platform
 
     import scipy
+
+    from paper_2308_07403_b200 import workloads as wl
 
     info = {"nproc": os.cpu_count(), "numpy": np.__version__, "scipy": scipy.__version__,
             "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
@@ -239,21 +268,18 @@ def cpu_host_info(graphs) -> dict:
     try:
         from threadpoolctl import threadpool_info, threadpool_limits
 
+        _pool_init(reference_kind())
         info["blas"] = [{k: i.get(k) for k in ("internal_api", "version", "num_threads")} for i in threadpool_info()]
+        graphs = [(wl.weights_from_present(wl.cfg2_present(k, s)), wl.cfg2_gamma(k))
+                  for k, s in (("er", 2000), ("lattice", 1000))]
         with threadpool_limits(1):
             t0 = time.perf_counter()
-            cpu_run(graphs[:2])
-            info["one_thread_s_per_graph"] = (time.perf_counter() - t0) / 2
+            for w, g in graphs:
+                _run_one(w, g)
+            info["one_thread_s_per_graph"] = (time.perf_counter() - t0) / len(graphs)
     except Exception as exc:  # noqa: BLE001 - informational only
         info["blas_error"] = repr(exc)
     return info
-
-
-def cpu_cores_used():
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import rdist_oracle as orc
-
-    return orc.blas_threads()
 
 
 def run_reference(args):
@@ -263,9 +289,10 @@ def run_reference(args):
     pool = CpuPool(per_core=2)
     for _ in range(args.warmup):
         pool.run()
-    dt = sum(pool.run() for _ in range(args.steps))
+    times = [pool.run() for _ in range(args.steps)]
     pool.close()
     per_step = len(pool.items)
+    dt = sum(times)
     value = per_step * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": args.gpus,
@@ -274,17 +301,180 @@ def run_reference(args):
         "config": {"workload": WORKLOAD.format("float64 (the reference's rounded_r_distance)"),
                    "graphs_per_gpu": GRAPHS_PER_GPU, "n": N,
                    "parallelism": f"host CPU, {pool.procs} single-threaded processes (one graph each at a time)"},
-        "cpu_baseline": {"value": value, "unit": "graphs/s", "cores": pool.procs, "kind": "port",
-                         "sample": f"{per_step} cfg2 graphs per step (half ER, half lattice), 2 per core, "
-                                   "oracle/rdist_oracle.run_rdist = reference run_rdist restated",
-                         "host": cpu_host_info(cpu_sample_graphs(2))},
+        "cpu_baseline": {"value": value, "unit": "graphs/s", "cores": pool.procs, "kind": pool.kind,
+                         "sample": pool.sample(), "host": cpu_host_info()},
         "e2e": {"value": value, "unit": "graphs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ---------------------------------------------------------------- launcher
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(n: int) -> int:
+    """--gpus N > 1 outside torch.distributed: run this script under
+    torch.distributed.run with N ranks (one per GPU) and return its status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve())]
+    return subprocess.call(cmd + sys.argv[1:])
+
+
+def launch_probe(args) -> int:
+    """Test hook (tests/test_bench_launcher.py): each rank joins a gloo group,
+    checks WORLD_SIZE == --gpus and the max-over-ranks reduction, prints one line."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank = env_int("WORLD_SIZE", 1), env_int("RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    print(json.dumps({"rank": rank, "world": dist.get_world_size(), "max_rank": float(t.item()),
+                      "local_world": env_int("LOCAL_WORLD_SIZE", world)}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 # ---------------------------------------------------------------- GPU side
+def digest(a: np.ndarray) -> bytes:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest()[:16]
+
+
+def cfg5_single(dev, sh, peak, max_over_ranks):
+    """Config 5 on one GPU: BASELINE's seed, in-place wide-step inversion,
+    D on the 4096 sampled columns against the reference's digests."""
+    import torch
+
+    from paper_2308_07403_b200 import _lib as L
+    from paper_2308_07403_b200 import single as S
+    from paper_2308_07403_b200 import workloads as wl
+
+    c = wl.CFG5
+    n, gamma = c["n"], c["gamma"]
+    t0 = time.perf_counter()
+    bits = wl.er_bits_parallel(n, c["p"], 0)
+    t_gen = time.perf_counter() - t0
+    bits_d = torch.from_numpy(bits.view(np.int32)).to(dev)
+    m = S.build_m_bits(bits_d, n, gamma)
+    # the first wide-path call on this device creates its streams and kernel
+    # attributes: warm it on the leading 8192 x 8192 principal submatrix
+    S.invert_in_place(S.build_m_bits(bits_d[:8192, :256].contiguous(), 8192, gamma), gamma)
+    work = torch.empty(L.lib().rdb_invert_workspace_bytes(n, 1), dtype=torch.uint8, device=dev)
+    info = L.pivot_info_tensor(1, dev)
+    torch.cuda.synchronize(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    L.check(L.lib().rdb_invert(m.data_ptr(), n, n, work.data_ptr(), info.data_ptr(), sh), "rdb_invert")
+    ev[1].record()
+    torch.cuda.synchronize(dev)
+    t = max_over_ranks(ev[0].elapsed_time(ev[1]))
+    rec = L.read_pivot_info(info)[0]
+    tf = 2.0 * n**3 / (t * 1e-3) / 1e12
+    out = {"n": n, "grid": "1x1", "ms": t, "tflops_total": tf, "tflops_per_gpu": tf, "frac_of_fp64_peak": tf / peak,
+           "pivot_flags": rec.flags, "min_pivot": rec.min_pivot, "host_bits_s": t_gen,
+           "kernel": "K2 wide 256-step Gauss-Jordan with look-ahead (gj_wide_row + gj_wide_update + nested NB=128 P1)"}
+    out["parity"] = _cfg5_parity_single(m, n, gamma)
+    return out
+
+
+def _cfg5_parity_single(m, n, gamma):
+    import torch
+
+    from paper_2308_07403_b200 import single as S
+
+    if not CFG5_FIXTURE.exists():
+        return "unchecked (tests/golden/cfg5_cols.npz missing)"
+    f = np.load(CFG5_FIXTURE)
+    cols = f["cols"]
+    d = S.d_columns(m, n, gamma, cols)
+    fin = d.isfinite()
+    u8 = d.clone()
+    u8[~fin] = 255
+    du = u8.to(dtype=torch.uint8).cpu().numpy()
+    bad = sum(digest(du[:, k]) != bytes(f["col_digest"][k]) for k in range(len(cols)))
+    return {"sampled_columns": int(len(cols)), "columns_differing_from_reference": int(bad),
+            "bit_exact": bad == 0, "reference": "digests of scipy lu_factor/lu_solve columns (tests/golden/make_golden_full.py)"}
+
+
+def cfg5_distributed(dev, rank, world, local_world, peak, max_over_ranks):
+    """Config 5 over all ranks: 2D block-cyclic grid, each rank builds only its
+    own tiles (bit rows of its row blocks, a PCG64 jump per run of rows), NCCL
+    panel broadcasts with look-ahead; D on the sampled columns gathered to rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_07403_b200 import distributed as D
+    from paper_2308_07403_b200 import workloads as wl
+
+    c = wl.CFG5
+    n, gamma = c["n"], c["gamma"]
+    pr, pc = GRIDS.get(world, (1, world))
+    lay = D.Layout(n, pr, pc)
+    grid = D.TorchGrid(lay)
+    r, cc = grid.me
+    rows = np.array([I * D.NB + i for I in lay.row_blocks(r) for i in range(D.NB)])
+    t0 = time.perf_counter()
+    procs = max(1, (os.cpu_count() or 1) // local_world)
+    bits_rows = _rows_parallel(n, c["p"], 0, rows, procs)
+    t_gen = time.perf_counter() - t0
+    br = torch.from_numpy(bits_rows.view(np.int32)).to(dev)
+    loc = D.local_m_from_bits(br, lay, r, cc, gamma)
+    del br
+    torch.cuda.synchronize(dev)
+    dist.barrier(device_ids=[dev.index])
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    minp, flags = D.invert_block_cyclic({grid.me: loc}, grid, D.CudaEngine())
+    ev[1].record()
+    torch.cuda.synchronize(dev)
+    t = max_over_ranks(ev[0].elapsed_time(ev[1]))
+    tf = 2.0 * n**3 / (t * 1e-3) / 1e12
+    out = {"n": n, "grid": f"{pr}x{pc}", "ms": t, "tflops_total": tf, "tflops_per_gpu": tf / world,
+           "frac_of_fp64_peak": tf / world / peak, "frac_of_n_gpu_peak": tf / (world * peak),
+           "pivot_flags": flags, "min_pivot": minp, "host_bits_s_rank0": t_gen,
+           "kernel": "distributed Gauss-Jordan NB=128: P1 + rdb_gemm_local (DMMA engine) + NCCL broadcasts, look-ahead"}
+    # parity: D of the sampled columns, assembled on rank 0
+    if CFG5_FIXTURE.exists():
+        f = np.load(CFG5_FIXTURE)
+        cols = f["cols"]
+        held, du = D.local_d_columns(loc, lay, r, cc, gamma, cols)
+        pieces = [None] * world if rank == 0 else None
+        dist.gather_object((r, held.cpu().numpy(), du.cpu().numpy()), pieces, dst=0)
+        if rank == 0:
+            full = np.zeros((n, len(cols)), np.uint8)
+            pos = {int(g): j for j, g in enumerate(cols)}
+            for pr_, hcols, block in pieces:
+                rws = np.array([I * D.NB + i for I in lay.row_blocks(pr_) for i in range(D.NB)])
+                for j, g in enumerate(hcols):
+                    full[rws, pos[int(g)]] = block[:, j]
+            bad = sum(digest(full[:, k]) != bytes(f["col_digest"][k]) for k in range(len(cols)))
+            out["parity"] = {"sampled_columns": int(len(cols)), "columns_differing_from_reference": int(bad),
+                             "bit_exact": bad == 0}
+    else:
+        out["parity"] = "unchecked (tests/golden/cfg5_cols.npz missing)"
+    return out
+
+
+def _rows_parallel(n, p, seed, rows, procs):
+    import multiprocessing as mp
+
+    from paper_2308_07403_b200 import workloads as wl
+
+    parts = [rows[i:i + 1024] for i in range(0, len(rows), 1024)]
+    if procs <= 1:
+        return np.concatenate([wl.er_bits_rows(n, p, seed, q) for q in parts])
+    with mp.get_context("fork").Pool(procs) as pool:
+        out = pool.starmap(wl.er_bits_rows, [(n, p, seed, q) for q in parts])
+    return np.concatenate(out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -292,20 +482,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=32)
     ap.add_argument("--e2e-chunk", type=int, default=256, help="graphs per pipelined chunk in the e2e engine")
     ap.add_argument("--e2e-steps", type=int, default=16,
                     help="steps of the streaming e2e measurement (at least --steps): the pipeline's fill and drain "
                          "(first upload, last download) are paid once per run, so short runs understate throughput")
     ap.add_argument("--d-dtype", default="uint8", choices=["uint8", "int32"],
                     help="D storage: compact lossless uint8 (255 = unreachable) or int32 (INT32_MAX)")
-    ap.add_argument("--single-n", type=int, default=32768,
-                    help="also time one N x N inversion per GPU (config-5 shape); 0 disables")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 inversion leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
+    if os.environ.get("RDB_BENCH_LAUNCH_PROBE") == "1":
+        return launch_probe(args)
 
     import torch
     import torch.distributed as dist
@@ -315,10 +507,16 @@ def main():
     from paper_2308_07403_b200 import workloads as wl
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    local_world = env_int("LOCAL_WORLD_SIZE", world)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init (nranks, NVLS/P2P) on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
+        assert dist.get_world_size() == args.gpus
     rb.load_library()
 
     bits, gammas, _ = wl.cfg2_batch(GRAPHS_PER_GPU, rank=rank)
@@ -373,21 +571,33 @@ def main():
     t_build = time_stage(lambda: buf.stage_build(batch, sh))
     t_inv = time_stage(lambda: (buf.stage_build(batch, sh), buf.stage_invert(batch, sh))) - t_build
     t_log = time_stage(lambda: buf.stage_log_ceil(batch, sh))
+    # K2 on the dense (ER) half alone: the Gauss-Jordan engine without the banded lattices
+    n_er = batch // 2
+    ber = B.BatchBuffers.allocate(N, n_er, dev)
+    ber.bits.copy_(buf.bits[:n_er])
+    ber.gammas.copy_(buf.gammas[:n_er])
+    t_b_er = time_stage(lambda: ber.stage_build(n_er, sh))
+    t_inv_er = time_stage(lambda: (ber.stage_build(n_er, sh), ber.stage_invert(n_er, sh))) - t_b_er
+    del ber
     clk = clocks.stop()
 
     n_pad = buf.n_pad
     flops_per_graph = 2.0 * n_pad**3
     # K2 skips the tiles of structurally zero blocks and the zero k-chunks of the
-    # column panel (block-sparse plan): the roofline uses the flop it executes;
-    # the dense-equivalent 2n^3 rate beside it
+    # column panel (block-sparse plan) and inverts the lattices by the banded path:
+    # the hardware fraction uses the flop it executes; the dense 2n^3 rate beside it
     exec_flops = B.executed_flops(bits, N)
+    exec_er = B.executed_flops(bits[:n_er], N)
     n_gj = int((~B.banded(bits, N)).sum())
     inv_tflops = exec_flops / (t_inv * 1e-3) / 1e12
     dense_tflops = flops_per_graph * batch / (t_inv * 1e-3) / 1e12
+    er_tflops = exec_er / (t_inv_er * 1e-3) / 1e12
     peak, peak_src = fp64_peak()
     hbm, hbm_src = hbm_peak()
     build_bytes = batch * (N * (N // 8) + 8 * n_pad * n_pad)
     log_bytes = batch * (8 * N * N + dsize * N * N)
+    roof_gps = peak * 1e12 / flops_per_graph  # per GPU: 2 n^3 at the DMMA peak
+    value = world * batch / (ms * 1e-3)
 
     # ---- lossless check of the compact D (outside every timed region): the
     # uint8 run must flag no graph and decode to the int32 run bit for bit
@@ -406,66 +616,57 @@ def main():
         assert same, "uint8 D differs from int32 D"
         d_check = "uint8 D decoded == int32 D on all graphs (bitwise), no range flags"
         del buf32, d8
-        torch.cuda.empty_cache()
+    del buf
+    torch.cuda.empty_cache()
 
-    # ---- single large inversion (config-5 shape; BASELINE's "inversion FP64 TFLOP/s"):
-    # M = I - gamma*A, A an ER pattern (p = 0.01) drawn on the device (untimed)
-    single = None
-    if args.single_n > 0:
-        sn = rb._lib.pad_to_nb(args.single_n)
-        warm = torch.eye(2048, dtype=torch.float64, device=dev)  # first single-matrix call sets up side stream
-        wwork = torch.empty(rb._lib.lib().rdb_invert_workspace_bytes(2048, 1), dtype=torch.uint8, device=dev)
-        winfo = rb._lib.pivot_info_tensor(1, dev)
-        rb._lib.check(rb._lib.lib().rdb_invert(warm.data_ptr(), 2048, 2048, wwork.data_ptr(), winfo.data_ptr(), sh),
-                      "rdb_invert")
-        gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-        m1 = (torch.rand((sn, sn), generator=gen, device=dev) < 0.01).to(torch.float64).mul_(-1e-4)
-        m1.diagonal().fill_(1.0)
-        work1 = torch.empty(rb._lib.lib().rdb_invert_workspace_bytes(sn, 1), dtype=torch.uint8, device=dev)
-        info1 = rb._lib.pivot_info_tensor(1, dev)
-        torch.cuda.synchronize(dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        ev[0].record(stream)
-        rb._lib.check(rb._lib.lib().rdb_invert(m1.data_ptr(), sn, sn, work1.data_ptr(), info1.data_ptr(), sh),
-                      "rdb_invert")
-        ev[1].record(stream)
-        torch.cuda.synchronize(dev)
-        t1 = max_over_ranks(ev[0].elapsed_time(ev[1]))
-        rec1 = rb._lib.read_pivot_info(info1)[0]
-        tf1 = 2.0 * sn**3 / (t1 * 1e-3) / 1e12
-        single = {"n": sn, "ms": t1, "tflops_per_gpu": tf1, "frac_of_fp64_peak": tf1 / fp64_peak()[0],
-                  "pivot_flags": rec1.flags, "min_pivot": rec1.min_pivot,
-                  "note": "one N x N M-matrix inverted per GPU (K2 with single-matrix look-ahead)"}
-        del m1, work1
-        torch.cuda.empty_cache()
-
-    # ---- e2e: pinned host bits -> engine -> pinned host int32 D
-    eng = B.APSPBatchEngine(N, batch, chunk=args.e2e_chunk, d_dtype=args.d_dtype)
-    bits_pin, gam_pin = eng.pin(bits, gammas)
-    for _ in range(max(1, args.warmup - 1)):
-        eng.run(bits_pin, gam_pin)
-    barrier()
-    # streaming: step s goes to output slot s % 2, so its kernels overlap the
-    # device->host copy of step s-1; every step's H2D and D2H is inside the region
-    e2e_steps = max(args.steps, args.e2e_steps)
-    t0 = time.perf_counter()
-    for s in range(e2e_steps):
-        if s >= 2:
+    # ---- e2e: pinned host bits -> engine -> pinned host D (uint8 headline, int32 beside it)
+    def e2e_run(d_dtype):
+        eng = B.APSPBatchEngine(N, batch, chunk=args.e2e_chunk, d_dtype=d_dtype)
+        bits_pin, gam_pin = eng.pin(bits, gammas)
+        for _ in range(max(1, args.warmup - 1)):
+            eng.run(bits_pin, gam_pin)
+        barrier()
+        # streaming: step s goes to output slot s % 2, so its kernels overlap the
+        # device->host copy of step s-1; every step's H2D and D2H is inside the region
+        steps = max(args.steps, args.e2e_steps)
+        t0 = time.perf_counter()
+        for s in range(steps):
+            if s >= 2:
+                eng.wait(s % 2, gam_pin, check=False)
+            eng.submit(bits_pin, gam_pin, s % 2)
+        for s in range(max(0, steps - 2), steps):
             eng.wait(s % 2, gam_pin, check=False)
-        eng.submit(bits_pin, gam_pin, s % 2)
-    for s in range(max(0, e2e_steps - 2), e2e_steps):
-        eng.wait(s % 2, gam_pin, check=False)
-    barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0) / e2e_steps
-    eng.submit(bits_pin, gam_pin, 0)
-    eng.wait(0, gam_pin, check=True)
+        barrier()
+        dt = max_over_ranks(time.perf_counter() - t0) / steps
+        eng.submit(bits_pin, gam_pin, 0)
+        eng.wait(0, gam_pin, check=True)
+        dsz = 1 if d_dtype == "uint8" else 4
+        res = {"value": world * batch / dt, "unit": "graphs/s", "h2d_bytes_per_step": int(bits.nbytes + gammas.nbytes),
+               "d2h_bytes_per_step": int(batch * N * N * dsz + batch * 16
+                                         + (batch * 8 * rb._lib.RDB_NCOUNTERS if d_dtype == "uint8" else 0)),
+               "ms_per_step": dt * 1e3, "steps": steps, "d_dtype": d_dtype,
+               "timing": "wall clock (perf_counter) around the whole stream incl. the first upload and the last "
+                         "download, barrier on both sides, max over ranks"}
+        del eng, bits_pin, gam_pin
+        torch.cuda.empty_cache()
+        return res
+
+    e2e = e2e_run(args.d_dtype)
+    e2e_other = e2e_run("int32" if args.d_dtype == "uint8" else "uint8")
+
+    # ---- config-5 inversion (BASELINE's "inversion FP64 TFLOP/s"): one GPU or the grid
+    cfg5 = None
+    if not args.no_cfg5:
+        cfg5 = (cfg5_single(dev, sh, peak, max_over_ranks) if world == 1
+                else cfg5_distributed(dev, rank, world, local_world, peak, max_over_ranks))
+        torch.cuda.empty_cache()
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    value = world * batch / (ms * 1e-3)
+    traffic, traffic_src = ncu_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -473,45 +674,47 @@ def main():
         "config": {"workload": WORKLOAD.format(args.d_dtype), "d_dtype": args.d_dtype, "d_check": d_check,
                    "graphs_per_gpu": batch, "global_batch": batch * world, "n": N,
                    "parallelism": f"dp{world} (independent graphs, no collective)",
-                   "l2": f"working set per step {(buf.m.numel() * 8 + buf.d.numel() * dsize) / 1e9:.1f} GB > 126 MB L2 "
-                         "(inputs larger than L2; no flush needed)"},
-        "inversion_tflops": inv_tflops, "inversion_frac_of_fp64_peak": inv_tflops / peak,
-        "inversion_dense_equivalent_tflops": dense_tflops,
-        "executed_flop_fraction": exec_flops / (flops_per_graph * batch),
+                   "l2": f"working set per step {(batch * n_pad * n_pad * 8 + batch * N * N * dsize) / 1e9:.1f} GB "
+                         "> 126 MB L2 (inputs larger than L2; no flush needed)"},
         "roofline": {"bound": "tensor", "kernel": "K2 blocked Gauss-Jordan (gj_panel + gj_rowpanel + gj_update, DMMA.8x8x4) "
                                                   "+ banded inverse of the block-tridiagonal graphs (band_factor + band_chain)",
                      "achieved": inv_tflops, "peak": peak, "unit": "TFLOP/s", "frac": inv_tflops / peak,
-                     "traffic": ncu_traffic(), "traffic_unit": "bytes per K2 call (8 GJ steps x 3 kernels x 2 sub-batches + plan + banded factor and chain, whole batch)",
-                     "traffic_source": "profiles/r01_ncu_full_cfg2.json", "peak_source": peak_src,
+                     "frac_executed": inv_tflops / peak,
+                     "dense_equivalent_tflops": dense_tflops, "frac_dense_2n3": dense_tflops / peak,
+                     "executed_flop_fraction": exec_flops / (flops_per_graph * batch),
+                     "graphs_per_s_roofline_per_gpu": roof_gps,
+                     "graphs_per_s_frac_of_roofline": value / (world * roof_gps),
+                     "k2_ms": t_inv,
+                     "k2_er_only": {"graphs": n_er, "ms": t_inv_er, "executed_flop": exec_er, "tflops": er_tflops,
+                                    "frac": er_tflops / peak,
+                                    "note": "the 128 ER graphs alone through the Gauss-Jordan engine (dense strips)"},
+                     "traffic": traffic, "traffic_unit": "DRAM bytes per K2 call (ncu --set full)",
+                     "traffic_source": traffic_src, "peak_source": peak_src,
                      "work_per_launch": f"{exec_flops:.4g} flop executed per K2 call = 2*128*128*16 per k-chunk over "
                                         f"the block-sparse plan's tiles and k-chunks for the {n_gj} Gauss-Jordan graphs + "
-                                        f"{B.band_flops(N):.4g} per banded graph x {batch - n_gj} "
-                                        f"({exec_flops / (flops_per_graph * batch):.3f} of the "
-                                        f"dense 2*n^3 = {flops_per_graph:.4g} flop per graph x {batch} graphs)"},
+                                        f"{B.band_flops(N):.4g} per banded graph x {batch - n_gj}; dense 2*n^3 = "
+                                        f"{flops_per_graph:.4g} flop per graph x {batch} graphs",
+                     "note": "frac > 1 is impossible for frac_executed; frac_dense_2n3 and graphs_per_s_frac_of_roofline "
+                             "exceed 1 because the block-sparse plan and the banded path skip work, not from hardware"},
         "kernels_ms": {"K1_build_m_bits": t_build, "K2_invert": t_inv, "K3_log_ceil": t_log},
         "hbm_kernels": {"K1_GBps": build_bytes / (t_build * 1e-3) / 1e9, "K3_GBps": log_bytes / (t_log * 1e-3) / 1e9,
-                        "peak_GBps": hbm, "peak_source": hbm_src},
-        "e2e": {"value": world * batch / e2e_s, "unit": "graphs/s", "h2d_bytes_per_step": int(bits.nbytes + gammas.nbytes),
-                "d2h_bytes_per_step": int(batch * N * N * dsize + batch * 16
-                                          + (batch * 8 * rb._lib.RDB_NCOUNTERS if buf.compact else 0)),
-                "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
-                "timing": "wall clock (perf_counter) around the whole stream incl. the first upload and the last "
-                          "download, barrier on both sides, max over ranks"},
+                        "K1_frac": build_bytes / (t_build * 1e-3) / 1e9 / hbm,
+                        "K3_frac": log_bytes / (t_log * 1e-3) / 1e9 / hbm, "peak_GBps": hbm, "peak_source": hbm_src},
+        "e2e": e2e,
+        "e2e_" + e2e_other["d_dtype"]: e2e_other,
         "gpu_launches": launches,
-        "single_matrix_inversion": single,
+        "inversion_cfg5": cfg5,
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
         pool = CpuPool(per_core=2)
         pool.run()  # worker start-up and graph generation, untimed
-        dt = pool.run()
+        runs = [pool.run() for _ in range(5)]  # the reference's _median_time protocol (experiments.py:263-270)
         pool.close()
+        dt = statistics.median(runs)
         line["cpu_baseline"] = {"value": len(pool.items) / dt, "unit": "graphs/s", "cores": pool.procs,
-                                "kind": "port",
-                                "sample": f"{len(pool.items)} cfg2 graphs (half ER, half lattice), 2 per core, "
-                                          f"{pool.procs} single-threaded processes through "
-                                          "oracle/rdist_oracle.run_rdist (reference run_rdist restated, scipy LAPACK)",
-                                "host": cpu_host_info(cpu_sample_graphs(2))}
+                                "kind": pool.kind, "sample": pool.sample() + "; median of 5 samples",
+                                "host": cpu_host_info()}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

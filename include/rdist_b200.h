@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RDB_ABI_VERSION 4
+#define RDB_ABI_VERSION 5
 #define RDB_NB 128 /* Gauss-Jordan panel width; inverted matrices are padded to a multiple */
 
 /* status codes */
@@ -140,12 +140,14 @@ int rdb_invert(double* a, int64_t n_pad, int64_t lda, void* work, rdb_pivot_info
  *     A, B, C row-major, m, n multiples of NB and k of 16; op is += (TMA
  *     reduce-add) when accumulate != 0, else =; row tile skip_row_tile and
  *     column tile skip_col_tile are left untouched (-1: none); column tile
- *     store_col_tile is always stored (=). Same DMMA engine as rdb_invert. */
+ *     store_col_tile is always stored (=); at most max_ctas persistent CTAs
+ *     (0: one per SM), so a look-ahead can keep SMs free for the panel work
+ *     and the NCCL kernels of the next step. Same DMMA engine as rdb_invert. */
 int rdb_gj_panel_inverse(double* a, int64_t lda, rdb_pivot_info* info, int first, int64_t p0,
                          void* stream);
 int rdb_gemm_local(const double* a, int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
                    int64_t m, int64_t n, int64_t k, int64_t skip_row_tile, int64_t skip_col_tile,
-                   int64_t store_col_tile, int accumulate, int negate, void* stream);
+                   int64_t store_col_tile, int accumulate, int negate, int64_t max_ctas, void* stream);
 
 /* Gauss-Jordan with partial (row) pivoting, first-max pivot choice as
  * LAPACK idamax; in place, any n. For generic matrices handed to

@@ -94,8 +94,11 @@ def rounded_r_distance(y: np.ndarray, gamma: float) -> np.ndarray:
 
 
 def run_rdist(w: np.ndarray, gamma: float, unweighted: bool = True) -> np.ndarray:
-    """The reference's timed closure (experiments.py:305-310)."""
-    r = r_distance(resolvent_y(w, gamma), gamma)
+    """The reference's timed closure (experiments.py:305-310): resolvent(with_residual=False)
+    computes its health flags too (resolvent.py:120-124), then r_distance and ceil."""
+    y = resolvent_y(w, gamma)
+    health(y)
+    r = r_distance(y, gamma)
     return np.ceil(r) if unweighted else r
 
 

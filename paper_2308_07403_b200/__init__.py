@@ -25,8 +25,16 @@ from .graphs import (
     write_distance_csv,
     write_edge_list,
 )
-from .linalg import PIVOT_RTOL, PowerIterationResult, SingularMatrixError, lu_invert, power_iteration, spectral_radius
-from .navigation import PathResult, greedy_descent, next_hop_table
+from .linalg import (
+    PIVOT_RTOL,
+    PowerIterationResult,
+    SingularMatrixError,
+    lu_invert,
+    mat_mul,
+    power_iteration,
+    spectral_radius,
+)
+from .navigation import AccuracyReport, PathResult, accuracy_report, greedy_descent, next_hop_table
 from .resolvent import (
     DELTA_MIN,
     NEGATIVE_ENTRY_TOL,
@@ -56,7 +64,8 @@ from .batch import (
 )
 from ._lib import NativeUnavailableError, load_library
 from .oracles import bfs_apsp, bfs_apsp_device
-from .sweep import SweepRecord, global_accuracy, local_accuracy, sweep_gamma_graph, sweep_point
+from .navigation import global_accuracy, local_accuracy  # noqa: E402  (device K6/K9, .sweep)
+from .sweep import SweepRecord, sweep_gamma_graph, sweep_point
 
 __version__ = "0.1.0"
 
@@ -74,7 +83,10 @@ __all__ = [
     "write_edge_list",
     "bfs_apsp",
     "bfs_apsp_device",
+    "AccuracyReport",
     "SweepRecord",
+    "accuracy_report",
+    "mat_mul",
     "global_accuracy",
     "local_accuracy",
     "sweep_gamma_graph",

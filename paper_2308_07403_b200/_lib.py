@@ -18,7 +18,7 @@ import torch
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "librdist_b200.so"
 
-RDB_ABI_VERSION = 4  # include/rdist_b200.h; load_library refuses a library built from another header
+RDB_ABI_VERSION = 5  # include/rdist_b200.h; load_library refuses a library built from another header
 RDB_NB = 128
 RDB_OK = 0
 RDB_PIV_NONPOS = 1
@@ -68,7 +68,7 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "rdb_gj_panel_inverse": (_int, [_vp, _i64, _vp, _int, _i64, _vp]),
     "rdb_gemm_local": (
         _int,
-        [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _int, _int, _vp],
+        [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _int, _int, _i64, _vp],
     ),
     "rdb_invert_pivoted_workspace_bytes": (_sz, [_i64]),
     "rdb_invert_pivoted": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),

@@ -16,6 +16,25 @@ namespace rdb {
 
 constexpr int NB = RDB_NB;  // Gauss-Jordan panel width (128)
 
+// ---------------------------------------------------------------- per-device host state
+// Function attributes, SM counts and the library's internal streams / events
+// are kept per CUDA device (the caller's current device), so one process may
+// drive several GPUs.
+constexpr int MAX_DEVICES = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAX_DEVICES) return -1;
+  return d;
+}
+// once-per-device flag for lazily applied settings (idempotent, so a benign race)
+struct DeviceFlags {
+  bool v[MAX_DEVICES] = {};
+  bool get(int d) const { return d >= 0 && v[d]; }
+  void set(int d) {
+    if (d >= 0) v[d] = true;
+  }
+};
+
 // ---------------------------------------------------------------- DMMA
 // D(8x8) += A(8x4, row) * B(4x8, col). Lane l holds A[l/4][l%4], B[l%4][l/4],
 // and C[l/4][2*(l%4) + {0,1}].

@@ -23,7 +23,10 @@
 // the Schur complements of the natural elimination order, so their
 // Gauss-Jordan pivots are LAPACK's diag(U) without row swaps
 // (linalg.py:33-34): they give the pivot record; any pivot <= 0 in any of the
-// inversions sets RDB_PIV_NONPOS (the caller then runs the pivoted kernel).
+// inversions sets RDB_PIV_NONPOS. The chain kernel has then overwritten M,
+// so the batch API (batch.redo_pivoted) rebuilds that graph's M from its
+// adjacency and inverts it with the partial-pivoting kernel, which decides
+// singularity as the reference's LAPACK path does.
 //
 // Kernels: band_detect_bits_kernel (flag per matrix from the adjacency bits),
 // band_factor_kernel (two matrices per CTA, a 4-warp group per sweep, all
@@ -431,14 +434,15 @@ int band_detect(const uint32_t* bits, int64_t n, int64_t batch, int* nonband, cu
 int band_invert(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t batch, const int* nonband,
                 double* ws, rdb_pivot_info* info, cudaStream_t st) {
   if (n_pad % S || n_pad / S < 2) return RDB_EINVAL;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr;
+  const int attr_dev = current_device();
+  if (!attr.get(attr_dev)) {
     if (cudaFuncSetAttribute(band_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(FactorSmem)) != cudaSuccess ||
         cudaFuncSetAttribute(band_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM) !=
             cudaSuccess)
       return RDB_ECUDA;
-    attr = true;
+    attr.set(attr_dev);
   }
   const int nb = (int)(n_pad / S);
   band_factor_kernel<<<(unsigned)((batch + GPC - 1) / GPC), 256 * GPC, sizeof(FactorSmem), st>>>(

@@ -237,14 +237,14 @@ static int make_ec_map(CUtensorMap* map, const double* base, int64_t rows, int64
   return make_c_map(map, base, rows, cols, ld, stride, batch, EC::HROWS, EC::WCOLS);
 }
 
-static int g_sms = 0;
+static int g_sms[MAX_DEVICES] = {};
 
 static int setup() {
-  if (g_sms) return RDB_OK;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return RDB_ECUDA;
-  if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return RDB_ECUDA;
+  const int dev = current_device();
+  if (dev < 0) return RDB_ECUDA;
+  if (g_sms[dev]) return RDB_OK;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return RDB_ECUDA;
   if (cudaFuncSetAttribute(gj_rowpanel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)EC::SMEM_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -252,29 +252,45 @@ static int setup() {
       cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)p1::SMEM_BYTES) != cudaSuccess)
     return RDB_ECUDA;
+  g_sms[dev] = sms;
   return RDB_OK;
 }
 
-// Side stream + events of the single-matrix look-ahead (one set per process;
-// the library is used from one device per process).
-static cudaStream_t g_side = nullptr;
-static cudaEvent_t g_ev_a = nullptr, g_ev_p = nullptr, g_ev_b = nullptr;
+// Internal streams and events, one set per device: the look-ahead side
+// stream (single-matrix and wide paths) and the sub-batch streams of a split
+// batch. Enqueueing is serialised by g_enqueue (invert_batched).
+constexpr int MAX_PARTS = 4;
+struct DevStreams {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_p = nullptr, ev_b = nullptr;
+  cudaStream_t part[MAX_PARTS] = {};
+  cudaEvent_t fork = nullptr, join[MAX_PARTS] = {};
+};
+static DevStreams g_streams[MAX_DEVICES];
 
-static int side_resources(cudaStream_t* side) {
-  if (!g_side) {
-    if (cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_ev_a, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_ev_p, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_ev_b, cudaEventDisableTiming) != cudaSuccess)
-      return RDB_ECUDA;
+static DevStreams* dev_streams() {
+  const int dev = current_device();
+  if (dev < 0) return nullptr;
+  DevStreams& d = g_streams[dev];
+  if (!d.side) {
+    if (cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_p, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.ev_b, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+    for (int i = 0; i < MAX_PARTS; ++i)
+      if (cudaStreamCreateWithFlags(&d.part[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&d.join[i], cudaEventDisableTiming) != cudaSuccess)
+        return nullptr;
   }
-  *side = g_side;
-  return RDB_OK;
+  return &d;
 }
 
 int sm_count() {
   setup();
-  return g_sms > 0 ? g_sms : 148;
+  const int dev = current_device();
+  return dev >= 0 && g_sms[dev] > 0 ? g_sms[dev] : 148;
 }
 
 #define RDB_HOST_DEV __host__ __device__ __forceinline__
@@ -559,11 +575,9 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   // (part 1); the next P1 (one CTA, latency-bound) then runs on a side stream
   // on one SM while the rest of the update (part 2) uses the other SMs.
   const bool lookahead = (batch == 1 && nt >= 3);
-  cudaStream_t side = nullptr;
-  if (lookahead) {
-    rc = side_resources(&side);
-    if (rc) return rc;
-  }
+  DevStreams* ds = lookahead ? dev_streams() : nullptr;
+  if (lookahead && !ds) return RDB_ECUDA;
+  cudaStream_t side = ds ? ds->side : nullptr;
   gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, idx_base, info, first,
                                                                        info_stride, nonband);
   for (int k = 0; k < nt; ++k) {
@@ -582,18 +596,18 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
     if (lookahead && k + 1 < nt) {
       // side stream, one SM: the next diagonal tile, then its inverse (P1);
       // main stream, the other SMs: every other tile of this update
-      cudaEventRecord(g_ev_a, st);
-      cudaStreamWaitEvent(side, g_ev_a, 0);
+      cudaEventRecord(ds->ev_a, st);
+      cudaStreamWaitEvent(side, ds->ev_a, 0);
       UpdateSched ua{a, cnt, lda, stride, nt, k, 1, 1};
       gj_update_kernel<<<1, EC::THREADS, EC::SMEM_BYTES, side>>>(amap, cmap, ua);
       const int p1n = (k + 1) * NB;
       gj_panel_kernel<<<1, p1::THREADS, p1::SMEM_BYTES, side>>>(a, lda, stride, p1n, idx_base + p1n, info, 0);
-      cudaEventRecord(g_ev_p, side);
+      cudaEventRecord(ds->ev_p, side);
       UpdateSched ub{a, cnt, lda, stride, nt, k, 1, 2, dyn ? dyn + 1 : nullptr};
       const int64_t tiles = (int64_t)(nt - 1) * nt - 1;
       const unsigned grid = (unsigned)(tiles < sm_count() - 1 ? tiles : sm_count() - 1);
       gj_update_kernel<<<grid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, ub);
-      cudaStreamWaitEvent(st, g_ev_p, 0);
+      cudaStreamWaitEvent(st, ds->ev_p, 0);
     } else {
       UpdateSched up{a, cnt, lda, stride, nt, k, (int)batch, 0, dyn ? dyn + 1 : nullptr};
       if (plan) {
@@ -613,9 +627,6 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
 // each part's kernels fill the others' tails (the last partial round of every persistent launch, the
 // second wave of the one-CTA-per-matrix panel inverses). Measured on config 2:
 // 18.44 -> 18.03 ms for 256 graphs (tools/two_stream.py).
-constexpr int MAX_PARTS = 4;
-static cudaStream_t g_part[MAX_PARTS] = {};
-static cudaEvent_t g_fork = nullptr, g_join[MAX_PARTS] = {};
 
 static size_t counter_bytes(int64_t n_pad, int64_t batch) {
   const size_t nt = (size_t)((n_pad + NB - 1) / NB);
@@ -773,33 +784,28 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   };
   const int parts = split_parts();
   if (batch >= split_min_batch() && batch >= 4 * parts && a && work && info && n % NB == 0 && stride >= n * lda) {
-    if (!g_fork) {
-      for (int i = 0; i < MAX_PARTS; ++i)
-        if (cudaStreamCreateWithFlags(&g_part[i], cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&g_join[i], cudaEventDisableTiming) != cudaSuccess)
-          return RDB_ECUDA;
-      if (cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess) return RDB_ECUDA;
-    }
+    DevStreams* ds = dev_streams();
+    if (!ds) return RDB_ECUDA;
     int* dyn = reinterpret_cast<int*>(wb + ws.dyn);
     if (cudaMemsetAsync(dyn, 0, 2 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
-    cudaEventRecord(g_fork, st);
+    cudaEventRecord(ds->fork, st);
     // the banded matrices on this stream, concurrently with the sub-batches
     int rc = use_band ? band_invert(a, n, lda, stride, batch, nonband, band_ws, info, st) : RDB_OK;
     int64_t lo = 0;
     for (int i = 0; i < parts && rc == RDB_OK; ++i) {
       const int64_t cnt = (batch - i + parts - 1) / parts;
-      cudaStreamWaitEvent(g_part[i], g_fork, 0);
+      cudaStreamWaitEvent(ds->part[i], ds->fork, 0);
       const PlanPart pp = part_plan(i, parts, lo);
       // row-block counters of the part, 16-byte aligned (counter_bytes has the slack)
       char* cw = wb + (((size_t)lo * ntl * sizeof(int) + 15) & ~(size_t)15);
       const bool dyn_on = dyn_sched();
-      rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, g_part[i], 1, 0,
+      rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, ds->part[i], 1, 0,
                        dyn_on ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr, parts,
                        nonband ? nonband + i : nullptr, (!dyn_on && cosched_cap()) ? sm_count() / parts : 0);
-      cudaEventRecord(g_join[i], g_part[i]);
+      cudaEventRecord(ds->join[i], ds->part[i]);
       lo += cnt;
     }
-    for (int i = 0; i < parts; ++i) cudaStreamWaitEvent(st, g_join[i], 0);
+    for (int i = 0; i < parts; ++i) cudaStreamWaitEvent(st, ds->join[i], 0);
     return rc;
   }
   const PlanPart pp = part_plan(0, 1, 0);
@@ -948,14 +954,15 @@ static size_t wide_scratch_bytes(int64_t n) { return (size_t)2 * WB * n * sizeof
 static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_info* info, cudaStream_t st) {
   int rc = setup();
   if (rc) return rc;
-  static bool attrs = false;
-  if (!attrs) {
+  static DeviceFlags attrs;
+  const int attrs_dev = current_device();
+  if (!attrs.get(attrs_dev)) {
     if (cudaFuncSetAttribute(gj_wide_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)EC::SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(gj_wide_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)EC::SMEM_BYTES) != cudaSuccess)
       return RDB_ECUDA;
-    attrs = true;
+    attrs.set(attrs_dev);
   }
   const int nt = (int)(n / NB);
   // workspace: [counters of the nested 256-block inverse | R (256 x n) | C (n x 256)]
@@ -968,8 +975,9 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
       (rc = make_ec_map(&rmap, R, WB, n, n, (int64_t)WB * n, 1)) ||
       (rc = make_ec_map(&smap, Cs, n, WB, WB, (int64_t)WB * n, 1)))
     return rc;
-  cudaStream_t side = nullptr;
-  if ((rc = side_resources(&side))) return rc;
+  DevStreams* ds = dev_streams();
+  if (!ds) return RDB_ECUDA;
+  cudaStream_t side = ds->side;
   // 1. (step 0) D = A_00^-1: the NB = 128 Gauss-Jordan on the 256 x 256 block
   rc = invert_core(a, WB, lda, 0, 1, cnt, info, st, 1, 0);
   if (rc) return rc;
@@ -984,15 +992,15 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
     // diagonal block is updated first and inverted (1.) on a side stream, one
     // SM, while the rest of the update runs on the other SMs
     if (ahead) {
-      cudaEventRecord(g_ev_a, st);
-      cudaStreamWaitEvent(side, g_ev_a, 0);
+      cudaEventRecord(ds->ev_a, st);
+      cudaStreamWaitEvent(side, ds->ev_a, 0);
       WideUpdateSched u1{a, R, lda, n, nt, p0t, 1};
       gj_wide_update_kernel<<<1, EC::THREADS, EC::SMEM_BYTES, side>>>(amap, cmap, smap, u1);
-      cudaEventRecord(g_ev_b, side);  // u1 has read the old column panel (the copy-back below overwrites it)
+      cudaEventRecord(ds->ev_b, side);  // u1 has read the old column panel (the copy-back below overwrites it)
       const int64_t q0 = p0 + WB;
       rc = invert_core(a + q0 * lda + q0, WB, lda, 0, 1, cnt, info, side, 0, q0);
       if (rc) return rc;
-      cudaEventRecord(g_ev_p, side);
+      cudaEventRecord(ds->ev_p, side);
       WideUpdateSched u2{a, R, lda, n, nt, p0t, 2};
       const int64_t tiles = (int64_t)(nt - 2) * nt - 4;
       const unsigned grid = (unsigned)(tiles < sm_count() - 1 ? tiles : sm_count() - 1);
@@ -1003,7 +1011,7 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
           amap, cmap, smap, us);
     }
     // 4. scratches -> band rows (R, columns outside the band) and band columns (C, rows outside)
-    if (ahead) cudaStreamWaitEvent(st, g_ev_b, 0);
+    if (ahead) cudaStreamWaitEvent(st, ds->ev_b, 0);
     const int64_t right = n - p0 - WB;
     if (p0 > 0 &&
         (cudaMemcpy2DAsync(a + p0 * lda, lda * 8, R, n * 8, p0 * 8, WB, cudaMemcpyDeviceToDevice, st) ||
@@ -1016,7 +1024,7 @@ static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_
                            cudaMemcpyDeviceToDevice, st)))
       return RDB_ECUDA;
     if (ahead) {
-      cudaStreamWaitEvent(st, g_ev_p, 0);
+      cudaStreamWaitEvent(st, ds->ev_p, 0);
     } else if (p + 1 < nt / 2) {  // no look-ahead: the next 256-block inverse here
       const int64_t q0 = p0 + WB;
       rc = invert_core(a + q0 * lda + q0, WB, lda, 0, 1, cnt, info, st, 0, q0);
@@ -1178,18 +1186,19 @@ extern "C" int rdb_gj_panel_inverse(double* a, int64_t lda, rdb_pivot_info* info
 extern "C" int rdb_gemm_local(const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
                               int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t skip_row_tile,
                               int64_t skip_col_tile, int64_t store_col_tile, int accumulate, int negate,
-                              void* stream) {
+                              int64_t max_ctas, void* stream) {
   if (!a || !b || !c || m <= 0 || n <= 0 || k <= 0 || m % NB || n % NB || k % eng::BK) return RDB_EINVAL;
   if ((lda & 1) || (ldb & 1) || (ldc & 1) || lda < k || ldb < n || ldc < n) return RDB_EINVAL;
   if (((uintptr_t)b & 15) || ((uintptr_t)c & 15)) return RDB_EINVAL;
   int rc = setup();
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr;
+  const int attr_dev = current_device();
+  if (!attr.get(attr_dev)) {
     if (cudaFuncSetAttribute(local_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)EC::SMEM_BYTES) != cudaSuccess)
       return RDB_ECUDA;
-    attr = true;
+    attr.set(attr_dev);
   }
   CUtensorMap amap;
   rc = make_a_map(&amap, a, m, k, lda, m * lda, 1);
@@ -1205,8 +1214,9 @@ extern "C" int rdb_gemm_local(const double* a, int64_t lda, const double* b, int
                    accumulate ? eng::EPI_REDUCE : eng::EPI_STORE, negate ? 1 : 0};
   const int64_t tiles = (int64_t)(mt - (sched.skip_row >= 0)) * (nt - (sched.skip_col >= 0));
   if (tiles <= 0) return RDB_OK;
-  local_gemm_kernel<<<persistent_grid(tiles), EC::THREADS, EC::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
-      amap, cmap, sched);
+  unsigned grid = persistent_grid(tiles);
+  if (max_ctas > 0 && grid > (unsigned)max_ctas) grid = (unsigned)max_ctas;
+  local_gemm_kernel<<<grid, EC::THREADS, EC::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(amap, cmap, sched);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }

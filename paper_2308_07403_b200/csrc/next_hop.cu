@@ -581,12 +581,13 @@ extern "C" int rdb_next_hop(const double* w, int64_t ldw, const double* dist, in
   if (wk.srt && n_targets <= 65535LL * PR_T) {
     // pruned path: weight-sorted columns, dist transposed, per-target lower bounds
     const int sort_smem = 2 * SORT_MAX * (int)sizeof(unsigned long long);
-    static bool attr = false;
-    if (!attr) {
+    static DeviceFlags attr;
+    const int attr_dev = current_device();
+    if (!attr.get(attr_dev)) {
       if (cudaFuncSetAttribute(csc_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_smem) !=
           cudaSuccess)
         return RDB_ECUDA;
-      attr = true;
+      attr.set(attr_dev);
     }
     csc_sort_kernel<<<(unsigned)n, 256, sort_smem, st>>>(wk.offs, wk.idx, wk.val, n, wk.srt);
     transpose_kernel<<<dim3((unsigned)((n + 31) / 32), (unsigned)((n_targets + 31) / 32)), dim3(32, 8), 0, st>>>(

@@ -4,8 +4,8 @@ Drop-in for pkg/src/rdist/linalg.py (lu_invert :18-39, power_iteration
 :57-94, spectral_radius :97-99). Inputs may be numpy arrays (returned
 results are numpy arrays, as in the reference) or CUDA tensors (results stay
 on the device). All arithmetic runs in the sm_100a kernels of
-``librdist_b200.so``; there is no CPU fallback. ``mat_mul`` is not part of
-the path and is not provided.
+``librdist_b200.so``; there is no CPU fallback. ``mat_mul`` (linalg.py:42-48,
+off the timed path) runs on the same DMMA engine (rdb_gemm_local).
 """
 
 from __future__ import annotations
@@ -59,6 +59,38 @@ def lu_invert(m):
     if on_device:
         return y.contiguous()
     return y.cpu().numpy().copy(order="C")
+
+
+def mat_mul(a, b):
+    """Matrix product with an explicit shape check (linalg.py:42-48): C = A B
+    on the FP64 DMMA engine (rdb_gemm_local), operands zero-padded to the
+    engine's 128 x 128 x 16 tiles. numpy in -> numpy out, CUDA in -> CUDA out."""
+    from . import _lib as L
+
+    dev_in = isinstance(a, torch.Tensor) and a.is_cuda
+    if not isinstance(a, torch.Tensor):
+        a = np.asarray(a, dtype=np.float64)
+    if not isinstance(b, torch.Tensor):
+        b = np.asarray(b, dtype=np.float64)
+    if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
+        raise ValueError(f"shape mismatch: {tuple(a.shape)} x {tuple(b.shape)}")
+    m, k = a.shape
+    n = b.shape[1]
+    dev = L.device()
+    if m == 0 or n == 0 or k == 0:
+        out = torch.zeros((m, n), dtype=torch.float64, device=dev)
+        return out if dev_in else out.cpu().numpy()
+    mp, np_ = L.pad_to_nb(m), L.pad_to_nb(n)
+    kp = (k + 15) // 16 * 16
+    ap = torch.zeros((mp, kp), dtype=torch.float64, device=dev)
+    bp = torch.zeros((kp, np_), dtype=torch.float64, device=dev)
+    ap[:m, :k] = torch.as_tensor(a, dtype=torch.float64, device=dev)
+    bp[:k, :n] = torch.as_tensor(b, dtype=torch.float64, device=dev)
+    cp = torch.empty((mp, np_), dtype=torch.float64, device=dev)
+    L.check(L.lib().rdb_gemm_local(ap.data_ptr(), kp, bp.data_ptr(), np_, cp.data_ptr(), np_, mp, np_, kp, -1, -1,
+                                   -1, 0, 0, 0, L.stream_handle()), "rdb_gemm_local(mat_mul)")
+    out = cp[:m, :n]
+    return out.contiguous() if dev_in else out.cpu().numpy().copy(order="C")
 
 
 def power_iteration(m, tol: float = 1e-6, max_iter: int | None = None) -> PowerIterationResult:

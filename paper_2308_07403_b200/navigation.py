@@ -7,7 +7,8 @@ vertex j minimising W[k][j] + dist[goal][k], lowest index on ties, stopping on
 walk is then a pointer chase over that row. ``next_hop_table`` evaluates the
 same step for many goals at once (the config-4 table; ``next_hop_table_shard``
 gives one rank its block of target rows). The reference module's accuracy
-metrics are in :mod:`.sweep` (K6 + K9 on the device).
+metrics (navigation.py:77-153: global_accuracy, local_accuracy,
+accuracy_report / AccuracyReport) run on the device (K6 + K9, :mod:`.sweep`).
 """
 
 from __future__ import annotations
@@ -27,6 +28,47 @@ class PathResult:
     length: float
     reached: bool
     steps_taken: int
+
+
+@dataclass(frozen=True)
+class AccuracyReport:
+    """navigation.py:27-32."""
+
+    global_fraction: float
+    local_fraction: float
+    pairs_evaluated: int
+    pairs_excluded_unreachable: int
+
+
+def global_accuracy(estimate, exact) -> float:
+    """Fraction of off-diagonal exact-finite pairs where estimate == exact
+    (navigation.py:77-88), counted on the device (K9)."""
+    from .sweep import global_accuracy as _g
+
+    return _g(estimate, exact)
+
+
+def local_accuracy(g, estimate, exact, atol: float = 0.0) -> float:
+    """Fraction of (goal, node) pairs whose estimate-predicted successor is a
+    truly closest successor (navigation.py:91-134), on the device (K6 + K9)."""
+    from .sweep import local_accuracy as _l
+
+    return _l(g, estimate, exact, atol=atol)
+
+
+def accuracy_report(g, global_estimate, local_estimate, exact, atol: float = 0.0) -> AccuracyReport:
+    """Both metrics at once (navigation.py:137-153): the rounded estimate feeds
+    the global metric, the raw one the local metric; pair counts from the
+    exact distances."""
+    ex = np.asarray(exact) if not isinstance(exact, torch.Tensor) else exact.detach().cpu().numpy()
+    off = ~np.eye(ex.shape[0], dtype=bool)
+    fin = np.isfinite(ex)
+    return AccuracyReport(
+        global_fraction=global_accuracy(global_estimate, exact),
+        local_fraction=local_accuracy(g, local_estimate, exact, atol=atol),
+        pairs_evaluated=int((off & fin).sum()),
+        pairs_excluded_unreachable=int((off & ~fin).sum()),
+    )
 
 
 def _dist_rows_device(dist, rows: np.ndarray) -> torch.Tensor:

@@ -28,13 +28,13 @@ class CpuTestEngine:
         self.minp = min(self.minp, float(torch.linalg.svdvals(blk).min()))
         blk.copy_(torch.linalg.inv(blk))
 
-    def row_panel(self, d, rows, skip_col):
+    def row_panel(self, d, rows, skip_col, max_ctas=0):
         for J in range(rows.shape[1] // NB):
             if J != skip_col:
                 sl = slice(J * NB, (J + 1) * NB)
                 rows[:, sl] = d @ rows[:, sl]
 
-    def update(self, c, cp, rp, skip_row, store_col):
+    def update(self, c, cp, rp, skip_row, store_col, max_ctas=0):
         for I in range(c.shape[0] // NB):
             if I == skip_row:
                 continue
@@ -75,11 +75,16 @@ def test_virtual_grid_cpu(grid):
     m = m_matrix(n, 3)
     lay = D.Layout(n, *grid)
     full = torch.from_numpy(m)
-    locs = {(r, c): D.scatter(full, lay, r, c) for r in range(grid[0]) for c in range(grid[1])}
-    minp, flags = D.invert_block_cyclic(locs, D.VirtualGrid(lay), CpuTestEngine())
-    y = D.gather(locs, lay).numpy()
-    np.testing.assert_allclose(y, np.linalg.inv(m), rtol=1e-12, atol=1e-15)
-    assert flags == 0 and minp > 0.5
+    ys = []
+    for lookahead in (False, True):
+        locs = {(r, c): D.scatter(full, lay, r, c) for r in range(grid[0]) for c in range(grid[1])}
+        minp, flags = D.invert_block_cyclic(locs, D.VirtualGrid(lay), CpuTestEngine(), lookahead=lookahead)
+        ys.append(D.gather(locs, lay).numpy())
+        np.testing.assert_allclose(ys[-1], np.linalg.inv(m), rtol=1e-12, atol=1e-15)
+        assert flags == 0 and minp > 0.5
+    # the look-ahead order (row / column block k+1 first, the rest after the
+    # next panel) gives every tile the same products in the same order
+    assert np.array_equal(ys[0], ys[1])
 
 
 def _free_port():

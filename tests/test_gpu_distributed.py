@@ -23,8 +23,9 @@ def m_on_device(n, gamma, seed):
     return m
 
 
-@pytest.mark.parametrize("grid", [(1, 2), (2, 1), (2, 2), (2, 4), (3, 2)])
-def test_virtual_grid_bitwise_equals_single_gpu(cuda, grid):
+@pytest.mark.parametrize("lookahead", [True, False])
+@pytest.mark.parametrize("grid", [(1, 1), (1, 2), (2, 1), (2, 2), (2, 4), (3, 2)])
+def test_virtual_grid_bitwise_equals_single_gpu(cuda, grid, lookahead):
     n, gamma = 1024, 1e-2
     m = m_on_device(n, gamma, 17)
     ref = m.clone()
@@ -32,7 +33,7 @@ def test_virtual_grid_bitwise_equals_single_gpu(cuda, grid):
     lay = D.Layout(n, *grid)
     locs = {(r, c): D.scatter(m, lay, r, c) for r in range(grid[0]) for c in range(grid[1])}
     eng = D.CudaEngine()
-    minp, flags = D.invert_block_cyclic(locs, D.VirtualGrid(lay), eng)
+    minp, flags = D.invert_block_cyclic(locs, D.VirtualGrid(lay), eng, lookahead=lookahead)
     y = D.gather(locs, lay)
     torch.cuda.synchronize()
     assert torch.equal(y, ref), float((y - ref).abs().max())
@@ -47,7 +48,7 @@ def test_gemm_local_skip_store(cuda):
     b = torch.randn(k, n, dtype=torch.float64, device="cuda")
     c0 = torch.randn(m, n, dtype=torch.float64, device="cuda")
     c = c0.clone()
-    L.check(L.lib().rdb_gemm_local(a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n, m, n, k, 1, -1, 2, 1, 1,
+    L.check(L.lib().rdb_gemm_local(a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n, m, n, k, 1, -1, 2, 1, 1, 0,
                                    L.stream_handle()), "gemm")
     exp = c0 - a @ b
     exp[:, 256:384] = -(a @ b)[:, 256:384]
@@ -83,3 +84,39 @@ def test_torch_grid_nccl_single_rank(cuda):
         assert flags == 0 and minp == rec.min_pivot
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 4)])
+def test_cfg5_pipeline_per_rank_virtual(cuda, grid):
+    """The bench's config-5 multi-GPU leg on one device: every rank builds its
+    local M from the bit rows of its own row blocks only (workloads.er_bits_rows,
+    a PCG64 jump per run of rows), the grid inverts with look-ahead, each rank
+    takes D of the sampled columns it holds; the assembled columns equal the
+    single-GPU pipeline's (single.py) bit for bit."""
+    from paper_2308_07403_b200 import single as S
+
+    n, p, gamma, seed = 2048, 0.02, 1e-3, 4
+    lay = D.Layout(n, *grid)
+    locs = {}
+    for r in range(grid[0]):
+        rows = [I * D.NB + i for I in lay.row_blocks(r) for i in range(D.NB)]
+        br = torch.from_numpy(wl.er_bits_rows(n, p, seed, rows).view(np.int32)).cuda()
+        for c in range(grid[1]):
+            locs[(r, c)] = D.local_m_from_bits(br, lay, r, c, gamma)
+    bits = torch.from_numpy(wl.er_bits_chunked(n, p, seed).view(np.int32)).cuda()
+    m = S.build_m_bits(bits, n, gamma)
+    assert torch.equal(D.gather(locs, lay), m)
+    minp, flags = D.invert_block_cyclic(locs, D.VirtualGrid(lay), D.CudaEngine())
+    assert flags == 0
+    cols = np.sort(np.random.default_rng(1).choice(n, 300, replace=False))
+    S.invert_in_place(m, gamma)
+    want = S.d_columns(m, n, gamma, cols)
+    want_u8 = torch.where(torch.isfinite(want), want, torch.full_like(want, 255)).to(torch.uint8)
+    got = torch.zeros((n, len(cols)), dtype=torch.uint8, device="cuda")
+    pos = {int(cg): j for j, cg in enumerate(cols)}
+    for (r, c), yl in locs.items():
+        held, du = D.local_d_columns(yl, lay, r, c, gamma, cols)
+        rows = torch.tensor([I * D.NB + i for I in lay.row_blocks(r) for i in range(D.NB)], device="cuda")
+        for j, cg in enumerate(held.tolist()):
+            got[rows, pos[cg]] = du[:, j]
+    assert torch.equal(got, want_u8)

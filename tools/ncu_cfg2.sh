@@ -6,7 +6,7 @@ set -e
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 $NCU --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches_bench.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --single-n 0 --e2e-steps 2 > gpurun_out/ncu_bench.log 2>&1
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-cfg5 --e2e-steps 2 > gpurun_out/ncu_bench.log 2>&1
 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_call.csv \
   python tools/prof_batch.py --batch 256 --iters 1 > gpurun_out/ncu_call.log 2>&1
 # torch's own launches (the input copies) precede the two calls
@@ -21,5 +21,5 @@ $NCU --set full --clock-control none --import-source on -s $SKIP -c $PER -o gpur
 python tools/ncu_summary.py gpurun_out/full_cfg2.ncu-rep --out gpurun_out/ncu_full_cfg2.json \
   --note "ncu --set full --clock-control none --import-source on -s $SKIP -c $PER python tools/prof_batch.py --batch 256 --iters 1: the second of two config-2 calls (256 graphs N=1024)" > /dev/null
 python tools/launch_shares.py gpurun_out/launches_bench.csv --out gpurun_out/launch_shares_cfg2.json \
-  --note "ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --single-n 0 --e2e-steps 2 (cold-cache, serialised: compare shares)" > /dev/null
+  --note "ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-cfg5 --e2e-steps 2 (cold-cache, serialised: compare shares)" > /dev/null
 rm -f gpurun_out/full_cfg2.ncu-rep
