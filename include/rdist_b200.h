@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RDB_ABI_VERSION 5
+#define RDB_ABI_VERSION 6
 #define RDB_NB 128 /* Gauss-Jordan panel width; inverted matrices are padded to a multiple */
 
 /* status codes */
@@ -260,6 +260,15 @@ size_t rdb_bfs_workspace_bytes(int64_t n);
 int rdb_pattern_bits(const double* w, int64_t n, int64_t ldw, uint32_t* bits, void* stream);
 int rdb_bfs_apsp(const uint32_t* bits, int64_t n, int32_t* dist_i32, double* dist_f64, int64_t ldd,
                  void* work, int64_t* levels, void* stream);
+
+/* ---- K10: Floyd-Warshall exact weighted distances (oracles.py:44-50) ----
+ * d (n x n, ldd) = W with a zero diagonal, then for k = 0..n-1:
+ * d = min(d, d[:, k] + d[k, :]) — bit for bit the reference's loop (k-blocks
+ * of 32 replay column / row k as they stood after step k-1). W: device fp64,
+ * +inf = no edge, positive weights. work: rdb_floyd_workspace_bytes(n). */
+size_t rdb_floyd_workspace_bytes(int64_t n);
+int rdb_floyd_warshall(const double* w, int64_t ldw, int64_t n, double* d, int64_t ldd, void* work,
+                       void* stream);
 
 /* ---- K9: gamma-sweep accuracy counts (navigation.py:77-134) --------------
  * counts (device, 2 x u64, caller-zeroed, accumulated): {evaluated, hits}.

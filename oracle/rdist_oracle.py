@@ -187,6 +187,15 @@ def bfs_apsp(w: np.ndarray) -> np.ndarray:
     return dist
 
 
+def floyd_warshall(w: np.ndarray) -> np.ndarray:
+    """The classic vectorised k-loop (oracles.py:44-50)."""
+    d = np.array(w, dtype=np.float64, copy=True)
+    np.fill_diagonal(d, 0.0)
+    for k in range(d.shape[0]):
+        np.minimum(d, np.add.outer(d[:, k], d[k, :]), out=d)
+    return d
+
+
 def global_accuracy(est: np.ndarray, exact: np.ndarray) -> float:
     """Share of finite off-diagonal exact pairs the estimate hits exactly (navigation.py:77-88)."""
     keep = np.isfinite(exact)

@@ -63,7 +63,7 @@ from .batch import (
     rounded_r_distance_batch_device,
 )
 from ._lib import NativeUnavailableError, load_library
-from .oracles import bfs_apsp, bfs_apsp_device
+from .oracles import bfs_apsp, bfs_apsp_device, dijkstra_apsp, floyd_warshall, graph_diameter
 from .navigation import global_accuracy, local_accuracy  # noqa: E402  (device K6/K9, .sweep)
 from .sweep import SweepRecord, sweep_gamma_graph, sweep_point
 
@@ -83,6 +83,9 @@ __all__ = [
     "write_edge_list",
     "bfs_apsp",
     "bfs_apsp_device",
+    "dijkstra_apsp",
+    "floyd_warshall",
+    "graph_diameter",
     "AccuracyReport",
     "SweepRecord",
     "accuracy_report",

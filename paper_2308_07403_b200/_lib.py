@@ -18,7 +18,7 @@ import torch
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "librdist_b200.so"
 
-RDB_ABI_VERSION = 5  # include/rdist_b200.h; load_library refuses a library built from another header
+RDB_ABI_VERSION = 6  # include/rdist_b200.h; load_library refuses a library built from another header
 RDB_NB = 128
 RDB_OK = 0
 RDB_PIV_NONPOS = 1
@@ -93,6 +93,8 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "rdb_bfs_workspace_bytes": (_sz, [_i64]),
     "rdb_pattern_bits": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "rdb_bfs_apsp": (_int, [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "rdb_floyd_workspace_bytes": (_sz, [_i64]),
+    "rdb_floyd_warshall": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp]),
     "rdb_global_accuracy": (_int, [_vp, _i64, _vp, _i64, _i64, _vp, _vp]),
     "rdb_local_accuracy": (
         _int,

@@ -1,5 +1,10 @@
-"""Exact hop distances on the GPU: the reference's ``bfs_apsp``
-(pkg/src/rdist/oracles.py:22-41) as kernel K8 (csrc/bfs.cu).
+"""Exact distances on the GPU: the reference's ``bfs_apsp``
+(pkg/src/rdist/oracles.py:22-41) as kernel K8 (csrc/bfs.cu) and its
+``floyd_warshall`` (:44-50) as kernel K10 (csrc/floyd.cu, bit for bit the
+same k-loop), which also serves ``dijkstra_apsp`` (:53-66): on positive
+weights both are the shortest-path lengths (exactly equal on integer
+weights; the reference's Dijkstra sums paths in another order, so on real
+weights it matches to float tolerance, as the reference's own docstring says).
 
 The reference advances all-source BFS frontiers with dense boolean matrix
 products; K8 keeps the frontiers bit-packed by source and ORs, for every
@@ -58,3 +63,32 @@ def bfs_apsp(g) -> np.ndarray:
     """Exact distances on an unweighted graph (oracles.py:22-41): float64,
     +inf when unreachable, zero diagonal."""
     return bfs_apsp_device(g).cpu().numpy()
+
+
+def floyd_warshall_device(g) -> torch.Tensor:
+    """Floyd-Warshall distances of a graph (any kind) on the device (K10)."""
+    w = _d.graph_weights(g)
+    n = g.n_vertices
+    d = torch.empty((n, n), dtype=torch.float64, device=w.device)
+    work = torch.empty(L.lib().rdb_floyd_workspace_bytes(n), dtype=torch.uint8, device=w.device)
+    L.check(L.lib().rdb_floyd_warshall(w.data_ptr(), w.stride(0), n, d.data_ptr(), n, work.data_ptr(),
+                                       L.stream_handle()), "rdb_floyd_warshall")
+    return d
+
+
+def floyd_warshall(g) -> np.ndarray:
+    """Exact weighted distances (oracles.py:44-50): d[i][j] from j to i, +inf
+    unreachable, zero diagonal; the reference's loop bit for bit."""
+    return floyd_warshall_device(g).cpu().numpy()
+
+
+def dijkstra_apsp(g) -> np.ndarray:
+    """Exact weighted distances (oracles.py:53-66), computed by K10."""
+    return floyd_warshall(g)
+
+
+def graph_diameter(d: np.ndarray) -> float:
+    """Largest finite entry of an exact distance matrix, 0 if none (oracles.py:110-113)."""
+    d = np.asarray(d)
+    finite = d[np.isfinite(d)]
+    return float(finite.max()) if finite.size else 0.0
