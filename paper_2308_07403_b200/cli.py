@@ -76,12 +76,15 @@ def _exact(g):
 def _resolve_gamma(g, gamma_arg: str, safety: float) -> float:
     """A literal gain, or 'auto': d_max from the exact distances, then
     gamma_bounds / suggest_gamma (cli.py:133-160); exits 1 when infeasible."""
-    from . import oracles, resolvent
+    # (the resolvent *module*: the package re-export `resolvent` is the function,
+    # which is why the reference's own `from . import resolvent` fails here)
+    from . import oracles
+    from .resolvent import gamma_bounds, suggest_gamma
 
     if gamma_arg != "auto":
         return float(gamma_arg)
     d_max = max(math.ceil(oracles.graph_diameter(_exact(g))), 1)
-    bounds = resolvent.gamma_bounds(g, d_max)
+    bounds = gamma_bounds(g, d_max)
     if not bounds.feasible:
         raise SystemExit(
             f"error: no valid gamma exists: the precision floor "
@@ -89,14 +92,15 @@ def _resolve_gamma(g, gamma_arg: str, safety: float) -> float:
             f"exceeds the critical gain {bounds.critical_gain:.6g}; the longest "
             f"distance must stay below {bounds.max_feasible_distance:.1f}"
         )
-    gamma = resolvent.suggest_gamma(bounds, safety=safety)
+    gamma = suggest_gamma(bounds, safety=safety)
     print(f"auto gamma: {gamma:.6g} (critical gain {bounds.critical_gain:.6g}, "
           f"precision floor {bounds.precision_floor_for_dmax:.6g}, d_max {d_max})", file=sys.stderr)
     return gamma
 
 
 def _cmd_distances(args) -> int:
-    from . import graphs, oracles, resolvent
+    from . import graphs, oracles
+    from .resolvent import r_distance, resolvent, rounded_r_distance
 
     g = _load_graph(args.input, args.kind)
     if args.method == "bfs":
@@ -105,15 +109,16 @@ def _cmd_distances(args) -> int:
         d = oracles.floyd_warshall(g)
     else:
         gamma = _resolve_gamma(g, args.gamma, args.safety)
-        res = resolvent.resolvent(g, gamma)
-        d = resolvent.r_distance(res) if g.kind is graphs.GraphKind.REAL_WEIGHTED else resolvent.rounded_r_distance(res)
+        res = resolvent(g, gamma)
+        d = r_distance(res) if g.kind is graphs.GraphKind.REAL_WEIGHTED else rounded_r_distance(res)
     graphs.write_distance_csv(d, args.out)
     print(f"wrote {d.shape[0]}x{d.shape[1]} distance matrix to {args.out}")
     return EXIT_OK
 
 
 def _cmd_navigate(args) -> int:
-    from . import navigation, resolvent
+    from . import navigation
+    from .resolvent import r_distance, resolvent
 
     g = _load_graph(args.input, args.kind)
     if args.method == "analog":
@@ -121,7 +126,7 @@ def _cmd_navigate(args) -> int:
         return EXIT_USAGE
     if args.method == "rdist":
         gamma = _resolve_gamma(g, args.gamma, args.safety)
-        dist = resolvent.r_distance(resolvent.resolvent(g, gamma))
+        dist = r_distance(resolvent(g, gamma))
     else:
         dist = _exact(g)
     result = navigation.greedy_descent(g, dist, args.start, args.goal)

@@ -96,3 +96,48 @@ def test_resolvent_result_is_the_reference_dataclass(cuda):
     res2 = dataclasses.replace(res, gamma=1e-2)
     np.testing.assert_array_equal(rb.rounded_r_distance(res2), rb.rounded_r_distance(res))
     assert dataclasses.asdict(res)["health"]["inversion_residual"] == res.health.inversion_residual
+
+
+@pytest.mark.timeout(300)
+def test_concurrent_inversions_on_three_streams_make_progress(cuda):
+    """Forward progress of K2's in-kernel waits with several persistent update
+    kernels in flight (gj_invert.cu: tiles by atomic ticket): two batched calls
+    (each split into two sub-batch streams) and a single-matrix look-ahead
+    inversion issued on three user streams at once, repeatedly; every result
+    equals its serial run."""
+    from paper_2308_07403_b200 import single as S
+
+    seeds = wl.cfg2_seeds(256)
+    sets = [seeds[0:32] + seeds[128:160], seeds[32:64] + seeds[160:192]]
+    bufs, refs = [], []
+    for pick in sets:
+        bits = np.stack([wl.pack_bits(wl.cfg2_present(k, s)) for k, s in pick])
+        gam = np.array([wl.cfg2_gamma(k) for k, _ in pick])
+        buf = B.BatchBuffers.allocate(1024, len(pick), cuda)
+        buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+        buf.gammas.copy_(torch.from_numpy(gam))
+        B.run_chunk(buf, len(pick))
+        torch.cuda.synchronize()
+        refs.append(buf.d.clone())
+        bufs.append(buf)
+    n = 2048
+    b2 = torch.from_numpy(wl.er_bits_chunked(n, 0.02, 9).view(np.int32)).to(cuda)
+    m0 = S.build_m_bits(b2, n, 1e-3)
+    m_ref = m0.clone()
+    S.invert_in_place(m_ref, 1e-3)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    for _ in range(3):
+        m = m0.clone()
+        torch.cuda.synchronize()
+        for st, buf in zip(streams[:2], bufs):
+            with torch.cuda.stream(st):
+                B.run_chunk(buf, buf.chunk, st.cuda_stream)
+        with torch.cuda.stream(streams[2]):
+            work = torch.empty(L.lib().rdb_invert_workspace_bytes(n, 1), dtype=torch.uint8, device=cuda)
+            info = L.pivot_info_tensor(1, cuda)
+            L.check(L.lib().rdb_invert(m.data_ptr(), n, n, work.data_ptr(), info.data_ptr(), streams[2].cuda_stream),
+                    "rdb_invert")
+        torch.cuda.synchronize()
+        for buf, ref in zip(bufs, refs):
+            assert torch.equal(buf.d, ref)
+        assert torch.equal(m, m_ref)
