@@ -35,12 +35,14 @@ using EC = eng::Default;  // engine warp layout
 __global__ void __launch_bounds__(p1::THREADS, 1)
     gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int64_t off, int idx0,
                     rdb_pivot_info* __restrict__ info, int first, int64_t info_stride = 1,
-                    const int* __restrict__ nonband = nullptr) {
+                    const int* __restrict__ nonband = nullptr, int want = 1) {
   // block at a + b*stride + off*(lda + 1); pivot indices recorded from idx0.
-  // Matrices the banded path inverts (nonband[b * info_stride] == 0) are skipped.
+  // Per-matrix path flags (batched calls): 0 banded inverse, 1 block-sparse
+  // Gauss-Jordan, 2 dense 256-wide Gauss-Jordan; only matrices whose flag is
+  // `want` are processed.
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
-  if (nonband && !nonband[b * info_stride]) return;
+  if (nonband && nonband[b * info_stride] != want) return;
 #ifdef RDB_EXP_NO_P1
   return;  // timing experiment only (tools/k2_split.py on a variant library): wrong results
 #endif
@@ -327,6 +329,7 @@ struct PlanPart {
   int* offs;    // [2][nt][batch]: per-matrix tile counts, then list offsets
   int* rp;      // [nt][batch * (nt - 1)] P2 entries g << 13 | c0 << 10 | nk << 6 | J
   int2* up;     // [nt][batch * (nt - 1) * nt] update entries {g << 12 | I << 6 | J, wait | c0 << 16 | nk << 20}
+  bool prebuilt = false;  // lists written by the caller (dense-wide nested inverse): no plan walk
 };
 
 // The plan in three launches, all parallel over matrices: gj_plan_walk<false>
@@ -552,7 +555,7 @@ static int64_t wide_min_n();
 static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                        rdb_pivot_info* info, cudaStream_t st, int first, int64_t idx_base, int* dyn = nullptr,
                        const PlanPart* plan = nullptr, int64_t info_stride = 1, const int* nonband = nullptr,
-                       int grid_cap = 0) {
+                       int grid_cap = 0, int want = 1) {
   if (!a || !work || !info || n <= 0 || batch <= 0) return RDB_EINVAL;
   if (n % NB != 0 || lda < n || (lda & 1) || (batch > 1 && stride < n * lda)) return RDB_EINVAL;
   if (((uintptr_t)a & 15) || ((uintptr_t)work & 15)) return RDB_EINVAL;
@@ -569,7 +572,7 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   if (rc) return rc;
   if (cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)batch * nt, st) != cudaSuccess) return RDB_ECUDA;
   if (plan && (batch == 1 || nt > PLAN_MAX_NT)) plan = nullptr;
-  if (plan)
+  if (plan && !plan->prebuilt)
     launch_plan(*plan, (int)batch, nt, st);
   // Single matrix: look-ahead. The next panel's column block is updated first
   // (part 1); the next P1 (one CTA, latency-bound) then runs on a side stream
@@ -579,12 +582,12 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   if (lookahead && !ds) return RDB_ECUDA;
   cudaStream_t side = ds ? ds->side : nullptr;
   gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, idx_base, info, first,
-                                                                       info_stride, nonband);
+                                                                       info_stride, nonband, want);
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
     if (k > 0 && !lookahead)
       gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, p0, idx_base + p0,
-                                                                           info, 0, info_stride, nonband);
+                                                                           info, 0, info_stride, nonband, want);
     if (nt == 1) break;
     RowPanelSched rp{a, lda, stride, nt, k, (int)batch, batch > 1 ? dyn : nullptr};
     if (plan) {
@@ -623,6 +626,249 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   return RDB_OK;
 }
 
+// ------------------------------------------------------------------ dense 256-wide batched path (DW)
+// Batched matrices whose strip pattern has no zero strip anywhere off the
+// diagonal (the Erdos-Renyi half of config 2: the block-sparse plan would run
+// every k-chunk anyway) take 256-wide Gauss-Jordan steps: every update tile
+// then runs 16 k-chunks per epilogue instead of 8, halving the engine's
+// per-tile switch + epilogue cost per flop (~2.4 us against 2.12 us per
+// k-chunk). Step p, band B = block rows/columns 2p, 2p+1, for every listed matrix:
+//   1. A_BB = A_BB^-1 in place: the NB = 128 Gauss-Jordan on the 256 x 256
+//      block (invert_core on the sub-blocks, P1 via the path flag `want` = 2,
+//      row panel / update tiles from prebuilt lists);
+//   2. A_BJ = A_BB A_BJ (J outside B), in place: tiles (r, J), r = 0, 1, K = 256.
+//      Both overwrite the B operand A_BJ they share: each signals when its
+//      operands have landed and stores only when both have (column counters);
+//   3. A_IJ += -(A_IB A_BJ) (I, J outside B, TMA reduce-add) and
+//      A_I,B = -(A_IB A_BB) (the two band tiles, store): the band tiles
+//      overwrite A_IB, every tile's A operand in row block I, so they store
+//      only when all nt tiles of that row have loaded it (row counters).
+// Same algebra as the NB = 128 steps (the nested inverse is their first two
+// steps on the band); rounding order differs, so the inverse agrees to
+// ~1e-15 relative and D is unchanged (tests compare with the reference).
+// All waits point to tiles of smaller index: tiles are taken by ticket.
+struct WBRowSched {
+  double* a;
+  int64_t lda, stride;
+  int nt, p0t, step;
+  const int* list;        // listed matrices (indices within the strided batch)
+  const int* list_count;  // device count
+  int* colcnt;            // [g][nt] cumulative column counters
+  int* dyn;
+  RDB_DEV int count() const { return *list_count * (nt - 2) * 2; }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int r = t & 1, q = t >> 1;
+    const int li = q / (nt - 2), jj = q - li * (nt - 2);
+    const int J = jj + (jj >= p0t ? 2 : 0);
+    const int g = list[li];
+    double* A = a + (int64_t)g * stride;
+    eng::Tile T;
+    T.a_col = p0t * NB;  // A operand: D rows r (128 x 256)
+    T.a_row = (p0t + r) * NB;
+    T.a_mat = g;
+    T.b = A + (int64_t)p0t * NB * lda + (int64_t)J * NB;  // A_BJ, 256 x 128
+    T.ldb = lda;
+    T.c_col = J * NB;
+    T.c_row = (p0t + r) * NB;
+    T.c_mat = g;
+    T.nk = 2 * NB / eng::BK;
+    T.mode = eng::EPI_STORE;
+    T.neg = 0;
+    int* c = colcnt + (int64_t)g * nt + J;
+    T.signal = c;
+    T.wait = c;
+    T.wait_target = 2 * (step - ((J >> 1) < step ? 1 : 0) + 1);
+    return T;
+  }
+};
+
+struct WBUpdateSched {
+  double* a;
+  int64_t lda, stride;
+  int nt, p0t, step;
+  const int* list;
+  const int* list_count;
+  int* rowcnt;  // [g][nt] cumulative row counters
+  int* dyn;
+  RDB_DEV int count() const { return *list_count * (nt - 2) * nt; }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int per = (nt - 2) * nt;
+    const int li = t / per, rem = t - li * per;
+    const int ri = rem / nt, jj = rem - ri * nt;
+    const int I = ri + (ri >= p0t ? 2 : 0);
+    const int g = list[li];
+    double* A = a + (int64_t)g * stride;
+    eng::Tile T;
+    T.a_col = p0t * NB;  // A operand: A_IB, 128 x 256
+    T.a_row = I * NB;
+    T.a_mat = g;
+    T.c_row = I * NB;
+    T.c_mat = g;
+    T.nk = 2 * NB / eng::BK;
+    T.neg = 1;
+    T.ldb = lda;
+    int* c = rowcnt + (int64_t)g * nt + I;
+    T.signal = c;
+    if (jj < nt - 2) {
+      const int J = jj + (jj >= p0t ? 2 : 0);
+      T.b = A + (int64_t)p0t * NB * lda + (int64_t)J * NB;  // the new row panel A_BJ
+      T.c_col = J * NB;
+      T.mode = eng::EPI_REDUCE;
+      T.wait = nullptr;
+      T.wait_target = 0;
+    } else {
+      const int h = jj - (nt - 2);
+      T.b = A + (int64_t)p0t * NB * lda + (int64_t)(p0t + h) * NB;  // columns h of A_BB (= its inverse)
+      T.c_col = (p0t + h) * NB;
+      T.mode = eng::EPI_STORE;
+      T.wait = c;
+      T.wait_target = nt * (step - ((I >> 1) < step ? 1 : 0) + 1);
+    }
+    return T;
+  }
+};
+
+__global__ void __launch_bounds__(EC::THREADS, 1)
+    gj_wb_row_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
+                     WBRowSched sched) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
+}
+
+__global__ void __launch_bounds__(EC::THREADS, 1)
+    gj_wb_update_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
+                        WBUpdateSched sched) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
+}
+
+// Per-part device state of the DW path (inside the batched workspace).
+struct DwPart {
+  int* list;    // [cnt] local indices of the part's DW matrices
+  int* count;   // 1 int
+  int* ncounts; // nested plan counts [2][2]
+  int* nrp;     // nested row-panel entries [2][cnt]
+  int2* nup;    // nested update entries [2][2 cnt]
+  int* ncnt;    // nested row-block counters (invert_core work, 16-byte aligned)
+  int* colcnt;  // [cnt][nt]
+  int* rowcnt;  // [cnt][nt]
+};
+
+// One CTA per part: classify the part's matrices (flag 1 -> 2 when every
+// off-diagonal block has all 8 column and all 8 row strips), zero their strip
+// patterns (the block-sparse plan then lists no tiles for them), and write the
+// part's list plus the nested-inverse plan lists, in matrix order.
+struct DwClassifyArgs {
+  unsigned char* pat;
+  int* flags;
+  int64_t batch;
+  int nt, parts;
+  DwPart part[4];
+};
+
+__global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
+  const int i = blockIdx.x;
+  const int nt = arg.nt, ld = pat_ld(nt);
+  const int64_t cnt = (arg.batch - i + arg.parts - 1) / arg.parts;
+  const DwPart& d = arg.part[i];
+  __shared__ int warp_tot[8];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t l0 = 0; l0 < cnt; l0 += 256) {
+    const int64_t l = l0 + threadIdx.x;
+    const int64_t m = i + (int64_t)arg.parts * l;
+    bool dense = false;
+    if (l < cnt && arg.flags[m] == 1) {
+      const unsigned char* P = arg.pat + m * 2 * nt * ld;
+      dense = true;
+      for (int I = 0; I < nt && dense; ++I)
+        for (int J = 0; J < nt; ++J)
+          if (I != J && (P[I * ld + J] != 0xFF || P[(nt + I) * ld + J] != 0xFF)) {
+            dense = false;
+            break;
+          }
+    }
+    // ordered compaction (block scan of the dense flags)
+    const unsigned bal = __ballot_sync(0xffffffffu, dense);
+    if (lane == 0) warp_tot[w] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int k = 0; k < w; ++k) off += warp_tot[k];
+    const int pos = off + __popc(bal & ((1u << lane) - 1));
+    if (dense) {
+      arg.flags[m] = 2;
+      unsigned char* P = arg.pat + m * 2 * nt * ld;
+      for (int e = 0; e < 2 * nt * ld; ++e) P[e] = 0;
+      d.list[pos] = (int)l;
+      for (int k = 0; k < 2; ++k) {
+        d.nrp[k * cnt + pos] = (int)(l << 13) | (8 << 6) | (1 - k);
+        d.nup[k * 2 * cnt + 2 * pos] = make_int2((int)(l << 12) | ((1 - k) << 6) | (1 - k), 1 | (8 << 20));
+        d.nup[k * 2 * cnt + 2 * pos + 1] = make_int2((int)(l << 12) | ((1 - k) << 6) | k, 1 | (8 << 20));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int k = 0; k < 8; ++k) tot += warp_tot[k];
+      base += tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *d.count = base;
+    d.ncounts[0] = d.ncounts[1] = base;          // nested row panels, steps 0 and 1
+    d.ncounts[2] = d.ncounts[3] = 2 * base;      // nested update tiles
+  }
+}
+
+// The DW steps for one part (its matrices a + l * pstride, l < pcnt).
+static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t pcnt, const DwPart& d,
+                   rdb_pivot_info* info, int64_t info_stride, const int* flags, int* dyn, cudaStream_t st) {
+  const int nt = (int)(n / NB);
+  if (cudaMemsetAsync(d.colcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess ||
+      cudaMemsetAsync(d.rowcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess)
+    return RDB_ECUDA;
+  static DeviceFlags attrs;
+  const int attrs_dev = current_device();
+  if (!attrs.get(attrs_dev)) {
+    if (cudaFuncSetAttribute(gj_wb_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)EC::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(gj_wb_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)EC::SMEM_BYTES) != cudaSuccess)
+      return RDB_ECUDA;
+    attrs.set(attrs_dev);
+  }
+  CUtensorMap amap, cmap;
+  int rc = make_a_map(&amap, a, n, n, lda, pstride, pcnt);
+  if (rc) return rc;
+  rc = make_ec_map(&cmap, a, n, n, lda, pstride, pcnt);
+  if (rc) return rc;
+  PlanPart np;
+  np.pat = nullptr;
+  np.pat_stride = 0;
+  np.offs = nullptr;
+  np.counts = d.ncounts;
+  np.rp = d.nrp;
+  np.up = d.nup;
+  np.prebuilt = true;
+  for (int p = 0; p < nt / 2; ++p) {
+    const int p0t = 2 * p;
+    const int64_t p0 = (int64_t)p0t * NB;
+    rc = invert_core(a + p0 * lda + p0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, p == 0 ? 1 : 0, p0, dyn, &np,
+                     info_stride, flags, 0, 2);
+    if (rc) return rc;
+    WBRowSched rs{a, lda, pstride, nt, p0t, p, d.list, d.count, d.colcnt, dyn};
+    gj_wb_row_kernel<<<persistent_grid(pcnt * (nt - 2) * 2), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, rs);
+    WBUpdateSched us{a, lda, pstride, nt, p0t, p, d.list, d.count, d.rowcnt, dyn ? dyn + 1 : nullptr};
+    gj_wb_update_kernel<<<persistent_grid(pcnt * (nt - 2) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap,
+                                                                                                   us);
+  }
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+
 // Sub-batches of a large batch on their own streams (default two halves):
 // each part's kernels fill the others' tails (the last partial round of every persistent launch, the
 // second wave of the one-CTA-per-matrix panel inverses). Measured on config 2:
@@ -647,7 +893,7 @@ int band_invert(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t b
                 double* ws, rdb_pivot_info* info, cudaStream_t st);
 
 struct BatchWs {
-  size_t cnt, dyn, blk, counts, rp, up, offs, band, band_ws, total;
+  size_t cnt, dyn, blk, counts, rp, up, offs, band, band_ws, dwl, dwc, dwnc, dwrp, dwup, dwcnt, dwcol, dwrow, total;
   BatchWs(int64_t n_pad, int64_t batch) {
     const size_t nt = (size_t)(n_pad / NB), b = (size_t)batch;
     cnt = 0;
@@ -660,13 +906,40 @@ struct BatchWs {
       offs = up + align256(b * nt * nt * (nt - 1) * sizeof(int2));
       band = offs + align256(b * 2 * nt * sizeof(int));
       band_ws = band + align256(b * sizeof(int));
-      total = band_ws + align256(b * band::ws_doubles(n_pad) * sizeof(double));
+      dwl = band_ws + align256(b * band::ws_doubles(n_pad) * sizeof(double));  // dense-wide path
+      dwc = dwl + align256(b * sizeof(int));
+      dwnc = dwc + align256((size_t)MAX_PARTS * 16 * sizeof(int));
+      dwrp = dwnc + align256((size_t)MAX_PARTS * 16 * sizeof(int));
+      dwup = dwrp + align256(2 * b * sizeof(int));
+      dwcnt = dwup + align256(4 * b * sizeof(int2));
+      dwcol = dwcnt + align256((2 * b + 4 * MAX_PARTS) * sizeof(int));
+      dwrow = dwcol + align256(b * nt * sizeof(int));
+      total = dwrow + align256(b * nt * sizeof(int));
     } else {
-      counts = rp = up = offs = band = band_ws = total = blk;
+      counts = rp = up = offs = band = band_ws = dwl = dwc = dwnc = dwrp = dwup = dwcnt = dwcol = dwrow = total = blk;
     }
   }
   bool has_plan() const { return total > blk; }
+  // the dense-wide state of part i of `parts` (matrices i, i + parts, ...; lo before it)
+  DwPart dw_part(char* wb, int i, int64_t lo, int nt) const {
+    DwPart d;
+    d.list = reinterpret_cast<int*>(wb + dwl) + lo;
+    d.count = reinterpret_cast<int*>(wb + dwc) + 16 * i;
+    d.ncounts = reinterpret_cast<int*>(wb + dwnc) + 16 * i;
+    d.nrp = reinterpret_cast<int*>(wb + dwrp) + 2 * lo;
+    d.nup = reinterpret_cast<int2*>(wb + dwup) + 4 * lo;
+    d.ncnt = reinterpret_cast<int*>(wb + dwcnt + ((2 * (size_t)lo * sizeof(int) + 15) & ~(size_t)15));
+    d.colcnt = reinterpret_cast<int*>(wb + dwcol) + lo * nt;
+    d.rowcnt = reinterpret_cast<int*>(wb + dwrow) + lo * nt;
+    return d;
+  }
 };
+
+// Dense 256-wide steps for fully dense batched matrices (A-B switch RDB_GJ_DW=0).
+static bool dw_enabled() {
+  const char* e = getenv("RDB_GJ_DW");
+  return !(e && e[0] == '0');
+}
 
 static bool skip_enabled() {
   const char* e = getenv("RDB_GJ_SKIP");  // A-B switch: 0 runs the dense schedule
@@ -783,7 +1056,27 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     return pp;
   };
   const int parts = split_parts();
-  if (batch >= split_min_batch() && batch >= 4 * parts && a && work && info && n % NB == 0 && stride >= n * lda) {
+  const bool split =
+      batch >= split_min_batch() && batch >= 4 * parts && a && work && info && n % NB == 0 && stride >= n * lda;
+  // dense-wide path: classify (flags 1 -> 2, patterns zeroed, per-part lists) before the fork
+  const bool use_dw = use_band && dw_enabled() && ntl >= 4 && ntl % 2 == 0 && batch >= 2 * (split ? parts : 1);
+  DwPart dwp[MAX_PARTS];
+  if (use_dw) {
+    DwClassifyArgs ca;
+    ca.pat = pat;
+    ca.flags = nonband;
+    ca.batch = batch;
+    ca.nt = (int)ntl;
+    ca.parts = split ? parts : 1;
+    int64_t lo = 0;
+    for (int i = 0; i < ca.parts; ++i) {
+      dwp[i] = ws.dw_part(wb, i, lo, (int)ntl);
+      ca.part[i] = dwp[i];
+      lo += (batch - i + ca.parts - 1) / ca.parts;
+    }
+    dw_classify_kernel<<<(unsigned)ca.parts, 256, 0, st>>>(ca);
+  }
+  if (split) {
     DevStreams* ds = dev_streams();
     if (!ds) return RDB_ECUDA;
     int* dyn = reinterpret_cast<int*>(wb + ws.dyn);
@@ -799,6 +1092,11 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       // row-block counters of the part, 16-byte aligned (counter_bytes has the slack)
       char* cw = wb + (((size_t)lo * ntl * sizeof(int) + 15) & ~(size_t)15);
       const bool dyn_on = dyn_sched();
+      if (use_dw) {
+        rc = dw_part(a + i * stride, n, lda, parts * stride, cnt, dwp[i], info + i, parts, nonband + i,
+                     dyn_on ? dyn + 2 * i : nullptr, ds->part[i]);
+        if (rc) break;
+      }
       rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, ds->part[i], 1, 0,
                        dyn_on ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr, parts,
                        nonband ? nonband + i : nullptr, (!dyn_on && cosched_cap()) ? sm_count() / parts : 0);
@@ -819,6 +1117,10 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   if (dyn_sched()) {
     dyn = reinterpret_cast<int*>(wb + ws.dyn);
     if (cudaMemsetAsync(dyn, 0, 2 * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
+  }
+  if (use_dw) {
+    const int rc = dw_part(a, n, lda, stride, batch, dwp[0], info, 1, nonband, dyn, st);
+    if (rc) return rc;
   }
   return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, dyn, use_plan ? &pp : nullptr, 1,
                      nonband);

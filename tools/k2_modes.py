@@ -23,10 +23,12 @@ MODES = {
     "default": {},
     "static_capped": {"RDB_GJ_DYNAMIC": "0"},
     "static_uncapped": {"RDB_GJ_DYNAMIC": "0", "RDB_GJ_COSCHED": "0"},
+    "no_dense_wide": {"RDB_GJ_DW": "0"},
     "no_split": {"RDB_GJ_SPLIT_MIN": "0"},
+    "no_split_no_dw": {"RDB_GJ_SPLIT_MIN": "0", "RDB_GJ_DW": "0"},
     "split3_capped": {"RDB_GJ_SPLIT_PARTS": "3"},
 }
-KNOBS = ("RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS")
+KNOBS = ("RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW")
 
 
 def main():
