@@ -267,6 +267,9 @@ struct DevStreams {
   cudaEvent_t ev_a = nullptr, ev_p = nullptr, ev_b = nullptr;
   cudaStream_t part[MAX_PARTS] = {};
   cudaEvent_t fork = nullptr, join[MAX_PARTS] = {};
+  // dense-wide look-ahead: one side stream + fork / join events per part
+  cudaStream_t dw_side[MAX_PARTS] = {};
+  cudaEvent_t dw_fork[MAX_PARTS] = {}, dw_join[MAX_PARTS] = {};
 };
 static DevStreams g_streams[MAX_DEVICES];
 
@@ -283,7 +286,10 @@ static DevStreams* dev_streams() {
       return nullptr;
     for (int i = 0; i < MAX_PARTS; ++i)
       if (cudaStreamCreateWithFlags(&d.part[i], cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&d.join[i], cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&d.join[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&d.dw_side[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&d.dw_fork[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&d.dw_join[i], cudaEventDisableTiming) != cudaSuccess)
         return nullptr;
   }
   return &d;
@@ -690,11 +696,31 @@ struct WBUpdateSched {
   const int* list_count;
   int* rowcnt;  // [g][nt] cumulative row counters
   int* dyn;
-  RDB_DEV int count() const { return *list_count * (nt - 2) * nt; }
+  // part 0: every tile; 1: the next band's 2 x 2 diagonal tiles only (look-ahead:
+  // the next band inverse can start); 2: every tile except those
+  int part = 0;
+  RDB_DEV int per() const { return part == 1 ? 4 : (nt - 2) * nt - (part == 2 ? 4 : 0); }
+  RDB_DEV int count() const { return *list_count * per(); }
   RDB_DEV eng::Tile tile(int t) const {
-    const int per = (nt - 2) * nt;
-    const int li = t / per, rem = t - li * per;
-    const int ri = rem / nt, jj = rem - ri * nt;
+    const int pm = per();
+    const int li = t / pm;
+    int rem = t - li * pm;
+    int ri, jj;
+    if (part == 1) {  // rows / columns p0t + 2, p0t + 3 = index p0t, p0t + 1 outside the band
+      ri = p0t + (rem >> 1);
+      jj = p0t + (rem & 1);
+    } else if (part == 0 || rem < p0t * nt) {
+      ri = rem / nt;
+      jj = rem - ri * nt;
+    } else if ((rem -= p0t * nt) < 2 * (nt - 2)) {  // the next band's rows without its two columns
+      ri = p0t + rem / (nt - 2);
+      jj = rem - (ri - p0t) * (nt - 2);
+      jj += (jj >= p0t) ? 2 : 0;
+    } else {
+      rem -= 2 * (nt - 2);
+      ri = p0t + 2 + rem / nt;
+      jj = rem - (ri - p0t - 2) * nt;
+    }
     const int I = ri + (ri >= p0t ? 2 : 0);
     const int g = list[li];
     double* A = a + (int64_t)g * stride;
@@ -825,7 +851,9 @@ __global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
 
 // The DW steps for one part (its matrices a + l * pstride, l < pcnt).
 static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t pcnt, const DwPart& d,
-                   rdb_pivot_info* info, int64_t info_stride, const int* flags, int* dyn, cudaStream_t st) {
+                   rdb_pivot_info* info, int64_t info_stride, const int* flags, int* dyn, cudaStream_t st,
+                   cudaStream_t side = nullptr, cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr,
+                   int* side_dyn = nullptr) {
   const int nt = (int)(n / NB);
   if (cudaMemsetAsync(d.colcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess ||
       cudaMemsetAsync(d.rowcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess)
@@ -853,17 +881,40 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
   np.rp = d.nrp;
   np.up = d.nup;
   np.prebuilt = true;
+  // Look-ahead: the next band's 2 x 2 diagonal tiles are updated first; its
+  // 256-block inverse then runs on the part's side stream (own ticket
+  // counters) while the rest of the update runs here. No tile of the rest
+  // reads or writes that block.
+  rc = invert_core(a, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, 1, 0, dyn, &np, info_stride, flags, 0, 2);
+  if (rc) return rc;
   for (int p = 0; p < nt / 2; ++p) {
     const int p0t = 2 * p;
-    const int64_t p0 = (int64_t)p0t * NB;
-    rc = invert_core(a + p0 * lda + p0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, p == 0 ? 1 : 0, p0, dyn, &np,
-                     info_stride, flags, 0, 2);
-    if (rc) return rc;
+    const bool ahead = side && p + 1 < nt / 2;
     WBRowSched rs{a, lda, pstride, nt, p0t, p, d.list, d.count, d.colcnt, dyn};
     gj_wb_row_kernel<<<persistent_grid(pcnt * (nt - 2) * 2), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, rs);
     WBUpdateSched us{a, lda, pstride, nt, p0t, p, d.list, d.count, d.rowcnt, dyn ? dyn + 1 : nullptr};
+    if (ahead) {
+      us.part = 1;
+      gj_wb_update_kernel<<<persistent_grid(pcnt * 4), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, us);
+      cudaEventRecord(ev_fork, st);
+      cudaStreamWaitEvent(side, ev_fork, 0);
+      const int64_t q0 = (int64_t)(p0t + 2) * NB;
+      rc = invert_core(a + q0 * lda + q0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, side, 0, q0, side_dyn, &np,
+                       info_stride, flags, 0, 2);
+      if (rc) return rc;
+      cudaEventRecord(ev_join, side);
+      us.part = 2;
+    }
     gj_wb_update_kernel<<<persistent_grid(pcnt * (nt - 2) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap,
                                                                                                    us);
+    if (ahead) {
+      cudaStreamWaitEvent(st, ev_join, 0);
+    } else if (p + 1 < nt / 2) {
+      const int64_t q0 = (int64_t)(p0t + 2) * NB;
+      rc = invert_core(a + q0 * lda + q0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, 0, q0, dyn, &np,
+                       info_stride, flags, 0, 2);
+      if (rc) return rc;
+    }
   }
   RDB_LAUNCH_CHECK();
   return RDB_OK;
@@ -934,6 +985,12 @@ struct BatchWs {
     return d;
   }
 };
+
+// Dense-wide look-ahead of the next band inverse on a side stream (A-B switch RDB_GJ_DW_LA=0).
+static bool dw_lookahead() {
+  const char* e = getenv("RDB_GJ_DW_LA");
+  return !(e && e[0] == '0');
+}
 
 // Dense 256-wide steps for fully dense batched matrices (A-B switch RDB_GJ_DW=0).
 static bool dw_enabled() {
@@ -1080,7 +1137,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     DevStreams* ds = dev_streams();
     if (!ds) return RDB_ECUDA;
     int* dyn = reinterpret_cast<int*>(wb + ws.dyn);
-    if (cudaMemsetAsync(dyn, 0, 2 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
+    if (cudaMemsetAsync(dyn, 0, 4 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
     cudaEventRecord(ds->fork, st);
     // the banded matrices on this stream, concurrently with the sub-batches
     int rc = use_band ? band_invert(a, n, lda, stride, batch, nonband, band_ws, info, st) : RDB_OK;
@@ -1094,7 +1151,8 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       const bool dyn_on = dyn_sched();
       if (use_dw) {
         rc = dw_part(a + i * stride, n, lda, parts * stride, cnt, dwp[i], info + i, parts, nonband + i,
-                     dyn_on ? dyn + 2 * i : nullptr, ds->part[i]);
+                     dyn_on ? dyn + 2 * i : nullptr, ds->part[i], dw_lookahead() ? ds->dw_side[i] : nullptr,
+                     ds->dw_fork[i], ds->dw_join[i], dyn_on ? dyn + 2 * MAX_PARTS + 2 * i : nullptr);
         if (rc) break;
       }
       rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, ds->part[i], 1, 0,
@@ -1116,10 +1174,13 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   int* dyn = nullptr;
   if (dyn_sched()) {
     dyn = reinterpret_cast<int*>(wb + ws.dyn);
-    if (cudaMemsetAsync(dyn, 0, 2 * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
+    if (cudaMemsetAsync(dyn, 0, 4 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
   }
   if (use_dw) {
-    const int rc = dw_part(a, n, lda, stride, batch, dwp[0], info, 1, nonband, dyn, st);
+    DevStreams* ds = dw_lookahead() ? dev_streams() : nullptr;
+    const int rc = dw_part(a, n, lda, stride, batch, dwp[0], info, 1, nonband, dyn, st, ds ? ds->dw_side[0] : nullptr,
+                           ds ? ds->dw_fork[0] : nullptr, ds ? ds->dw_join[0] : nullptr,
+                           dyn ? dyn + 2 * MAX_PARTS : nullptr);
     if (rc) return rc;
   }
   return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, dyn, use_plan ? &pp : nullptr, 1,

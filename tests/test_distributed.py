@@ -129,3 +129,30 @@ def test_torch_grid_gloo(grid):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     err, minp, flags = q.get(timeout=10)
     assert err < 1e-12 and flags == 0 and minp > 0.5
+
+
+def test_er_bits_rows_jump_equals_full_draw():
+    # a rank draws only its own rows: PCG64 jumps reproduce gen_random_dense's stream
+    from paper_2308_07403_b200 import workloads as wl
+
+    n, p, seed = 700, 0.03, 11
+    full = wl.er_bits_chunked(n, p, seed, chunk_rows=128)
+    rows = np.array([3, 4, 5, 130, 131, 699])
+    assert np.array_equal(wl.er_bits_rows(n, p, seed, rows), full[rows])
+    assert np.array_equal(wl.er_bits_parallel(n, p, seed, procs=3, chunk_rows=200), full)
+    np.testing.assert_array_equal(wl.unpack_bits(full, n), wl.er_present(n, p, seed))
+
+
+@pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 3)])
+def test_local_m_from_bits_is_the_scatter_of_m(grid):
+    from paper_2308_07403_b200 import workloads as wl
+
+    n, p, gamma = 768, 0.05, 1e-2
+    lay = D.Layout(n, *grid)
+    present = wl.er_present(n, p, 2)
+    m = torch.from_numpy(np.eye(n) - gamma * present)
+    for r in range(grid[0]):
+        rows = [I * NB + i for I in lay.row_blocks(r) for i in range(NB)]
+        br = torch.from_numpy(wl.er_bits_rows(n, p, 2, rows).view(np.int32))
+        for c in range(grid[1]):
+            assert torch.equal(D.local_m_from_bits(br, lay, r, c, gamma), D.scatter(m, lay, r, c))

@@ -24,11 +24,12 @@ MODES = {
     "static_capped": {"RDB_GJ_DYNAMIC": "0"},
     "static_uncapped": {"RDB_GJ_DYNAMIC": "0", "RDB_GJ_COSCHED": "0"},
     "no_dense_wide": {"RDB_GJ_DW": "0"},
+    "dw_no_lookahead": {"RDB_GJ_DW_LA": "0"},
     "no_split": {"RDB_GJ_SPLIT_MIN": "0"},
     "no_split_no_dw": {"RDB_GJ_SPLIT_MIN": "0", "RDB_GJ_DW": "0"},
     "split3_capped": {"RDB_GJ_SPLIT_PARTS": "3"},
 }
-KNOBS = ("RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW")
+KNOBS = ("RDB_GJ_WIDE_MIN", "RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW", "RDB_GJ_DW_LA")
 
 
 def main():
@@ -84,7 +85,8 @@ def main():
         work = torch.empty(L.lib().rdb_invert_workspace_bytes(n, 1), dtype=torch.uint8, device=dev)
         info = L.pivot_info_tensor(1, dev)
         ref = None
-        for name, env in (("dynamic_tickets", {}), ("static", {"RDB_GJ_DYNAMIC": "0"})):
+        for name, env in (("dynamic_tickets", {}), ("static", {"RDB_GJ_DYNAMIC": "0"}),
+                          ("wide_256_steps", {"RDB_GJ_WIDE_MIN": "1024"})):
             for k in KNOBS:
                 os.environ.pop(k, None)
             os.environ.update(env)

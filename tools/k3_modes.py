@@ -1,0 +1,70 @@
+"""A/B timing of K3 on the config-2 batch (256 inverses already in HBM):
+the TMA-streamed kernel (default) vs the register-pipelined lean kernel
+(RDB_K3_STREAM=0), uint8 and int32 D; outputs must be identical.
+
+usage: python tools/k3_modes.py [--out gpurun_out/k3_modes.json]
+"""
+
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2308_07403_b200 import _lib as L  # noqa: E402
+from paper_2308_07403_b200 import batch as B  # noqa: E402
+from paper_2308_07403_b200 import workloads as wl  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    L.load_library()
+    dev = torch.device("cuda", 0)
+    bits, gammas, _ = wl.cfg2_batch(256)
+    peak = float(json.loads(Path("MEASURED_PEAKS.json").read_text())["hbm_gbs"]) if Path("MEASURED_PEAKS.json").exists() else 6548.8
+    out = []
+    for dt in ("uint8", "int32"):
+        buf = B.BatchBuffers.allocate(1024, 256, dev, d_dtype=dt)
+        buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+        buf.gammas.copy_(torch.from_numpy(gammas))
+        sh = torch.cuda.current_stream().cuda_stream
+        B.run_chunk(buf, 256, sh)
+        torch.cuda.synchronize()
+        ref = None
+        for mode in ("1", "0"):
+            os.environ["RDB_K3_STREAM"] = mode
+            buf.counters.zero_()
+            buf.stage_log_ceil(256, sh)
+            torch.cuda.synchronize()
+            d = buf.d.clone()
+            cnt = buf.counters.clone()
+            if ref is None:
+                ref = (d, cnt)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            for _ in range(a.reps):
+                buf.stage_log_ceil(256, sh)
+            ev[1].record()
+            torch.cuda.synchronize()
+            ms = ev[0].elapsed_time(ev[1]) / a.reps
+            nbytes = 256 * (8 * 1024 * 1024 + (1 if dt == "uint8" else 4) * 1024 * 1024)
+            rec = {"d_dtype": dt, "stream": mode == "1", "ms": ms, "GBps": nbytes / ms / 1e6,
+                   "frac_of_hbm": nbytes / ms / 1e6 / peak, "d_identical": bool(torch.equal(d, ref[0])),
+                   "counters_identical": bool(torch.equal(cnt, ref[1]))}
+            print(json.dumps(rec), flush=True)
+            out.append(rec)
+        del buf
+        torch.cuda.empty_cache()
+    if a.out:
+        Path(a.out).write_text(json.dumps(out, indent=1) + "\n")
+
+
+if __name__ == "__main__":
+    main()
