@@ -601,172 +601,6 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
   }
 }
 
-// D-only K3 for whole matrices, streamed through shared memory by the bulk-copy
-// engine (TMA, SASS UBLKCP): each CTA owns a contiguous range of rows and keeps
-// STREAM_STAGES whole rows in flight (one cp.async.bulk of 8 n bytes per row,
-// completion on an mbarrier), so the bytes in flight per SM no longer depend
-// on registers (the lean kernel's limiter: 46% occupancy, long-scoreboard
-// stalls at 64 registers). Thread t converts columns 4t, 4t + 1024, ... of the
-// row from shared memory with the lean kernel's arithmetic (FP32 MUFU estimate,
-// exact FP64 path within twice its error bound of an integer) and stores 4
-// contiguous D's. Rows of one matrix share gamma; counters per warp per row.
-#ifndef STREAM_STAGES
-#define STREAM_STAGES 8
-#endif
-#ifndef STREAM_CTAS_PER_SM
-#define STREAM_CTAS_PER_SM 3
-#endif
-constexpr int kStreamMaxN = 2048;  // 16 KB rows
-
-template <int DK>
-__global__ void __launch_bounds__(256, 1)
-    log_ceil_stream_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
-                           const double* __restrict__ gammas, double gamma, void* __restrict__ dout, int64_t ldo,
-                           int64_t stride_o, unsigned long long* __restrict__ counters, int stages) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full[16];
-  double* rows_buf = reinterpret_cast<double*>(smem_raw);
-  const int64_t total = n * batch;
-  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * per;
-  const int64_t r1 = r0 + per < total ? r0 + per : total;
-  if (r0 >= r1) return;
-  const uint32_t row_bytes = (uint32_t)(n * 8);
-  const int t = threadIdx.x, lane = t & 31;
-  auto issue = [&](int64_t r, int s) {
-    const int64_t b = r / n, i = r - b * n;
-    mbar_arrive_expect_tx(&full[s], row_bytes);
-    bulk_g2s(rows_buf + (int64_t)s * n, y + b * stride_y + i * ldy, row_bytes, &full[s]);
-  };
-  if (t == 0) {
-    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-    for (int s = 0; s < stages && r0 + s < r1; ++s) issue(r0 + s, s);
-  }
-  __syncthreads();
-  const ConstTab tab;
-  int64_t cur_b = -1;
-  double g = 0.0, lg = 0.0, inv_lg = 0.0;
-  float inv_lg2f = 0.f, thr0 = 0.f;
-  for (int64_t r = r0, k = 0; r < r1; ++r, ++k) {
-    const int s = (int)(k % stages);
-    const int64_t b = r / n;
-    const int i = (int)(r - b * n);
-    if (b != cur_b) {
-      cur_b = b;
-      g = gammas ? gammas[b] : gamma;
-      lg = log(g);
-      inv_lg = 1.0 / lg;
-      const double inv_lg2 = 0.6931471805599453 * inv_lg;
-      inv_lg2f = (float)inv_lg2;
-      thr0 = (float)(1e-6 * fabs(inv_lg2));
-    }
-    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
-    const double* row = rows_buf + (int64_t)s * n;
-    const int64_t orow = b * stride_o + (int64_t)i * ldo;
-    unsigned neg = 0, bad = 0, dmax = 0;
-    for (int j = 4 * t; j < n; j += 1024) {
-      const double2 p = *reinterpret_cast<const double2*>(row + j);
-      const double2 q = *reinterpret_cast<const double2*>(row + j + 2);
-      const double v[4] = {p.x, p.y, q.x, q.y};
-      int d[4];
-      unsigned need = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        bool nd;
-        const bool dg = j + e == i;
-        const int de = dceil_estimate_f32(v[e], inv_lg2f, thr0, nd);
-        need |= (unsigned)(nd && !dg) << e;
-        d[e] = (dg || nd) ? 0 : de;
-        neg += dg && v[e] < NEGATIVE_ENTRY_TOL;  // the diagonal skips the exact path
-      }
-      if (need) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (need & (1u << e)) {
-            const double rr = exact_value(v[e], g, lg, inv_lg);
-            d[e] = __double2int_ru(rr);
-            neg += v[e] < NEGATIVE_ENTRY_TOL;
-            if (DK == DK_U8) {
-              const bool unreachable = rr == __longlong_as_double(0x7FF0000000000000LL);
-              const bool ok = rr == rr && (unsigned)d[e] <= (unsigned)RDB_D8_MAX;
-              bad += !ok && !unreachable;
-              d[e] = unreachable ? RDB_D8_UNREACHABLE : (ok ? d[e] : RDB_D8_MAX);
-            }
-          }
-      }
-      if (DK == DK_U8) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const unsigned u = (need >> e) & 1u ? 0u : (unsigned)d[e];
-          dmax = max(dmax, u);
-          d[e] = (need >> e) & 1u ? d[e] : (int)min(u, (unsigned)RDB_D8_MAX);
-        }
-        *reinterpret_cast<uchar4*>(static_cast<uint8_t*>(dout) + orow + j) =
-            make_uchar4((uint8_t)d[0], (uint8_t)d[1], (uint8_t)d[2], (uint8_t)d[3]);
-      } else {
-        *reinterpret_cast<int4*>(static_cast<int32_t*>(dout) + orow + j) = make_int4(d[0], d[1], d[2], d[3]);
-      }
-    }
-    if (DK == DK_U8 && __syncthreads_or(dmax > (unsigned)RDB_D8_MAX)) {
-      // rare: common-path D's above 254 were clamped; count them from the row still in smem
-      for (int j = t; j < n; j += 256) {
-        bool nd;
-        const int de = dceil_estimate_f32(row[j], inv_lg2f, thr0, nd);
-        if (!nd && j != i) bad += (unsigned)de > (unsigned)RDB_D8_MAX;
-      }
-    }
-    if (counters) {
-      neg = __reduce_add_sync(0xffffffffu, neg);
-      if (DK == DK_U8) bad = __reduce_add_sync(0xffffffffu, bad);
-      if (lane == 0) {
-        if (neg) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_NEGATIVE], (unsigned long long)neg);
-        if (DK == DK_U8 && bad) atomicAdd(&counters[b * RDB_NCOUNTERS + RDB_CNT_D8_RANGE], (unsigned long long)bad);
-      }
-    }
-    __syncthreads();  // every thread is done with stage s
-    if (t == 0 && r + stages < r1) {
-      fence_proxy_async();
-      issue(r + stages, s);
-    }
-  }
-}
-
-static bool stream_enabled() {
-  const char* e = getenv("RDB_K3_STREAM");  // A-B switch: 0 takes the register-pipelined lean kernel
-  return !(e && e[0] == '0');
-}
-
-// Launch the streamed K3 when the shape allows (whole rows of <= 16 KB, 16-byte
-// aligned rows, n % 4 == 0); returns false otherwise.
-template <int DK>
-static bool launch_stream(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
-                          const double* gammas, double gamma, void* dout, int64_t ldo, int64_t stride_o,
-                          unsigned long long* counters, cudaStream_t st) {
-  if (!stream_enabled() || n % 4 || n > kStreamMaxN || (ldy & 1) || (stride_y & 1) || ((uintptr_t)y & 15))
-    return false;
-  if ((ldo & 3) || (stride_o & 3) || ((uintptr_t)dout & (DK == DK_U8 ? 3 : 15))) return false;
-  const int stages = (int)((STREAM_STAGES * 8192) / (n * 8)) < 16 ? (int)((STREAM_STAGES * 8192) / (n * 8)) : 16;
-  if (stages < 2) return false;
-  const size_t smem = (size_t)stages * n * 8;
-  static DeviceFlags attr;
-  const int attr_dev = current_device();
-  if (!attr.get(attr_dev)) {
-    if (cudaFuncSetAttribute(log_ceil_stream_kernel<DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kStreamMaxN * 8 * 16)) != cudaSuccess)
-      return false;
-    attr.set(attr_dev);
-  }
-  int sms = 148;
-  if (attr_dev >= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, attr_dev);
-  const int64_t rows = n * batch;
-  const int64_t want = (int64_t)sms * STREAM_CTAS_PER_SM;
-  const unsigned grid = (unsigned)(rows < want ? rows : want);
-  log_ceil_stream_kernel<DK><<<grid, 256, smem, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, dout, ldo, stride_o,
-                                                     counters, stages);
-  return true;
-}
-
 template <bool A, bool B, int C>
 static void launch(bool vec, unsigned blocks, cudaStream_t st, const double* y, Shape n, int64_t ldy,
                    int64_t stride_y, int64_t batch, const double* gammas, double gamma, double* r,
@@ -799,9 +633,8 @@ int log_ceil_shaped(const double* y, Shape sh, int64_t ldy, int64_t stride_y, in
   const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
   if (key == 1 && vec && !reachable && !sh.gcol && sh.row0 == 0 && sh.col0 == 0 && sh.rows == n &&
       !(ldo & 3) && !(stride_o & 3) && al(d32_out, 16) && n < (int64_t)1 << 31) {
-    if (!launch_stream<DK_I32>(y, n, ldy, stride_y, batch, gammas, gamma, d32_out, ldo, stride_o, counters, st))
-      log_ceil_lean_kernel<DK_I32><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d32_out, ldo,
-                                                           stride_o, counters);
+    log_ceil_lean_kernel<DK_I32><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d32_out, ldo,
+                                                         stride_o, counters);
     RDB_LAUNCH_CHECK();
     return RDB_OK;
   }
@@ -844,9 +677,8 @@ int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64
   const unsigned blocks = (unsigned)(want < 148 * LEAN_GRID_PER_SM ? want : 148 * LEAN_GRID_PER_SM);
   if (!(ldy & 1) && !(stride_y & 1) && !(ldo & 3) && !(stride_o & 3) && al(y, 16) && al(d8_out, 4) &&
       n < (int64_t)1 << 31) {
-    if (!launch_stream<DK_U8>(y, n, ldy, stride_y, batch, gammas, gamma, d8_out, ldo, stride_o, counters, st))
-      log_ceil_lean_kernel<DK_U8><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d8_out, ldo,
-                                                          stride_o, counters);
+    log_ceil_lean_kernel<DK_U8><<<blocks, 256, 0, st>>>(y, n, ldy, stride_y, batch, gammas, gamma, d8_out, ldo,
+                                                        stride_o, counters);
   } else {
     launch<false, false, DK_U8>(false, blocks, st, y, Shape{n, n, 0, 0, nullptr}, ldy, stride_y, batch, gammas,
                                 gamma, nullptr, nullptr, nullptr, ldo, stride_o, nullptr, 0, counters, d8_out);

@@ -90,6 +90,7 @@ def main():
             for k in KNOBS:
                 os.environ.pop(k, None)
             os.environ.update(env)
+            work = torch.empty(L.lib().rdb_invert_workspace_bytes(n, 1), dtype=torch.uint8, device=dev)
             ts = []
             for _ in range(args.reps):
                 m1.copy_(m0)

@@ -1,6 +1,9 @@
-"""A/B timing of K3 on the config-2 batch (256 inverses already in HBM):
-the TMA-streamed kernel (default) vs the register-pipelined lean kernel
-(RDB_K3_STREAM=0), uint8 and int32 D; outputs must be identical.
+"""A/B timing of K3 on the config-2 batch (256 inverses already in HBM), uint8
+and int32 D, for the default library and variant libraries (--libs); outputs
+must be identical. Used to measure a TMA-streamed K3 (warp-private rings of row
+buffers filled by cp.async.bulk; profiles/r02_k3_stream_variants.json): no
+variant beat the register-pipelined lean kernel, which is issue-bound
+(45 instructions per element at 72% issue utilisation, ncu), so it was not kept.
 
 usage: python tools/k3_modes.py [--out gpurun_out/k3_modes.json]
 """
@@ -24,8 +27,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--libs", default="", help="comma-separated variant libraries (stream mode only)")
     a = ap.parse_args()
     L.load_library()
+    variants = [x for x in a.libs.split(",") if x]
     dev = torch.device("cuda", 0)
     bits, gammas, _ = wl.cfg2_batch(256)
     peak = float(json.loads(Path("MEASURED_PEAKS.json").read_text())["hbm_gbs"]) if Path("MEASURED_PEAKS.json").exists() else 6548.8
@@ -38,8 +43,10 @@ def main():
         B.run_chunk(buf, 256, sh)
         torch.cuda.synchronize()
         ref = None
-        for mode in ("1", "0"):
-            os.environ["RDB_K3_STREAM"] = mode
+        for mode in ["1", "0"] + variants:
+            if mode not in ("1", "0"):
+                L._lib = L.load_library(mode)
+            os.environ["RDB_K3_STREAM"] = "0" if mode == "0" else "1"
             buf.counters.zero_()
             buf.stage_log_ceil(256, sh)
             torch.cuda.synchronize()
@@ -55,11 +62,13 @@ def main():
             torch.cuda.synchronize()
             ms = ev[0].elapsed_time(ev[1]) / a.reps
             nbytes = 256 * (8 * 1024 * 1024 + (1 if dt == "uint8" else 4) * 1024 * 1024)
-            rec = {"d_dtype": dt, "stream": mode == "1", "ms": ms, "GBps": nbytes / ms / 1e6,
+            rec = {"d_dtype": dt, "stream": mode != "0", "lib": mode if mode not in ("0", "1") else "default", "ms": ms, "GBps": nbytes / ms / 1e6,
                    "frac_of_hbm": nbytes / ms / 1e6 / peak, "d_identical": bool(torch.equal(d, ref[0])),
                    "counters_identical": bool(torch.equal(cnt, ref[1]))}
             print(json.dumps(rec), flush=True)
             out.append(rec)
+        if variants:
+            L._lib = L.load_library()
         del buf
         torch.cuda.empty_cache()
     if a.out:
