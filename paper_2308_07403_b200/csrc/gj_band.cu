@@ -48,7 +48,10 @@ constexpr int CW = 4;          // warps (block columns) per chain CTA
 
 // Workspace per matrix: G[nb] and H[nb] in A-fragment order, D[nb] and K[nb] row-major.
 size_t ws_doubles(int64_t n_pad) { return (size_t)4 * (size_t)(n_pad / S) * BLK; }
-constexpr int GPC = 2;         // matrices per factor CTA
+#ifndef RDB_BAND_GPC
+#define RDB_BAND_GPC 2
+#endif
+constexpr int GPC = RDB_BAND_GPC;  // matrices per factor CTA
 
 RDB_DEV void gbar(int id) { asm volatile("bar.sync %0, 128;\n" ::"r"(id) : "memory"); }
 
