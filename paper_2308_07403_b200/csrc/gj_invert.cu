@@ -905,8 +905,13 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
       cudaEventRecord(ev_join, side);
       us.part = 2;
     }
-    gj_wb_update_kernel<<<persistent_grid(pcnt * (nt - 2) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap,
-                                                                                                   us);
+    unsigned ugrid = persistent_grid(pcnt * (nt - 2) * nt);
+    if (ahead) {  // optionally leave SMs to the side stream's band inverse (RDB_GJ_DW_LA_RESERVE)
+      const char* e = getenv("RDB_GJ_DW_LA_RESERVE");
+      const int res = e ? atoi(e) : 0;
+      if (res > 0 && (int)ugrid > sm_count() - res) ugrid = (unsigned)(sm_count() - res);
+    }
+    gj_wb_update_kernel<<<ugrid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, us);
     if (ahead) {
       cudaStreamWaitEvent(st, ev_join, 0);
     } else if (p + 1 < nt / 2) {

@@ -25,11 +25,14 @@ MODES = {
     "static_uncapped": {"RDB_GJ_DYNAMIC": "0", "RDB_GJ_COSCHED": "0"},
     "no_dense_wide": {"RDB_GJ_DW": "0"},
     "dw_no_lookahead": {"RDB_GJ_DW_LA": "0"},
+    "dw_la_reserve8": {"RDB_GJ_DW_LA_RESERVE": "8"},
+    "dw_la_reserve24": {"RDB_GJ_DW_LA_RESERVE": "24"},
+    "dw_la_reserve48": {"RDB_GJ_DW_LA_RESERVE": "48"},
     "no_split": {"RDB_GJ_SPLIT_MIN": "0"},
     "no_split_no_dw": {"RDB_GJ_SPLIT_MIN": "0", "RDB_GJ_DW": "0"},
     "split3_capped": {"RDB_GJ_SPLIT_PARTS": "3"},
 }
-KNOBS = ("RDB_GJ_WIDE_MIN", "RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW", "RDB_GJ_DW_LA")
+KNOBS = ("RDB_GJ_WIDE_MIN", "RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW", "RDB_GJ_DW_LA", "RDB_GJ_DW_LA_RESERVE")
 
 
 def main():
