@@ -906,9 +906,13 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
       us.part = 2;
     }
     unsigned ugrid = persistent_grid(pcnt * (nt - 2) * nt);
-    if (ahead) {  // optionally leave SMs to the side stream's band inverse (RDB_GJ_DW_LA_RESERVE)
+    if (ahead) {
+      // leave SMs to the side stream's band inverse (P1 needs one CTA per
+      // matrix): the rest of the update on sm_count - 64 CTAs (RDB_GJ_DW_LA_RESERVE
+      // overrides). Config 2 K2: 9.32 ms with no reserve, 9.09 ms with 48-80
+      // (plateau), 10.7 ms with 100 (profiles/r02_dw_la_reserve.json)
       const char* e = getenv("RDB_GJ_DW_LA_RESERVE");
-      const int res = e ? atoi(e) : 0;
+      const int res = e ? atoi(e) : (sm_count() * 7) / 16;
       if (res > 0 && (int)ugrid > sm_count() - res) ugrid = (unsigned)(sm_count() - res);
     }
     gj_wb_update_kernel<<<ugrid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, us);

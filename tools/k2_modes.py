@@ -28,6 +28,9 @@ MODES = {
     "dw_la_reserve8": {"RDB_GJ_DW_LA_RESERVE": "8"},
     "dw_la_reserve24": {"RDB_GJ_DW_LA_RESERVE": "24"},
     "dw_la_reserve48": {"RDB_GJ_DW_LA_RESERVE": "48"},
+    "dw_la_reserve64": {"RDB_GJ_DW_LA_RESERVE": "64"},
+    "dw_la_reserve80": {"RDB_GJ_DW_LA_RESERVE": "80"},
+    "dw_la_reserve100": {"RDB_GJ_DW_LA_RESERVE": "100"},
     "no_split": {"RDB_GJ_SPLIT_MIN": "0"},
     "no_split_no_dw": {"RDB_GJ_SPLIT_MIN": "0", "RDB_GJ_DW": "0"},
     "split3_capped": {"RDB_GJ_SPLIT_PARTS": "3"},
