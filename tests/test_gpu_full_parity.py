@@ -45,7 +45,8 @@ def _fixture_rows(golden, rank):
 @pytest.mark.parametrize("d_dtype", ["uint8", "int32"])
 def test_cfg2_bench_batch_every_graph_vs_reference(cuda, golden, rank, d_dtype):
     """The exact bench step (batch.run_chunk on the whole 256-graph batch,
-    default knobs: block-sparse plan, banded lattices, split sub-batches),
+    default knobs: dense-wide and block-sparse plans, banded lattices, split
+    sub-batches; captured as a CUDA graph and replayed, as bench.py times it),
     every graph against the reference's D."""
     f, sel = _fixture_rows(golden, rank)
     bits, gammas, seeds = wl.cfg2_batch(256, rank=rank)
@@ -54,7 +55,10 @@ def test_cfg2_bench_batch_every_graph_vs_reference(cuda, golden, rank, d_dtype):
     buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
     buf.gammas.copy_(torch.from_numpy(gammas))
     buf.counters.zero_()
-    B.run_chunk(buf, 256)
+    # the bench step: the whole pipeline call captured as a CUDA graph, replayed
+    pipe = B.CapturedPipeline(buf, 256)
+    buf.d.zero_()
+    pipe.replay()
     torch.cuda.synchronize()
     B.check_infos(L.read_pivot_info(buf.info), gammas)  # every graph certified (no pivoted redo)
     d = buf.d.cpu().numpy()
@@ -75,11 +79,13 @@ def test_cfg2_engine_every_graph_vs_reference(cuda, golden):
     bits, gammas, seeds = wl.cfg2_batch(256)
     eng = B.APSPBatchEngine(1024, 256, chunk=256, d_dtype="uint8")
     bp, gp = eng.pin(bits, gammas)
-    du = eng.run(bp, gp)
-    assert du.dtype == np.uint8
-    got = np.array([d_digest(x) for x in du], dtype="S16")
-    bad = np.flatnonzero(got != f["digest"][sel])
-    assert bad.size == 0, _explain(seeds, gammas, du, bad)
+    for _ in range(4):  # first uses of a (slot, D slot) run eagerly, later ones replay captured graphs
+        du = eng.run(bp, gp).copy()
+        assert du.dtype == np.uint8
+        got = np.array([d_digest(x) for x in du], dtype="S16")
+        bad = np.flatnonzero(got != f["digest"][sel])
+        assert bad.size == 0, _explain(seeds, gammas, du, bad)
+    assert eng.graphs  # the replays above went through captured graphs
 
 
 def test_cfg2_fixture_facts(golden):
