@@ -429,7 +429,7 @@ def cfg5_distributed(dev, rank, world, local_world, peak, max_over_ranks):
     loc = D.local_m_from_bits(br, lay, r, cc, gamma)
     del br
     torch.cuda.synchronize(dev)
-    dist.barrier(device_ids=[dev.index])
+    dist.barrier(device_ids=[dev.index]) if dist.get_backend() == "nccl" else dist.barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record()
     minp, flags = D.invert_block_cyclic({grid.me: loc}, grid, D.CudaEngine())
@@ -513,12 +513,19 @@ def main():
     local_world = env_int("LOCAL_WORLD_SIZE", world)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    # RDB_BENCH_DIST_BACKEND=gloo is a functional test hook only (ranks may then
+    # share a GPU; collectives go through the host); timings use NCCL
+    backend = os.environ.get("RDB_BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init (nranks, NVLS/P2P) on stderr
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init (nranks, NVLS/P2P) on stderr
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         assert dist.get_world_size() == args.gpus
     rb.load_library()
 
@@ -533,7 +540,7 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier(device_ids=[local]) if backend == "nccl" else dist.barrier()
         torch.cuda.synchronize(dev)
 
     def max_over_ranks(x: float) -> float:
@@ -671,6 +678,8 @@ def main():
     if not args.no_cfg5:
         cfg5 = (cfg5_single(dev, sh, peak, max_over_ranks) if world == 1
                 else cfg5_distributed(dev, rank, world, local_world, peak, max_over_ranks))
+        if world > 1 and backend != "nccl":
+            cfg5["note"] = f"functional run over {backend} (ranks share GPUs): not a timing"
         torch.cuda.empty_cache()
 
     if rank != 0:
