@@ -43,6 +43,9 @@ __global__ void __launch_bounds__(p1::THREADS, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
   if (nonband && nonband[b * info_stride] != want) return;
+#ifdef RDB_EXP_NO_NESTED_P1
+  if (want == 2) return;  // timing experiment only (wrong results)
+#endif
 #ifdef RDB_EXP_NO_P1
   return;  // timing experiment only (tools/k2_split.py on a variant library): wrong results
 #endif
@@ -885,13 +888,17 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
   // 256-block inverse then runs on the part's side stream (own ticket
   // counters) while the rest of the update runs here. No tile of the rest
   // reads or writes that block.
+#ifndef RDB_EXP_NO_NESTED
   rc = invert_core(a, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, 1, 0, dyn, &np, info_stride, flags, 0, 2);
   if (rc) return rc;
+#endif
   for (int p = 0; p < nt / 2; ++p) {
     const int p0t = 2 * p;
     const bool ahead = side && p + 1 < nt / 2;
     WBRowSched rs{a, lda, pstride, nt, p0t, p, d.list, d.count, d.colcnt, dyn};
+#ifndef RDB_EXP_NO_WBROW  // timing experiments only (wrong results)
     gj_wb_row_kernel<<<persistent_grid(pcnt * (nt - 2) * 2), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, rs);
+#endif
     WBUpdateSched us{a, lda, pstride, nt, p0t, p, d.list, d.count, d.rowcnt, dyn ? dyn + 1 : nullptr};
     if (ahead) {
       us.part = 1;
@@ -899,9 +906,11 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
       cudaEventRecord(ev_fork, st);
       cudaStreamWaitEvent(side, ev_fork, 0);
       const int64_t q0 = (int64_t)(p0t + 2) * NB;
+#ifndef RDB_EXP_NO_NESTED  // timing experiments only (wrong results)
       rc = invert_core(a + q0 * lda + q0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, side, 0, q0, side_dyn, &np,
                        info_stride, flags, 0, 2);
       if (rc) return rc;
+#endif
       cudaEventRecord(ev_join, side);
       us.part = 2;
     }
