@@ -383,7 +383,12 @@ RDB_DEV int dceil_estimate_f32(double v, float inv_lg2f, float thr0, bool& need)
   const int hi = __double2hiint(v), lo = __double2loint(v);
   const int ex = hi >> 20;  // sign bit set (v <= -0) -> ex < 0 -> need
   const float mf = __int_as_float(((hi & 0x000FFFFF) << 3) | ((unsigned)lo >> 29) | 0x3F800000);
-  const float q = ((float)(ex - 1023) + __log2f(mf)) * inv_lg2f;
+  // lg2.approx.ftz: mf is in [1, 2), never subnormal, so the flush-to-zero
+  // form drops __log2f's subnormal guard (3 instructions per element); its
+  // absolute error on [1, 2) is below 2^-22, the bound used above
+  float lg2m;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg2m) : "f"(mf));
+  const float q = ((float)(ex - 1023) + lg2m) * inv_lg2f;
   need = ((unsigned)(ex - 1) >= 2046u) | !(fabsf(q - rintf(q)) > fmaf(4e-7f, fabsf(q), thr0));
   return __float2int_ru(q);
 }
@@ -474,15 +479,25 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
       const double v[4] = {p.x, p.y, q.x, q.y};
       int d[4];
       unsigned need = 0;
+#if RDB_K3_MUFU && RDB_K3_F32
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        bool nd;
+        const int de = dceil_estimate_f32(v[e], inv_lg2f, thr0, nd);
+        need |= (unsigned)nd << e;
+        d[e] = nd ? 0 : de;
+      }
+      if ((unsigned)(i - j) < 4u) {  // the block holding the diagonal (one in n / 4): D = 0 there
+        need &= ~(1u << (i - j));
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (j + e == i) d[e] = 0;
+      }
+#else
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         bool nd;
         const bool dg = j + e == i;
-#if RDB_K3_MUFU && RDB_K3_F32
-        const int de = dceil_estimate_f32(v[e], inv_lg2f, thr0, nd);
-        need |= (unsigned)(nd && !dg) << e;
-        d[e] = (dg || nd) ? 0 : de;
-#else
 #if RDB_K3_MUFU
         const double r = dceil_estimate_mufu(v[e], inv_lg2, thr, nd);
 #else
@@ -490,11 +505,11 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
 #endif
         need |= (unsigned)(nd && !dg) << e;
         d[e] = (dg || nd) ? 0 : __double2int_ru(r);
-#endif
 #if !RDB_K3_MUFU
         neg += v[e] < NEGATIVE_ENTRY_TOL;
 #endif
       }
+#endif
       if (need) {  // rare: exact path (static indices keep v / d in registers)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
