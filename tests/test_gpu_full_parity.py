@@ -162,3 +162,26 @@ def test_cfg5_sampled_columns_vs_reference(cuda, golden):
     torch.cuda.empty_cache()
     bfs, _ = rb.oracles.bfs_apsp_bits(bits_d, n, torch.int32)
     assert torch.equal(d32, bfs)
+
+
+def test_captured_pipeline_replays_new_inputs(cuda, golden):
+    """The CUDA graph fixes the buffers, not the data: captured on rank 0's batch,
+    refilled in place with rank 1's bits and gains, replayed, it gives rank 1's
+    reference D on every graph (the serving pattern)."""
+    f = golden("cfg2_full")
+    bits0, gam0, _ = wl.cfg2_batch(256, rank=0)
+    bits1, gam1, seeds1 = wl.cfg2_batch(256, rank=1)
+    buf = B.BatchBuffers.allocate(1024, 256, cuda, d_dtype="uint8")
+    buf.bits.copy_(torch.from_numpy(bits0.view(np.int32)))
+    buf.gammas.copy_(torch.from_numpy(gam0))
+    buf.counters.zero_()
+    pipe = B.CapturedPipeline(buf, 256)
+    buf.bits.copy_(torch.from_numpy(bits1.view(np.int32)))
+    buf.gammas.copy_(torch.from_numpy(gam1))
+    pipe.replay()
+    torch.cuda.synchronize()
+    du = buf.d.cpu().numpy()
+    sel = np.flatnonzero(f["rank"] == 1)
+    got = np.array([d_digest(x) for x in du], dtype="S16")
+    bad = np.flatnonzero(got != f["digest"][sel])
+    assert bad.size == 0, _explain(seeds1, gam1, du, bad)
