@@ -569,7 +569,15 @@ def main():
     e1.record(stream)
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-    launches = args.steps * B.launches_per_call(N, batch)
+    # kernels per step: counted from the captured graph's kernel nodes (all are
+    # this library's: no torch op is captured); eager: the host restatement
+    per_step_kernels = None
+    if pipe is not None:
+        try:
+            per_step_kernels = pipe.kernel_nodes()
+        except Exception:  # noqa: BLE001 - falls back to the restatement
+            per_step_kernels = None
+    launches = args.steps * (per_step_kernels if per_step_kernels else B.launches_per_call(N, batch))
 
     # ---- per-kernel-family timing (same stream, same inputs), K2 = dominant
     def time_stage(fn, reps=3):
@@ -725,6 +733,8 @@ def main():
         "e2e": e2e,
         "e2e_" + e2e_other["d_dtype"]: e2e_other,
         "gpu_launches": launches,
+        "kernels_per_step": {"graph_kernel_nodes": per_step_kernels,
+                             "host_restatement": B.launches_per_call(N, batch)},
         "cuda_graph": not args.no_graph,
         "inversion_cfg5": cfg5,
         "clocks": clk,

@@ -175,12 +175,31 @@ class CapturedPipeline:
         self.buf, self.count = buf, count
         run_chunk(buf, count)  # eager first: library setup (streams, attributes) stays outside the capture
         torch.cuda.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
+        try:  # keep the cudaGraph_t so kernel_nodes() can inspect it
+            self.graph = torch.cuda.CUDAGraph(keep_graph=True)
+        except TypeError:
+            self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             run_chunk(buf, count, torch.cuda.current_stream().cuda_stream)
+        if hasattr(self.graph, "instantiate"):
+            self.graph.instantiate()
 
     def replay(self) -> None:
         self.graph.replay()
+
+    def kernel_nodes(self) -> int:
+        """Kernel launches one replay performs, counted from the captured graph's
+        nodes (cudaGraphGetNodes / cudaGraphNodeGetType)."""
+        from cuda.bindings import runtime as rt
+
+        g = self.graph.raw_cuda_graph()
+        err, _, count = rt.cudaGraphGetNodes(g, 0)
+        err, nodes, count = rt.cudaGraphGetNodes(g, count)
+        kernels = 0
+        for nd in nodes[:count]:
+            err, t = rt.cudaGraphNodeGetType(nd)
+            kernels += t == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel
+        return int(kernels)
 
 
 def d8_range_errors(counters: torch.Tensor) -> np.ndarray:
@@ -195,13 +214,21 @@ SPLIT_MIN_BATCH, SPLIT_PARTS = 64, 2  # csrc/gj_invert.cu defaults (RDB_GJ_SPLIT
 
 def launches_per_call(n: int, batch: int) -> int:
     """Kernels one rdb_apsp_bits_batched[_d8] call launches with the default
-    knobs: K1, the strip-pattern kernel, per sub-batch the plan (count walk,
-    scan, write walk) and 3 per panel (P1, P2, U), and K3."""
+    knobs (checked against the kernel nodes of a captured call: 131 for the
+    config-2 batch): band detection, K1, the strip patterns, the dense-wide
+    classification, the banded factor and chain, K3; per sub-batch the dense-wide
+    steps (nested band inverse 6 per band, row panel 1 per band, update 1 per band
+    + 1 for each look-ahead split) and the block-sparse plan (3) with 3 per panel
+    (P1, P2, U, launched even when their lists are empty)."""
     nt = L.pad_to_nb(n) // L.RDB_NB
     parts = SPLIT_PARTS if batch >= SPLIT_MIN_BATCH and batch >= 4 * SPLIT_PARTS else 1
     plan = batch > 1 and nt <= PLAN_MAX_NT
-    # with the plan: + band detection, band factor and band chain (gj_band.cu)
-    return 2 + (1 + 3 * parts + 3 if plan else 0) + parts * 3 * nt
+    if not plan:
+        return 2 + parts * 3 * nt
+    dw = nt >= 4 and nt % 2 == 0 and batch >= 2 * parts
+    bands = nt // 2
+    per_part = 3 + 3 * nt + ((6 + bands + 8 * (bands - 1) + 1) if dw else 0)
+    return 1 + 1 + 1 + (1 if dw else 0) + 2 + 1 + parts * per_part
 
 
 STRIPS = 8  # 16-column strips (engine k-chunks) per 128-column block
