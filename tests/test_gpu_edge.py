@@ -141,3 +141,37 @@ def test_concurrent_inversions_on_three_streams_make_progress(cuda):
         for buf, ref in zip(bufs, refs):
             assert torch.equal(buf.d, ref)
         assert torch.equal(m, m_ref)
+
+
+@pytest.mark.parametrize("n,count", [(512, 72), (1024, 24), (1536, 24)])  # 72: the two-stream split
+def test_mixed_batch_dense_wide_plan_and_band_paths(cuda, monkeypatch, n, count):
+    """One batched call whose matrices take all three inversion paths at once:
+    fully dense ER graphs (dense 256-wide steps), graphs with zero strips
+    (block-sparse NB = 128 plan) and block-tridiagonal graphs (banded inverse),
+    interleaved so both sub-batch streams hold a mix; D equal to the oracle and
+    to the same call with the dense-wide path switched off (RDB_GJ_DW=0)."""
+    rng = np.random.default_rng(n)
+    i, j = np.indices((n, n))
+    presents = []
+    for k in range(count):
+        kind = k % 3
+        if kind == 0:
+            q = rng.random((n, n)) < 0.03  # dense: every strip has edges
+        elif kind == 1:
+            q = np.zeros((n, n), bool)  # two components: zero off-diagonal blocks
+            h = n // 2
+            q[:h, :h] = rng.random((h, h)) < 0.03
+            q[h:, h:] = rng.random((n - h, n - h)) < 0.03
+        else:
+            q = (np.abs(i - j) <= 20) & (np.abs(i // 32 - j // 32) <= 1) & (rng.random((n, n)) < 0.3)
+        np.fill_diagonal(q, False)
+        presents.append(q)
+    gam = np.array([1e-2, 1e-2, 0.05] * (count // 3))
+    bits = np.stack([wl.pack_bits(q) for q in presents])
+    d_dw = rb.rounded_r_distance_batch(bits, gam, n)
+    monkeypatch.setenv("RDB_GJ_DW", "0")
+    d_plan = rb.rounded_r_distance_batch(bits, gam, n)
+    np.testing.assert_array_equal(d_dw, d_plan)
+    for b in range(0, len(presents), 5):
+        ref = orc.d_to_int32(orc.run_rdist(wl.weights_from_present(presents[b]), gam[b]))
+        np.testing.assert_array_equal(d_dw[b], ref, err_msg=f"graph {b}")
