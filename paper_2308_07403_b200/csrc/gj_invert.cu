@@ -1167,15 +1167,31 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       // row-block counters of the part, 16-byte aligned (counter_bytes has the slack)
       char* cw = wb + (((size_t)lo * ntl * sizeof(int) + 15) & ~(size_t)15);
       const bool dyn_on = dyn_sched();
+      // With the dense-wide path the part's block-sparse plan (its other
+      // matrices; for config 2 an empty schedule) runs on the part's side
+      // stream, concurrently with the dense-wide steps (disjoint matrices, own
+      // ticket counters), ahead of the look-ahead work queued there later.
+      const bool plan_aside = use_dw && dw_lookahead();
+      cudaStream_t plan_st = plan_aside ? ds->dw_side[i] : ds->part[i];
+      if (plan_aside) {
+        cudaEventRecord(ds->dw_fork[i], ds->part[i]);
+        cudaStreamWaitEvent(plan_st, ds->dw_fork[i], 0);
+      }
+      rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, plan_st, 1, 0,
+                       dyn_on ? (plan_aside ? dyn + 2 * MAX_PARTS + 2 * i : dyn + 2 * i) : nullptr,
+                       use_plan ? &pp : nullptr, parts, nonband ? nonband + i : nullptr,
+                       (!dyn_on && cosched_cap()) ? sm_count() / parts : 0);
+      if (rc) break;
       if (use_dw) {
         rc = dw_part(a + i * stride, n, lda, parts * stride, cnt, dwp[i], info + i, parts, nonband + i,
                      dyn_on ? dyn + 2 * i : nullptr, ds->part[i], dw_lookahead() ? ds->dw_side[i] : nullptr,
                      ds->dw_fork[i], ds->dw_join[i], dyn_on ? dyn + 2 * MAX_PARTS + 2 * i : nullptr);
         if (rc) break;
       }
-      rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, ds->part[i], 1, 0,
-                       dyn_on ? dyn + 2 * i : nullptr, use_plan ? &pp : nullptr, parts,
-                       nonband ? nonband + i : nullptr, (!dyn_on && cosched_cap()) ? sm_count() / parts : 0);
+      if (plan_aside) {  // the side stream's last work (plan, then look-ahead) joins the part
+        cudaEventRecord(ds->dw_join[i], plan_st);
+        cudaStreamWaitEvent(ds->part[i], ds->dw_join[i], 0);
+      }
       cudaEventRecord(ds->join[i], ds->part[i]);
       lo += cnt;
     }
