@@ -65,35 +65,14 @@ RDB_DEV void frag_rc(int e, int& row, int& col) {
   col = 4 * (kh >> 1) + (lane & 3);
 }
 
-RDB_DEV void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-RDB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-RDB_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-RDB_DEV void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-// One 4-warp group's shared memory. The sweeps prefetch the next block row's
-// operands (cp.async) while the current row's 32 x 32 inverse runs: X and AN
-// are double-buffered (the diagonal block and the block the next step's first
-// product reads), AF holds the block this step's second product reads.
-struct Group {
-  double X[2][SBUF], AN[2][SBUF], AF[SBUF], P[SBUF];
+struct Group {  // one 4-warp group's shared memory
+  double X[SBUF], A[SBUF], P[SBUF];
   double prow[2][S], pcol[2][S];
 };
 struct FactorSmem {
   Group g[2 * GPC];
   int flags[2 * GPC];
 };
-
-// 128 threads: asynchronous global row-major block -> shared block (each thread
-// its own 16-byte pieces; complete with cp_async_wait* + a group barrier)
-RDB_DEV void load_block_async(double* dst, const double* __restrict__ src, int64_t ld, int t) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int e = t + 128 * q, r = e >> 4, c2 = e & 15;
-    cp_async16(dst + r * LD + 2 * c2, src + (int64_t)r * ld + 2 * c2);
-  }
-}
 
 // 128 threads: global row-major block (ld) <-> shared block
 RDB_DEV void load_block(double* dst, const double* __restrict__ src, int64_t ld, int t) {
@@ -282,68 +261,50 @@ __global__ void __launch_bounds__(256 * GPC, 1)
     Group& g = s.g[grp];
     auto blk = [&](int r, int c) { return A + (int64_t)(S * r) * lda + S * c; };
     if ((grp & 1) == 0) {
-      // forward: D_r = T_r + L_r G_{r-1}; G_r = -D_r^-1 U_r
-      load_block_async(g.X[0], blk(0, 0), lda, t);
-      cp_async_commit();
-      for (int r = 0; r < nb; ++r) {
-        const int c = r & 1;
-        cp_async_wait0();
-        gbar(id);  // X[c] (and AN[c] = L_r) have landed; the previous step's reads are done
-        if (r < nb - 1) load_block_async(g.AF, blk(r, r + 1), lda, t);  // U_r, this step
-        cp_async_commit();
-        if (r + 1 < nb) {  // next row: T_{r+1}, L_{r+1}
-          load_block_async(g.X[c ^ 1], blk(r + 1, r + 1), lda, t);
-          load_block_async(g.AN[c ^ 1], blk(r + 1, r), lda, t);
-        }
-        cp_async_commit();
-        if (r > 0) gemm(g.X[c], g.X[c], g.AN[c], g.P, false, t, id);
-        store_block(Dl + (int64_t)r * BLK, S, g.X[c], t);
-        inverse(g, g.X[c], id, t, true, S * r, minp, mini, flags);
-        if (r < nb - 1) {
-          cp_async_wait1();
+      for (int r = 0; r < nb; ++r) {  // D_r = T_r + L_r G_{r-1}; G_r = -D_r^-1 U_r
+        load_block(g.X, blk(r, r), lda, t);
+        if (r > 0) {
+          load_block(g.A, blk(r, r - 1), lda, t);
           gbar(id);
-          gemm(g.P, nullptr, g.X[c], g.AF, true, t, id);
+          gemm(g.X, g.X, g.A, g.P, false, t, id);
+        } else {
+          gbar(id);
+        }
+        store_block(Dl + (int64_t)r * BLK, S, g.X, t);
+        inverse(g, g.X, id, t, true, S * r, minp, mini, flags);
+        if (r < nb - 1) {
+          load_block(g.A, blk(r, r + 1), lda, t);
+          gbar(id);
+          gemm(g.P, nullptr, g.X, g.A, true, t, id);
           store_frag(G + (int64_t)r * BLK, g.P, t);
         }
       }
-      cp_async_wait0();
     } else {
-      // backward: K_r = U_r H_{r+1}; S_r = T_r + K_r; H_r = -S_r^-1 L_r
-      load_block_async(g.X[(nb - 1) & 1], blk(nb - 1, nb - 1), lda, t);
-      cp_async_commit();
-      for (int r = nb - 1; r >= 0; --r) {
-        const int c = r & 1;
-        cp_async_wait0();
-        gbar(id);  // X[c] (and AN[c] = U_r) have landed
-        if (r > 0) load_block_async(g.AF, blk(r, r - 1), lda, t);  // L_r, this step
-        cp_async_commit();
-        if (r > 0) {  // next row (r - 1): T_{r-1}, U_{r-1}
-          load_block_async(g.X[c ^ 1], blk(r - 1, r - 1), lda, t);
-          load_block_async(g.AN[c ^ 1], blk(r - 1, r), lda, t);
-        }
-        cp_async_commit();
+      for (int r = nb - 1; r >= 0; --r) {  // K_r = U_r H_{r+1}; S_r = T_r + K_r; H_r = -S_r^-1 L_r
+        load_block(g.X, blk(r, r), lda, t);
         if (r < nb - 1) {
-          gemm(g.AN[c], nullptr, g.AN[c], g.P, false, t, id);
-          store_block(K + (int64_t)r * BLK, S, g.AN[c], t);
+          load_block(g.A, blk(r, r + 1), lda, t);
+          gbar(id);
+          gemm(g.A, nullptr, g.A, g.P, false, t, id);
+          store_block(K + (int64_t)r * BLK, S, g.A, t);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int e = t + 128 * q, rr = e >> 5, cc = e & 31;
-            g.X[c][rr * LD + cc] += g.AN[c][rr * LD + cc];
+            g.X[rr * LD + cc] += g.A[rr * LD + cc];
           }
         } else {
           const int e0 = t;
           for (int e = e0; e < BLK; e += 128) K[(int64_t)r * BLK + e] = 0.0;
         }
         gbar(id);
-        inverse(g, g.X[c], id, t, false, 0, minp, mini, flags);
+        inverse(g, g.X, id, t, false, 0, minp, mini, flags);
         if (r > 0) {
-          cp_async_wait1();
+          load_block(g.A, blk(r, r - 1), lda, t);
           gbar(id);
-          gemm(g.P, nullptr, g.X[c], g.AF, true, t, id);
+          gemm(g.P, nullptr, g.X, g.A, true, t, id);
           store_frag(H + (int64_t)r * BLK, g.P, t);
         }
       }
-      cp_async_wait0();
     }
   }
   if (t == 0) s.flags[grp] = flags;
@@ -365,6 +326,11 @@ __global__ void __launch_bounds__(256 * GPC, 1)
 // the workspace (and its own Y_jj), writes every block of M.
 constexpr size_t CHAIN_SMEM = (size_t)CW * (SBUF + 2 * BLK) * sizeof(double);
 
+RDB_DEV void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+RDB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+RDB_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 __global__ void __launch_bounds__(CW * 32, 2)
     band_chain_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int nb, const int* __restrict__ nonband,
