@@ -121,3 +121,18 @@ def test_cfg3_d_equals_bfs_full(cuda):
     _, d = rb._device.log_ceil(y, c["n"], c["gamma"], want_dceil=True)
     exact = oracles.bfs_apsp_device(g)
     assert torch.equal(d, exact)
+
+
+@pytest.mark.parametrize("name", SWEEP_FIXTURES)
+def test_accuracy_report_matches_reference(cuda, golden, name):
+    # navigation.accuracy_report (navigation.py:137-153): rounded estimate -> global,
+    # raw estimate -> local, pair counts from the exact distances
+    f = golden(name)
+    g = graph_of(f)
+    raw, exact = f["acc_raw"], f["exact"]
+    rep = rb.accuracy_report(g, np.ceil(raw), raw, exact)
+    assert rep.global_fraction == float(f["acc_global_rounded"])
+    assert rep.local_fraction == float(f["acc_local_raw"])
+    off = ~np.eye(exact.shape[0], dtype=bool)
+    assert rep.pairs_evaluated == int((off & np.isfinite(exact)).sum()) == int(f["evaluated_global"])
+    assert rep.pairs_excluded_unreachable == int((off & ~np.isfinite(exact)).sum())

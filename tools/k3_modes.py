@@ -10,7 +10,6 @@ usage: python tools/k3_modes.py [--out gpurun_out/k3_modes.json]
 
 import argparse
 import json
-import os
 import sys
 from pathlib import Path
 
@@ -43,10 +42,9 @@ def main():
         B.run_chunk(buf, 256, sh)
         torch.cuda.synchronize()
         ref = None
-        for mode in ["1", "0"] + variants:
-            if mode not in ("1", "0"):
+        for mode in ["default"] + variants:
+            if mode != "default":
                 L._lib = L.load_library(mode)
-            os.environ["RDB_K3_STREAM"] = "0" if mode == "0" else "1"
             buf.counters.zero_()
             buf.stage_log_ceil(256, sh)
             torch.cuda.synchronize()
@@ -62,7 +60,7 @@ def main():
             torch.cuda.synchronize()
             ms = ev[0].elapsed_time(ev[1]) / a.reps
             nbytes = 256 * (8 * 1024 * 1024 + (1 if dt == "uint8" else 4) * 1024 * 1024)
-            rec = {"d_dtype": dt, "stream": mode != "0", "lib": mode if mode not in ("0", "1") else "default", "ms": ms, "GBps": nbytes / ms / 1e6,
+            rec = {"d_dtype": dt, "lib": mode, "ms": ms, "GBps": nbytes / ms / 1e6,
                    "frac_of_hbm": nbytes / ms / 1e6 / peak, "d_identical": bool(torch.equal(d, ref[0])),
                    "counters_identical": bool(torch.equal(cnt, ref[1]))}
             print(json.dumps(rec), flush=True)
