@@ -105,7 +105,9 @@ struct UpdateSched {
   int64_t lda, stride;
   int nt, pt, batch;
   // part 0: every tile. Single-matrix look-ahead (batch == 1): part 1 is the
-  // next panel's diagonal tile (pt+1, pt+1) alone, part 2 every other tile
+  // next panel's diagonal tile (pt+1, pt+1) alone, part 2 every other tile;
+  // or part 3 the whole row block pt+1 (the next P1 and row panel need it) and
+  // part 4 every tile outside it
   int part;
   int* dyn = nullptr;  // dynamic tile counter (batched calls)
   // block-sparse plan (batched calls, part 0): entries {g << 12 | I << 6 | J,
@@ -115,7 +117,8 @@ struct UpdateSched {
   const int* count_ptr = nullptr;
   RDB_DEV int count() const {
     if (list) return *count_ptr;
-    return part == 0 ? batch * (nt - 1) * nt : (part == 1 ? 1 : (nt - 1) * nt - 1);
+    return part == 0 ? batch * (nt - 1) * nt
+                     : (part == 1 ? 1 : (part == 2 ? (nt - 1) * nt - 1 : (part == 3 ? nt : (nt - 2) * nt)));
   }
   RDB_DEV eng::Tile tile(int t) const {
     if (list) {
@@ -139,6 +142,13 @@ struct UpdateSched {
     } else if (part == 1) {
       Ir = pt;  // row pt+1
       jj = 0;   // column pt+1
+    } else if (part == 3) {
+      Ir = pt;  // row pt+1, every column (the panel column last)
+      jj = t;
+    } else if (part == 4) {
+      Ir = t / nt;  // rows other than pt+1
+      jj = t - Ir * nt;
+      Ir += (Ir >= pt) ? 1 : 0;
     } else {
       const int head = pt * nt;
       if (t < head) {
@@ -558,6 +568,14 @@ static unsigned persistent_grid(int64_t tiles) {
 static int invert_wide(double* a, int64_t n, int64_t lda, void* work, rdb_pivot_info* info, cudaStream_t st);
 static int64_t wide_min_n();
 
+// SMs the single-matrix row look-ahead gives the side stream (0: the older
+// diagonal-tile look-ahead with a one-round row-panel launch per step)
+static int la_side_sms() {
+  const char* e = getenv("RDB_GJ_LA_SIDE");
+  const int v = e ? atoi(e) : 16;
+  return v < 0 ? 0 : v;
+}
+
 // Blocked Gauss-Jordan with NB = 128 panels. `first` resets the pivot record
 // (step 0); idx_base offsets the reported pivot indices (a diagonal sub-block
 // inverted as part of a larger matrix).
@@ -592,6 +610,11 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
   cudaStream_t side = ds ? ds->side : nullptr;
   gj_panel_kernel<<<(unsigned)batch, p1::THREADS, p1::SMEM_BYTES, st>>>(a, lda, stride, 0, idx_base, info, first,
                                                                        info_stride, nonband, want);
+  // Row look-ahead (single matrix, RDB_GJ_LA_SIDE SMs, default 16): the side
+  // stream updates the whole next row block, inverts its diagonal tile and
+  // forms its row panel while the rest of the update runs on the other SMs,
+  // so the next step starts with its row panel done (no one-round P2 launch).
+  const int la_side = lookahead ? la_side_sms() : 0;
   for (int k = 0; k < nt; ++k) {
     const int p0 = k * NB;
     if (k > 0 && !lookahead)
@@ -603,9 +626,27 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
       rp.list = plan->rp + (int64_t)k * batch * (nt - 1);
       rp.count_ptr = plan->counts + k;
     }
-    gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES, st>>>(
-        amap, cmap, rp);
-    if (lookahead && k + 1 < nt) {
+    if (!(la_side > 0 && k > 0))  // with the row look-ahead, step k's row panel was formed on the side stream
+      gj_rowpanel_kernel<<<persistent_grid((int64_t)batch * (nt - 1)), EC::THREADS, EC::SMEM_BYTES, st>>>(
+          amap, cmap, rp);
+    if (la_side > 0 && k + 1 < nt) {
+      cudaEventRecord(ds->ev_a, st);
+      cudaStreamWaitEvent(side, ds->ev_a, 0);
+      UpdateSched ua{a, cnt, lda, stride, nt, k, 1, 3, dyn ? dyn + 3 : nullptr};
+      gj_update_kernel<<<(unsigned)(nt < la_side ? nt : la_side), EC::THREADS, EC::SMEM_BYTES, side>>>(amap, cmap, ua);
+      const int p1n = (k + 1) * NB;
+      gj_panel_kernel<<<1, p1::THREADS, p1::SMEM_BYTES, side>>>(a, lda, stride, p1n, idx_base + p1n, info, 0);
+      RowPanelSched rn{a, lda, stride, nt, k + 1, 1, nullptr};
+      gj_rowpanel_kernel<<<(unsigned)(nt - 1 < la_side ? nt - 1 : la_side), EC::THREADS, EC::SMEM_BYTES, side>>>(
+          amap, cmap, rn);
+      cudaEventRecord(ds->ev_p, side);
+      UpdateSched ub{a, cnt, lda, stride, nt, k, 1, 4, dyn ? dyn + 1 : nullptr};
+      const int64_t tiles = (int64_t)(nt - 2) * nt;
+      const int main_grid = sm_count() - la_side;
+      gj_update_kernel<<<(unsigned)(tiles < main_grid ? tiles : main_grid), EC::THREADS, EC::SMEM_BYTES, st>>>(
+          amap, cmap, ub);
+      cudaStreamWaitEvent(st, ds->ev_p, 0);
+    } else if (lookahead && k + 1 < nt) {
       // side stream, one SM: the next diagonal tile, then its inverse (P1);
       // main stream, the other SMs: every other tile of this update
       cudaEventRecord(ds->ev_a, st);

@@ -35,7 +35,7 @@ MODES = {
     "no_split_no_dw": {"RDB_GJ_SPLIT_MIN": "0", "RDB_GJ_DW": "0"},
     "split3_capped": {"RDB_GJ_SPLIT_PARTS": "3"},
 }
-KNOBS = ("RDB_GJ_WIDE_MIN", "RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW", "RDB_GJ_DW_LA", "RDB_GJ_DW_LA_RESERVE")
+KNOBS = ("RDB_GJ_LA_SIDE", "RDB_GJ_WIDE_MIN", "RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW", "RDB_GJ_DW_LA", "RDB_GJ_DW_LA_RESERVE")
 
 
 def main():
@@ -91,8 +91,9 @@ def main():
         work = torch.empty(L.lib().rdb_invert_workspace_bytes(n, 1), dtype=torch.uint8, device=dev)
         info = L.pivot_info_tensor(1, dev)
         ref = None
-        for name, env in (("dynamic_tickets", {}), ("static", {"RDB_GJ_DYNAMIC": "0"}),
-                          ("wide_256_steps", {"RDB_GJ_WIDE_MIN": "1024"})):
+        for name, env in (("default", {}), ("diag_lookahead", {"RDB_GJ_LA_SIDE": "0"}),
+                          ("row_lookahead_8", {"RDB_GJ_LA_SIDE": "8"}), ("row_lookahead_24", {"RDB_GJ_LA_SIDE": "24"}),
+                          ("row_lookahead_32", {"RDB_GJ_LA_SIDE": "32"}), ("static", {"RDB_GJ_DYNAMIC": "0"})):
             for k in KNOBS:
                 os.environ.pop(k, None)
             os.environ.update(env)
