@@ -404,14 +404,21 @@ extern "C" size_t rdb_invert_pivoted_workspace_bytes(int64_t n) {
   return base + blocked_small_bytes() + (np != n ? (size_t)np * np * sizeof(double) + 256 : 0);
 }
 
+// identity-padded np x np copy of the n x n input (the blocked path's operand)
 __global__ void piv_pad_kernel(const double* __restrict__ src, int64_t n, int64_t ld_src, double* __restrict__ dst,
-                               int64_t np, int to_padded) {
+                               int64_t np) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < np * np; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / np, j = e - i * np;
-    if (to_padded)
-      dst[e] = (i < n && j < n) ? src[i * ld_src + j] : (i == j ? 1.0 : 0.0);
-    else if (i < n && j < n)
-      const_cast<double*>(src)[i * ld_src + j] = dst[e];
+    dst[e] = (i < n && j < n) ? src[i * ld_src + j] : (i == j ? 1.0 : 0.0);
+  }
+}
+
+// the leading n x n block of the padded inverse back into the caller's matrix
+__global__ void piv_unpad_kernel(const double* __restrict__ src, int64_t np, double* __restrict__ dst, int64_t n,
+                                 int64_t ld_dst) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    dst[i * ld_dst + j] = src[i * np + j];
   }
 }
 
@@ -432,7 +439,7 @@ extern "C" int rdb_invert_pivoted(double* a, int64_t n, int64_t lda, void* work,
       m = reinterpret_cast<double*>(ws + blocked_small_bytes());
       m = reinterpret_cast<double*>(((uintptr_t)m + 255) & ~(uintptr_t)255);
       ldm = np;
-      piv_pad_kernel<<<1184, 256, 0, st>>>(a, n, lda, m, np, 1);
+      piv_pad_kernel<<<1184, 256, 0, st>>>(a, n, lda, m, np);
     }
     int rc = invert_pivoted_blocked(m, np, ldm, n, ws, perm, info, st);
     if (rc) return rc;
@@ -442,7 +449,7 @@ extern "C" int rdb_invert_pivoted(double* a, int64_t n, int64_t lda, void* work,
         cudaFuncSetAttribute(piv_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return RDB_ECUDA;
     piv_gather_kernel<<<(unsigned)(np < 1024 ? np : 1024), 256, smem, st>>>(m, np, ldm, idx);
-    if (m != a) piv_pad_kernel<<<1184, 256, 0, st>>>(a, n, lda, m, np, 0);
+    if (m != a) piv_unpad_kernel<<<1184, 256, 0, st>>>(m, np, a, n, lda);
     RDB_LAUNCH_CHECK();
     return RDB_OK;
   }
