@@ -120,6 +120,68 @@ RDB_DEV void atomic_max_nonneg(double* addr, double v) {
 
 }  // namespace rdb
 
+// ---------------------------------------------------------------- SM timeline (diagnostic builds)
+// Built with -DRDB_TRACE (tools/sm_timeline.py): every warp of a traced kernel
+// appends {globaltimer at entry, at exit, SM id, kernel kind} to a device
+// buffer, from which the tool rebuilds per-SM busy intervals of one call
+// (where SMs sit idle between the launches of the concurrent streams).
+// Off by default: RDB_TRACE_SCOPE expands to nothing.
+#ifdef RDB_TRACE
+namespace rdb {
+namespace trace {
+constexpr int SEGS = 192;  // per-SM segments of the buffer (SM ids < 192)
+struct Rec {
+  unsigned long long t0, t1;
+  int sm, kind;
+};
+static __device__ Rec* g_buf;
+static __device__ unsigned g_seg;        // records per segment
+static __device__ unsigned g_n[SEGS];    // records per segment so far
+RDB_DEV unsigned long long now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct Guard {
+  int kind;
+  unsigned long long t0;
+  RDB_DEV explicit Guard(int k) : kind(k), t0(now()) {}
+  RDB_DEV ~Guard() {
+    if ((threadIdx.x & 31) != 0 || !g_buf) return;
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    if (sm >= (unsigned)SEGS) return;
+    const unsigned i = atomicAdd(&g_n[sm], 1u);  // contention only within the SM
+    if (i >= g_seg) return;
+    g_buf[(size_t)sm * g_seg + i] = Rec{t0, now(), (int)sm, kind};
+  }
+};
+// points this translation unit's copy at buf (cap records, SEGS segments), counts reset
+static inline int attach(void* buf, unsigned cap) {
+  unsigned zero[SEGS] = {};
+  const unsigned seg = cap / SEGS;
+  if (cudaMemcpyToSymbol(g_buf, &buf, sizeof(buf)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_seg, &seg, sizeof(seg)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_n, zero, sizeof(zero)) != cudaSuccess)
+    return -1;
+  return 0;
+}
+static inline unsigned count() {  // total records kept
+  unsigned n[SEGS] = {}, seg = 0, tot = 0;
+  cudaMemcpyFromSymbol(n, g_n, sizeof(n));
+  cudaMemcpyFromSymbol(&seg, g_seg, sizeof(seg));
+  for (int i = 0; i < SEGS; ++i) tot += n[i] < seg ? n[i] : seg;
+  return tot;
+}
+}  // namespace trace
+}  // namespace rdb
+#define RDB_TRACE_SCOPE(kind) rdb::trace::Guard _rdb_trace_guard(kind)
+#else
+#define RDB_TRACE_SCOPE(kind) \
+  do {                        \
+  } while (0)
+#endif
+
 namespace rdb {
 void set_cuda_error(cudaError_t e);  // remembered for rdb_last_cuda_error()
 }

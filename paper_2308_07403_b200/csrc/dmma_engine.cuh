@@ -242,11 +242,23 @@ struct DynOf<S, decltype((void)S::dyn)> {
   RDB_DEV static int* get(const S& s) { return s.dyn; }
 };
 
-RDB_DEV int grab_tile(int* dyn, int ntiles, int lane) {
+// Sched::dyn_ctas (when present and > 0): the CTAs of every launch sharing the
+// counter (a helper launch on another stream joins the same tile list; the
+// reset then waits for all of their final grabs); else this grid's.
+template <class S, class = void>
+struct DynCtasOf {
+  RDB_DEV static int get(const S&) { return (int)gridDim.x; }
+};
+template <class S>
+struct DynCtasOf<S, decltype((void)S::dyn_ctas)> {
+  RDB_DEV static int get(const S& s) { return s.dyn_ctas > 0 ? s.dyn_ctas : (int)gridDim.x; }
+};
+
+RDB_DEV int grab_tile(int* dyn, int ntiles, int ctas, int lane) {
   int v = 0;
   if (lane == 0) {
     v = atomicAdd(dyn, 1);
-    if (v == ntiles + (int)gridDim.x - 1) atomicExch(dyn, 0);
+    if (v == ntiles + ctas - 1) atomicExch(dyn, 0);
   }
   return __shfl_sync(0xffffffffu, v, 0);
 }
@@ -290,8 +302,9 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
     int st = 0;
     uint32_t ph = 0;
     int* const dyn = DynOf<Sched>::get(sched);
-    for (int t = dyn ? grab_tile(dyn, ntiles, lane) : (int)blockIdx.x;;
-         t = dyn ? grab_tile(dyn, ntiles, lane) : t + (int)gridDim.x) {
+    const int ctas = DynCtasOf<Sched>::get(sched);
+    for (int t = dyn ? grab_tile(dyn, ntiles, ctas, lane) : (int)blockIdx.x;;
+         t = dyn ? grab_tile(dyn, ntiles, ctas, lane) : t + (int)gridDim.x) {
       if (t >= ntiles) {
         if (dyn) {  // tell the MMA warps: no more tiles
           mbar_wait(&s.empty[st], ph ^ 1);

@@ -209,6 +209,7 @@ using namespace band;
 // word-by-word loop.
 __global__ void band_detect_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t batch,
                                         int* __restrict__ nonband) {
+  RDB_TRACE_SCOPE(42);
   const int64_t wpr = (n + 31) / 32;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -245,6 +246,7 @@ __global__ void band_detect_bits_kernel(const uint32_t* __restrict__ bits, int64
 __global__ void __launch_bounds__(256 * GPC, 1)
     band_factor_kernel(const double* __restrict__ a, int64_t lda, int64_t stride, int nb, int64_t batch,
                        const int* __restrict__ nonband, double* __restrict__ ws, rdb_pivot_info* __restrict__ info) {
+  RDB_TRACE_SCOPE(40);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FactorSmem& s = *reinterpret_cast<FactorSmem*>(smem_raw);
   const int grp = threadIdx.x >> 7, t = threadIdx.x & 127, id = 1 + grp;
@@ -335,6 +337,7 @@ RDB_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "mem
 __global__ void __launch_bounds__(CW * 32, 2)
     band_chain_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int nb, const int* __restrict__ nonband,
                       const double* __restrict__ ws, rdb_pivot_info* __restrict__ info) {
+  RDB_TRACE_SCOPE(41);
   const int64_t m = blockIdx.y;
   if (nonband[m]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -457,3 +460,12 @@ int band_invert(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t b
 }
 
 }  // namespace rdb
+
+#ifdef RDB_TRACE
+namespace rdb {
+namespace band {
+int trace_attach(void* buf, unsigned cap) { return trace::attach(buf, cap); }
+unsigned trace_count() { return trace::count(); }
+}  // namespace band
+}  // namespace rdb
+#endif

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(p1::THREADS, 1)
     gj_panel_kernel(double* __restrict__ a, int64_t lda, int64_t stride, int64_t off, int idx0,
                     rdb_pivot_info* __restrict__ info, int first, int64_t info_stride = 1,
                     const int* __restrict__ nonband = nullptr, int want = 1) {
+  RDB_TRACE_SCOPE(want == 2 ? 1 : (want == 0 ? 5 : 0));
   // block at a + b*stride + off*(lda + 1); pivot indices recorded from idx0.
   // Per-matrix path flags (batched calls): 0 banded inverse, 1 block-sparse
   // Gauss-Jordan, 2 dense 256-wide Gauss-Jordan; only matrices whose flag is
@@ -203,6 +204,7 @@ struct UpdateSched {
 __global__ void __launch_bounds__(EC::THREADS, 1)
     gj_rowpanel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
                        RowPanelSched sched) {
+  RDB_TRACE_SCOPE(2);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(EC::THREADS, 1)
 __global__ void __launch_bounds__(EC::THREADS, 1)
     gj_update_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
                      UpdateSched sched) {
+  RDB_TRACE_SCOPE(3);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
@@ -366,6 +369,7 @@ template <bool WRITE>
 __global__ void __launch_bounds__(1024)
     gj_plan_walk(const unsigned char* __restrict__ pat, int64_t pat_stride, int batch, int nt,
                  int* __restrict__ offs, int* __restrict__ rp, int2* __restrict__ up) {
+  RDB_TRACE_SCOPE(30);
   // offs: [2][nt][batch] per-matrix counts (WRITE = false) / exclusive offsets (WRITE = true)
   extern __shared__ __align__(16) unsigned char s_pat[];  // per warp: C then R, nt rows of ld bytes each
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -457,6 +461,7 @@ __global__ void __launch_bounds__(1024)
 // (a warp per row); the totals go to counts[0 .. 2 nt).
 __global__ void __launch_bounds__(1024)
     gj_plan_scan(int* __restrict__ offs, int batch, int nt, int* __restrict__ counts) {
+  RDB_TRACE_SCOPE(31);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   for (int row = wid; row < 2 * nt; row += nw) {
     int* v = offs + (int64_t)row * batch;
@@ -743,6 +748,7 @@ struct WBUpdateSched {
   // part 0: every tile; 1: the next band's 2 x 2 diagonal tiles only (look-ahead:
   // the next band inverse can start); 2: every tile except those
   int part = 0;
+  int dyn_ctas = 0;  // > 0: CTAs of the main and the helper launch sharing dyn
   RDB_DEV int per() const { return part == 1 ? 4 : (nt - 2) * nt - (part == 2 ? 4 : 0); }
   RDB_DEV int count() const { return *list_count * per(); }
   RDB_DEV eng::Tile tile(int t) const {
@@ -801,6 +807,7 @@ struct WBUpdateSched {
 __global__ void __launch_bounds__(EC::THREADS, 1)
     gj_wb_row_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
                      WBRowSched sched) {
+  RDB_TRACE_SCOPE(4);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
@@ -808,6 +815,7 @@ __global__ void __launch_bounds__(EC::THREADS, 1)
 __global__ void __launch_bounds__(EC::THREADS, 1)
     gj_wb_update_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
                         WBUpdateSched sched) {
+  RDB_TRACE_SCOPE(10 + sched.part);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
@@ -822,6 +830,8 @@ struct DwPart {
   int* ncnt;    // nested row-block counters (invert_core work, 16-byte aligned)
   int* colcnt;  // [cnt][nt]
   int* rowcnt;  // [cnt][nt]
+  int* list_s;  // [cnt] listed matrices whose first step is sparse (count[1]), in list order
+  int* list_d;  // [cnt] the others (count[2]): their first step runs the dense tiles
 };
 
 // One CTA per part: classify the part's matrices (flag 1 -> 2 when every
@@ -831,19 +841,21 @@ struct DwPart {
 struct DwClassifyArgs {
   unsigned char* pat;
   int* flags;
+  const int* s0bad;  // per matrix: nonzero = keeps the dense first step (dw_s0_gather_kernel); nullptr: all do
   int64_t batch;
   int nt, parts;
   DwPart part[4];
 };
 
 __global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
+  RDB_TRACE_SCOPE(32);
   const int i = blockIdx.x;
   const int nt = arg.nt, ld = pat_ld(nt);
   const int64_t cnt = (arg.batch - i + arg.parts - 1) / arg.parts;
   const DwPart& d = arg.part[i];
-  __shared__ int warp_tot[8];
-  __shared__ int base;
-  if (threadIdx.x == 0) base = 0;
+  __shared__ int warp_tot[8], warp_s[8];
+  __shared__ int base, base_s;
+  if (threadIdx.x == 0) base = base_s = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t l0 = 0; l0 < cnt; l0 += 256) {
@@ -861,12 +873,22 @@ __global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
           }
     }
     // ordered compaction (block scan of the dense flags)
-    const unsigned bal = __ballot_sync(0xffffffffu, dense);
-    if (lane == 0) warp_tot[w] = __popc(bal);
+    const bool sp = dense && arg.s0bad && !arg.s0bad[m];
+    const unsigned bal = __ballot_sync(0xffffffffu, dense), bal_s = __ballot_sync(0xffffffffu, sp);
+    if (lane == 0) {
+      warp_tot[w] = __popc(bal);
+      warp_s[w] = __popc(bal_s);
+    }
     __syncthreads();
-    int off = base;
-    for (int k = 0; k < w; ++k) off += warp_tot[k];
+    int off = base, off_s = base_s;
+    for (int k = 0; k < w; ++k) {
+      off += warp_tot[k];
+      off_s += warp_s[k];
+    }
     const int pos = off + __popc(bal & ((1u << lane) - 1));
+    const int pos_s = off_s + __popc(bal_s & ((1u << lane) - 1));
+    if (sp) d.list_s[pos_s] = (int)l;
+    else if (dense) d.list_d[pos - pos_s] = (int)l;  // (dense ones before it) - (sparse ones before it)
     if (dense) {
       arg.flags[m] = 2;
       unsigned char* P = arg.pat + m * 2 * nt * ld;
@@ -880,24 +902,256 @@ __global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int k = 0; k < 8; ++k) tot += warp_tot[k];
+      int tot = 0, tot_s = 0;
+      for (int k = 0; k < 8; ++k) {
+        tot += warp_tot[k];
+        tot_s += warp_s[k];
+      }
       base += tot;
+      base_s += tot_s;
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    *d.count = base;
+    d.count[0] = base;
+    d.count[1] = base_s;
+    d.count[2] = base - base_s;
     d.ncounts[0] = d.ncounts[1] = base;          // nested row panels, steps 0 and 1
     d.ncounts[2] = d.ncounts[3] = 2 * base;      // nested update tiles
   }
 }
 
+// ---- sparse first step of the DW path (matrices built from bit-packed adjacency)
+// Step 0 reads the input M = I - gamma W itself: its block row 0 (A_0J, J
+// outside the band) and block column 0 (A_I0) hold only the graph's edges
+// (config 2's Erdos-Renyi graphs: ~5 per row / column of a 256-wide block), so
+// the step's rank-256 products are sparse:
+//   A_0J = D A_0J                   (D = A_00^-1 from the nested inverse)
+//   A_iJ = A_iJ - sum_k a_ik A_kJ   (i outside the band, k over the edges of
+//   A_i0 = -sum_k a_ik D_k,:         row i into block 0, in increasing k)
+// — the same algebra as the dense tiles of step 0 (a zero a_ik contributes an
+// exact zero), summed in a different order (the inverse agrees to rounding,
+// D is unchanged; tests compare with the reference). The dense step-0 tiles
+// (1/4 of the matrix's flop at n = 1024) are skipped; what is left is one
+// pass over the matrix in HBM (read M_i, write A_i).
+//   dw_s0_gather_kernel: the edges of block column 0 (per row i) and block
+//     row 0 (per column j), with their values, into compact lists (a snapshot:
+//     the step overwrites them in place), in increasing k; a matrix with more
+//     than S0_CAP edges in any such row or column keeps the dense step;
+//   dw_s0_row_kernel: A_0J = D A_0J, 16 rows of D in shared memory per CTA;
+//   dw_s0_update_kernel: the rows outside the band, 64-column strips of
+//     block row 0 (as updated) in shared memory per CTA.
+// The lists live in the matrix's slice of the banded path's scratch, which
+// the banded inverse uses only for banded matrices (never dense-wide ones).
+constexpr int S0_CAP = 24;
+
+// List layout inside a matrix's slice (R = n - 256 rows / columns outside the
+// band): row lists row-major (a warp reads one row's entries in one pass),
+// column lists entry-major (consecutive threads read consecutive columns):
+// vals_r [R][CAP] double | vals_c [CAP][R] double | idx_r [R][CAP] u8 |
+// idx_c [CAP][R] u8 | cnt_r [R] u8 | cnt_c [R] u8.
+struct S0Lists {
+  double *vr, *vc;
+  unsigned char *ir, *ic, *nr, *nc;
+  RDB_HOST_DEV S0Lists(void* base, int R) {
+    vr = static_cast<double*>(base);
+    vc = vr + (size_t)S0_CAP * R;
+    ir = reinterpret_cast<unsigned char*>(vc + (size_t)S0_CAP * R);
+    ic = ir + (size_t)S0_CAP * R;
+    nr = ic + (size_t)S0_CAP * R;
+    nc = nr + R;
+  }
+};
+
+struct S0Args {
+  double* a;
+  int64_t lda, pstride;
+  char* lists;            // part-local matrix l's lists at lists + l * lstride
+  int64_t lstride;
+  int n;                  // n_pad
+  const int* list;        // list_s
+  const int* count;       // count[1] = entries of list_s
+  int* colcnt;
+  int* rowcnt;
+};
+
+// grid (ceil(R / 256), batch): rows and columns 256 + 256 x + t of matrix m
+// (flags == 1: not banded); bad[m] |= 1 when one has more than S0_CAP edges.
+__global__ void __launch_bounds__(256) dw_s0_gather_kernel(const double* __restrict__ a, int64_t lda, int64_t stride,
+                                                           const uint32_t* __restrict__ bits, int64_t n_bits, int n,
+                                                           const int* __restrict__ flags, char* __restrict__ lists,
+                                                           int64_t lstride, int* __restrict__ bad) {
+  constexpr int B0 = 2 * NB;
+  const int64_t m = blockIdx.y;
+  if (flags[m] != 1) return;
+  const int R = n - B0;
+  const int64_t wpr = (n_bits + 31) / 32;
+  const uint32_t* bm = bits + m * n_bits * wpr;
+  const double* A = a + m * stride;
+  const S0Lists L(lists + m * lstride, R);
+  const int nb0 = (int)(n_bits < B0 ? n_bits : B0), w0 = (nb0 + 31) / 32;
+  const int t = (int)blockIdx.x * 256 + threadIdx.x;  // row / column index - B0
+  __shared__ uint32_t sw[B0][9];                       // the chunk's 8 words of rows k < nb0 (padded)
+  const int64_t q0 = (B0 + (int64_t)blockIdx.x * 256) / 32;
+  for (int e = threadIdx.x; e < nb0 * 8; e += 256) {
+    const int k = e >> 3, q = e & 7;
+    sw[k][q] = q0 + q < wpr ? bm[k * wpr + q0 + q] : 0u;
+  }
+  __syncthreads();
+  __shared__ unsigned char pos[2][256][S0_CAP];  // edge positions, then one batch of value loads
+  if (t >= R) return;
+  unsigned char* pr = pos[0][threadIdx.x];
+  unsigned char* pc = pos[1][threadIdx.x];
+  const int64_t i = B0 + t, j = B0 + t;
+  int cr = 0, cc = 0;
+  {  // row i: edges k < nb0 (the row's 8 words loaded together)
+    uint32_t wr[B0 / 32];
+#pragma unroll
+    for (int q = 0; q < B0 / 32; ++q) wr[q] = (q < w0 && i < n_bits) ? bm[i * wpr + q] : 0u;
+#pragma unroll
+    for (int q = 0; q < B0 / 32; ++q) {
+      uint32_t w = wr[q];
+      while (w) {
+        const int k = 32 * q + __ffs(w) - 1;
+        w &= w - 1;
+        if (cr < S0_CAP) pr[cr] = (unsigned char)k;
+        ++cr;
+      }
+    }
+  }
+  {  // column j: edges k < nb0
+    const int q = threadIdx.x >> 5, b = threadIdx.x & 31;
+    for (int k = 0; k < nb0; ++k)
+      if ((sw[k][q] >> b) & 1) {
+        if (cc < S0_CAP) pc[cc] = (unsigned char)k;
+        ++cc;
+      }
+  }
+  const int nr = cr < S0_CAP ? cr : S0_CAP, nc = cc < S0_CAP ? cc : S0_CAP;
+  double vr[S0_CAP], vc[S0_CAP];
+#pragma unroll
+  for (int e = 0; e < S0_CAP; ++e) {  // independent loads, issued together
+    vr[e] = e < nr ? A[i * lda + pr[e]] : 0.0;
+    vc[e] = e < nc ? A[(int64_t)pc[e] * lda + j] : 0.0;
+  }
+#pragma unroll
+  for (int e = 0; e < S0_CAP; ++e) {
+    if (e < nr) {
+      L.ir[(size_t)t * S0_CAP + e] = pr[e];
+      L.vr[(size_t)t * S0_CAP + e] = vr[e];
+    }
+    if (e < nc) {
+      L.ic[(size_t)e * R + t] = pc[e];
+      L.vc[(size_t)e * R + t] = vc[e];
+    }
+  }
+  L.nr[t] = (unsigned char)nr;
+  L.nc[t] = (unsigned char)nc;
+  const int over = cr > S0_CAP || cc > S0_CAP;
+  if (over) atomicOr(bad + m, 1);
+}
+
+// A_0J = D A_0J: rows 8 b .. 8 b + 7 of block row 0 (D's rows in shared
+// memory, transposed: an edge k reads Dt[k][0..7] as 4 16-byte loads; row
+// pitch 10 doubles), every column outside the band (thread t: columns
+// 256 + t + 256 q). Small register and shared-memory footprint: many CTAs
+// per SM hide the list loads' latency. grid (32, list capacity).
+__global__ void __launch_bounds__(256, 4) dw_s0_row_kernel(S0Args g) {
+  RDB_TRACE_SCOPE(6);
+  constexpr int B0 = 2 * NB, RB = 8;
+  if ((int)blockIdx.y >= g.count[1]) return;
+  const int l = g.list[blockIdx.y];
+  double* A = g.a + (int64_t)l * g.pstride;
+  const int R = g.n - B0;
+  const S0Lists L(g.lists + (int64_t)l * g.lstride, R);
+  const int tid = threadIdx.x, r0 = (int)blockIdx.x * RB;
+  const int nt = g.n / NB;
+  if (blockIdx.x == 0 && tid < nt) {  // the step-0 counts the dense tiles would have signalled
+    g.colcnt[(int64_t)l * nt + tid] = tid >= 2 ? 2 : 0;
+    g.rowcnt[(int64_t)l * nt + tid] = tid >= 2 ? nt : 0;
+  }
+  __shared__ __align__(16) double Dt[B0][RB + 2];
+  for (int e = tid; e < RB * B0; e += 256) Dt[e % B0][e / B0] = A[(int64_t)(r0 + e / B0) * g.lda + e % B0];
+  __syncthreads();
+  for (int t = tid; t < R; t += 256) {
+    double acc[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+    const int nc = L.nc[t];
+    for (int e = 0; e < nc; ++e) {
+      const int k = L.ic[(size_t)e * R + t];
+      const double v = L.vc[(size_t)e * R + t];
+      const double2* d = reinterpret_cast<const double2*>(&Dt[k][0]);
+#pragma unroll
+      for (int r = 0; r < RB / 2; ++r) {
+        const double2 x = d[r];
+        acc[2 * r] = fma(x.x, v, acc[2 * r]);
+        acc[2 * r + 1] = fma(x.y, v, acc[2 * r + 1]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) A[(int64_t)(r0 + r) * g.lda + B0 + t] = acc[r];
+  }
+}
+
+// Rows [r0, r1) outside the band: A_i = M'_i - sum_k a_ik A_k (block row 0
+// as updated, read from L2), M' = M with block column 0 zeroed. A warp per
+// row: its edge list in one load (lane e holds entry e), then passes over
+// 256 columns (4 16-byte chunks per lane). Low register count: 4 CTAs per SM
+// keep enough loads in flight. grid ((r1 - r0) / 8, list capacity).
+__global__ void __launch_bounds__(256, 4) dw_s0_update_kernel(S0Args g, int r0, int r1) {
+  RDB_TRACE_SCOPE(7);
+  constexpr int B0 = 2 * NB;
+  if ((int)blockIdx.y >= g.count[1]) return;
+  const int l = g.list[blockIdx.y];
+  double* A = g.a + (int64_t)l * g.pstride;
+  const int R = g.n - B0;
+  const S0Lists L(g.lists + (int64_t)l * g.lstride, R);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = r0 + (int)blockIdx.x * 8 + warp;
+  if (i >= r1) return;
+  const int t = i - B0;
+  const int cnt = L.nr[t];
+  int kl = 0;
+  double vl = 0.0;
+  if (lane < cnt) {
+    kl = L.ir[(size_t)t * S0_CAP + lane];
+    vl = L.vr[(size_t)t * S0_CAP + lane];
+  }
+  double* Ai = A + (int64_t)i * g.lda;
+  for (int jb = 2 * lane; jb < g.n; jb += 256) {  // n % 256 == 0
+    double2 o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) o[u] = jb + 64 * u < B0 ? make_double2(0.0, 0.0) : ldg2(Ai + jb + 64 * u);
+    for (int e = 0; e < cnt; ++e) {
+      const int k = __shfl_sync(0xffffffffu, kl, e);
+      const double mk = -__shfl_sync(0xffffffffu, vl, e);
+      const double2* pr = reinterpret_cast<const double2*>(A + (int64_t)k * g.lda + jb);
+      double2 pk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pk[u] = __ldg(pr + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        o[u].x = fma(mk, pk[u].x, o[u].x);
+        o[u].y = fma(mk, pk[u].y, o[u].y);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) stg2(Ai + jb + 64 * u, o[u]);
+  }
+}
+
+static void launch_s0_update(const S0Args& g, int r0, int r1, int64_t pcnt, cudaStream_t st) {
+  dw_s0_update_kernel<<<dim3((unsigned)((r1 - r0) / 8), (unsigned)pcnt), 256, 0, st>>>(g, r0, r1);
+}
+
+static bool dw_helper();
+
 // The DW steps for one part (its matrices a + l * pstride, l < pcnt).
 static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t pcnt, const DwPart& d,
                    rdb_pivot_info* info, int64_t info_stride, const int* flags, int* dyn, cudaStream_t st,
                    cudaStream_t side = nullptr, cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr,
-                   int* side_dyn = nullptr) {
+                   int* side_dyn = nullptr, const S0Args* s0 = nullptr) {
   const int nt = (int)(n / NB);
   if (cudaMemsetAsync(d.colcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess ||
       cudaMemsetAsync(d.rowcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess)
@@ -936,11 +1190,20 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
   for (int p = 0; p < nt / 2; ++p) {
     const int p0t = 2 * p;
     const bool ahead = side && p + 1 < nt / 2;
-    WBRowSched rs{a, lda, pstride, nt, p0t, p, d.list, d.count, d.colcnt, dyn};
+    // step 0 of the sparse-first-step matrices: their own kernels; the dense
+    // tiles of step 0 take the other listed matrices (list_d, count[2])
+    const bool sp = s0 && p == 0;
+    const int* list = sp ? d.list_d : d.list;
+    const int* list_count = sp ? d.count + 2 : d.count;
+    if (sp) dw_s0_row_kernel<<<dim3(2 * NB / 8, (unsigned)pcnt), 256, 0, st>>>(*s0);
+    WBRowSched rs{a, lda, pstride, nt, p0t, p, list, list_count, d.colcnt, dyn};
 #ifndef RDB_EXP_NO_WBROW  // timing experiments only (wrong results)
     gj_wb_row_kernel<<<persistent_grid(pcnt * (nt - 2) * 2), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, rs);
 #endif
-    WBUpdateSched us{a, lda, pstride, nt, p0t, p, d.list, d.count, d.rowcnt, dyn ? dyn + 1 : nullptr};
+    // sparse step 0, rows of the next band first (its inverse can then start)
+    if (sp) launch_s0_update(*s0, 2 * NB, 4 * NB, pcnt, st);
+    if (sp && !ahead && n > 4 * NB) launch_s0_update(*s0, 4 * NB, (int)n, pcnt, st);
+    WBUpdateSched us{a, lda, pstride, nt, p0t, p, list, list_count, d.rowcnt, dyn ? dyn + 1 : nullptr};
     if (ahead) {
       us.part = 1;
       gj_wb_update_kernel<<<persistent_grid(pcnt * 4), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, us);
@@ -954,19 +1217,33 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
 #endif
       cudaEventRecord(ev_join, side);
       us.part = 2;
+      if (sp && n > 4 * NB)  // the other rows of the sparse step, beside the next band's inverse
+        launch_s0_update(*s0, 4 * NB, (int)n, pcnt, st);
     }
-    unsigned ugrid = persistent_grid(pcnt * (nt - 2) * nt);
+    const unsigned full = persistent_grid(pcnt * (nt - 2) * nt);
+    unsigned ugrid = full, helper = 0;
     if (ahead) {
       // leave SMs to the side stream's band inverse (P1 needs one CTA per
       // matrix): the rest of the update on sm_count - 64 CTAs (RDB_GJ_DW_LA_RESERVE
       // overrides). Config 2 K2: 9.32 ms with no reserve, 9.09 ms with 48-80
-      // (plateau), 10.7 ms with 100 (profiles/r02_dw_la_reserve.json)
+      // (plateau), 10.7 ms with 100 (profiles/r02_dw_la_reserve.json). Once
+      // the band inverse is done, a helper launch on the side stream takes
+      // the reserved SMs back: it draws tickets from the same counter, so the
+      // rest of the update runs on every SM (the SM timeline showed the
+      // reserve idle for ~0.9 ms of the last look-ahead step otherwise,
+      // profiles/r02_sm_timeline_k2.json).
       const char* e = getenv("RDB_GJ_DW_LA_RESERVE");
       const int res = e ? atoi(e) : (sm_count() * 7) / 16;
       if (res > 0 && (int)ugrid > sm_count() - res) ugrid = (unsigned)(sm_count() - res);
+      if (dyn && dw_helper() && full > ugrid) helper = full - ugrid;
+      if (helper) us.dyn_ctas = (int)(ugrid + helper);
     }
     gj_wb_update_kernel<<<ugrid, EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, us);
     if (ahead) {
+      if (helper) {
+        gj_wb_update_kernel<<<helper, EC::THREADS, EC::SMEM_BYTES, side>>>(amap, cmap, us);
+        cudaEventRecord(ev_join, side);
+      }
       cudaStreamWaitEvent(st, ev_join, 0);
     } else if (p + 1 < nt / 2) {
       const int64_t q0 = (int64_t)(p0t + 2) * NB;
@@ -1003,7 +1280,8 @@ int band_invert(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t b
                 double* ws, rdb_pivot_info* info, cudaStream_t st);
 
 struct BatchWs {
-  size_t cnt, dyn, blk, counts, rp, up, offs, band, band_ws, dwl, dwc, dwnc, dwrp, dwup, dwcnt, dwcol, dwrow, total;
+  size_t cnt, dyn, blk, counts, rp, up, offs, band, band_ws, dwl, dwc, dwnc, dwrp, dwup, dwcnt, dwcol, dwrow, dws0,
+      dwls, dwld, total;
   BatchWs(int64_t n_pad, int64_t batch) {
     const size_t nt = (size_t)(n_pad / NB), b = (size_t)batch;
     cnt = 0;
@@ -1024,9 +1302,13 @@ struct BatchWs {
       dwcnt = dwup + align256(4 * b * sizeof(int2));
       dwcol = dwcnt + align256((2 * b + 4 * MAX_PARTS) * sizeof(int));
       dwrow = dwcol + align256(b * nt * sizeof(int));
-      total = dwrow + align256(b * nt * sizeof(int));
+      dws0 = dwrow + align256(b * nt * sizeof(int));  // sparse first step: bad flags, list_s, list_d
+      dwls = dws0 + align256(b * sizeof(int));
+      dwld = dwls + align256(b * sizeof(int));
+      total = dwld + align256(b * sizeof(int));
     } else {
-      counts = rp = up = offs = band = band_ws = dwl = dwc = dwnc = dwrp = dwup = dwcnt = dwcol = dwrow = total = blk;
+      counts = rp = up = offs = band = band_ws = dwl = dwc = dwnc = dwrp = dwup = dwcnt = dwcol = dwrow = dws0 = dwls =
+          dwld = total = blk;
     }
   }
   bool has_plan() const { return total > blk; }
@@ -1041,11 +1323,24 @@ struct BatchWs {
     d.ncnt = reinterpret_cast<int*>(wb + dwcnt + ((2 * (size_t)lo * sizeof(int) + 15) & ~(size_t)15));
     d.colcnt = reinterpret_cast<int*>(wb + dwcol) + lo * nt;
     d.rowcnt = reinterpret_cast<int*>(wb + dwrow) + lo * nt;
+    d.list_s = reinterpret_cast<int*>(wb + dwls) + lo;
+    d.list_d = reinterpret_cast<int*>(wb + dwld) + lo;
     return d;
   }
 };
 
+// Sparse first step of the dense-wide path (A-B switch RDB_GJ_DW_S0=0).
+static bool dw_s0_enabled() {
+  const char* e = getenv("RDB_GJ_DW_S0");
+  return !(e && e[0] == '0');
+}
+
 // Dense-wide look-ahead of the next band inverse on a side stream (A-B switch RDB_GJ_DW_LA=0).
+static bool dw_helper() {  // RDB_GJ_DW_HELPER=0: no helper launch (A/B)
+  const char* e = getenv("RDB_GJ_DW_HELPER");
+  return !(e && e[0] == '0');
+}
+
 static bool dw_lookahead() {
   const char* e = getenv("RDB_GJ_DW_LA");
   return !(e && e[0] == '0');
@@ -1177,10 +1472,33 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   // dense-wide path: classify (flags 1 -> 2, patterns zeroed, per-part lists) before the fork
   const bool use_dw = use_band && dw_enabled() && ntl >= 4 && ntl % 2 == 0 && batch >= 2 * (split ? parts : 1);
   DwPart dwp[MAX_PARTS];
+  const bool use_s0 = use_dw && dw_s0_enabled();
+  int* s0flags = use_s0 ? reinterpret_cast<int*>(wb + ws.dws0) : nullptr;
+  const int64_t lstride = (int64_t)(band::ws_doubles(n) * sizeof(double));  // lists in the banded scratch
+  auto s0_args = [&](const DwPart& d, int i, int parts_) {
+    S0Args g;
+    g.a = a + i * stride;
+    g.lda = lda;
+    g.pstride = parts_ * stride;
+    g.lists = wb + ws.band_ws + i * lstride;
+    g.lstride = parts_ * lstride;
+    g.n = (int)n;
+    g.list = d.list_s;
+    g.count = d.count;
+    g.colcnt = d.colcnt;
+    g.rowcnt = d.rowcnt;
+    return g;
+  };
   if (use_dw) {
+    if (use_s0) {
+      if (cudaMemsetAsync(s0flags, 0, (size_t)batch * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
+      dw_s0_gather_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)batch), 256, 0, st>>>(
+          a, lda, stride, bits, n_bits, (int)n, nonband, wb + ws.band_ws, lstride, s0flags);
+    }
     DwClassifyArgs ca;
     ca.pat = pat;
     ca.flags = nonband;
+    ca.s0bad = s0flags;
     ca.batch = batch;
     ca.nt = (int)ntl;
     ca.parts = split ? parts : 1;
@@ -1224,9 +1542,11 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
                        (!dyn_on && cosched_cap()) ? sm_count() / parts : 0);
       if (rc) break;
       if (use_dw) {
+        const S0Args g0 = use_s0 ? s0_args(dwp[i], i, parts) : S0Args{};
         rc = dw_part(a + i * stride, n, lda, parts * stride, cnt, dwp[i], info + i, parts, nonband + i,
                      dyn_on ? dyn + 2 * i : nullptr, ds->part[i], dw_lookahead() ? ds->dw_side[i] : nullptr,
-                     ds->dw_fork[i], ds->dw_join[i], dyn_on ? dyn + 2 * MAX_PARTS + 2 * i : nullptr);
+                     ds->dw_fork[i], ds->dw_join[i], dyn_on ? dyn + 2 * MAX_PARTS + 2 * i : nullptr,
+                     use_s0 ? &g0 : nullptr);
         if (rc) break;
       }
       if (plan_aside) {  // the side stream's last work (plan, then look-ahead) joins the part
@@ -1253,9 +1573,10 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   }
   if (use_dw) {
     DevStreams* ds = dw_lookahead() ? dev_streams() : nullptr;
+    const S0Args g0 = use_s0 ? s0_args(dwp[0], 0, 1) : S0Args{};
     const int rc = dw_part(a, n, lda, stride, batch, dwp[0], info, 1, nonband, dyn, st, ds ? ds->dw_side[0] : nullptr,
                            ds ? ds->dw_fork[0] : nullptr, ds ? ds->dw_join[0] : nullptr,
-                           dyn ? dyn + 2 * MAX_PARTS : nullptr);
+                           dyn ? dyn + 2 * MAX_PARTS : nullptr, use_s0 ? &g0 : nullptr);
     if (rc) return rc;
   }
   return invert_core(a, n, lda, stride, batch, work, info, st, 1, 0, dyn, use_plan ? &pp : nullptr, 1,
@@ -1365,6 +1686,7 @@ struct WideUpdateSched {  // rows I outside the band; J outside -> reduce into A
 __global__ void __launch_bounds__(EC::THREADS, 1)
     gj_wide_row_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap rmap,
                        WideRowSched sched) {
+  RDB_TRACE_SCOPE(8);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&rmap});
 }
@@ -1372,6 +1694,7 @@ __global__ void __launch_bounds__(EC::THREADS, 1)
 __global__ void __launch_bounds__(EC::THREADS, 1)
     gj_wide_update_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
                           const __grid_constant__ CUtensorMap smap, WideUpdateSched sched) {
+  RDB_TRACE_SCOPE(9);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap, &smap});
 }
@@ -1513,6 +1836,7 @@ struct LocalSched {
 __global__ void __launch_bounds__(EC::THREADS, 1)
     local_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
                       LocalSched sched) {
+  RDB_TRACE_SCOPE(20);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
@@ -1679,3 +2003,23 @@ extern "C" int rdb_residual(const double* m, int64_t ldm, const double* y, int64
   return RDB_OK;
 }
 
+
+#ifdef RDB_TRACE
+// Diagnostic builds only (tools/sm_timeline.py): records go to buf[0, cap/2)
+// from this file's kernels and to buf[cap/2, cap) from the banded path's.
+namespace rdb {
+namespace band {
+int trace_attach(void* buf, unsigned cap);
+unsigned trace_count();
+}  // namespace band
+}  // namespace rdb
+extern "C" int rdb_trace_attach(void* buf, unsigned cap) {
+  const unsigned h = cap / 2;
+  if (trace::attach(buf, h) || band::trace_attach(static_cast<trace::Rec*>(buf) + h, cap - h)) return RDB_ECUDA;
+  return RDB_OK;
+}
+extern "C" void rdb_trace_counts(unsigned* out) {
+  out[0] = trace::count();
+  out[1] = band::trace_count();
+}
+#endif
