@@ -27,6 +27,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
@@ -323,16 +325,63 @@ def band_flops(n: int) -> float:
     return float((nb - 1) * (nb + 5) + 3 * nb) * 2.0 * BAND**3
 
 
+S0_CAP = 24  # sparse first step: edges per row / column of the step-0 blocks (csrc/gj_invert.cu S0_CAP)
+DW_MIN_BATCH = 2  # dense-wide path: at least 2 matrices per sub-batch
+
+
+def sparse_first_step(bits: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """Host restatement of the dense-wide path's classification
+    (dw_classify_kernel, dw_s0_gather_kernel): per matrix, whether it takes the
+    dense 256-wide steps (not banded, every off-diagonal strip non-zero) and,
+    of those, whether its first step is sparse (at most S0_CAP edges in every
+    row of block column 0 and every column of block row 0, outside the
+    256-wide band). Returns (dense_wide, sparse_first) boolean masks."""
+    bits = np.asarray(bits).view(np.uint32)
+    batch = bits.shape[0]
+    nt = L.pad_to_nb(n) // L.RDB_NB
+    none = np.zeros(batch, bool)
+    off_env = lambda k: os.environ.get(k, "1").startswith("0")  # noqa: E731  (A-B switches read by the library)
+    if (batch < DW_MIN_BATCH or nt < 4 or nt % 2 or nt > PLAN_MAX_NT or n < 2 * L.RDB_NB or off_env("RDB_GJ_DW")
+            or off_env("RDB_GJ_BAND") or off_env("RDB_GJ_SKIP")):
+        return none, none
+    band = banded(bits, n)
+    pat = strip_pattern(bits, n)
+    off = ~np.eye(nt, dtype=bool)
+    dense = ~band & (pat[:, :, off] == 0xFF).all(axis=(1, 2))
+    b0 = 2 * L.RDB_NB
+    from .workloads import unpack_bits
+
+    sparse = np.zeros(batch, bool)
+    for b in np.flatnonzero(dense) if not off_env("RDB_GJ_DW_S0") else []:
+        p = unpack_bits(bits[b], n)
+        sparse[b] = p[b0:, :b0].sum(axis=1).max(initial=0) <= S0_CAP and p[:b0, b0:].sum(axis=0).max(initial=0) <= S0_CAP
+    return dense, sparse
+
+
 def executed_flops(bits: np.ndarray, n: int) -> float:
     """FP64 flop K2 executes on this batch with the default knobs: the banded
     path for block-tridiagonal graphs, the block-sparse Gauss-Jordan plan
-    (2 * 128 * 128 * 16 per k-chunk) for the others."""
-    batch = np.asarray(bits).shape[0]
+    (2 * 128 * 128 * 16 per k-chunk) for the others (the dense-wide steps
+    execute the same 2 n^3 as the plan on a fully dense matrix), less the
+    dense first step of the matrices whose first step is sparse (which
+    execute 2 * 256 flop per edge of block row 0 and 2 * n per edge of block
+    column 0 instead)."""
+    bits = np.asarray(bits)
+    batch = bits.shape[0]
     nt = L.pad_to_nb(n) // L.RDB_NB
     if batch > 1 and nt <= PLAN_MAX_NT:
         band = banded(bits, n)
-        chunks = gj_plan_chunks(strip_pattern(np.asarray(bits)[~band], n)).sum() if (~band).any() else 0
+        chunks = gj_plan_chunks(strip_pattern(bits[~band], n)).sum() if (~band).any() else 0
         extra = band.sum() * band_flops(n)
+        _, sparse = sparse_first_step(bits, n)
+        if sparse.any():
+            from .workloads import unpack_bits
+
+            b0, npad = 2 * L.RDB_NB, nt * L.RDB_NB
+            dense_step0 = 2.0 * b0 * b0 * (npad - b0) + 2.0 * (npad - b0) * b0 * npad
+            for b in np.flatnonzero(sparse):
+                p = unpack_bits(bits[b].view(np.uint32), n)
+                extra += 2.0 * b0 * p[:b0, b0:].sum() + 2.0 * npad * p[b0:, :b0].sum() - dense_step0
     else:
         chunks = batch * nt**3 * STRIPS
         extra = 0.0

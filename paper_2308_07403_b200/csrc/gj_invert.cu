@@ -286,6 +286,7 @@ struct DevStreams {
   // dense-wide look-ahead: one side stream + fork / join events per part
   cudaStream_t dw_side[MAX_PARTS] = {};
   cudaEvent_t dw_fork[MAX_PARTS] = {}, dw_join[MAX_PARTS] = {};
+  cudaEvent_t s0_ready[MAX_PARTS] = {};  // sparse first step: the part's edge lists gathered
 };
 static DevStreams g_streams[MAX_DEVICES];
 
@@ -305,7 +306,8 @@ static DevStreams* dev_streams() {
           cudaEventCreateWithFlags(&d.join[i], cudaEventDisableTiming) != cudaSuccess ||
           cudaStreamCreateWithFlags(&d.dw_side[i], cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&d.dw_fork[i], cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&d.dw_join[i], cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&d.dw_join[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&d.s0_ready[i], cudaEventDisableTiming) != cudaSuccess)
         return nullptr;
   }
   return &d;
@@ -863,14 +865,19 @@ __global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
     const int64_t m = i + (int64_t)arg.parts * l;
     bool dense = false;
     if (l < cnt && arg.flags[m] == 1) {
-      const unsigned char* P = arg.pat + m * 2 * nt * ld;
+      // the 2 nt rows of ld bytes as 32-bit words, no early exit (independent loads)
+      const uint32_t* P = reinterpret_cast<const uint32_t*>(arg.pat + m * 2 * nt * ld);
+      const int wpr = ld / 4;
       dense = true;
-      for (int I = 0; I < nt && dense; ++I)
-        for (int J = 0; J < nt; ++J)
-          if (I != J && (P[I * ld + J] != 0xFF || P[(nt + I) * ld + J] != 0xFF)) {
-            dense = false;
-            break;
-          }
+      for (int wi = 0; wi < 2 * nt * wpr; ++wi) {
+        const uint32_t v = P[wi];
+        const int I = (wi / wpr) % nt, J0 = 4 * (wi % wpr);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int J = J0 + b;
+          if (J < nt && J != I && ((v >> (8 * b)) & 0xFFu) != 0xFFu) dense = false;
+        }
+      }
     }
     // ordered compaction (block scan of the dense flags)
     const bool sp = dense && arg.s0bad && !arg.s0bad[m];
@@ -891,8 +898,8 @@ __global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
     else if (dense) d.list_d[pos - pos_s] = (int)l;  // (dense ones before it) - (sparse ones before it)
     if (dense) {
       arg.flags[m] = 2;
-      unsigned char* P = arg.pat + m * 2 * nt * ld;
-      for (int e = 0; e < 2 * nt * ld; ++e) P[e] = 0;
+      uint32_t* P = reinterpret_cast<uint32_t*>(arg.pat + m * 2 * nt * ld);
+      for (int e = 0; e < 2 * nt * ld / 4; ++e) P[e] = 0u;
       d.list[pos] = (int)l;
       for (int k = 0; k < 2; ++k) {
         d.nrp[k * cnt + pos] = (int)(l << 13) | (8 << 6) | (1 - k);
@@ -973,38 +980,50 @@ struct S0Args {
   const int* count;       // count[1] = entries of list_s
   int* colcnt;
   int* rowcnt;
+  // gather / split (dw_s0_gather_kernel, dw_s0_split_kernel)
+  const uint32_t* bits;   // part-local matrix l at bits + l * bstride (rows of wpr words)
+  int64_t bstride, n_bits;
+  int* bad;               // part-local matrix l's flag at bad[l * bad_stride]
+  int64_t bad_stride;
+  const int* dw_list;     // the part's dense-wide list (count[0] entries)
+  int* list_s;
+  int* list_d;
+  int* counts;            // count[1], count[2] written by the split
 };
 
-// grid (ceil(R / 256), batch): rows and columns 256 + 256 x + t of matrix m
-// (flags == 1: not banded); bad[m] |= 1 when one has more than S0_CAP edges.
-__global__ void __launch_bounds__(256) dw_s0_gather_kernel(const double* __restrict__ a, int64_t lda, int64_t stride,
-                                                           const uint32_t* __restrict__ bits, int64_t n_bits, int n,
-                                                           const int* __restrict__ flags, char* __restrict__ lists,
-                                                           int64_t lstride, int* __restrict__ bad) {
+// grid (ceil(R / 256), list capacity), 512 threads, for the part's
+// dense-wide matrices: thread t < 256 gathers row 256 + 256 x + t, thread
+// 256 + t column 256 + 256 x + t; bad |= 1 when one has more than S0_CAP
+// edges. Runs on the part's side stream beside the first band inverse.
+__global__ void __launch_bounds__(512, 2) dw_s0_gather_kernel(S0Args g) {
+  RDB_TRACE_SCOPE(33);
   constexpr int B0 = 2 * NB;
-  const int64_t m = blockIdx.y;
-  if (flags[m] != 1) return;
+  if ((int)blockIdx.y >= g.counts[0]) return;
+  const int l = g.dw_list[blockIdx.y];
+  const int n = g.n;
+  const int64_t n_bits = g.n_bits, lda = g.lda;
   const int R = n - B0;
   const int64_t wpr = (n_bits + 31) / 32;
-  const uint32_t* bm = bits + m * n_bits * wpr;
-  const double* A = a + m * stride;
-  const S0Lists L(lists + m * lstride, R);
+  const uint32_t* bm = g.bits + (int64_t)l * g.bstride;
+  const double* A = g.a + (int64_t)l * g.pstride;
+  const S0Lists L(g.lists + (int64_t)l * g.lstride, R);
   const int nb0 = (int)(n_bits < B0 ? n_bits : B0), w0 = (nb0 + 31) / 32;
-  const int t = (int)blockIdx.x * 256 + threadIdx.x;  // row / column index - B0
-  __shared__ uint32_t sw[B0][9];                       // the chunk's 8 words of rows k < nb0 (padded)
+  const bool col = threadIdx.x >= 256;
+  const int tl = threadIdx.x & 255;
+  const int t = (int)blockIdx.x * 256 + tl;  // row / column index - B0
+  __shared__ uint32_t sw[B0][9];             // the chunk's 8 words of rows k < nb0 (padded)
+  __shared__ unsigned char pos[512][S0_CAP]; // edge positions, then one batch of value loads
   const int64_t q0 = (B0 + (int64_t)blockIdx.x * 256) / 32;
-  for (int e = threadIdx.x; e < nb0 * 8; e += 256) {
+  for (int e = threadIdx.x; e < nb0 * 8; e += 512) {
     const int k = e >> 3, q = e & 7;
     sw[k][q] = q0 + q < wpr ? bm[k * wpr + q0 + q] : 0u;
   }
   __syncthreads();
-  __shared__ unsigned char pos[2][256][S0_CAP];  // edge positions, then one batch of value loads
   if (t >= R) return;
-  unsigned char* pr = pos[0][threadIdx.x];
-  unsigned char* pc = pos[1][threadIdx.x];
-  const int64_t i = B0 + t, j = B0 + t;
-  int cr = 0, cc = 0;
-  {  // row i: edges k < nb0 (the row's 8 words loaded together)
+  unsigned char* ps = pos[threadIdx.x];
+  int c = 0;
+  if (!col) {  // row i = B0 + t: edges k < nb0 (the row's 8 words loaded together)
+    const int64_t i = B0 + t;
     uint32_t wr[B0 / 32];
 #pragma unroll
     for (int q = 0; q < B0 / 32; ++q) wr[q] = (q < w0 && i < n_bits) ? bm[i * wpr + q] : 0u;
@@ -1014,41 +1033,82 @@ __global__ void __launch_bounds__(256) dw_s0_gather_kernel(const double* __restr
       while (w) {
         const int k = 32 * q + __ffs(w) - 1;
         w &= w - 1;
-        if (cr < S0_CAP) pr[cr] = (unsigned char)k;
-        ++cr;
+        if (c < S0_CAP) ps[c] = (unsigned char)k;
+        ++c;
       }
     }
-  }
-  {  // column j: edges k < nb0
-    const int q = threadIdx.x >> 5, b = threadIdx.x & 31;
+  } else {  // column j = B0 + t: edges k < nb0
+    const int q = tl >> 5, b = tl & 31;
     for (int k = 0; k < nb0; ++k)
       if ((sw[k][q] >> b) & 1) {
-        if (cc < S0_CAP) pc[cc] = (unsigned char)k;
-        ++cc;
+        if (c < S0_CAP) ps[c] = (unsigned char)k;
+        ++c;
       }
   }
-  const int nr = cr < S0_CAP ? cr : S0_CAP, nc = cc < S0_CAP ? cc : S0_CAP;
-  double vr[S0_CAP], vc[S0_CAP];
+  const int nc = c < S0_CAP ? c : S0_CAP;
+  const double* src = col ? A + B0 + t : A + (int64_t)(B0 + t) * lda;  // column: row k at src + k lda
+  const int64_t step = col ? lda : 1;
+  constexpr int H = S0_CAP / 2;
+  for (int e0 = 0; e0 < nc; e0 += H) {  // H independent loads at a time (one batch for most)
+    double v[H];
 #pragma unroll
-  for (int e = 0; e < S0_CAP; ++e) {  // independent loads, issued together
-    vr[e] = e < nr ? A[i * lda + pr[e]] : 0.0;
-    vc[e] = e < nc ? A[(int64_t)pc[e] * lda + j] : 0.0;
-  }
+    for (int e = 0; e < H; ++e) v[e] = e0 + e < nc ? src[ps[e0 + e] * step] : 0.0;
 #pragma unroll
-  for (int e = 0; e < S0_CAP; ++e) {
-    if (e < nr) {
-      L.ir[(size_t)t * S0_CAP + e] = pr[e];
-      L.vr[(size_t)t * S0_CAP + e] = vr[e];
-    }
-    if (e < nc) {
-      L.ic[(size_t)e * R + t] = pc[e];
-      L.vc[(size_t)e * R + t] = vc[e];
-    }
+    for (int e = 0; e < H; ++e)
+      if (e0 + e < nc) {
+        if (!col) {
+          L.ir[(size_t)t * S0_CAP + e0 + e] = ps[e0 + e];
+          L.vr[(size_t)t * S0_CAP + e0 + e] = v[e];
+        } else {
+          L.ic[(size_t)(e0 + e) * R + t] = ps[e0 + e];
+          L.vc[(size_t)(e0 + e) * R + t] = v[e];
+        }
+      }
   }
-  L.nr[t] = (unsigned char)nr;
-  L.nc[t] = (unsigned char)nc;
-  const int over = cr > S0_CAP || cc > S0_CAP;
-  if (over) atomicOr(bad + m, 1);
+  (col ? L.nc : L.nr)[t] = (unsigned char)nc;
+  if (c > S0_CAP) atomicOr(g.bad + (int64_t)l * g.bad_stride, 1);
+}
+
+// One CTA: the part's dense-wide list split by the gather's flags into
+// list_s (sparse first step) and list_d, both in list order.
+__global__ void __launch_bounds__(1024) dw_s0_split_kernel(S0Args g) {
+  __shared__ int wt[32], ws[32];
+  __shared__ int base, base_s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = base_s = 0;
+  __syncthreads();
+  const int cnt = g.counts[0];
+  for (int p0 = 0; p0 < cnt; p0 += 1024) {
+    const int p = p0 + threadIdx.x;
+    const int l = p < cnt ? g.dw_list[p] : 0;
+    const bool in = p < cnt, sp = in && !g.bad[(int64_t)l * g.bad_stride];
+    const unsigned bi = __ballot_sync(0xffffffffu, in), bs = __ballot_sync(0xffffffffu, sp);
+    if (lane == 0) {
+      wt[w] = __popc(bi);
+      ws[w] = __popc(bs);
+    }
+    __syncthreads();
+    int off = base, off_s = base_s;
+    for (int k = 0; k < w; ++k) {
+      off += wt[k];
+      off_s += ws[k];
+    }
+    const int pos = off + __popc(bi & ((1u << lane) - 1)), pos_s = off_s + __popc(bs & ((1u << lane) - 1));
+    if (sp) g.list_s[pos_s] = l;
+    else if (in) g.list_d[pos - pos_s] = l;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 32; ++k) {
+        base += wt[k];
+        base_s += ws[k];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    g.counts[1] = base_s;
+    g.counts[2] = base - base_s;
+  }
 }
 
 // A_0J = D A_0J: rows 8 b .. 8 b + 7 of block row 0 (D's rows in shared
@@ -1151,7 +1211,7 @@ static bool dw_helper();
 static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t pcnt, const DwPart& d,
                    rdb_pivot_info* info, int64_t info_stride, const int* flags, int* dyn, cudaStream_t st,
                    cudaStream_t side = nullptr, cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr,
-                   int* side_dyn = nullptr, const S0Args* s0 = nullptr) {
+                   int* side_dyn = nullptr, const S0Args* s0 = nullptr, cudaEvent_t s0_ready = nullptr) {
   const int nt = (int)(n / NB);
   if (cudaMemsetAsync(d.colcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess ||
       cudaMemsetAsync(d.rowcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess)
@@ -1183,10 +1243,24 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
   // 256-block inverse then runs on the part's side stream (own ticket
   // counters) while the rest of the update runs here. No tile of the rest
   // reads or writes that block.
+  // sparse first step: the edge lists are gathered (and the list split) on the
+  // side stream while the first band inverse runs here (already enqueued by
+  // the caller when s0_ready is given)
+  if (s0 && !s0_ready) {
+    cudaStream_t gs = side ? side : st;
+    if (side) {
+      cudaEventRecord(ev_fork, st);
+      cudaStreamWaitEvent(side, ev_fork, 0);
+    }
+    dw_s0_gather_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)pcnt), 512, 0, gs>>>(*s0);
+    dw_s0_split_kernel<<<1, 1024, 0, gs>>>(*s0);
+    if (side) cudaEventRecord(ev_join, side);
+  }
 #ifndef RDB_EXP_NO_NESTED
   rc = invert_core(a, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, 1, 0, dyn, &np, info_stride, flags, 0, 2);
   if (rc) return rc;
 #endif
+  if (s0 && (side || s0_ready)) cudaStreamWaitEvent(st, s0_ready ? s0_ready : ev_join, 0);
   for (int p = 0; p < nt / 2; ++p) {
     const int p0t = 2 * p;
     const bool ahead = side && p + 1 < nt / 2;
@@ -1475,6 +1549,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   const bool use_s0 = use_dw && dw_s0_enabled();
   int* s0flags = use_s0 ? reinterpret_cast<int*>(wb + ws.dws0) : nullptr;
   const int64_t lstride = (int64_t)(band::ws_doubles(n) * sizeof(double));  // lists in the banded scratch
+  const int64_t wpr = (n_bits + 31) / 32;
   auto s0_args = [&](const DwPart& d, int i, int parts_) {
     S0Args g;
     g.a = a + i * stride;
@@ -1487,18 +1562,23 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     g.count = d.count;
     g.colcnt = d.colcnt;
     g.rowcnt = d.rowcnt;
+    g.bits = bits + (int64_t)i * n_bits * wpr;
+    g.bstride = parts_ * n_bits * wpr;
+    g.n_bits = n_bits;
+    g.bad = s0flags + i;
+    g.bad_stride = parts_;
+    g.dw_list = d.list;
+    g.list_s = d.list_s;
+    g.list_d = d.list_d;
+    g.counts = d.count;
     return g;
   };
   if (use_dw) {
-    if (use_s0) {
-      if (cudaMemsetAsync(s0flags, 0, (size_t)batch * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
-      dw_s0_gather_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)batch), 256, 0, st>>>(
-          a, lda, stride, bits, n_bits, (int)n, nonband, wb + ws.band_ws, lstride, s0flags);
-    }
+    if (use_s0 && cudaMemsetAsync(s0flags, 0, (size_t)batch * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
     DwClassifyArgs ca;
     ca.pat = pat;
     ca.flags = nonband;
-    ca.s0bad = s0flags;
+    ca.s0bad = nullptr;  // every dense-wide matrix in list_d; the per-part split (after the gather) refines it
     ca.batch = batch;
     ca.nt = (int)ntl;
     ca.parts = split ? parts : 1;
@@ -1536,17 +1616,25 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
         cudaEventRecord(ds->dw_fork[i], ds->part[i]);
         cudaStreamWaitEvent(plan_st, ds->dw_fork[i], 0);
       }
+      // sparse first step: gather the part's edge lists on the side stream
+      // first (ahead of the plan), beside the part's first band inverse
+      const S0Args g0 = use_s0 ? s0_args(dwp[i], i, parts) : S0Args{};
+      const bool s0_aside = use_s0 && plan_aside;
+      if (s0_aside) {
+        dw_s0_gather_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)cnt), 512, 0, plan_st>>>(g0);
+        dw_s0_split_kernel<<<1, 1024, 0, plan_st>>>(g0);
+        cudaEventRecord(ds->s0_ready[i], plan_st);
+      }
       rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, plan_st, 1, 0,
                        dyn_on ? (plan_aside ? dyn + 2 * MAX_PARTS + 2 * i : dyn + 2 * i) : nullptr,
                        use_plan ? &pp : nullptr, parts, nonband ? nonband + i : nullptr,
                        (!dyn_on && cosched_cap()) ? sm_count() / parts : 0);
       if (rc) break;
       if (use_dw) {
-        const S0Args g0 = use_s0 ? s0_args(dwp[i], i, parts) : S0Args{};
         rc = dw_part(a + i * stride, n, lda, parts * stride, cnt, dwp[i], info + i, parts, nonband + i,
                      dyn_on ? dyn + 2 * i : nullptr, ds->part[i], dw_lookahead() ? ds->dw_side[i] : nullptr,
                      ds->dw_fork[i], ds->dw_join[i], dyn_on ? dyn + 2 * MAX_PARTS + 2 * i : nullptr,
-                     use_s0 ? &g0 : nullptr);
+                     use_s0 ? &g0 : nullptr, s0_aside ? ds->s0_ready[i] : nullptr);
         if (rc) break;
       }
       if (plan_aside) {  // the side stream's last work (plan, then look-ahead) joins the part

@@ -155,4 +155,15 @@ def test_band_detection_restatement():
     assert B.band_flops(1024) == (31 * 37 + 96) * 2 * 32**3
     fl = B.executed_flops(bits, 1024)
     er = B.gj_plan_chunks(B.strip_pattern(bits[kinds == "er"], 1024)).sum() * 2 * 128 * 128 * 16
-    assert fl == er + (kinds == "lattice").sum() * B.band_flops(1024)
+    assert er == (kinds == "er").sum() * 2 * 1024**3  # fully dense pattern
+    # every cfg2 ER graph takes the dense-wide steps with a sparse first step:
+    # its dense step 0 (row panel 256 x 256 x 768, update 768 x 256 x 1024) is
+    # replaced by 2 * 256 flop per edge of block row 0 and 2 * 1024 per edge of
+    # block column 0
+    dense, sparse = B.sparse_first_step(bits, 1024)
+    np.testing.assert_array_equal(dense, kinds == "er")
+    np.testing.assert_array_equal(sparse, kinds == "er")
+    step0 = 2 * 256 * 256 * 768 + 2 * 768 * 256 * 1024
+    sp = sum(2 * 256 * p[:256, 256:].sum() + 2 * 1024 * p[256:, :256].sum()
+             for p in (wl.unpack_bits(bits[b].view(np.uint32), 1024) for b in np.flatnonzero(kinds == "er")))
+    assert fl == er - (kinds == "er").sum() * step0 + sp + (kinds == "lattice").sum() * B.band_flops(1024)

@@ -26,7 +26,7 @@ from paper_2308_07403_b200 import workloads as wl  # noqa: E402
 
 KINDS = {0: "P1 plan", 1: "P1 nested (DW band)", 5: "P1 band path", 2: "rowpanel NB128", 3: "update NB128",
          4: "DW row panel", 10: "DW update (all)", 11: "DW update (next band 2x2)", 12: "DW update (rest)",
-         8: "wide row", 9: "wide update", 20: "local gemm", 30: "plan walk", 31: "plan scan", 32: "dw classify",
+         8: "wide row", 9: "wide update", 20: "local gemm", 30: "plan walk", 33: "DW sparse step-0 gather", 31: "plan scan", 32: "dw classify",
          6: "DW sparse step-0 row panel", 7: "DW sparse step-0 update", 40: "band factor", 41: "band chain", 42: "band detect"}
 REC = np.dtype([("t0", "<u8"), ("t1", "<u8"), ("sm", "<i4"), ("kind", "<i4")])
 
@@ -149,6 +149,15 @@ def main():
     print(json.dumps({k: v for k, v in out.items() if k != "busy_sms_per_bin"}, indent=1))
     lo = [(i, round(float(x), 1)) for i, x in enumerate(occ) if x < 0.85 * nsm]
     print("bins below 85% busy (index, busy SMs):", lo[:200])
+    # what runs in those bins: SMs per kernel kind active in the bin
+    low = {}
+    for i, _ in lo:
+        b0, b1 = edges[i], edges[i + 1]
+        act = recs[(recs["t0"] < b1) & (recs["t1"] > b0)]
+        low[i] = {KINDS.get(int(k), str(int(k))): int(np.unique(act["sm"][act["kind"] == k]).size)
+                  for k in np.unique(act["kind"])}
+        print(f"  bin {i} ({(b0 - t_lo) / 1e3:.0f} us): {low[i]}")
+    out["low_bins"] = low
     if a.out:
         Path(a.out).write_text(json.dumps(out, indent=1) + "\n")
 
