@@ -216,12 +216,15 @@ SPLIT_MIN_BATCH, SPLIT_PARTS = 64, 2  # csrc/gj_invert.cu defaults (RDB_GJ_SPLIT
 
 def launches_per_call(n: int, batch: int) -> int:
     """Kernels one rdb_apsp_bits_batched[_d8] call launches with the default
-    knobs (checked against the kernel nodes of a captured call: 131 for the
+    knobs (checked against the kernel nodes of a captured call: 148 for the
     config-2 batch): band detection, K1, the strip patterns, the dense-wide
     classification, the banded factor and chain, K3; per sub-batch the dense-wide
     steps (nested band inverse 6 per band, row panel 1 per band, update 1 per band
-    + 1 for each look-ahead split) and the block-sparse plan (3) with 3 per panel
-    (P1, P2, U, launched even when their lists are empty)."""
+    + 1 for each look-ahead split + 1 helper launch per look-ahead step; the
+    sparse first step's gather, split, row panel and two row ranges, plus its
+    edge count before K1) and the
+    block-sparse plan (3) with 3 per panel (P1, P2, U, launched even when their
+    lists are empty)."""
     nt = L.pad_to_nb(n) // L.RDB_NB
     parts = SPLIT_PARTS if batch >= SPLIT_MIN_BATCH and batch >= 4 * SPLIT_PARTS else 1
     plan = batch > 1 and nt <= PLAN_MAX_NT
@@ -229,8 +232,10 @@ def launches_per_call(n: int, batch: int) -> int:
         return 2 + parts * 3 * nt
     dw = nt >= 4 and nt % 2 == 0 and batch >= 2 * parts
     bands = nt // 2
-    per_part = 3 + 3 * nt + ((6 + bands + 8 * (bands - 1) + 1) if dw else 0)
-    return 1 + 1 + 1 + (1 if dw else 0) + 2 + 1 + parts * per_part
+    s0 = 5 if os.environ.get("RDB_GJ_DW_S0", "1") != "0" else 0  # per part (+ one count kernel before K1)
+    helpers = bands - 1 if os.environ.get("RDB_GJ_DW_HELPER", "1") != "0" else 0
+    per_part = 3 + 3 * nt + ((6 + bands + 8 * (bands - 1) + 1 + helpers + s0) if dw else 0)
+    return 1 + 1 + 1 + (1 if dw else 0) + (1 if dw and s0 else 0) + 2 + 1 + parts * per_part
 
 
 STRIPS = 8  # 16-column strips (engine k-chunks) per 128-column block

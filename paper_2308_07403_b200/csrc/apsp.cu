@@ -4,29 +4,46 @@
 // per-graph run_rdist closure (pkg/src/rdist/experiments.py:305-310:
 // resolvent(with_residual=False) -> r_distance -> ceil) for a whole batch of
 // unweighted graphs, with per-graph gains.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rdb {
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
-                   rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits, int64_t n_bits, bool band_ready);
+                   rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits, int64_t n_bits, bool band_ready,
+                   int phase, const double* m_gammas, int** s0bad_out);
 int* band_flags(void* work, int64_t n, int64_t batch);
 int band_detect(const uint32_t* bits, int64_t n, int64_t batch, int* nonband, cudaStream_t st);
 int build_m_bits_banded(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch, const double* gammas,
-                        double* out, int64_t stride_o, const int* nonband, cudaStream_t st);
+                        double* out, int64_t stride_o, const int* nonband, cudaStream_t st, const int* s0bad);
 
-// K1 and K2 of the pipelines: banded matrices are detected first, so K1
-// writes only their band (the banded inverse overwrites the rest).
+// K1 and K2 of the pipelines: the matrices are classified from the bits
+// first (banded, dense-wide with a sparse first step, other), so K1 writes
+// only what K2 reads: the band of a banded matrix, the block M_00 of a
+// sparse-first-step matrix (K2 writes the rest from the bits), else all of M.
 static int build_and_invert(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch, const double* gammas,
                             double* mwork, void* work, rdb_pivot_info* info, cudaStream_t st) {
   const int64_t stride = n_pad * n_pad;
   int* nonband = band_flags(work, n_pad, batch);
+  int* s0bad = nullptr;
+  const char* e = getenv("RDB_GJ_DW_SYNTH");  // A-B switch: 0 builds all of M and lets K2 read it
+  if (nonband && e && e[0] == '0') {
+    int rc = band_detect(bits, n, batch, nonband, st);
+    if (rc) return rc;
+    rc = build_m_bits_banded(bits, n, n_pad, batch, gammas, mwork, stride, nonband, st, nullptr);
+    if (rc) return rc;
+    return invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, true, 0, nullptr, nullptr);
+  }
   if (nonband) {
-    const int rc = band_detect(bits, n, batch, nonband, st);
+    int rc = band_detect(bits, n, batch, nonband, st);
+    if (rc) return rc;
+    rc = invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, true, 1, gammas, &s0bad);
     if (rc) return rc;
   }
-  int rc = build_m_bits_banded(bits, n, n_pad, batch, gammas, mwork, stride, nonband, st);
+  int rc = build_m_bits_banded(bits, n, n_pad, batch, gammas, mwork, stride, nonband, st, s0bad);
   if (rc) return rc;
-  return invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, nonband != nullptr);
+  return invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, nonband != nullptr,
+                        nonband ? 2 : 0, gammas, nullptr);
 }
 int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
                 const double* gammas, double gamma, uint8_t* d8_out, int64_t ldo, int64_t stride_o,

@@ -989,7 +989,79 @@ struct S0Args {
   int* list_s;
   int* list_d;
   int* counts;            // count[1], count[2] written by the split
+  // M built from the adjacency bits (the APSP pipelines): part-local matrix l
+  // is I - gam[l * gam_stride] A; the gather then takes the edge values from
+  // the gain, and the sparse step writes rows outside the band from the bits
+  // (K1 built only the 256 x 256 block M_00 of these matrices). nullptr: M is
+  // the caller's, read from memory.
+  const double* gam;
+  int64_t gam_stride;
 };
+
+// The edges of row or column B0 + t (thread's role) into / out of block 0, in
+// increasing k, into ps (at most S0_CAP kept); returns the total count.
+RDB_DEV int s0_positions(const uint32_t* bm, int64_t wpr, int64_t n_bits, int nb0, bool col, int t, int tl,
+                         const uint32_t (*sw)[9], unsigned char* ps) {
+  constexpr int B0 = 2 * NB;
+  const int w0 = (nb0 + 31) / 32;
+  int c = 0;
+  if (!col) {  // row i = B0 + t: edges k < nb0 (the row's 8 words loaded together)
+    const int64_t i = B0 + t;
+    uint32_t wr[B0 / 32];
+#pragma unroll
+    for (int q = 0; q < B0 / 32; ++q) wr[q] = (q < w0 && i < n_bits) ? bm[i * wpr + q] : 0u;
+#pragma unroll
+    for (int q = 0; q < B0 / 32; ++q) {
+      uint32_t w = wr[q];
+      while (w) {
+        const int k = 32 * q + __ffs(w) - 1;
+        w &= w - 1;
+        if (c < S0_CAP) ps[c] = (unsigned char)k;
+        ++c;
+      }
+    }
+  } else {  // column j = B0 + t: edges k < nb0 (sw: the chunk's words of rows k)
+    const int q = tl >> 5, b = tl & 31;
+    for (int k = 0; k < nb0; ++k)
+      if ((sw[k][q] >> b) & 1) {
+        if (c < S0_CAP) ps[c] = (unsigned char)k;
+        ++c;
+      }
+  }
+  return c;
+}
+
+// bits words of rows k < nb0 for the 256-column chunk x (columns B0 + 256 x ..)
+RDB_DEV void s0_stage_words(const uint32_t* bm, int64_t wpr, int nb0, uint32_t (*sw)[9]) {
+  const int64_t q0 = (2 * NB + (int64_t)blockIdx.x * 256) / 32;
+  for (int e = threadIdx.x; e < nb0 * 8; e += blockDim.x) {
+    const int k = e >> 3, q = e & 7;
+    sw[k][q] = q0 + q < wpr ? bm[k * wpr + q0 + q] : 0u;
+  }
+}
+
+// Before K1 (APSP pipelines, M from bits): grid (ceil(R / 256), batch), 512
+// threads, dense-wide matrices (flags == 2): bad[m] |= 1 when a row of block
+// column 0 or a column of block row 0 has more than S0_CAP edges. The others
+// take the sparse first step, and K1 builds only their block M_00.
+__global__ void __launch_bounds__(512) dw_s0_count_kernel(const uint32_t* __restrict__ bits, int64_t n_bits, int n,
+                                                          const int* __restrict__ flags, int* __restrict__ bad) {
+  constexpr int B0 = 2 * NB;
+  const int64_t m = blockIdx.y;
+  if (flags[m] != 2) return;
+  const int R = n - B0;
+  const int64_t wpr = (n_bits + 31) / 32;
+  const uint32_t* bm = bits + m * n_bits * wpr;
+  const int nb0 = (int)(n_bits < B0 ? n_bits : B0);
+  const bool col = threadIdx.x >= 256;
+  const int tl = threadIdx.x & 255, t = (int)blockIdx.x * 256 + tl;
+  __shared__ uint32_t sw[B0][9];
+  __shared__ unsigned char pos[512][S0_CAP];
+  s0_stage_words(bm, wpr, nb0, sw);
+  __syncthreads();
+  if (t >= R) return;
+  if (s0_positions(bm, wpr, n_bits, nb0, col, t, tl, sw, pos[threadIdx.x]) > S0_CAP) atomicOr(bad + m, 1);
+}
 
 // grid (ceil(R / 256), list capacity), 512 threads, for the part's
 // dense-wide matrices: thread t < 256 gathers row 256 + 256 x + t, thread
@@ -1007,52 +1079,26 @@ __global__ void __launch_bounds__(512, 2) dw_s0_gather_kernel(S0Args g) {
   const uint32_t* bm = g.bits + (int64_t)l * g.bstride;
   const double* A = g.a + (int64_t)l * g.pstride;
   const S0Lists L(g.lists + (int64_t)l * g.lstride, R);
-  const int nb0 = (int)(n_bits < B0 ? n_bits : B0), w0 = (nb0 + 31) / 32;
+  const int nb0 = (int)(n_bits < B0 ? n_bits : B0);
   const bool col = threadIdx.x >= 256;
   const int tl = threadIdx.x & 255;
   const int t = (int)blockIdx.x * 256 + tl;  // row / column index - B0
   __shared__ uint32_t sw[B0][9];             // the chunk's 8 words of rows k < nb0 (padded)
   __shared__ unsigned char pos[512][S0_CAP]; // edge positions, then one batch of value loads
-  const int64_t q0 = (B0 + (int64_t)blockIdx.x * 256) / 32;
-  for (int e = threadIdx.x; e < nb0 * 8; e += 512) {
-    const int k = e >> 3, q = e & 7;
-    sw[k][q] = q0 + q < wpr ? bm[k * wpr + q0 + q] : 0u;
-  }
+  s0_stage_words(bm, wpr, nb0, sw);
   __syncthreads();
   if (t >= R) return;
   unsigned char* ps = pos[threadIdx.x];
-  int c = 0;
-  if (!col) {  // row i = B0 + t: edges k < nb0 (the row's 8 words loaded together)
-    const int64_t i = B0 + t;
-    uint32_t wr[B0 / 32];
-#pragma unroll
-    for (int q = 0; q < B0 / 32; ++q) wr[q] = (q < w0 && i < n_bits) ? bm[i * wpr + q] : 0u;
-#pragma unroll
-    for (int q = 0; q < B0 / 32; ++q) {
-      uint32_t w = wr[q];
-      while (w) {
-        const int k = 32 * q + __ffs(w) - 1;
-        w &= w - 1;
-        if (c < S0_CAP) ps[c] = (unsigned char)k;
-        ++c;
-      }
-    }
-  } else {  // column j = B0 + t: edges k < nb0
-    const int q = tl >> 5, b = tl & 31;
-    for (int k = 0; k < nb0; ++k)
-      if ((sw[k][q] >> b) & 1) {
-        if (c < S0_CAP) ps[c] = (unsigned char)k;
-        ++c;
-      }
-  }
+  const int c = s0_positions(bm, wpr, n_bits, nb0, col, t, tl, sw, ps);
   const int nc = c < S0_CAP ? c : S0_CAP;
   const double* src = col ? A + B0 + t : A + (int64_t)(B0 + t) * lda;  // column: row k at src + k lda
   const int64_t step = col ? lda : 1;
+  const double ng = g.gam ? -g.gam[(int64_t)l * g.gam_stride] : 0.0;  // M from bits: every edge is -gamma
   constexpr int H = S0_CAP / 2;
   for (int e0 = 0; e0 < nc; e0 += H) {  // H independent loads at a time (one batch for most)
     double v[H];
 #pragma unroll
-    for (int e = 0; e < H; ++e) v[e] = e0 + e < nc ? src[ps[e0 + e] * step] : 0.0;
+    for (int e = 0; e < H; ++e) v[e] = e0 + e < nc ? (g.gam ? ng : src[ps[e0 + e] * step]) : 0.0;
 #pragma unroll
     for (int e = 0; e < H; ++e)
       if (e0 + e < nc) {
@@ -1066,7 +1112,7 @@ __global__ void __launch_bounds__(512, 2) dw_s0_gather_kernel(S0Args g) {
       }
   }
   (col ? L.nc : L.nr)[t] = (unsigned char)nc;
-  if (c > S0_CAP) atomicOr(g.bad + (int64_t)l * g.bad_stride, 1);
+  if (!g.gam && c > S0_CAP) atomicOr(g.bad + (int64_t)l * g.bad_stride, 1);  // (M from bits: counted before K1)
 }
 
 // One CTA: the part's dense-wide list split by the gather's flags into
@@ -1179,10 +1225,27 @@ __global__ void __launch_bounds__(256, 4) dw_s0_update_kernel(S0Args g, int r0, 
     vl = L.vr[(size_t)t * S0_CAP + lane];
   }
   double* Ai = A + (int64_t)i * g.lda;
+  // M from bits: M'_ij = [i == j] - gamma [edge i -> j] (j >= B0), no read of M
+  const int64_t wpr = (g.n_bits + 31) / 32;
+  const uint32_t* brow = g.bits + (int64_t)l * g.bstride + (int64_t)i * wpr;
+  const double ng = g.gam ? -g.gam[(int64_t)l * g.gam_stride] : 0.0;
   for (int jb = 2 * lane; jb < g.n; jb += 256) {  // n % 256 == 0
     double2 o[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) o[u] = jb + 64 * u < B0 ? make_double2(0.0, 0.0) : ldg2(Ai + jb + 64 * u);
+    for (int u = 0; u < 4; ++u) {
+      const int j = jb + 64 * u;
+      if (j < B0) {
+        o[u] = make_double2(0.0, 0.0);
+      } else if (g.gam) {
+        const uint32_t wd = (i < g.n_bits && (j >> 5) < wpr) ? __ldg(brow + (j >> 5)) : 0u;
+        o[u].x = ((wd >> (j & 31)) & 1u) && j < g.n_bits ? ng : 0.0;
+        o[u].y = ((wd >> ((j + 1) & 31)) & 1u) && j + 1 < g.n_bits ? ng : 0.0;
+        if (j == i) o[u].x = 1.0;
+        if (j + 1 == i) o[u].y = 1.0;
+      } else {
+        o[u] = ldg2(Ai + j);
+      }
+    }
     for (int e = 0; e < cnt; ++e) {
       const int k = __shfl_sync(0xffffffffu, kl, e);
       const double mk = -__shfl_sync(0xffffffffu, vl, e);
@@ -1493,13 +1556,21 @@ int* band_flags(void* work, int64_t n, int64_t batch) {
   return reinterpret_cast<int*>(static_cast<char*>(work) + ws.band);
 }
 
+// phase (the APSP pipelines, M built from bits as I - gamma A): 1 = classify
+// only, before K1 (patterns, dense-wide lists, sparse-first-step counts; the
+// matrices whose first step is sparse are returned in *s0bad_out as
+// s0bad[m] == 0 with flags[m] == 2, and K1 builds only their block M_00);
+// 2 = the inversion after K1 (classification skipped); 0 = both, M given.
+// m_gammas: the gains of M = I - gamma A (phases 1 and 2), else nullptr.
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                    rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits = nullptr, int64_t n_bits = 0,
-                   bool band_ready = false) {
+                   bool band_ready = false, int phase = 0, const double* m_gammas = nullptr,
+                   int** s0bad_out = nullptr) {
   std::lock_guard<std::mutex> guard(g_enqueue);
+  if (s0bad_out) *s0bad_out = nullptr;
   if (batch == 1 && n >= wide_min_n() && n % (2 * NB) == 0 && a && work && info && lda >= n && !(lda & 1) &&
       !((uintptr_t)a & 15) && !((uintptr_t)work & 15))
-    return invert_wide(a, n, lda, work, info, st);
+    return phase == 1 ? RDB_OK : invert_wide(a, n, lda, work, info, st);
   const BatchWs ws(n, batch);
   char* const wb = static_cast<char*>(work);
   const bool use_plan = batch > 1 && ws.has_plan() && skip_enabled() && a && work && n % NB == 0 &&
@@ -1511,7 +1582,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   if (band_ready && !use_band) return RDB_EINVAL;  // K1 has skipped the off-band blocks: must not run GJ on them
   int* nonband = use_band ? reinterpret_cast<int*>(wb + ws.band) : nullptr;
   double* band_ws = use_band ? reinterpret_cast<double*>(wb + ws.band_ws) : nullptr;
-  if (use_plan) {
+  if (use_plan && phase != 2) {
     if (cudaMemsetAsync(pat, 0, (size_t)(batch * 2 * ntl * pld), st) != cudaSuccess) return RDB_ECUDA;
     if (use_band && !band_ready) {
       const int rc = band_detect(bits, n_bits, batch, nonband, st);
@@ -1548,6 +1619,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   DwPart dwp[MAX_PARTS];
   const bool use_s0 = use_dw && dw_s0_enabled();
   int* s0flags = use_s0 ? reinterpret_cast<int*>(wb + ws.dws0) : nullptr;
+  const bool synth = use_s0 && m_gammas && bits;  // M = I - gamma A: the sparse step reads the bits, not M
   const int64_t lstride = (int64_t)(band::ws_doubles(n) * sizeof(double));  // lists in the banded scratch
   const int64_t wpr = (n_bits + 31) / 32;
   auto s0_args = [&](const DwPart& d, int i, int parts_) {
@@ -1571,9 +1643,11 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     g.list_s = d.list_s;
     g.list_d = d.list_d;
     g.counts = d.count;
+    g.gam = synth ? m_gammas + i : nullptr;
+    g.gam_stride = parts_;
     return g;
   };
-  if (use_dw) {
+  if (use_dw && phase != 2) {
     if (use_s0 && cudaMemsetAsync(s0flags, 0, (size_t)batch * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
     DwClassifyArgs ca;
     ca.pat = pat;
@@ -1589,6 +1663,22 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       lo += (batch - i + ca.parts - 1) / ca.parts;
     }
     dw_classify_kernel<<<(unsigned)ca.parts, 256, 0, st>>>(ca);
+    if (synth)  // counted now: K1 builds only M_00 of the matrices whose first step is sparse
+      dw_s0_count_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)batch), 512, 0, st>>>(
+          bits, n_bits, (int)n, nonband, s0flags);
+  } else if (use_dw) {
+    int64_t lo = 0;
+    for (int i = 0; i < (split ? parts : 1); ++i) {
+      dwp[i] = ws.dw_part(wb, i, lo, (int)ntl);
+      lo += (batch - i + (split ? parts : 1) - 1) / (split ? parts : 1);
+    }
+    if (use_s0 && !synth && cudaMemsetAsync(s0flags, 0, (size_t)batch * sizeof(int), st) != cudaSuccess)
+      return RDB_ECUDA;
+  }
+  if (phase == 1) {
+    if (s0bad_out && synth) *s0bad_out = s0flags;
+    RDB_LAUNCH_CHECK();
+    return RDB_OK;
   }
   if (split) {
     DevStreams* ds = dev_streams();
