@@ -46,6 +46,7 @@ __global__ void build_m_bits_kernel(const uint32_t* __restrict__ bits, int64_t n
                                     int64_t batch, const double* __restrict__ gammas, double gamma,
                                     double* __restrict__ out, int64_t ldo, int64_t stride_o,
                                     const int* __restrict__ nonband, const int* __restrict__ s0bad) {
+  RDB_TRACE_SCOPE(51);
   // one warp per output row (grid-stride over batch * n_pad rows); lane l
   // writes columns 2l, 2l+1 of every 64-column chunk: 512 B per store wave.
   // nonband (APSP pipelines): a matrix the banded inverse takes (nonband[b] ==
@@ -242,3 +243,11 @@ extern "C" int rdb_edges_to_bits(const int32_t* src, const int32_t* dst, int64_t
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
+
+#ifdef RDB_TRACE
+namespace rdb {
+namespace k1 {
+int trace_attach(void* buf, unsigned cap) { return trace::attach(buf, cap); }
+}  // namespace k1
+}  // namespace rdb
+#endif

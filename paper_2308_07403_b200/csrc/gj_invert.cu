@@ -843,64 +843,62 @@ struct DwPart {
 struct DwClassifyArgs {
   unsigned char* pat;
   int* flags;
-  const int* s0bad;  // per matrix: nonzero = keeps the dense first step (dw_s0_gather_kernel); nullptr: all do
   int64_t batch;
   int nt, parts;
   DwPart part[4];
 };
 
-__global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
+__global__ void __launch_bounds__(1024) dw_classify_kernel(DwClassifyArgs arg) {
   RDB_TRACE_SCOPE(32);
   const int i = blockIdx.x;
-  const int nt = arg.nt, ld = pat_ld(nt);
+  const int nt = arg.nt, ld = pat_ld(nt), wpm = 2 * nt * ld / 4;  // pattern words per matrix
   const int64_t cnt = (arg.batch - i + arg.parts - 1) / arg.parts;
   const DwPart& d = arg.part[i];
-  __shared__ int warp_tot[8], warp_s[8];
-  __shared__ int base, base_s;
-  if (threadIdx.x == 0) base = base_s = 0;
-  __syncthreads();
+  __shared__ int warp_tot[32];
+  __shared__ int base;
+  __shared__ unsigned char dense_s[1024];
+  if (threadIdx.x == 0) base = 0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t l0 = 0; l0 < cnt; l0 += 256) {
-    const int64_t l = l0 + threadIdx.x;
-    const int64_t m = i + (int64_t)arg.parts * l;
-    bool dense = false;
-    if (l < cnt && arg.flags[m] == 1) {
-      // the 2 nt rows of ld bytes as 32-bit words, no early exit (independent loads)
-      const uint32_t* P = reinterpret_cast<const uint32_t*>(arg.pat + m * 2 * nt * ld);
-      const int wpr = ld / 4;
-      dense = true;
-      for (int wi = 0; wi < 2 * nt * wpr; ++wi) {
-        const uint32_t v = P[wi];
-        const int I = (wi / wpr) % nt, J0 = 4 * (wi % wpr);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int J = J0 + b;
-          if (J < nt && J != I && ((v >> (8 * b)) & 0xFFu) != 0xFFu) dense = false;
-        }
-      }
-    }
-    // ordered compaction (block scan of the dense flags)
-    const bool sp = dense && arg.s0bad && !arg.s0bad[m];
-    const unsigned bal = __ballot_sync(0xffffffffu, dense), bal_s = __ballot_sync(0xffffffffu, sp);
-    if (lane == 0) {
-      warp_tot[w] = __popc(bal);
-      warp_s[w] = __popc(bal_s);
+  for (int64_t l0 = 0; l0 < cnt; l0 += 1024) {
+    const int64_t nl = cnt - l0 < 1024 ? cnt - l0 : 1024;
+    __syncthreads();
+    {
+      const int64_t l = l0 + threadIdx.x;
+      dense_s[threadIdx.x] = l < cnt && arg.flags[i + (int64_t)arg.parts * l] == 1;
     }
     __syncthreads();
-    int off = base, off_s = base_s;
-    for (int k = 0; k < w; ++k) {
-      off += warp_tot[k];
-      off_s += warp_s[k];
+    // every (matrix, pattern word) of the chunk across the CTA: a zero strip
+    // off the diagonal clears the matrix's flag
+    for (int64_t e = threadIdx.x; e < nl * wpm; e += 1024) {
+      const int64_t ll = e / wpm;
+      const int wi = (int)(e - ll * wpm);
+      if (!dense_s[ll]) continue;
+      const int64_t m = i + (int64_t)arg.parts * (l0 + ll);
+      const uint32_t v = reinterpret_cast<const uint32_t*>(arg.pat + m * 2 * nt * ld)[wi];
+      const int I = (wi / (ld / 4)) % nt, J0 = 4 * (wi % (ld / 4));
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int J = J0 + b;
+        if (J < nt && J != I && ((v >> (8 * b)) & 0xFFu) != 0xFFu) dense_s[ll] = 0;
+      }
     }
+    __syncthreads();
+    // ordered compaction (block scan of the dense flags)
+    const int64_t l = l0 + threadIdx.x;
+    const int64_t m = i + (int64_t)arg.parts * l;
+    const bool dense = threadIdx.x < nl && dense_s[threadIdx.x];
+    const unsigned bal = __ballot_sync(0xffffffffu, dense);
+    if (lane == 0) warp_tot[w] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int k = 0; k < w; ++k) off += warp_tot[k];
     const int pos = off + __popc(bal & ((1u << lane) - 1));
-    const int pos_s = off_s + __popc(bal_s & ((1u << lane) - 1));
-    if (sp) d.list_s[pos_s] = (int)l;
-    else if (dense) d.list_d[pos - pos_s] = (int)l;  // (dense ones before it) - (sparse ones before it)
     if (dense) {
       arg.flags[m] = 2;
       uint32_t* P = reinterpret_cast<uint32_t*>(arg.pat + m * 2 * nt * ld);
-      for (int e = 0; e < 2 * nt * ld / 4; ++e) P[e] = 0u;
+      for (int e = 0; e < wpm; ++e) P[e] = 0u;
       d.list[pos] = (int)l;
+      d.list_d[pos] = (int)l;  // (the sparse-first-step split refines list_s / list_d)
       for (int k = 0; k < 2; ++k) {
         d.nrp[k * cnt + pos] = (int)(l << 13) | (8 << 6) | (1 - k);
         d.nup[k * 2 * cnt + 2 * pos] = make_int2((int)(l << 12) | ((1 - k) << 6) | (1 - k), 1 | (8 << 20));
@@ -909,20 +907,16 @@ __global__ void __launch_bounds__(256) dw_classify_kernel(DwClassifyArgs arg) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      int tot = 0, tot_s = 0;
-      for (int k = 0; k < 8; ++k) {
-        tot += warp_tot[k];
-        tot_s += warp_s[k];
-      }
+      int tot = 0;
+      for (int k = 0; k < 32; ++k) tot += warp_tot[k];
       base += tot;
-      base_s += tot_s;
     }
-    __syncthreads();
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     d.count[0] = base;
-    d.count[1] = base_s;
-    d.count[2] = base - base_s;
+    d.count[1] = 0;
+    d.count[2] = base;
     d.ncounts[0] = d.ncounts[1] = base;          // nested row panels, steps 0 and 1
     d.ncounts[2] = d.ncounts[3] = 2 * base;      // nested update tiles
   }
@@ -1652,7 +1646,6 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     DwClassifyArgs ca;
     ca.pat = pat;
     ca.flags = nonband;
-    ca.s0bad = nullptr;  // every dense-wide matrix in list_d; the per-part split (after the gather) refines it
     ca.batch = batch;
     ca.nt = (int)ntl;
     ca.parts = split ? parts : 1;
@@ -1662,7 +1655,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       ca.part[i] = dwp[i];
       lo += (batch - i + ca.parts - 1) / ca.parts;
     }
-    dw_classify_kernel<<<(unsigned)ca.parts, 256, 0, st>>>(ca);
+    dw_classify_kernel<<<(unsigned)ca.parts, 1024, 0, st>>>(ca);
     if (synth)  // counted now: K1 builds only M_00 of the matrices whose first step is sparse
       dw_s0_count_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)batch), 512, 0, st>>>(
           bits, n_bits, (int)n, nonband, s0flags);
@@ -2191,9 +2184,20 @@ int trace_attach(void* buf, unsigned cap);
 unsigned trace_count();
 }  // namespace band
 }  // namespace rdb
-extern "C" int rdb_trace_attach(void* buf, unsigned cap) {
-  const unsigned h = cap / 2;
-  if (trace::attach(buf, h) || band::trace_attach(static_cast<trace::Rec*>(buf) + h, cap - h)) return RDB_ECUDA;
+namespace rdb {
+namespace k1 {
+int trace_attach(void* buf, unsigned cap);
+}
+namespace k3 {
+int trace_attach(void* buf, unsigned cap);
+}
+}  // namespace rdb
+extern "C" int rdb_trace_attach(void* buf, unsigned cap) {  // four quarters: K2, banded path, K1, K3
+  const unsigned q = cap / 4;
+  trace::Rec* r = static_cast<trace::Rec*>(buf);
+  if (trace::attach(buf, q) || band::trace_attach(buf ? r + q : nullptr, q) ||
+      k1::trace_attach(buf ? r + 2 * q : nullptr, q) || k3::trace_attach(buf ? r + 3 * q : nullptr, q))
+    return RDB_ECUDA;
   return RDB_OK;
 }
 extern "C" void rdb_trace_counts(unsigned* out) {

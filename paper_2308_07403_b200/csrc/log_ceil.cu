@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
     log_ceil_lean_kernel(const double* __restrict__ y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
                          const double* __restrict__ gammas, double gamma, void* __restrict__ dout, int64_t ldo,
                          int64_t stride_o, unsigned long long* __restrict__ counters) {
+  RDB_TRACE_SCOPE(50);
 #if RDB_K3_MUFU
   const ConstTab tab;  // exact path only
   const int lane = threadIdx.x & 31;
@@ -728,3 +729,11 @@ extern "C" int rdb_log_ceil(const double* y, int64_t n, int64_t ldy, int64_t str
   return rdb::log_ceil(y, n, ldy, stride_y, batch, gammas, gamma, r_out, dceil_out, d32_out, ldo,
                        stride_o, reachable, ldm, counters, static_cast<cudaStream_t>(stream));
 }
+
+#ifdef RDB_TRACE
+namespace rdb {
+namespace k3 {
+int trace_attach(void* buf, unsigned cap) { return trace::attach(buf, cap); }
+}  // namespace k3
+}  // namespace rdb
+#endif

@@ -37,6 +37,9 @@ MODES = {
     "dw_helper_reserve32": {"RDB_GJ_DW_LA_RESERVE": "32"},
     "dw_helper_reserve80": {"RDB_GJ_DW_LA_RESERVE": "80"},
     "dw_helper_reserve100": {"RDB_GJ_DW_LA_RESERVE": "100"},
+    "dw_helper_reserve90": {"RDB_GJ_DW_LA_RESERVE": "90"},
+    "dw_helper_reserve106": {"RDB_GJ_DW_LA_RESERVE": "106"},
+    "dw_helper_reserve120": {"RDB_GJ_DW_LA_RESERVE": "120"},
     "no_split": {"RDB_GJ_SPLIT_MIN": "0"},
     "no_split_no_dw": {"RDB_GJ_SPLIT_MIN": "0", "RDB_GJ_DW": "0"},
     "split3_capped": {"RDB_GJ_SPLIT_PARTS": "3"},
