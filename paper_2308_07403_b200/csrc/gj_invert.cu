@@ -944,62 +944,74 @@ __global__ void __launch_bounds__(1024) dw_classify_kernel(DwClassifyArgs arg) {
 //     block row 0 (as updated) in shared memory per CTA.
 // The lists live in the matrix's slice of the banded path's scratch, which
 // the banded inverse uses only for banded matrices (never dense-wide ones).
-constexpr int S0_CAP = 24;
+// Edges kept per row / column of the step-0 blocks: B0 = 256 (one-level
+// steps, ~5 per row for config 2) or 512 (the two-level path's outer step,
+// ~10 per row); a matrix with more in any row or column keeps the dense step.
+template <int B0>
+struct S0 {
+  static constexpr int CAP = B0 == 256 ? 24 : 32;
+};
+constexpr int S0_CAP = S0<256>::CAP;  // (host restatement: batch.py S0_CAP)
 
-// List layout inside a matrix's slice (R = n - 256 rows / columns outside the
+// List layout inside a matrix's slice (R = n - B0 rows / columns outside the
 // band): row lists row-major (a warp reads one row's entries in one pass),
 // column lists entry-major (consecutive threads read consecutive columns):
-// vals_r [R][CAP] double | vals_c [CAP][R] double | idx_r [R][CAP] u8 |
-// idx_c [CAP][R] u8 | cnt_r [R] u8 | cnt_c [R] u8.
+// vals_r [R][CAP] double | vals_c [CAP][R] double | idx_r [R][CAP] u16 |
+// idx_c [CAP][R] u16 | cnt_r [R] u8 | cnt_c [R] u8.
 struct S0Lists {
   double *vr, *vc;
-  unsigned char *ir, *ic, *nr, *nc;
-  RDB_HOST_DEV S0Lists(void* base, int R) {
+  unsigned short *ir, *ic;
+  unsigned char *nr, *nc;
+  RDB_HOST_DEV S0Lists(void* base, int R, int cap) {
     vr = static_cast<double*>(base);
-    vc = vr + (size_t)S0_CAP * R;
-    ir = reinterpret_cast<unsigned char*>(vc + (size_t)S0_CAP * R);
-    ic = ir + (size_t)S0_CAP * R;
-    nr = ic + (size_t)S0_CAP * R;
+    vc = vr + (size_t)cap * R;
+    ir = reinterpret_cast<unsigned short*>(vc + (size_t)cap * R);
+    ic = ir + (size_t)cap * R;
+    nr = reinterpret_cast<unsigned char*>(ic + (size_t)cap * R);
     nc = nr + R;
   }
+  static size_t bytes(int R, int cap) { return (size_t)R * cap * (2 * sizeof(double) + 4) + 2 * (size_t)R; }
 };
 
 struct S0Args {
-  double* a;
+  double* a;              // the (sub)problem: matrix l at a + l * pstride, n x n, row pitch lda
   int64_t lda, pstride;
   char* lists;            // part-local matrix l's lists at lists + l * lstride
   int64_t lstride;
-  int n;                  // n_pad
+  int n;                  // the problem's size (multiple of 256)
   const int* list;        // list_s
   const int* count;       // count[1] = entries of list_s
-  int* colcnt;
+  int* colcnt;            // one-level path: the step-0 counts of the dense tiles (nullptr: none)
   int* rowcnt;
   // gather / split (dw_s0_gather_kernel, dw_s0_split_kernel)
   const uint32_t* bits;   // part-local matrix l at bits + l * bstride (rows of wpr words)
-  int64_t bstride, n_bits;
-  int* bad;               // part-local matrix l's flag at bad[l * bad_stride]
+  int64_t bstride, wpr, n_bits;  // n_bits: vertices inside the problem (<= n)
+  int* bad;               // part-local matrix l's flags at bad[l * bad_stride] (bit bad_bit: dense step)
   int64_t bad_stride;
-  const int* dw_list;     // the part's dense-wide list (count[0] entries)
+  int bad_bit;
+  const int* n_list;      // entries of the part's dense-wide list
+  const int* dw_list;     // the part's dense-wide list
   int* list_s;
   int* list_d;
-  int* counts;            // count[1], count[2] written by the split
+  int* counts;            // counts[0..2] written by the split (list, list_s, list_d entries)
   // M built from the adjacency bits (the APSP pipelines): part-local matrix l
   // is I - gam[l * gam_stride] A; the gather then takes the edge values from
   // the gain, and the sparse step writes rows outside the band from the bits
-  // (K1 built only the 256 x 256 block M_00 of these matrices). nullptr: M is
-  // the caller's, read from memory.
+  // (K1 built only what the first band inverse reads). nullptr: M is the
+  // caller's, read from memory.
   const double* gam;
   int64_t gam_stride;
 };
 
 // The edges of row or column B0 + t (thread's role) into / out of block 0, in
-// increasing k, into ps (at most S0_CAP kept); returns the total count.
+// increasing k, into ps (at most CAP kept); returns the total count.
+template <int B0>
 RDB_DEV int s0_positions(const uint32_t* bm, int64_t wpr, int64_t n_bits, int nb0, bool col, int t, int tl,
-                         const uint32_t (*sw)[9], unsigned char* ps) {
-  constexpr int B0 = 2 * NB;
+                         const uint32_t (*sw)[9], unsigned short* ps) {
+  constexpr int CAP = S0<B0>::CAP;
   const int w0 = (nb0 + 31) / 32;
   int c = 0;
-  if (!col) {  // row i = B0 + t: edges k < nb0 (the row's 8 words loaded together)
+  if (!col) {  // row i = B0 + t: edges k < nb0 (the row's words loaded together)
     const int64_t i = B0 + t;
     uint32_t wr[B0 / 32];
 #pragma unroll
@@ -1010,7 +1022,7 @@ RDB_DEV int s0_positions(const uint32_t* bm, int64_t wpr, int64_t n_bits, int nb
       while (w) {
         const int k = 32 * q + __ffs(w) - 1;
         w &= w - 1;
-        if (c < S0_CAP) ps[c] = (unsigned char)k;
+        if (c < CAP) ps[c] = (unsigned short)k;
         ++c;
       }
     }
@@ -1018,7 +1030,7 @@ RDB_DEV int s0_positions(const uint32_t* bm, int64_t wpr, int64_t n_bits, int nb
     const int q = tl >> 5, b = tl & 31;
     for (int k = 0; k < nb0; ++k)
       if ((sw[k][q] >> b) & 1) {
-        if (c < S0_CAP) ps[c] = (unsigned char)k;
+        if (c < CAP) ps[c] = (unsigned short)k;
         ++c;
       }
   }
@@ -1026,8 +1038,9 @@ RDB_DEV int s0_positions(const uint32_t* bm, int64_t wpr, int64_t n_bits, int nb
 }
 
 // bits words of rows k < nb0 for the 256-column chunk x (columns B0 + 256 x ..)
+template <int B0>
 RDB_DEV void s0_stage_words(const uint32_t* bm, int64_t wpr, int nb0, uint32_t (*sw)[9]) {
-  const int64_t q0 = (2 * NB + (int64_t)blockIdx.x * 256) / 32;
+  const int64_t q0 = (B0 + (int64_t)blockIdx.x * 256) / 32;
   for (int e = threadIdx.x; e < nb0 * 8; e += blockDim.x) {
     const int k = e >> 3, q = e & 7;
     sw[k][q] = q0 + q < wpr ? bm[k * wpr + q0 + q] : 0u;
@@ -1035,60 +1048,63 @@ RDB_DEV void s0_stage_words(const uint32_t* bm, int64_t wpr, int nb0, uint32_t (
 }
 
 // Before K1 (APSP pipelines, M from bits): grid (ceil(R / 256), batch), 512
-// threads, dense-wide matrices (flags == 2): bad[m] |= 1 when a row of block
-// column 0 or a column of block row 0 has more than S0_CAP edges. The others
-// take the sparse first step, and K1 builds only their block M_00.
-__global__ void __launch_bounds__(512) dw_s0_count_kernel(const uint32_t* __restrict__ bits, int64_t n_bits, int n,
-                                                          const int* __restrict__ flags, int* __restrict__ bad) {
-  constexpr int B0 = 2 * NB;
+// threads, dense-wide matrices (flags == 2), the problem = the leading n x n
+// block: bad[m] |= bit when a row of block column 0 or a column of block row 0
+// (B0 wide) has more than CAP edges.
+template <int B0>
+__global__ void __launch_bounds__(512) dw_s0_count_kernel(const uint32_t* __restrict__ bits, int64_t n_bits,
+                                                          int n, const int* __restrict__ flags, int* __restrict__ bad,
+                                                          int bit) {
   const int64_t m = blockIdx.y;
   if (flags[m] != 2) return;
   const int R = n - B0;
   const int64_t wpr = (n_bits + 31) / 32;
   const uint32_t* bm = bits + m * n_bits * wpr;
-  const int nb0 = (int)(n_bits < B0 ? n_bits : B0);
+  const int64_t nb = n_bits < n ? n_bits : n;
+  const int nb0 = (int)(nb < B0 ? nb : B0);
   const bool col = threadIdx.x >= 256;
   const int tl = threadIdx.x & 255, t = (int)blockIdx.x * 256 + tl;
   __shared__ uint32_t sw[B0][9];
-  __shared__ unsigned char pos[512][S0_CAP];
-  s0_stage_words(bm, wpr, nb0, sw);
+  __shared__ unsigned short pos[512][S0<B0>::CAP];
+  s0_stage_words<B0>(bm, wpr, nb0, sw);
   __syncthreads();
   if (t >= R) return;
-  if (s0_positions(bm, wpr, n_bits, nb0, col, t, tl, sw, pos[threadIdx.x]) > S0_CAP) atomicOr(bad + m, 1);
+  // (columns past the problem's n are outside: the chunk covers B0 + 256 x + [0, 256) < n)
+  if (s0_positions<B0>(bm, wpr, nb, nb0, col, t, tl, sw, pos[threadIdx.x]) > S0<B0>::CAP) atomicOr(bad + m, bit);
 }
 
 // grid (ceil(R / 256), list capacity), 512 threads, for the part's
-// dense-wide matrices: thread t < 256 gathers row 256 + 256 x + t, thread
-// 256 + t column 256 + 256 x + t; bad |= 1 when one has more than S0_CAP
+// dense-wide matrices: thread t < 256 gathers row B0 + 256 x + t, thread
+// 256 + t column B0 + 256 x + t; bad |= bit when one has more than CAP
 // edges. Runs on the part's side stream beside the first band inverse.
+template <int B0>
 __global__ void __launch_bounds__(512, 2) dw_s0_gather_kernel(S0Args g) {
   RDB_TRACE_SCOPE(33);
-  constexpr int B0 = 2 * NB;
-  if ((int)blockIdx.y >= g.counts[0]) return;
+  constexpr int CAP = S0<B0>::CAP;
+  if ((int)blockIdx.y >= *g.n_list) return;
   const int l = g.dw_list[blockIdx.y];
   const int n = g.n;
-  const int64_t n_bits = g.n_bits, lda = g.lda;
+  const int64_t n_bits = g.n_bits, lda = g.lda, wpr = g.wpr;
   const int R = n - B0;
-  const int64_t wpr = (n_bits + 31) / 32;
   const uint32_t* bm = g.bits + (int64_t)l * g.bstride;
   const double* A = g.a + (int64_t)l * g.pstride;
-  const S0Lists L(g.lists + (int64_t)l * g.lstride, R);
+  const S0Lists L(g.lists + (int64_t)l * g.lstride, R, CAP);
   const int nb0 = (int)(n_bits < B0 ? n_bits : B0);
   const bool col = threadIdx.x >= 256;
   const int tl = threadIdx.x & 255;
   const int t = (int)blockIdx.x * 256 + tl;  // row / column index - B0
   __shared__ uint32_t sw[B0][9];             // the chunk's 8 words of rows k < nb0 (padded)
-  __shared__ unsigned char pos[512][S0_CAP]; // edge positions, then one batch of value loads
-  s0_stage_words(bm, wpr, nb0, sw);
+  __shared__ unsigned short pos[512][CAP];   // edge positions, then one batch of value loads
+  s0_stage_words<B0>(bm, wpr, nb0, sw);
   __syncthreads();
   if (t >= R) return;
-  unsigned char* ps = pos[threadIdx.x];
-  const int c = s0_positions(bm, wpr, n_bits, nb0, col, t, tl, sw, ps);
-  const int nc = c < S0_CAP ? c : S0_CAP;
+  unsigned short* ps = pos[threadIdx.x];
+  const int c = s0_positions<B0>(bm, wpr, n_bits, nb0, col, t, tl, sw, ps);
+  const int nc = c < CAP ? c : CAP;
   const double* src = col ? A + B0 + t : A + (int64_t)(B0 + t) * lda;  // column: row k at src + k lda
   const int64_t step = col ? lda : 1;
   const double ng = g.gam ? -g.gam[(int64_t)l * g.gam_stride] : 0.0;  // M from bits: every edge is -gamma
-  constexpr int H = S0_CAP / 2;
+  constexpr int H = 12;
   for (int e0 = 0; e0 < nc; e0 += H) {  // H independent loads at a time (one batch for most)
     double v[H];
 #pragma unroll
@@ -1097,8 +1113,8 @@ __global__ void __launch_bounds__(512, 2) dw_s0_gather_kernel(S0Args g) {
     for (int e = 0; e < H; ++e)
       if (e0 + e < nc) {
         if (!col) {
-          L.ir[(size_t)t * S0_CAP + e0 + e] = ps[e0 + e];
-          L.vr[(size_t)t * S0_CAP + e0 + e] = v[e];
+          L.ir[(size_t)t * CAP + e0 + e] = ps[e0 + e];
+          L.vr[(size_t)t * CAP + e0 + e] = v[e];
         } else {
           L.ic[(size_t)(e0 + e) * R + t] = ps[e0 + e];
           L.vc[(size_t)(e0 + e) * R + t] = v[e];
@@ -1106,22 +1122,22 @@ __global__ void __launch_bounds__(512, 2) dw_s0_gather_kernel(S0Args g) {
       }
   }
   (col ? L.nc : L.nr)[t] = (unsigned char)nc;
-  if (!g.gam && c > S0_CAP) atomicOr(g.bad + (int64_t)l * g.bad_stride, 1);  // (M from bits: counted before K1)
+  if (!g.gam && c > CAP) atomicOr(g.bad + (int64_t)l * g.bad_stride, g.bad_bit);  // (M from bits: counted before K1)
 }
 
-// One CTA: the part's dense-wide list split by the gather's flags into
-// list_s (sparse first step) and list_d, both in list order.
+// One CTA: the part's dense-wide list split by the flags' bit into list_s
+// (sparse first step) and list_d, both in list order.
 __global__ void __launch_bounds__(1024) dw_s0_split_kernel(S0Args g) {
   __shared__ int wt[32], ws[32];
   __shared__ int base, base_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) base = base_s = 0;
   __syncthreads();
-  const int cnt = g.counts[0];
+  const int cnt = *g.n_list;
   for (int p0 = 0; p0 < cnt; p0 += 1024) {
     const int p = p0 + threadIdx.x;
     const int l = p < cnt ? g.dw_list[p] : 0;
-    const bool in = p < cnt, sp = in && !g.bad[(int64_t)l * g.bad_stride];
+    const bool in = p < cnt, sp = in && !(g.bad[(int64_t)l * g.bad_stride] & g.bad_bit);
     const unsigned bi = __ballot_sync(0xffffffffu, in), bs = __ballot_sync(0xffffffffu, sp);
     if (lane == 0) {
       wt[w] = __popc(bi);
@@ -1146,6 +1162,7 @@ __global__ void __launch_bounds__(1024) dw_s0_split_kernel(S0Args g) {
     __syncthreads();
   }
   if (threadIdx.x == 0) {
+    g.counts[0] = base;
     g.counts[1] = base_s;
     g.counts[2] = base - base_s;
   }
@@ -1154,19 +1171,20 @@ __global__ void __launch_bounds__(1024) dw_s0_split_kernel(S0Args g) {
 // A_0J = D A_0J: rows 8 b .. 8 b + 7 of block row 0 (D's rows in shared
 // memory, transposed: an edge k reads Dt[k][0..7] as 4 16-byte loads; row
 // pitch 10 doubles), every column outside the band (thread t: columns
-// 256 + t + 256 q). Small register and shared-memory footprint: many CTAs
-// per SM hide the list loads' latency. grid (32, list capacity).
+// B0 + t + 256 q). Small register and shared-memory footprint: many CTAs
+// per SM hide the list loads' latency. grid (B0 / 8, list capacity).
+template <int B0>
 __global__ void __launch_bounds__(256, 4) dw_s0_row_kernel(S0Args g) {
   RDB_TRACE_SCOPE(6);
-  constexpr int B0 = 2 * NB, RB = 8;
+  constexpr int RB = 8, CAP = S0<B0>::CAP;
   if ((int)blockIdx.y >= g.count[1]) return;
   const int l = g.list[blockIdx.y];
   double* A = g.a + (int64_t)l * g.pstride;
   const int R = g.n - B0;
-  const S0Lists L(g.lists + (int64_t)l * g.lstride, R);
+  const S0Lists L(g.lists + (int64_t)l * g.lstride, R, CAP);
   const int tid = threadIdx.x, r0 = (int)blockIdx.x * RB;
   const int nt = g.n / NB;
-  if (blockIdx.x == 0 && tid < nt) {  // the step-0 counts the dense tiles would have signalled
+  if (g.colcnt && blockIdx.x == 0 && tid < nt) {  // the step-0 counts the dense tiles would have signalled
     g.colcnt[(int64_t)l * nt + tid] = tid >= 2 ? 2 : 0;
     g.rowcnt[(int64_t)l * nt + tid] = tid >= 2 ? nt : 0;
   }
@@ -1199,14 +1217,15 @@ __global__ void __launch_bounds__(256, 4) dw_s0_row_kernel(S0Args g) {
 // row: its edge list in one load (lane e holds entry e), then passes over
 // 256 columns (4 16-byte chunks per lane). Low register count: 4 CTAs per SM
 // keep enough loads in flight. grid ((r1 - r0) / 8, list capacity).
+template <int B0>
 __global__ void __launch_bounds__(256, 4) dw_s0_update_kernel(S0Args g, int r0, int r1) {
   RDB_TRACE_SCOPE(7);
-  constexpr int B0 = 2 * NB;
+  constexpr int CAP = S0<B0>::CAP;
   if ((int)blockIdx.y >= g.count[1]) return;
   const int l = g.list[blockIdx.y];
   double* A = g.a + (int64_t)l * g.pstride;
   const int R = g.n - B0;
-  const S0Lists L(g.lists + (int64_t)l * g.lstride, R);
+  const S0Lists L(g.lists + (int64_t)l * g.lstride, R, CAP);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = r0 + (int)blockIdx.x * 8 + warp;
   if (i >= r1) return;
@@ -1215,13 +1234,12 @@ __global__ void __launch_bounds__(256, 4) dw_s0_update_kernel(S0Args g, int r0, 
   int kl = 0;
   double vl = 0.0;
   if (lane < cnt) {
-    kl = L.ir[(size_t)t * S0_CAP + lane];
-    vl = L.vr[(size_t)t * S0_CAP + lane];
+    kl = L.ir[(size_t)t * CAP + lane];
+    vl = L.vr[(size_t)t * CAP + lane];
   }
   double* Ai = A + (int64_t)i * g.lda;
   // M from bits: M'_ij = [i == j] - gamma [edge i -> j] (j >= B0), no read of M
-  const int64_t wpr = (g.n_bits + 31) / 32;
-  const uint32_t* brow = g.bits + (int64_t)l * g.bstride + (int64_t)i * wpr;
+  const uint32_t* brow = g.bits + (int64_t)l * g.bstride + (int64_t)i * g.wpr;
   const double ng = g.gam ? -g.gam[(int64_t)l * g.gam_stride] : 0.0;
   for (int jb = 2 * lane; jb < g.n; jb += 256) {  // n % 256 == 0
     double2 o[4];
@@ -1231,7 +1249,7 @@ __global__ void __launch_bounds__(256, 4) dw_s0_update_kernel(S0Args g, int r0, 
       if (j < B0) {
         o[u] = make_double2(0.0, 0.0);
       } else if (g.gam) {
-        const uint32_t wd = (i < g.n_bits && (j >> 5) < wpr) ? __ldg(brow + (j >> 5)) : 0u;
+        const uint32_t wd = (i < g.n_bits && j < g.n_bits) ? __ldg(brow + (j >> 5)) : 0u;
         o[u].x = ((wd >> (j & 31)) & 1u) && j < g.n_bits ? ng : 0.0;
         o[u].y = ((wd >> ((j + 1) & 31)) & 1u) && j + 1 < g.n_bits ? ng : 0.0;
         if (j == i) o[u].x = 1.0;
@@ -1258,8 +1276,15 @@ __global__ void __launch_bounds__(256, 4) dw_s0_update_kernel(S0Args g, int r0, 
   }
 }
 
+template <int B0>
+static void launch_s0_gather(const S0Args& g, int64_t pcnt, cudaStream_t st) {
+  dw_s0_gather_kernel<B0><<<dim3((unsigned)((g.n - B0 + 255) / 256), (unsigned)pcnt), 512, 0, st>>>(g);
+  dw_s0_split_kernel<<<1, 1024, 0, st>>>(g);
+}
+
+template <int B0>
 static void launch_s0_update(const S0Args& g, int r0, int r1, int64_t pcnt, cudaStream_t st) {
-  dw_s0_update_kernel<<<dim3((unsigned)((r1 - r0) / 8), (unsigned)pcnt), 256, 0, st>>>(g, r0, r1);
+  if (r1 > r0) dw_s0_update_kernel<B0><<<dim3((unsigned)((r1 - r0) / 8), (unsigned)pcnt), 256, 0, st>>>(g, r0, r1);
 }
 
 static bool dw_helper();
@@ -1309,8 +1334,7 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
       cudaEventRecord(ev_fork, st);
       cudaStreamWaitEvent(side, ev_fork, 0);
     }
-    dw_s0_gather_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)pcnt), 512, 0, gs>>>(*s0);
-    dw_s0_split_kernel<<<1, 1024, 0, gs>>>(*s0);
+    launch_s0_gather<2 * NB>(*s0, pcnt, gs);
     if (side) cudaEventRecord(ev_join, side);
   }
 #ifndef RDB_EXP_NO_NESTED
@@ -1326,14 +1350,14 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
     const bool sp = s0 && p == 0;
     const int* list = sp ? d.list_d : d.list;
     const int* list_count = sp ? d.count + 2 : d.count;
-    if (sp) dw_s0_row_kernel<<<dim3(2 * NB / 8, (unsigned)pcnt), 256, 0, st>>>(*s0);
+    if (sp) dw_s0_row_kernel<2 * NB><<<dim3(2 * NB / 8, (unsigned)pcnt), 256, 0, st>>>(*s0);
     WBRowSched rs{a, lda, pstride, nt, p0t, p, list, list_count, d.colcnt, dyn};
 #ifndef RDB_EXP_NO_WBROW  // timing experiments only (wrong results)
     gj_wb_row_kernel<<<persistent_grid(pcnt * (nt - 2) * 2), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, rs);
 #endif
     // sparse step 0, rows of the next band first (its inverse can then start)
-    if (sp) launch_s0_update(*s0, 2 * NB, 4 * NB, pcnt, st);
-    if (sp && !ahead && n > 4 * NB) launch_s0_update(*s0, 4 * NB, (int)n, pcnt, st);
+    if (sp) launch_s0_update<2 * NB>(*s0, 2 * NB, 4 * NB, pcnt, st);
+    if (sp && !ahead) launch_s0_update<2 * NB>(*s0, 4 * NB, (int)n, pcnt, st);
     WBUpdateSched us{a, lda, pstride, nt, p0t, p, list, list_count, d.rowcnt, dyn ? dyn + 1 : nullptr};
     if (ahead) {
       us.part = 1;
@@ -1349,7 +1373,7 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
       cudaEventRecord(ev_join, side);
       us.part = 2;
       if (sp && n > 4 * NB)  // the other rows of the sparse step, beside the next band's inverse
-        launch_s0_update(*s0, 4 * NB, (int)n, pcnt, st);
+        launch_s0_update<2 * NB>(*s0, 4 * NB, (int)n, pcnt, st);
     }
     const unsigned full = persistent_grid(pcnt * (nt - 2) * nt);
     unsigned ugrid = full, helper = 0;
@@ -1630,9 +1654,12 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     g.rowcnt = d.rowcnt;
     g.bits = bits + (int64_t)i * n_bits * wpr;
     g.bstride = parts_ * n_bits * wpr;
+    g.wpr = wpr;
     g.n_bits = n_bits;
     g.bad = s0flags + i;
     g.bad_stride = parts_;
+    g.bad_bit = 1;
+    g.n_list = d.count;
     g.dw_list = d.list;
     g.list_s = d.list_s;
     g.list_d = d.list_d;
@@ -1657,8 +1684,8 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     }
     dw_classify_kernel<<<(unsigned)ca.parts, 1024, 0, st>>>(ca);
     if (synth)  // counted now: K1 builds only M_00 of the matrices whose first step is sparse
-      dw_s0_count_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)batch), 512, 0, st>>>(
-          bits, n_bits, (int)n, nonband, s0flags);
+      dw_s0_count_kernel<2 * NB><<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)batch), 512, 0, st>>>(
+          bits, n_bits, (int)n, nonband, s0flags, 1);
   } else if (use_dw) {
     int64_t lo = 0;
     for (int i = 0; i < (split ? parts : 1); ++i) {
@@ -1704,8 +1731,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       const S0Args g0 = use_s0 ? s0_args(dwp[i], i, parts) : S0Args{};
       const bool s0_aside = use_s0 && plan_aside;
       if (s0_aside) {
-        dw_s0_gather_kernel<<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)cnt), 512, 0, plan_st>>>(g0);
-        dw_s0_split_kernel<<<1, 1024, 0, plan_st>>>(g0);
+        launch_s0_gather<2 * NB>(g0, cnt, plan_st);
         cudaEventRecord(ds->s0_ready[i], plan_st);
       }
       rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, plan_st, 1, 0,
