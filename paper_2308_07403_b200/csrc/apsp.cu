@@ -11,11 +11,12 @@
 namespace rdb {
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                    rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits, int64_t n_bits, bool band_ready,
-                   int phase, const double* m_gammas, int** s0bad_out);
+                   int phase, const double* m_gammas, int** s0bad_out, int* s0_levels_out);
 int* band_flags(void* work, int64_t n, int64_t batch);
 int band_detect(const uint32_t* bits, int64_t n, int64_t batch, int* nonband, cudaStream_t st);
 int build_m_bits_banded(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch, const double* gammas,
-                        double* out, int64_t stride_o, const int* nonband, cudaStream_t st, const int* s0bad);
+                        double* out, int64_t stride_o, const int* nonband, cudaStream_t st, const int* s0bad,
+                        int s0_w);
 
 // K1 and K2 of the pipelines: the matrices are classified from the bits
 // first (banded, dense-wide with a sparse first step, other), so K1 writes
@@ -30,20 +31,24 @@ static int build_and_invert(const uint32_t* bits, int64_t n, int64_t n_pad, int6
   if (nonband && e && e[0] == '0') {
     int rc = band_detect(bits, n, batch, nonband, st);
     if (rc) return rc;
-    rc = build_m_bits_banded(bits, n, n_pad, batch, gammas, mwork, stride, nonband, st, nullptr);
+    rc = build_m_bits_banded(bits, n, n_pad, batch, gammas, mwork, stride, nonband, st, nullptr, 0);
     if (rc) return rc;
-    return invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, true, 0, nullptr, nullptr);
+    return invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, true, 0, nullptr, nullptr,
+                          nullptr);
   }
+  int levels = 1;
   if (nonband) {
     int rc = band_detect(bits, n, batch, nonband, st);
     if (rc) return rc;
-    rc = invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, true, 1, gammas, &s0bad);
+    rc = invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, true, 1, gammas, &s0bad,
+                        &levels);
     if (rc) return rc;
   }
-  int rc = build_m_bits_banded(bits, n, n_pad, batch, gammas, mwork, stride, nonband, st, s0bad);
+  int rc = build_m_bits_banded(bits, n, n_pad, batch, gammas, mwork, stride, nonband, st, s0bad,
+                               levels == 2 ? (int)(n_pad / 2) : 0);
   if (rc) return rc;
   return invert_batched(mwork, n_pad, n_pad, stride, batch, work, info, st, bits, n, nonband != nullptr,
-                        nonband ? 2 : 0, gammas, nullptr);
+                        nonband ? 2 : 0, gammas, nullptr, nullptr);
 }
 int log_ceil_d8(const double* y, int64_t n, int64_t ldy, int64_t stride_y, int64_t batch,
                 const double* gammas, double gamma, uint8_t* d8_out, int64_t ldo, int64_t stride_o,

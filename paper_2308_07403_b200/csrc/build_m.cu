@@ -45,7 +45,7 @@ __global__ void build_m_kernel(const double* __restrict__ w, int64_t ldw, int64_
 __global__ void build_m_bits_kernel(const uint32_t* __restrict__ bits, int64_t n, int64_t n_pad,
                                     int64_t batch, const double* __restrict__ gammas, double gamma,
                                     double* __restrict__ out, int64_t ldo, int64_t stride_o,
-                                    const int* __restrict__ nonband, const int* __restrict__ s0bad) {
+                                    const int* __restrict__ nonband, const int* __restrict__ s0bad, int s0_w) {
   RDB_TRACE_SCOPE(51);
   // one warp per output row (grid-stride over batch * n_pad rows); lane l
   // writes columns 2l, 2l+1 of every 64-column chunk: 512 B per store wave.
@@ -62,12 +62,21 @@ __global__ void build_m_bits_kernel(const uint32_t* __restrict__ bits, int64_t n
     const uint32_t* row = bits + (b * n + i) * wpr;
     double* O = out + b * stride_o + i * ldo;
     int64_t jb = 0, je = n_pad;
-    // dense-wide matrix with a sparse first step (s0bad[b] == 0, flags 2): only
-    // the 256 x 256 block M_00 (the first band inverse); the step writes the
-    // rest from the bits (gj_invert.cu dw_s0_*)
-    if (s0bad && nonband[b] == 2 && !s0bad[b]) {
-      if (i >= 2 * NB) continue;
-      je = 2 * NB;
+    // dense-wide matrix with a sparse first step (flags 2, s0bad bit 1 clear):
+    // only the 256 x 256 block M_00 (the first band inverse); the step writes
+    // the rest from the bits (gj_invert.cu dw_s0_*). Two-level path (s0_w =
+    // W > 0): bit 2 clear = a sparse outer step, so only the leading W x W
+    // block (with bit 1 clear: only its 256 x 256 block M_00).
+    if (s0bad && nonband[b] == 2) {
+      const int f = s0bad[b];
+      int64_t lim = n_pad;
+      if (s0_w > 0) {
+        if (!(f & 2)) lim = (f & 1) ? s0_w : 2 * NB;
+      } else if (!(f & 1)) {
+        lim = 2 * NB;
+      }
+      if (i >= lim) continue;
+      je = lim;
     }
     if (nonband && !nonband[b]) {
       const int64_t bi = i / 32;
@@ -176,7 +185,7 @@ extern "C" int rdb_build_m_bits(const uint32_t* bits, int64_t n, int64_t n_pad, 
   const int64_t rows = n_pad * batch;
   const int64_t blocks = (rows + 7) / 8 < 148 * 32 ? (rows + 7) / 8 : 148 * 32;
   build_m_bits_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      bits, n, n_pad, batch, gammas, gamma, out, ldo, stride_o, nullptr, nullptr);
+      bits, n, n_pad, batch, gammas, gamma, out, ldo, stride_o, nullptr, nullptr, 0);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
@@ -186,7 +195,8 @@ namespace rdb {
 // rows only for the matrices the banded inverse takes, the block M_00 only
 // for the dense-wide matrices whose first step is sparse (s0bad, may be null).
 int build_m_bits_banded(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t batch, const double* gammas,
-                        double* out, int64_t stride_o, const int* nonband, cudaStream_t st, const int* s0bad) {
+                        double* out, int64_t stride_o, const int* nonband, cudaStream_t st, const int* s0bad,
+                        int s0_w) {
   if (!nonband) return rdb_build_m_bits(bits, n, n_pad, batch, gammas, 0.0, out, n_pad, stride_o, st);
   if (!bits || !out || !gammas || n <= 0 || n_pad < n || n_pad % 64 || batch <= 0 || batch > 65535 ||
       ((uintptr_t)out & 15))
@@ -194,7 +204,7 @@ int build_m_bits_banded(const uint32_t* bits, int64_t n, int64_t n_pad, int64_t 
   const int64_t rows = n_pad * batch;
   const int64_t blocks = (rows + 7) / 8 < 148 * 32 ? (rows + 7) / 8 : 148 * 32;
   build_m_bits_kernel<<<(unsigned)blocks, 256, 0, st>>>(bits, n, n_pad, batch, gammas, 0.0, out, n_pad, stride_o,
-                                                        nonband, s0bad);
+                                                        nonband, s0bad, s0_w);
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }

@@ -822,6 +822,115 @@ __global__ void __launch_bounds__(EC::THREADS, 1)
   eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
 }
 
+// ---- two-level dense-wide path (n = 1024): two outer steps of width W = n/2
+// (bt = W / 128 tiles), their band inverses W x W dense-wide inversions
+// (dw_part on the sub-block). Outer step p, band B = tiles [b0t, b0t + bt):
+//   row panel: A_BJ = D A_BJ (J outside B), tiles (r, J), K = W, in place on
+//     the B operand they share: each signals when its operands have landed,
+//     stores when all bt have (column counters, target bt);
+//   update: A_IJ += -(A_IB A_BJ) (J outside B, reduce) and A_IB = -(A_IB D)
+//     (store, after all nt tiles of row I have loaded A_IB: row counters,
+//     target nt).
+// Each column / row block takes part in one outer row panel / update, so the
+// counters (zeroed before each step) need no step arithmetic.
+struct W2RowSched {
+  double* a;
+  int64_t lda, stride;
+  int nt, b0t, bt;
+  const int* list;
+  const int* list_count;
+  int* colcnt;
+  int* dyn;
+  RDB_DEV int count() const { return *list_count * (nt - bt) * bt; }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int r = t % bt, q = t / bt;
+    const int li = q / (nt - bt), jj = q - li * (nt - bt);
+    const int J = jj + (jj >= b0t ? bt : 0);
+    const int g = list[li];
+    double* A = a + (int64_t)g * stride;
+    eng::Tile T;
+    T.a_col = b0t * NB;  // A operand: D rows r (128 x W)
+    T.a_row = (b0t + r) * NB;
+    T.a_mat = g;
+    T.b = A + (int64_t)b0t * NB * lda + (int64_t)J * NB;  // A_BJ, W x 128
+    T.ldb = lda;
+    T.c_col = J * NB;
+    T.c_row = (b0t + r) * NB;
+    T.c_mat = g;
+    T.nk = bt * NB / eng::BK;
+    T.mode = eng::EPI_STORE;
+    T.neg = 0;
+    int* c = colcnt + (int64_t)g * nt + J;
+    T.signal = c;
+    T.wait = c;
+    T.wait_target = bt;
+    return T;
+  }
+};
+
+struct W2UpdateSched {
+  double* a;
+  int64_t lda, stride;
+  int nt, b0t, bt;
+  const int* list;
+  const int* list_count;
+  int* rowcnt;
+  int* dyn;
+  int dyn_ctas = 0;
+  RDB_DEV int count() const { return *list_count * (nt - bt) * nt; }
+  RDB_DEV eng::Tile tile(int t) const {
+    const int pm = (nt - bt) * nt;
+    const int li = t / pm, rem = t - li * pm;
+    const int ri = rem / nt, jj = rem - ri * nt;
+    const int I = ri + (ri >= b0t ? bt : 0);
+    const int g = list[li];
+    double* A = a + (int64_t)g * stride;
+    eng::Tile T;
+    T.a_col = b0t * NB;  // A operand: A_IB, 128 x W
+    T.a_row = I * NB;
+    T.a_mat = g;
+    T.c_row = I * NB;
+    T.c_mat = g;
+    T.nk = bt * NB / eng::BK;
+    T.neg = 1;
+    T.ldb = lda;
+    int* c = rowcnt + (int64_t)g * nt + I;
+    T.signal = c;
+    if (jj < nt - bt) {
+      const int J = jj + (jj >= b0t ? bt : 0);
+      T.b = A + (int64_t)b0t * NB * lda + (int64_t)J * NB;  // the new row panel A_BJ
+      T.c_col = J * NB;
+      T.mode = eng::EPI_REDUCE;
+      T.wait = nullptr;
+      T.wait_target = 0;
+    } else {
+      const int h = jj - (nt - bt);
+      T.b = A + (int64_t)b0t * NB * lda + (int64_t)(b0t + h) * NB;  // columns h of D
+      T.c_col = (b0t + h) * NB;
+      T.mode = eng::EPI_STORE;
+      T.wait = c;
+      T.wait_target = nt;
+    }
+    return T;
+  }
+};
+
+__global__ void __launch_bounds__(EC::THREADS, 1)
+    gj_w2_row_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
+                     W2RowSched sched) {
+  RDB_TRACE_SCOPE(14);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
+}
+
+__global__ void __launch_bounds__(EC::THREADS, 1)
+    gj_w2_update_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap,
+                        W2UpdateSched sched) {
+  RDB_TRACE_SCOPE(15);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  eng::run<EC>(smem_raw, &amap, sched, eng::BulkEpilogue<EC>{&cmap});
+}
+
 // Per-part device state of the DW path (inside the batched workspace).
 struct DwPart {
   int* list;    // [cnt] local indices of the part's DW matrices
@@ -1022,7 +1131,7 @@ RDB_DEV int s0_positions(const uint32_t* bm, int64_t wpr, int64_t n_bits, int nb
       while (w) {
         const int k = 32 * q + __ffs(w) - 1;
         w &= w - 1;
-        if (c < CAP) ps[c] = (unsigned short)k;
+        if (ps && c < CAP) ps[c] = (unsigned short)k;
         ++c;
       }
     }
@@ -1030,7 +1139,7 @@ RDB_DEV int s0_positions(const uint32_t* bm, int64_t wpr, int64_t n_bits, int nb
     const int q = tl >> 5, b = tl & 31;
     for (int k = 0; k < nb0; ++k)
       if ((sw[k][q] >> b) & 1) {
-        if (c < CAP) ps[c] = (unsigned short)k;
+        if (ps && c < CAP) ps[c] = (unsigned short)k;
         ++c;
       }
   }
@@ -1039,20 +1148,21 @@ RDB_DEV int s0_positions(const uint32_t* bm, int64_t wpr, int64_t n_bits, int nb
 
 // bits words of rows k < nb0 for the 256-column chunk x (columns B0 + 256 x ..)
 template <int B0>
-RDB_DEV void s0_stage_words(const uint32_t* bm, int64_t wpr, int nb0, uint32_t (*sw)[9]) {
-  const int64_t q0 = (B0 + (int64_t)blockIdx.x * 256) / 32;
+RDB_DEV void s0_stage_words(const uint32_t* bm, int64_t wpr, int nb0, uint32_t (*sw)[9], int x) {
+  const int64_t q0 = (B0 + (int64_t)x * 256) / 32;
   for (int e = threadIdx.x; e < nb0 * 8; e += blockDim.x) {
     const int k = e >> 3, q = e & 7;
     sw[k][q] = q0 + q < wpr ? bm[k * wpr + q0 + q] : 0u;
   }
 }
 
-// Before K1 (APSP pipelines, M from bits): grid (ceil(R / 256), batch), 512
-// threads, dense-wide matrices (flags == 2), the problem = the leading n x n
-// block: bad[m] |= bit when a row of block column 0 or a column of block row 0
-// (B0 wide) has more than CAP edges.
+// Before K1 (APSP pipelines, M from bits): grid (2 ceil(R / 256), batch), 256
+// threads (x even: rows, odd: columns of chunk x / 2), dense-wide matrices
+// (flags == 2), the problem = the leading n x n block: bad[m] |= bit when a
+// row of block column 0 or a column of block row 0 (B0 wide) has more than
+// CAP edges.
 template <int B0>
-__global__ void __launch_bounds__(512) dw_s0_count_kernel(const uint32_t* __restrict__ bits, int64_t n_bits,
+__global__ void __launch_bounds__(256) dw_s0_count_kernel(const uint32_t* __restrict__ bits, int64_t n_bits,
                                                           int n, const int* __restrict__ flags, int* __restrict__ bad,
                                                           int bit) {
   const int64_t m = blockIdx.y;
@@ -1062,23 +1172,22 @@ __global__ void __launch_bounds__(512) dw_s0_count_kernel(const uint32_t* __rest
   const uint32_t* bm = bits + m * n_bits * wpr;
   const int64_t nb = n_bits < n ? n_bits : n;
   const int nb0 = (int)(nb < B0 ? nb : B0);
-  const bool col = threadIdx.x >= 256;
-  const int tl = threadIdx.x & 255, t = (int)blockIdx.x * 256 + tl;
+  const bool col = blockIdx.x & 1;
+  const int x = blockIdx.x >> 1, tl = threadIdx.x, t = x * 256 + tl;
   __shared__ uint32_t sw[B0][9];
-  __shared__ unsigned short pos[512][S0<B0>::CAP];
-  s0_stage_words<B0>(bm, wpr, nb0, sw);
+  if (col) s0_stage_words<B0>(bm, wpr, nb0, sw, x);
   __syncthreads();
   if (t >= R) return;
   // (columns past the problem's n are outside: the chunk covers B0 + 256 x + [0, 256) < n)
-  if (s0_positions<B0>(bm, wpr, nb, nb0, col, t, tl, sw, pos[threadIdx.x]) > S0<B0>::CAP) atomicOr(bad + m, bit);
+  if (s0_positions<B0>(bm, wpr, nb, nb0, col, t, tl, sw, nullptr) > S0<B0>::CAP) atomicOr(bad + m, bit);
 }
 
-// grid (ceil(R / 256), list capacity), 512 threads, for the part's
-// dense-wide matrices: thread t < 256 gathers row B0 + 256 x + t, thread
-// 256 + t column B0 + 256 x + t; bad |= bit when one has more than CAP
+// grid (2 ceil(R / 256), list capacity), 256 threads, for the part's
+// dense-wide matrices: x even, thread t gathers row B0 + 256 (x / 2) + t; x
+// odd, column B0 + 256 (x / 2) + t; bad |= bit when one has more than CAP
 // edges. Runs on the part's side stream beside the first band inverse.
 template <int B0>
-__global__ void __launch_bounds__(512, 2) dw_s0_gather_kernel(S0Args g) {
+__global__ void __launch_bounds__(256, 4) dw_s0_gather_kernel(S0Args g) {
   RDB_TRACE_SCOPE(33);
   constexpr int CAP = S0<B0>::CAP;
   if ((int)blockIdx.y >= *g.n_list) return;
@@ -1090,12 +1199,12 @@ __global__ void __launch_bounds__(512, 2) dw_s0_gather_kernel(S0Args g) {
   const double* A = g.a + (int64_t)l * g.pstride;
   const S0Lists L(g.lists + (int64_t)l * g.lstride, R, CAP);
   const int nb0 = (int)(n_bits < B0 ? n_bits : B0);
-  const bool col = threadIdx.x >= 256;
-  const int tl = threadIdx.x & 255;
-  const int t = (int)blockIdx.x * 256 + tl;  // row / column index - B0
-  __shared__ uint32_t sw[B0][9];             // the chunk's 8 words of rows k < nb0 (padded)
-  __shared__ unsigned short pos[512][CAP];   // edge positions, then one batch of value loads
-  s0_stage_words<B0>(bm, wpr, nb0, sw);
+  const bool col = blockIdx.x & 1;
+  const int x = blockIdx.x >> 1, tl = threadIdx.x;
+  const int t = x * 256 + tl;               // row / column index - B0
+  __shared__ uint32_t sw[B0][9];            // the chunk's 8 words of rows k < nb0 (padded)
+  __shared__ unsigned short pos[256][CAP];  // edge positions, then one batch of value loads
+  if (col) s0_stage_words<B0>(bm, wpr, nb0, sw, x);
   __syncthreads();
   if (t >= R) return;
   unsigned short* ps = pos[threadIdx.x];
@@ -1278,7 +1387,7 @@ __global__ void __launch_bounds__(256, 4) dw_s0_update_kernel(S0Args g, int r0, 
 
 template <int B0>
 static void launch_s0_gather(const S0Args& g, int64_t pcnt, cudaStream_t st) {
-  dw_s0_gather_kernel<B0><<<dim3((unsigned)((g.n - B0 + 255) / 256), (unsigned)pcnt), 512, 0, st>>>(g);
+  dw_s0_gather_kernel<B0><<<dim3((unsigned)(2 * ((g.n - B0 + 255) / 256)), (unsigned)pcnt), 256, 0, st>>>(g);
   dw_s0_split_kernel<<<1, 1024, 0, st>>>(g);
 }
 
@@ -1293,7 +1402,8 @@ static bool dw_helper();
 static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t pcnt, const DwPart& d,
                    rdb_pivot_info* info, int64_t info_stride, const int* flags, int* dyn, cudaStream_t st,
                    cudaStream_t side = nullptr, cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr,
-                   int* side_dyn = nullptr, const S0Args* s0 = nullptr, cudaEvent_t s0_ready = nullptr) {
+                   int* side_dyn = nullptr, const S0Args* s0 = nullptr, cudaEvent_t s0_ready = nullptr,
+                   int first_rec = 1, int64_t idx_off = 0) {
   const int nt = (int)(n / NB);
   if (cudaMemsetAsync(d.colcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess ||
       cudaMemsetAsync(d.rowcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess)
@@ -1338,7 +1448,8 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
     if (side) cudaEventRecord(ev_join, side);
   }
 #ifndef RDB_EXP_NO_NESTED
-  rc = invert_core(a, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, 1, 0, dyn, &np, info_stride, flags, 0, 2);
+  rc = invert_core(a, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, first_rec, idx_off, dyn, &np, info_stride, flags,
+                   0, 2);
   if (rc) return rc;
 #endif
   if (s0 && (side || s0_ready)) cudaStreamWaitEvent(st, s0_ready ? s0_ready : ev_join, 0);
@@ -1366,8 +1477,8 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
       cudaStreamWaitEvent(side, ev_fork, 0);
       const int64_t q0 = (int64_t)(p0t + 2) * NB;
 #ifndef RDB_EXP_NO_NESTED  // timing experiments only (wrong results)
-      rc = invert_core(a + q0 * lda + q0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, side, 0, q0, side_dyn, &np,
-                       info_stride, flags, 0, 2);
+      rc = invert_core(a + q0 * lda + q0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, side, 0, idx_off + q0, side_dyn,
+                       &np, info_stride, flags, 0, 2);
       if (rc) return rc;
 #endif
       cudaEventRecord(ev_join, side);
@@ -1402,11 +1513,83 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
       cudaStreamWaitEvent(st, ev_join, 0);
     } else if (p + 1 < nt / 2) {
       const int64_t q0 = (int64_t)(p0t + 2) * NB;
-      rc = invert_core(a + q0 * lda + q0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, 0, q0, dyn, &np,
+      rc = invert_core(a + q0 * lda + q0, 2 * NB, lda, pstride, pcnt, d.ncnt, info, st, 0, idx_off + q0, dyn, &np,
                        info_stride, flags, 0, 2);
       if (rc) return rc;
     }
   }
+  RDB_LAUNCH_CHECK();
+  return RDB_OK;
+}
+
+// The two-level DW steps for one part (n = 2 W): D0 = the leading W x W
+// block's inverse (dw_part on it, with its own sparse first step), the outer
+// step 0 (sparse for the matrices listed in s_out, dense tiles for the
+// others), D1 = the trailing block's inverse (dw_part, dense), the outer
+// step 1 (dense). The gathers of both levels are queued by the caller before
+// s0_ready (or here, inline, when it is null). Against the one-level steps
+// this replaces the dense 256-wide steps 1..3 of an n = 1024 matrix (3/4 of
+// its flop) by one 512-wide step plus two 512 x 512 inversions (62% of it).
+static int dw2_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t pcnt, const DwPart& d,
+                    const DwPart& din, rdb_pivot_info* info, int64_t info_stride, const int* flags, int* dyn,
+                    cudaStream_t st, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join, int* side_dyn,
+                    const S0Args* s_in, const S0Args* s_out, cudaEvent_t s0_ready) {
+  const int64_t W = n / 2;
+  const int nt = (int)(n / NB), bt = (int)(W / NB);
+  static DeviceFlags attrs;
+  const int attrs_dev = current_device();
+  if (!attrs.get(attrs_dev)) {
+    if (cudaFuncSetAttribute(gj_w2_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EC::SMEM_BYTES) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(gj_w2_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)EC::SMEM_BYTES) != cudaSuccess)
+      return RDB_ECUDA;
+    attrs.set(attrs_dev);
+  }
+  CUtensorMap amap, cmap;
+  int rc = make_a_map(&amap, a, n, n, lda, pstride, pcnt);
+  if (rc) return rc;
+  rc = make_ec_map(&cmap, a, n, n, lda, pstride, pcnt);
+  if (rc) return rc;
+  if ((s_in || s_out) && !s0_ready) {  // gathers inline, ahead of everything else here
+    if (s_in) launch_s0_gather<2 * NB>(*s_in, pcnt, st);
+    if (s_out) launch_s0_gather<4 * NB>(*s_out, pcnt, st);
+    cudaEventRecord(ev_join, st);
+    s0_ready = ev_join;
+  }
+  // A: D0 = A_00^-1 (W x W)
+  rc = dw_part(a, W, lda, pstride, pcnt, din, info, info_stride, flags, dyn, st, side, ev_fork, ev_join, side_dyn,
+               s_in, s_in ? s0_ready : nullptr, 1, 0);
+  if (rc) return rc;
+  if (s_out && s0_ready) cudaStreamWaitEvent(st, s0_ready, 0);
+  // B: outer step 0 (band 0)
+  auto outer_step = [&](int b0t, const int* list, const int* list_count) {
+    if (cudaMemsetAsync(d.colcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess ||
+        cudaMemsetAsync(d.rowcnt, 0, sizeof(int) * (size_t)pcnt * nt, st) != cudaSuccess)
+      return RDB_ECUDA;
+    W2RowSched rs{a, lda, pstride, nt, b0t, bt, list, list_count, d.colcnt, dyn};
+    gj_w2_row_kernel<<<persistent_grid(pcnt * (nt - bt) * bt), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, rs);
+    if (b0t == 0 && s_out)  // the sparse outer step's rows (their own matrices) before the dense tiles
+      launch_s0_update<4 * NB>(*s_out, (int)W, (int)n, pcnt, st);
+    W2UpdateSched us{a, lda, pstride, nt, b0t, bt, list, list_count, d.rowcnt, dyn ? dyn + 1 : nullptr};
+    gj_w2_update_kernel<<<persistent_grid(pcnt * (nt - bt) * nt), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap,
+                                                                                                      us);
+    return RDB_OK;
+  };
+  if (s_out) dw_s0_row_kernel<4 * NB><<<dim3((unsigned)(W / 8), (unsigned)pcnt), 256, 0, st>>>(*s_out);
+  rc = outer_step(0, s_out ? d.list_d : d.list, s_out ? d.count + 2 : d.count);
+  if (rc) return rc;
+  // C: D1 = (Schur complement)^-1, the trailing W x W block (dense); its
+  // pivots continue the record of A (indices from W)
+  DwPart dc = din;
+  dc.list = d.list;
+  dc.count = d.count;
+  rc = dw_part(a + W * lda + W, W, lda, pstride, pcnt, dc, info, info_stride, flags, dyn, st, side, ev_fork, ev_join,
+               side_dyn, nullptr, nullptr, 0, W);
+  if (rc) return rc;
+  // D: outer step 1 (band 1), every listed matrix
+  rc = outer_step(bt, d.list, d.count);
+  if (rc) return rc;
   RDB_LAUNCH_CHECK();
   return RDB_OK;
 }
@@ -1436,7 +1619,7 @@ int band_invert(double* a, int64_t n_pad, int64_t lda, int64_t stride, int64_t b
 
 struct BatchWs {
   size_t cnt, dyn, blk, counts, rp, up, offs, band, band_ws, dwl, dwc, dwnc, dwrp, dwup, dwcnt, dwcol, dwrow, dws0,
-      dwls, dwld, total;
+      dwls, dwld, dwls2, dwld2, total;
   BatchWs(int64_t n_pad, int64_t batch) {
     const size_t nt = (size_t)(n_pad / NB), b = (size_t)batch;
     cnt = 0;
@@ -1460,10 +1643,12 @@ struct BatchWs {
       dws0 = dwrow + align256(b * nt * sizeof(int));  // sparse first step: bad flags, list_s, list_d
       dwls = dws0 + align256(b * sizeof(int));
       dwld = dwls + align256(b * sizeof(int));
-      total = dwld + align256(b * sizeof(int));
+      dwls2 = dwld + align256(b * sizeof(int));  // two-level path: the outer step's list_s, list_d
+      dwld2 = dwls2 + align256(b * sizeof(int));
+      total = dwld2 + align256(b * sizeof(int));
     } else {
       counts = rp = up = offs = band = band_ws = dwl = dwc = dwnc = dwrp = dwup = dwcnt = dwcol = dwrow = dws0 = dwls =
-          dwld = total = blk;
+          dwld = dwls2 = dwld2 = total = blk;
     }
   }
   bool has_plan() const { return total > blk; }
@@ -1482,7 +1667,26 @@ struct BatchWs {
     d.list_d = reinterpret_cast<int*>(wb + dwld) + lo;
     return d;
   }
+  // two-level path: the outer level (its own sparse-step lists) and the inner
+  // level (the W x W inversions: the one-level lists, counts at count + 4)
+  DwPart dw2_outer(char* wb, int i, int64_t lo, int nt) const {
+    DwPart d = dw_part(wb, i, lo, nt);
+    d.list_s = reinterpret_cast<int*>(wb + dwls2) + lo;
+    d.list_d = reinterpret_cast<int*>(wb + dwld2) + lo;
+    return d;
+  }
+  DwPart dw2_inner(char* wb, int i, int64_t lo, int nt) const {
+    DwPart d = dw_part(wb, i, lo, nt);
+    d.count += 4;
+    return d;
+  }
 };
+
+// Two-level dense-wide steps for n = 1024 (A-B switch RDB_GJ_DW2=0).
+static bool dw2_enabled() {
+  const char* e = getenv("RDB_GJ_DW2");
+  return !(e && e[0] == '0');
+}
 
 // Sparse first step of the dense-wide path (A-B switch RDB_GJ_DW_S0=0).
 static bool dw_s0_enabled() {
@@ -1583,7 +1787,7 @@ int* band_flags(void* work, int64_t n, int64_t batch) {
 int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t batch, void* work,
                    rdb_pivot_info* info, cudaStream_t st, const uint32_t* bits = nullptr, int64_t n_bits = 0,
                    bool band_ready = false, int phase = 0, const double* m_gammas = nullptr,
-                   int** s0bad_out = nullptr) {
+                   int** s0bad_out = nullptr, int* s0_levels_out = nullptr) {
   std::lock_guard<std::mutex> guard(g_enqueue);
   if (s0bad_out) *s0bad_out = nullptr;
   if (batch == 1 && n >= wide_min_n() && n % (2 * NB) == 0 && a && work && info && lda >= n && !(lda & 1) &&
@@ -1640,26 +1844,31 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   const bool synth = use_s0 && m_gammas && bits;  // M = I - gamma A: the sparse step reads the bits, not M
   const int64_t lstride = (int64_t)(band::ws_doubles(n) * sizeof(double));  // lists in the banded scratch
   const int64_t wpr = (n_bits + 31) / 32;
-  auto s0_args = [&](const DwPart& d, int i, int parts_) {
+  // two-level path (n = 1024): outer steps of width W = n / 2 = 512
+  const bool use_dw2 = use_dw && n == 4 * 2 * NB && dw2_enabled();
+  // the sparse first step of a problem (the leading pn x pn block; one-level:
+  // the matrix, bit 1; two-level: inner = the leading W block, bit 1, outer =
+  // the matrix, bit 2, lists past the inner ones in the matrix's slice)
+  auto s0_args = [&](const DwPart& d, int i, int parts_, int64_t pn, int bit, const int* n_list) {
     S0Args g;
     g.a = a + i * stride;
     g.lda = lda;
     g.pstride = parts_ * stride;
-    g.lists = wb + ws.band_ws + i * lstride;
+    g.lists = wb + ws.band_ws + i * lstride + (bit == 2 ? (int64_t)256 * 1024 : 0);
     g.lstride = parts_ * lstride;
-    g.n = (int)n;
+    g.n = (int)pn;
     g.list = d.list_s;
     g.count = d.count;
-    g.colcnt = d.colcnt;
-    g.rowcnt = d.rowcnt;
+    g.colcnt = bit == 2 ? nullptr : d.colcnt;
+    g.rowcnt = bit == 2 ? nullptr : d.rowcnt;
     g.bits = bits + (int64_t)i * n_bits * wpr;
     g.bstride = parts_ * n_bits * wpr;
     g.wpr = wpr;
-    g.n_bits = n_bits;
+    g.n_bits = n_bits < pn ? n_bits : pn;
     g.bad = s0flags + i;
     g.bad_stride = parts_;
-    g.bad_bit = 1;
-    g.n_list = d.count;
+    g.bad_bit = bit;
+    g.n_list = n_list;
     g.dw_list = d.list;
     g.list_s = d.list_s;
     g.list_d = d.list_d;
@@ -1683,9 +1892,15 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       lo += (batch - i + ca.parts - 1) / ca.parts;
     }
     dw_classify_kernel<<<(unsigned)ca.parts, 1024, 0, st>>>(ca);
-    if (synth)  // counted now: K1 builds only M_00 of the matrices whose first step is sparse
-      dw_s0_count_kernel<2 * NB><<<dim3((unsigned)((n - 2 * NB + 255) / 256), (unsigned)batch), 512, 0, st>>>(
+    if (synth && !use_dw2)  // counted now: K1 builds only M_00 of the matrices whose first step is sparse
+      dw_s0_count_kernel<2 * NB><<<dim3((unsigned)(2 * ((n - 2 * NB + 255) / 256)), (unsigned)batch), 256, 0, st>>>(
           bits, n_bits, (int)n, nonband, s0flags, 1);
+    if (synth && use_dw2) {  // both levels: the leading 512 block (bit 1) and the matrix (bit 2)
+      dw_s0_count_kernel<2 * NB><<<dim3((unsigned)(2 * ((n / 2 - 2 * NB + 255) / 256)), (unsigned)batch), 256, 0,
+                                   st>>>(bits, n_bits, (int)(n / 2), nonband, s0flags, 1);
+      dw_s0_count_kernel<4 * NB><<<dim3((unsigned)(2 * ((n - 4 * NB + 255) / 256)), (unsigned)batch), 256, 0, st>>>(
+          bits, n_bits, (int)n, nonband, s0flags, 2);
+    }
   } else if (use_dw) {
     int64_t lo = 0;
     for (int i = 0; i < (split ? parts : 1); ++i) {
@@ -1697,6 +1912,7 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
   }
   if (phase == 1) {
     if (s0bad_out && synth) *s0bad_out = s0flags;
+    if (s0_levels_out) *s0_levels_out = use_dw2 ? 2 : 1;
     RDB_LAUNCH_CHECK();
     return RDB_OK;
   }
@@ -1728,10 +1944,16 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
       }
       // sparse first step: gather the part's edge lists on the side stream
       // first (ahead of the plan), beside the part's first band inverse
-      const S0Args g0 = use_s0 ? s0_args(dwp[i], i, parts) : S0Args{};
+      const DwPart d2o = use_dw2 ? ws.dw2_outer(wb, i, lo, (int)ntl) : DwPart{};
+      const DwPart d2i = use_dw2 ? ws.dw2_inner(wb, i, lo, (int)ntl) : DwPart{};
+      const S0Args g0 = !use_s0 ? S0Args{}
+                        : use_dw2 ? s0_args(d2i, i, parts, n / 2, 1, dwp[i].count)
+                                  : s0_args(dwp[i], i, parts, n, 1, dwp[i].count);
+      const S0Args g2 = use_s0 && use_dw2 ? s0_args(d2o, i, parts, n, 2, dwp[i].count) : S0Args{};
       const bool s0_aside = use_s0 && plan_aside;
       if (s0_aside) {
         launch_s0_gather<2 * NB>(g0, cnt, plan_st);
+        if (use_dw2) launch_s0_gather<4 * NB>(g2, cnt, plan_st);
         cudaEventRecord(ds->s0_ready[i], plan_st);
       }
       rc = invert_core(a + i * stride, n, lda, parts * stride, cnt, cw, info + i, plan_st, 1, 0,
@@ -1739,7 +1961,13 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
                        use_plan ? &pp : nullptr, parts, nonband ? nonband + i : nullptr,
                        (!dyn_on && cosched_cap()) ? sm_count() / parts : 0);
       if (rc) break;
-      if (use_dw) {
+      if (use_dw2) {
+        rc = dw2_part(a + i * stride, n, lda, parts * stride, cnt, d2o, d2i, info + i, parts, nonband + i,
+                      dyn_on ? dyn + 2 * i : nullptr, ds->part[i], dw_lookahead() ? ds->dw_side[i] : nullptr,
+                      ds->dw_fork[i], ds->dw_join[i], dyn_on ? dyn + 2 * MAX_PARTS + 2 * i : nullptr,
+                      use_s0 ? &g0 : nullptr, use_s0 ? &g2 : nullptr, s0_aside ? ds->s0_ready[i] : nullptr);
+        if (rc) break;
+      } else if (use_dw) {
         rc = dw_part(a + i * stride, n, lda, parts * stride, cnt, dwp[i], info + i, parts, nonband + i,
                      dyn_on ? dyn + 2 * i : nullptr, ds->part[i], dw_lookahead() ? ds->dw_side[i] : nullptr,
                      ds->dw_fork[i], ds->dw_join[i], dyn_on ? dyn + 2 * MAX_PARTS + 2 * i : nullptr,
@@ -1768,9 +1996,19 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     dyn = reinterpret_cast<int*>(wb + ws.dyn);
     if (cudaMemsetAsync(dyn, 0, 4 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
   }
-  if (use_dw) {
+  if (use_dw2) {
     DevStreams* ds = dw_lookahead() ? dev_streams() : nullptr;
-    const S0Args g0 = use_s0 ? s0_args(dwp[0], 0, 1) : S0Args{};
+    const DwPart d2o = ws.dw2_outer(wb, 0, 0, (int)ntl), d2i = ws.dw2_inner(wb, 0, 0, (int)ntl);
+    const S0Args g0 = use_s0 ? s0_args(d2i, 0, 1, n / 2, 1, dwp[0].count) : S0Args{};
+    const S0Args g2 = use_s0 ? s0_args(d2o, 0, 1, n, 2, dwp[0].count) : S0Args{};
+    const int rc = dw2_part(a, n, lda, stride, batch, d2o, d2i, info, 1, nonband, dyn, st,
+                            ds ? ds->dw_side[0] : nullptr, ds ? ds->dw_fork[0] : nullptr,
+                            ds ? ds->dw_join[0] : nullptr, dyn ? dyn + 2 * MAX_PARTS : nullptr,
+                            use_s0 ? &g0 : nullptr, use_s0 ? &g2 : nullptr, nullptr);
+    if (rc) return rc;
+  } else if (use_dw) {
+    DevStreams* ds = dw_lookahead() ? dev_streams() : nullptr;
+    const S0Args g0 = use_s0 ? s0_args(dwp[0], 0, 1, n, 1, dwp[0].count) : S0Args{};
     const int rc = dw_part(a, n, lda, stride, batch, dwp[0], info, 1, nonband, dyn, st, ds ? ds->dw_side[0] : nullptr,
                            ds ? ds->dw_fork[0] : nullptr, ds ? ds->dw_join[0] : nullptr,
                            dyn ? dyn + 2 * MAX_PARTS : nullptr, use_s0 ? &g0 : nullptr);

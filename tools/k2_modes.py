@@ -34,6 +34,7 @@ MODES = {
     "dw_no_helper": {"RDB_GJ_DW_HELPER": "0"},
     "dw_no_s0": {"RDB_GJ_DW_S0": "0"},
     "no_synth": {"RDB_GJ_DW_SYNTH": "0"},
+    "no_dw2": {"RDB_GJ_DW2": "0"},
     "dw_helper_reserve32": {"RDB_GJ_DW_LA_RESERVE": "32"},
     "dw_helper_reserve80": {"RDB_GJ_DW_LA_RESERVE": "80"},
     "dw_helper_reserve100": {"RDB_GJ_DW_LA_RESERVE": "100"},
@@ -44,7 +45,7 @@ MODES = {
     "no_split_no_dw": {"RDB_GJ_SPLIT_MIN": "0", "RDB_GJ_DW": "0"},
     "split3_capped": {"RDB_GJ_SPLIT_PARTS": "3"},
 }
-KNOBS = ("RDB_GJ_LA_SIDE", "RDB_GJ_WIDE_MIN", "RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW", "RDB_GJ_DW_LA", "RDB_GJ_DW_LA_RESERVE", "RDB_GJ_DW_HELPER", "RDB_GJ_DW_S0", "RDB_GJ_DW_SYNTH")
+KNOBS = ("RDB_GJ_LA_SIDE", "RDB_GJ_WIDE_MIN", "RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW", "RDB_GJ_DW_LA", "RDB_GJ_DW_LA_RESERVE", "RDB_GJ_DW_HELPER", "RDB_GJ_DW_S0", "RDB_GJ_DW_SYNTH", "RDB_GJ_DW2")
 
 
 def main():
