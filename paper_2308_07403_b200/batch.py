@@ -214,28 +214,47 @@ PLAN_MAX_NT = 64  # block-sparse plan limit (csrc/gj_invert.cu PLAN_MAX_NT)
 SPLIT_MIN_BATCH, SPLIT_PARTS = 64, 2  # csrc/gj_invert.cu defaults (RDB_GJ_SPLIT_MIN / RDB_GJ_SPLIT_PARTS)
 
 
+def _dw_launches(bands: int, s0: bool, helpers: bool) -> int:
+    """Kernels of one one-level dense-wide inversion (dw_part) of a part:
+    the first band inverse (6), per band its row panel and update (+ the
+    look-ahead's first update, the next band's inverse (6) and a helper launch
+    for every band but the last); with a sparse first step its row panel and
+    two row ranges of its update (the second only when there are rows past
+    the next band)."""
+    n = 6 + 2 * bands + 7 * (bands - 1) + (bands - 1 if helpers else 0)
+    return n + (2 + (1 if bands > 2 else 0) if s0 else 0)
+
+
 def launches_per_call(n: int, batch: int) -> int:
     """Kernels one rdb_apsp_bits_batched[_d8] call launches with the default
-    knobs (checked against the kernel nodes of a captured call: 148 for the
+    knobs (checked against the kernel nodes of a captured call: 159 for the
     config-2 batch): band detection, K1, the strip patterns, the dense-wide
-    classification, the banded factor and chain, K3; per sub-batch the dense-wide
-    steps (nested band inverse 6 per band, row panel 1 per band, update 1 per band
-    + 1 for each look-ahead split + 1 helper launch per look-ahead step; the
-    sparse first step's gather, split, row panel and two row ranges, plus its
-    edge count before K1) and the
-    block-sparse plan (3) with 3 per panel (P1, P2, U, launched even when their
-    lists are empty)."""
+    classification and its edge counts before K1 (one per level), the banded
+    factor and chain, K3; per sub-batch the block-sparse plan (3) with 3 per
+    panel (P1, P2, U, launched even when their lists are empty), the gathers
+    and list splits of the sparse first steps (2 per level) and the dense-wide
+    inversion: one-level (:func:`_dw_launches`) or, for n = 1024, two-level
+    (two 512 x 512 one-level inversions, the outer steps' row panel and update
+    (2 each) and the sparse outer step's row panel and update (2))."""
     nt = L.pad_to_nb(n) // L.RDB_NB
     parts = SPLIT_PARTS if batch >= SPLIT_MIN_BATCH and batch >= 4 * SPLIT_PARTS else 1
     plan = batch > 1 and nt <= PLAN_MAX_NT
     if not plan:
         return 2 + parts * 3 * nt
-    dw = nt >= 4 and nt % 2 == 0 and batch >= 2 * parts
-    bands = nt // 2
-    s0 = 5 if os.environ.get("RDB_GJ_DW_S0", "1") != "0" else 0  # per part (+ one count kernel before K1)
-    helpers = bands - 1 if os.environ.get("RDB_GJ_DW_HELPER", "1") != "0" else 0
-    per_part = 3 + 3 * nt + ((6 + bands + 8 * (bands - 1) + 1 + helpers + s0) if dw else 0)
-    return 1 + 1 + 1 + (1 if dw else 0) + (1 if dw and s0 else 0) + 2 + 1 + parts * per_part
+    dw = nt >= 4 and nt % 2 == 0 and batch >= 2 * parts and not _off("RDB_GJ_DW")
+    s0 = dw and not _off("RDB_GJ_DW_S0")
+    helpers = not _off("RDB_GJ_DW_HELPER")
+    two = dw and two_level(n, batch)
+    levels = 2 if two else 1
+    if not dw:
+        per_part = 0
+    elif two:
+        per_part = (2 * levels if s0 else 0) + _dw_launches(2, s0, helpers) + _dw_launches(2, False, helpers) + 4 + (
+            2 if s0 else 0)
+    else:
+        per_part = (2 if s0 else 0) + _dw_launches(nt // 2, s0, helpers)
+    return (1 + 1 + 1 + (1 if dw else 0) + (levels if s0 else 0) + 2 + 1
+            + parts * (3 + 3 * nt + per_part))
 
 
 STRIPS = 8  # 16-column strips (engine k-chunks) per 128-column block
@@ -330,63 +349,109 @@ def band_flops(n: int) -> float:
     return float((nb - 1) * (nb + 5) + 3 * nb) * 2.0 * BAND**3
 
 
-S0_CAP = 24  # sparse first step: edges per row / column of the step-0 blocks (csrc/gj_invert.cu S0_CAP)
+S0_CAP = 24  # sparse first step: edges per row / column of 256-wide step-0 blocks (csrc/gj_invert.cu S0<256>)
+S0_CAP_512 = 32  # ... of the two-level path's 512-wide outer step-0 blocks (S0<512>)
 DW_MIN_BATCH = 2  # dense-wide path: at least 2 matrices per sub-batch
 
 
-def sparse_first_step(bits: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray]:
+def _off(key: str) -> bool:
+    """An A-B switch the library reads from the environment, set to 0."""
+    return os.environ.get(key, "1").startswith("0")
+
+
+def _sparse_step(p: np.ndarray, n: int, b0: int, cap: int) -> bool:
+    """At most ``cap`` edges in every row of p[b0:n, :b0] and every column of
+    p[:b0, b0:n] (the step-0 blocks of the leading n x n problem)."""
+    return bool(p[b0:n, :b0].sum(axis=1).max(initial=0) <= cap and p[:b0, b0:n].sum(axis=0).max(initial=0) <= cap)
+
+
+def two_level(n: int, batch: int) -> bool:
+    """The dense-wide matrices of this batch take the two-level path (n = 1024:
+    two 512-wide outer steps, csrc/gj_invert.cu dw2_part)."""
+    return L.pad_to_nb(n) == 1024 and batch >= DW_MIN_BATCH and not _off("RDB_GJ_DW2")
+
+
+def dense_wide_classes(bits: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     """Host restatement of the dense-wide path's classification
-    (dw_classify_kernel, dw_s0_gather_kernel): per matrix, whether it takes the
-    dense 256-wide steps (not banded, every off-diagonal strip non-zero) and,
-    of those, whether its first step is sparse (at most S0_CAP edges in every
-    row of block column 0 and every column of block row 0, outside the
-    256-wide band). Returns (dense_wide, sparse_first) boolean masks."""
+    (dw_classify_kernel, dw_s0_count / gather kernels): per matrix, whether it
+    takes the dense-wide steps (not banded, every off-diagonal strip non-zero)
+    and, of those, whether its first 256-wide step is sparse (at most S0_CAP
+    edges in every row of block column 0 and column of block row 0; on the
+    two-level path: of the leading 512 x 512 block) and whether the two-level
+    path's 512-wide outer step 0 is sparse (at most S0_CAP_512).
+    Returns (dense_wide, sparse_256, sparse_512) boolean masks."""
     bits = np.asarray(bits).view(np.uint32)
     batch = bits.shape[0]
     nt = L.pad_to_nb(n) // L.RDB_NB
     none = np.zeros(batch, bool)
-    off_env = lambda k: os.environ.get(k, "1").startswith("0")  # noqa: E731  (A-B switches read by the library)
-    if (batch < DW_MIN_BATCH or nt < 4 or nt % 2 or nt > PLAN_MAX_NT or n < 2 * L.RDB_NB or off_env("RDB_GJ_DW")
-            or off_env("RDB_GJ_BAND") or off_env("RDB_GJ_SKIP")):
-        return none, none
+    if (batch < DW_MIN_BATCH or nt < 4 or nt % 2 or nt > PLAN_MAX_NT or n < 2 * L.RDB_NB or _off("RDB_GJ_DW")
+            or _off("RDB_GJ_BAND") or _off("RDB_GJ_SKIP")):
+        return none, none, none
     band = banded(bits, n)
     pat = strip_pattern(bits, n)
     off = ~np.eye(nt, dtype=bool)
     dense = ~band & (pat[:, :, off] == 0xFF).all(axis=(1, 2))
-    b0 = 2 * L.RDB_NB
     from .workloads import unpack_bits
 
-    sparse = np.zeros(batch, bool)
-    for b in np.flatnonzero(dense) if not off_env("RDB_GJ_DW_S0") else []:
+    two = two_level(n, batch)
+    s256, s512 = none.copy(), none.copy()
+    for b in np.flatnonzero(dense) if not _off("RDB_GJ_DW_S0") else []:
         p = unpack_bits(bits[b], n)
-        sparse[b] = p[b0:, :b0].sum(axis=1).max(initial=0) <= S0_CAP and p[:b0, b0:].sum(axis=0).max(initial=0) <= S0_CAP
-    return dense, sparse
+        s256[b] = _sparse_step(p, 512 if two else n, 256, S0_CAP)
+        s512[b] = two and _sparse_step(p, n, 512, S0_CAP_512)
+    return dense, s256, s512
+
+
+def sparse_first_step(bits: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """(dense_wide, sparse 256-wide first step) of :func:`dense_wide_classes`."""
+    dense, s256, _ = dense_wide_classes(bits, n)
+    return dense, s256
+
+
+def _dw_flops(p: np.ndarray, n: int, sparse0: bool) -> float:
+    """Flop of one one-level dense-wide inversion of the leading n x n block:
+    2 n^3, less the dense 256-wide step 0 when it is sparse (2 * 256 per edge of
+    block row 0, 2 * n per edge of block column 0 instead)."""
+    fl = 2.0 * n**3
+    if sparse0:
+        b0 = 256
+        fl += 2.0 * b0 * p[:b0, b0:n].sum() + 2.0 * n * p[b0:n, :b0].sum() - (2.0 * b0 * b0 * (n - b0)
+                                                                              + 2.0 * (n - b0) * b0 * n)
+    return fl
 
 
 def executed_flops(bits: np.ndarray, n: int) -> float:
     """FP64 flop K2 executes on this batch with the default knobs: the banded
     path for block-tridiagonal graphs, the block-sparse Gauss-Jordan plan
-    (2 * 128 * 128 * 16 per k-chunk) for the others (the dense-wide steps
-    execute the same 2 n^3 as the plan on a fully dense matrix), less the
-    dense first step of the matrices whose first step is sparse (which
-    execute 2 * 256 flop per edge of block row 0 and 2 * n per edge of block
-    column 0 instead)."""
+    (2 * 128 * 128 * 16 per k-chunk) for the others, except the dense-wide
+    matrices: one-level, 2 n^3 less a sparse first step (:func:`_dw_flops`);
+    two-level (n = 1024, W = 512), the two W x W inversions (the leading one
+    with its own sparse first step), the outer step 0 (sparse: 2 W per edge of
+    block row 0, 2 n per edge of block column 0; else its dense row panel and
+    update, 2 W^3 + 2 W^2 n) and the outer step 1 (2 W^3 + 2 W^2 n)."""
     bits = np.asarray(bits)
     batch = bits.shape[0]
     nt = L.pad_to_nb(n) // L.RDB_NB
     if batch > 1 and nt <= PLAN_MAX_NT:
         band = banded(bits, n)
-        chunks = gj_plan_chunks(strip_pattern(bits[~band], n)).sum() if (~band).any() else 0
+        dense, s256, s512 = dense_wide_classes(bits, n)
+        plan = ~band & ~dense
+        chunks = gj_plan_chunks(strip_pattern(bits[plan], n)).sum() if plan.any() else 0
         extra = band.sum() * band_flops(n)
-        _, sparse = sparse_first_step(bits, n)
-        if sparse.any():
-            from .workloads import unpack_bits
+        from .workloads import unpack_bits
 
-            b0, npad = 2 * L.RDB_NB, nt * L.RDB_NB
-            dense_step0 = 2.0 * b0 * b0 * (npad - b0) + 2.0 * (npad - b0) * b0 * npad
-            for b in np.flatnonzero(sparse):
-                p = unpack_bits(bits[b].view(np.uint32), n)
-                extra += 2.0 * b0 * p[:b0, b0:].sum() + 2.0 * npad * p[b0:, :b0].sum() - dense_step0
+        npad = nt * L.RDB_NB
+        two = two_level(n, batch)
+        for b in np.flatnonzero(dense):
+            p = unpack_bits(bits[b].view(np.uint32), n)
+            p = np.pad(p, ((0, npad - n), (0, npad - n)))
+            if not two:
+                extra += _dw_flops(p, npad, bool(s256[b]))
+                continue
+            w = npad // 2
+            step = 2.0 * w**3 + 2.0 * w * w * npad
+            outer0 = 2.0 * w * p[:w, w:].sum() + 2.0 * npad * p[w:, :w].sum() if s512[b] else step
+            extra += _dw_flops(p, w, bool(s256[b])) + outer0 + 2.0 * w**3 + step
     else:
         chunks = batch * nt**3 * STRIPS
         extra = 0.0

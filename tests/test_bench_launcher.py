@@ -18,7 +18,12 @@ def test_bench_self_launches_n_ranks():
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2"], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
-    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    # the two ranks print concurrently (lines may interleave): decode every object in the stream
+    dec, lines, pos, text = json.JSONDecoder(), [], 0, out.stdout
+    while (pos := text.find("{", pos)) >= 0:
+        obj, end = dec.raw_decode(text, pos)
+        lines.append(obj)
+        pos = end
     assert sorted(x["rank"] for x in lines) == [0, 1]
     assert all(x["world"] == 2 and x["max_rank"] == 1.0 and x["local_world"] == 2 for x in lines)
 

@@ -135,8 +135,9 @@ def test_cfg2_lattice_half_runs_about_a_sixth_of_the_chunks():
     assert (t[kinds == "er"] == 8 * 512).all()  # ER p = 0.02: every strip holds edges
     # bandwidth 32: half of the tiles, and 2 of 8 k-chunks of the update tiles
     assert (t[kinds == "lattice"] < 800).all()
-    # kernels per pipeline call: the kernel nodes of the captured call on the B200 (bench.py) are 148
-    assert B.launches_per_call(1024, 256) == 148
+    # kernels per pipeline call: the kernel nodes of the captured call on the B200 (bench.py) are 159
+    # (148 with the one-level dense-wide steps)
+    assert B.launches_per_call(1024, 256) == 159
 
 
 def test_band_detection_restatement():
@@ -156,14 +157,23 @@ def test_band_detection_restatement():
     fl = B.executed_flops(bits, 1024)
     er = B.gj_plan_chunks(B.strip_pattern(bits[kinds == "er"], 1024)).sum() * 2 * 128 * 128 * 16
     assert er == (kinds == "er").sum() * 2 * 1024**3  # fully dense pattern
-    # every cfg2 ER graph takes the dense-wide steps with a sparse first step:
-    # its dense step 0 (row panel 256 x 256 x 768, update 768 x 256 x 1024) is
-    # replaced by 2 * 256 flop per edge of block row 0 and 2 * 1024 per edge of
-    # block column 0
-    dense, sparse = B.sparse_first_step(bits, 1024)
+    # every cfg2 ER graph takes the two-level dense-wide path (n = 1024, W = 512)
+    # with sparse first steps at both levels: the leading 512 x 512 inversion
+    # (2 * 512^3 less its dense 256-wide step 0 = row panel 256 x 256 x 256 +
+    # update 256 x 256 x 512, plus 2 * 256 flop per edge of its block row 0 and
+    # 2 * 512 per edge of its block column 0), the sparse outer step 0 (2 * 512
+    # per edge of the outer block row 0, 2 * 1024 per edge of block column 0),
+    # the trailing 512 x 512 inversion (2 * 512^3) and the dense outer step 1
+    # (row panel 512 x 512 x 512 + update 512 x 512 x 1024)
+    dense, s256, s512 = B.dense_wide_classes(bits, 1024)
     np.testing.assert_array_equal(dense, kinds == "er")
-    np.testing.assert_array_equal(sparse, kinds == "er")
-    step0 = 2 * 256 * 256 * 768 + 2 * 768 * 256 * 1024
-    sp = sum(2 * 256 * p[:256, 256:].sum() + 2 * 1024 * p[256:, :256].sum()
-             for p in (wl.unpack_bits(bits[b].view(np.uint32), 1024) for b in np.flatnonzero(kinds == "er")))
-    assert fl == er - (kinds == "er").sum() * step0 + sp + (kinds == "lattice").sum() * B.band_flops(1024)
+    np.testing.assert_array_equal(s256, kinds == "er")
+    np.testing.assert_array_equal(s512, kinds == "er")
+    inner0 = 2 * 256 * 256 * 256 + 2 * 256 * 256 * 512
+    step = 2 * 512**3 + 2 * 512 * 512 * 1024
+    want = 0
+    for b in np.flatnonzero(kinds == "er"):
+        p = wl.unpack_bits(bits[b].view(np.uint32), 1024)
+        want += (2 * 512**3 - inner0 + 2 * 256 * p[:256, 256:512].sum() + 2 * 512 * p[256:512, :256].sum()
+                 + 2 * 512 * p[:512, 512:].sum() + 2 * 1024 * p[512:, :512].sum() + 2 * 512**3 + step)
+    assert fl == want + (kinds == "lattice").sum() * B.band_flops(1024)
