@@ -65,7 +65,7 @@ def test_abi_version_and_errors_without_gpu():
     plan = (al(b * 8 * 4 + 64) + 256 + al(b * 2 * 8 * 8) + al(4 * 2 * 8 * 4) + al(b * 8 * 7 * 4)
             + al(b * 8 * 8 * 7 * 8) + al(b * 2 * 8 * 4) + al(b * 4) + al(b * 4 * 32 * 32 * 32 * 8))
     dw = (al(b * 4) + al(4 * 16 * 4) + al(4 * 16 * 4) + al(2 * b * 4) + al(4 * b * 8) + al((2 * b + 16) * 4)
-          + al(b * nt * 4) + al(b * nt * 4) + 3 * al(b * 4))  # + sparse-first-step flags and lists
+          + al(b * nt * 4) + al(b * nt * 4) + 5 * al(b * 4))  # + sparse-first-step flags and lists (2 levels)
     assert lib.rdb_invert_workspace_bytes(1024, 256) == plan + dw
     assert lib.rdb_invert_batched_bits(None, 128, 128, 128 * 128, 2, None, 100, None, None, None) == 1
     assert lib.rdb_invert_workspace_bytes(0, 1) == 0
