@@ -706,8 +706,11 @@ def main():
                    "parallelism": f"dp{world} (independent graphs, no collective)",
                    "l2": f"working set per step {(batch * n_pad * n_pad * 8 + batch * N * N * dsize) / 1e9:.1f} GB "
                          "> 126 MB L2 (inputs larger than L2; no flush needed)"},
-        "roofline": {"bound": "tensor", "kernel": "K2 blocked Gauss-Jordan (gj_panel + gj_rowpanel + gj_update, DMMA.8x8x4) "
-                                                  "+ banded inverse of the block-tridiagonal graphs (band_factor + band_chain)",
+        "roofline": {"bound": "tensor", "kernel": "K2 Gauss-Jordan on DMMA.8x8x4: ER graphs two-level dense-wide (sparse first "
+                                                  "steps from the bits, 512-wide outer steps gj_w2_row/gj_w2_update, "
+                                                  "512 x 512 inner inversions gj_wb_row/gj_wb_update + nested gj_panel/"
+                                                  "gj_rowpanel/gj_update) + banded inverse of the block-tridiagonal "
+                                                  "graphs (band_factor + band_chain)",
                      "achieved": inv_tflops, "peak": peak, "unit": "TFLOP/s", "frac": inv_tflops / peak,
                      "frac_executed": inv_tflops / peak,
                      "dense_equivalent_tflops": dense_tflops, "frac_dense_2n3": dense_tflops / peak,
@@ -720,12 +723,15 @@ def main():
                                     "note": "the 128 ER graphs alone through the Gauss-Jordan engine (dense strips)"},
                      "traffic": traffic, "traffic_unit": "DRAM bytes per K2 call (ncu --set full)",
                      "traffic_source": traffic_src, "peak_source": peak_src,
-                     "work_per_launch": f"{exec_flops:.4g} flop executed per K2 call = 2*128*128*16 per k-chunk over "
-                                        f"the block-sparse plan's tiles and k-chunks for the {n_gj} Gauss-Jordan graphs + "
-                                        f"{B.band_flops(N):.4g} per banded graph x {batch - n_gj}; dense 2*n^3 = "
-                                        f"{flops_per_graph:.4g} flop per graph x {batch} graphs",
+                     "work_per_launch": f"{exec_flops:.4g} flop executed per K2 call (batch.executed_flops): the "
+                                        f"{n_gj} Gauss-Jordan graphs' dense-wide steps (2 n^3 less the sparse first "
+                                        f"steps' dense tiles, which execute 2 flop per edge and output element "
+                                        f"instead) + {B.band_flops(N):.4g} per banded graph x {batch - n_gj}; dense "
+                                        f"2*n^3 = {flops_per_graph:.4g} flop per graph x {batch} graphs",
                      "note": "frac > 1 is impossible for frac_executed; frac_dense_2n3 and graphs_per_s_frac_of_roofline "
-                             "exceed 1 because the block-sparse plan and the banded path skip work, not from hardware"},
+                             "exceed 1 because the sparse first steps and the banded path skip work, not from hardware; "
+                             "frac_executed counts only DMMA flop, so the HBM-bound sparse steps (one pass over the "
+                             "matrix, 2 flop per edge) lower it while they shorten the call"},
         "kernels_ms": {"K1_build_m_bits": t_build, "K2_invert": t_inv, "K3_log_ceil": t_log},
         "hbm_kernels": {"K1_GBps": build_bytes / (t_build * 1e-3) / 1e9, "K3_GBps": log_bytes / (t_log * 1e-3) / 1e9,
                         "K1_frac": build_bytes / (t_build * 1e-3) / 1e9 / hbm,

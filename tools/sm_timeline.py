@@ -27,7 +27,7 @@ from paper_2308_07403_b200 import workloads as wl  # noqa: E402
 KINDS = {0: "P1 plan", 1: "P1 nested (DW band)", 5: "P1 band path", 2: "rowpanel NB128", 3: "update NB128",
          4: "DW row panel", 10: "DW update (all)", 11: "DW update (next band 2x2)", 12: "DW update (rest)",
          8: "wide row", 9: "wide update", 20: "local gemm", 30: "plan walk", 33: "DW sparse step-0 gather", 31: "plan scan", 32: "dw classify",
-         50: "K3 log_ceil", 51: "K1 build_m_bits", 6: "DW sparse step-0 row panel", 7: "DW sparse step-0 update", 40: "band factor", 41: "band chain", 42: "band detect"}
+         14: "W2 outer row panel", 15: "W2 outer update", 50: "K3 log_ceil", 51: "K1 build_m_bits", 6: "DW sparse step-0 row panel", 7: "DW sparse step-0 update", 40: "band factor", 41: "band chain", 42: "band detect"}
 REC = np.dtype([("t0", "<u8"), ("t1", "<u8"), ("sm", "<i4"), ("kind", "<i4")])
 
 
