@@ -158,6 +158,15 @@ def main():
                   for k in np.unique(act["kind"])}
         print(f"  bin {i} ({(b0 - t_lo) / 1e3:.0f} us): {low[i]}")
     out["low_bins"] = low
+    # every bin: SMs per kind (kinds with at least 8 SMs)
+    allb = []
+    for i in range(nb):
+        b0, b1 = edges[i], edges[i + 1]
+        act = recs[(recs["t0"] < b1) & (recs["t1"] > b0)]
+        d = {KINDS.get(int(k), str(int(k))): int(np.unique(act["sm"][act["kind"] == k]).size)
+             for k in np.unique(act["kind"])}
+        allb.append({k: v for k, v in d.items() if v >= 8})
+    out["bins_kinds"] = allb
     if a.out:
         Path(a.out).write_text(json.dumps(out, indent=1) + "\n")
 
