@@ -1048,9 +1048,10 @@ __global__ void __launch_bounds__(1024) dw_classify_kernel(DwClassifyArgs arg) {
 //     row 0 (per column j), with their values, into compact lists (a snapshot:
 //     the step overwrites them in place), in increasing k; a matrix with more
 //     than S0_CAP edges in any such row or column keeps the dense step;
-//   dw_s0_row_kernel: A_0J = D A_0J, 16 rows of D in shared memory per CTA;
-//   dw_s0_update_kernel: the rows outside the band, 64-column strips of
-//     block row 0 (as updated) in shared memory per CTA.
+//   dw_s0_row_kernel: A_0J = D A_0J, 16 rows of D (transposed) in shared
+//     memory per CTA, a half-warp per output column;
+//   dw_s0_update_kernel: the rows outside the band, a warp per row, block
+//     row 0 (as updated) read from L2.
 // The lists live in the matrix's slice of the banded path's scratch, which
 // the banded inverse uses only for banded matrices (never dense-wide ones).
 // Edges kept per row / column of the step-0 blocks: B0 = 256 (one-level
@@ -1063,10 +1064,10 @@ struct S0 {
 constexpr int S0_CAP = S0<256>::CAP;  // (host restatement: batch.py S0_CAP)
 
 // List layout inside a matrix's slice (R = n - B0 rows / columns outside the
-// band): row lists row-major (a warp reads one row's entries in one pass),
-// column lists entry-major (consecutive threads read consecutive columns):
-// vals_r [R][CAP] double | vals_c [CAP][R] double | idx_r [R][CAP] u16 |
-// idx_c [CAP][R] u16 | cnt_r [R] u8 | cnt_c [R] u8.
+// band): row and column lists both row-major (a half-warp reads one row's /
+// column's entries in one pass, two 16-bit indices per lane):
+// vals_r [R][CAP] double | vals_c [R][CAP] double | idx_r [R][CAP] u16 |
+// idx_c [R][CAP] u16 | cnt_r [R] u8 | cnt_c [R] u8.
 struct S0Lists {
   double *vr, *vc;
   unsigned short *ir, *ic;
@@ -1225,8 +1226,8 @@ __global__ void __launch_bounds__(256, 4) dw_s0_gather_kernel(S0Args g) {
           L.ir[(size_t)t * CAP + e0 + e] = ps[e0 + e];
           L.vr[(size_t)t * CAP + e0 + e] = v[e];
         } else {
-          L.ic[(size_t)(e0 + e) * R + t] = ps[e0 + e];
-          L.vc[(size_t)(e0 + e) * R + t] = v[e];
+          L.ic[(size_t)t * CAP + e0 + e] = ps[e0 + e];
+          L.vc[(size_t)t * CAP + e0 + e] = v[e];
         }
       }
   }
@@ -1277,48 +1278,155 @@ __global__ void __launch_bounds__(1024) dw_s0_split_kernel(S0Args g) {
   }
 }
 
-// A_0J = D A_0J: rows 8 b .. 8 b + 7 of block row 0 (D's rows in shared
-// memory, transposed: an edge k reads Dt[k][0..7] as 4 16-byte loads; row
-// pitch 10 doubles), every column outside the band (thread t: columns
-// B0 + t + 256 q). Small register and shared-memory footprint: many CTAs
-// per SM hide the list loads' latency. grid (B0 / 8, list capacity).
+// The row panel's sparse products, one half-warp (16 lanes, lane c) per
+// output column: o += sum_e a_e * S[idx_e][c] over the column's edge list, in
+// list order (increasing k: the same sums, bit for bit, as a lane-per-column
+// kernel would form). S is a 16-row strip of the dense operand in shared
+// memory, transposed, so every edge costs one conflict-free 128-byte read
+// per half-warp; the list (CAP 16-bit indices, row-major) sits in the
+// half-warp's registers, two entries per lane, and is broadcast a pair at a
+// time by one shuffle. CONSTV: every edge value is the same (M built from
+// adjacency bits: -gamma); otherwise lane c also holds the values of entries
+// 2c and 2c + 1. The lists are loaded without looking at their counts first
+// (the slots past a count are allocated, never used), so no load depends on
+// another.
+RDB_DEV double s0_fma(double a, double s, double o) { return fma(a, s, o); }
+// shared-memory reads by 32-bit shared address (the strip's base is converted
+// once per thread; through a generic pointer the compiler rebuilt the shared
+// window base at every read)
+RDB_DEV void s0_lds(unsigned addr, double& v) { asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr)); }
+
+// sbase: shared address of S[0][c]; PITCHB: bytes per row of S. S has one
+// more row than the operand, all zeros (row ZROW): s0_fix points every list
+// slot at or past the row's count there (and zeroes its value), so the loop
+// body has no predicate — such a slot adds cv * 0 = 0 to an accumulator that
+// is never -0 (it starts from +0, 1 or an edge value), i.e. nothing.
+template <int ZROW>
+RDB_DEV void s0_fix(unsigned& pk, double& v0, double& v1, int c, int cnt) {
+  if (2 * c + 1 >= cnt) {
+    pk = (pk & 0xFFFFu) | ((unsigned)ZROW << 16);
+    v1 = 0.0;
+  }
+  if (2 * c >= cnt) {
+    pk = (unsigned)ZROW | ((unsigned)ZROW << 16);
+    v0 = 0.0;
+  }
+}
+
+// Two independent lists at once (two output columns of the half-warp): twice
+// the loads in flight per warp; the trip count covers the longest of the
+// four lists of the warp (shorter ones run on into the zero row).
+template <int PITCHB, bool CONSTV, class T>
+RDB_DEV void s0_accumulate2(T& oa, T& ob, unsigned sbase, int cmax, unsigned packed_a, unsigned packed_b, double va0,
+                            double va1, double vb0, double vb1, double cv) {
+#pragma unroll 2
+  for (int p = 0; 2 * p < cmax; ++p) {
+    const unsigned pa = __shfl_sync(0xffffffffu, packed_a, p, 16);
+    const unsigned pb = __shfl_sync(0xffffffffu, packed_b, p, 16);
+    double a0 = cv, a1 = cv, b0 = cv, b1 = cv;
+    if (!CONSTV) {
+      a0 = __shfl_sync(0xffffffffu, va0, p, 16);
+      a1 = __shfl_sync(0xffffffffu, va1, p, 16);
+      b0 = __shfl_sync(0xffffffffu, vb0, p, 16);
+      b1 = __shfl_sync(0xffffffffu, vb1, p, 16);
+    }
+    T sa0, sa1, sb0, sb1;
+    s0_lds(sbase + (pa & 0xFFFFu) * PITCHB, sa0);
+    s0_lds(sbase + (pb & 0xFFFFu) * PITCHB, sb0);
+    s0_lds(sbase + (pa >> 16) * PITCHB, sa1);
+    s0_lds(sbase + (pb >> 16) * PITCHB, sb1);
+    oa = s0_fma(a0, sa0, oa);
+    ob = s0_fma(b0, sb0, ob);
+    oa = s0_fma(a1, sa1, oa);
+    ob = s0_fma(b1, sb1, ob);
+  }
+}
+
+// A_0J = D A_0J: rows k0 .. k0 + 15 of block row 0 per CTA (k0 = 16
+// blockIdx.x). D's 16 rows sit transposed in shared memory (S[m][kk] =
+// D[k0 + kk][m], pitch 17: conflict-free both ways), so column j of the
+// result is the combination of the rows S[m] its edges m -> j select: a
+// half-warp per column, 16 columns per batch (their lists loaded QB columns
+// at a time, all loads in flight together), staged through a private 16 x 16
+// tile so the stores are 128-byte row segments. grid (B0 / 16, list
+// capacity), 256 threads, 2-3 CTAs per SM.
 template <int B0>
-__global__ void __launch_bounds__(256, 4) dw_s0_row_kernel(S0Args g) {
+struct S0Row {
+  static constexpr int P = 17;
+  static constexpr size_t SMEM = ((size_t)(B0 + 1) * P + 16 * 16 * P) * sizeof(double);  // + the zero row
+};
+
+template <int B0, bool CONSTV>
+RDB_DEV void s0_row_columns(const S0Args& g, const S0Lists& L, double* A, unsigned sbase, double* O, int R, int k0,
+                            int hw, int c, double cv) {
+  constexpr int CAP = S0<B0>::CAP, P = S0Row<B0>::P, QB = CONSTV ? 16 : 4;
+  for (int t0 = hw * 16; t0 < R; t0 += 256) {  // this half-warp's 16 columns B0 + t0 ..
+    const int cnts = t0 + c < R ? L.nc[t0 + c] : 0;
+#pragma unroll 1
+    for (int q0 = 0; q0 < 16; q0 += QB) {
+      unsigned pk[QB];
+      double v0[QB], v1[QB];
+#pragma unroll
+      for (int q = 0; q < QB; ++q) {
+        const size_t t = (size_t)min(t0 + q0 + q, R - 1);
+        pk[q] = *reinterpret_cast<const unsigned*>(L.ic + t * CAP + 2 * c);
+        v0[q] = v1[q] = 0.0;
+        if (!CONSTV) {
+          v0[q] = L.vc[t * CAP + 2 * c];
+          v1[q] = L.vc[t * CAP + 2 * c + 1];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QB; q += 2) {
+        const int cnt_a = __shfl_sync(0xffffffffu, cnts, q0 + q, 16);
+        const int cnt_b = __shfl_sync(0xffffffffu, cnts, q0 + q + 1, 16);
+        const int cm = max(cnt_a, cnt_b);
+        const int cmax = max(cm, __shfl_xor_sync(0xffffffffu, cm, 16));
+        s0_fix<B0>(pk[q], v0[q], v1[q], c, cnt_a);
+        s0_fix<B0>(pk[q + 1], v0[q + 1], v1[q + 1], c, cnt_b);
+        double oa = 0.0, ob = 0.0;
+        s0_accumulate2<P * 8, CONSTV, double>(oa, ob, sbase, cmax, pk[q], pk[q + 1], v0[q], v1[q], v0[q + 1],
+                                              v1[q + 1], cv);
+        O[c * P + q0 + q] = oa;
+        O[c * P + q0 + q + 1] = ob;
+      }
+    }
+    __syncwarp();
+    if (t0 + c < R) {
+#pragma unroll 4
+      for (int r = 0; r < 16; ++r) A[(int64_t)(k0 + r) * g.lda + B0 + t0 + c] = O[r * P + c];
+    }
+    __syncwarp();
+  }
+}
+
+template <int B0>
+__global__ void __launch_bounds__(256) dw_s0_row_kernel(S0Args g) {
   RDB_TRACE_SCOPE(6);
-  constexpr int RB = 8, CAP = S0<B0>::CAP;
+  constexpr int CAP = S0<B0>::CAP, P = S0Row<B0>::P;
   if ((int)blockIdx.y >= g.count[1]) return;
   const int l = g.list[blockIdx.y];
   double* A = g.a + (int64_t)l * g.pstride;
   const int R = g.n - B0;
   const S0Lists L(g.lists + (int64_t)l * g.lstride, R, CAP);
-  const int tid = threadIdx.x, r0 = (int)blockIdx.x * RB;
+  const int tid = threadIdx.x, k0 = (int)blockIdx.x * 16;
   const int nt = g.n / NB;
   if (g.colcnt && blockIdx.x == 0 && tid < nt) {  // the step-0 counts the dense tiles would have signalled
     g.colcnt[(int64_t)l * nt + tid] = tid >= 2 ? 2 : 0;
     g.rowcnt[(int64_t)l * nt + tid] = tid >= 2 ? nt : 0;
   }
-  __shared__ __align__(16) double Dt[B0][RB + 2];
-  for (int e = tid; e < RB * B0; e += 256) Dt[e % B0][e / B0] = A[(int64_t)(r0 + e / B0) * g.lda + e % B0];
+  extern __shared__ __align__(16) double s0_smem[];
+  double* S = s0_smem;
+  for (int e = tid; e < 16 * B0; e += 256) S[(e % B0) * P + e / B0] = A[(int64_t)(k0 + e / B0) * g.lda + e % B0];
+  if (tid < P) S[B0 * P + tid] = 0.0;
   __syncthreads();
-  for (int t = tid; t < R; t += 256) {
-    double acc[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) acc[r] = 0.0;
-    const int nc = L.nc[t];
-    for (int e = 0; e < nc; ++e) {
-      const int k = L.ic[(size_t)e * R + t];
-      const double v = L.vc[(size_t)e * R + t];
-      const double2* d = reinterpret_cast<const double2*>(&Dt[k][0]);
-#pragma unroll
-      for (int r = 0; r < RB / 2; ++r) {
-        const double2 x = d[r];
-        acc[2 * r] = fma(x.x, v, acc[2 * r]);
-        acc[2 * r + 1] = fma(x.y, v, acc[2 * r + 1]);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r) A[(int64_t)(r0 + r) * g.lda + B0 + t] = acc[r];
-  }
+  const int hw = tid >> 4, c = tid & 15;
+  double* O = s0_smem + (size_t)(B0 + 1) * P + hw * 16 * P;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(S + c);
+  if (g.gam)  // a_mj = -gamma
+    s0_row_columns<B0, true>(g, L, A, sbase, O, R, k0, hw, c, -g.gam[(int64_t)l * g.gam_stride]);
+  else
+    s0_row_columns<B0, false>(g, L, A, sbase, O, R, k0, hw, c, 0.0);
 }
 
 // Rows [r0, r1) outside the band: A_i = M'_i - sum_k a_ik A_k (block row 0
@@ -1391,6 +1499,22 @@ static void launch_s0_gather(const S0Args& g, int64_t pcnt, cudaStream_t st) {
   dw_s0_split_kernel<<<1, 1024, 0, st>>>(g);
 }
 
+// (dynamic shared memory above 48 KB: opted in once per device)
+template <int B0>
+static void s0_attrs() {
+  static DeviceFlags attrs;
+  const int dev = current_device();
+  if (attrs.get(dev)) return;
+  cudaFuncSetAttribute(dw_s0_row_kernel<B0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S0Row<B0>::SMEM);
+  attrs.set(dev);
+}
+
+template <int B0>
+static void launch_s0_row(const S0Args& g, int64_t pcnt, cudaStream_t st) {
+  s0_attrs<B0>();
+  dw_s0_row_kernel<B0><<<dim3(B0 / 16, (unsigned)pcnt), 256, S0Row<B0>::SMEM, st>>>(g);
+}
+
 template <int B0>
 static void launch_s0_update(const S0Args& g, int r0, int r1, int64_t pcnt, cudaStream_t st) {
   if (r1 > r0) dw_s0_update_kernel<B0><<<dim3((unsigned)((r1 - r0) / 8), (unsigned)pcnt), 256, 0, st>>>(g, r0, r1);
@@ -1461,7 +1585,7 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
     const bool sp = s0 && p == 0;
     const int* list = sp ? d.list_d : d.list;
     const int* list_count = sp ? d.count + 2 : d.count;
-    if (sp) dw_s0_row_kernel<2 * NB><<<dim3(2 * NB / 8, (unsigned)pcnt), 256, 0, st>>>(*s0);
+    if (sp) launch_s0_row<2 * NB>(*s0, pcnt, st);
     WBRowSched rs{a, lda, pstride, nt, p0t, p, list, list_count, d.colcnt, dyn};
 #ifndef RDB_EXP_NO_WBROW  // timing experiments only (wrong results)
     gj_wb_row_kernel<<<persistent_grid(pcnt * (nt - 2) * 2), EC::THREADS, EC::SMEM_BYTES, st>>>(amap, cmap, rs);
@@ -1576,7 +1700,7 @@ static int dw2_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t 
                                                                                                       us);
     return RDB_OK;
   };
-  if (s_out) dw_s0_row_kernel<4 * NB><<<dim3((unsigned)(W / 8), (unsigned)pcnt), 256, 0, st>>>(*s_out);
+  if (s_out) launch_s0_row<4 * NB>(*s_out, pcnt, st);
   rc = outer_step(0, s_out ? d.list_d : d.list, s_out ? d.count + 2 : d.count);
   if (rc) return rc;
   // C: D1 = (Schur complement)^-1, the trailing W x W block (dense); its

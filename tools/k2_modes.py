@@ -44,6 +44,11 @@ MODES = {
     "no_split": {"RDB_GJ_SPLIT_MIN": "0"},
     "no_split_no_dw": {"RDB_GJ_SPLIT_MIN": "0", "RDB_GJ_DW": "0"},
     "split3_capped": {"RDB_GJ_SPLIT_PARTS": "3"},
+    "split4": {"RDB_GJ_SPLIT_PARTS": "4"},
+    "reserve40": {"RDB_GJ_DW_LA_RESERVE": "40"},
+    "reserve56": {"RDB_GJ_DW_LA_RESERVE": "56"},
+    "reserve72": {"RDB_GJ_DW_LA_RESERVE": "72"},
+    "split3_reserve48": {"RDB_GJ_SPLIT_PARTS": "3", "RDB_GJ_DW_LA_RESERVE": "48"},
 }
 KNOBS = ("RDB_GJ_LA_SIDE", "RDB_GJ_WIDE_MIN", "RDB_GJ_COSCHED", "RDB_GJ_DYNAMIC", "RDB_GJ_SPLIT_MIN", "RDB_GJ_SPLIT_PARTS", "RDB_GJ_DW", "RDB_GJ_DW_LA", "RDB_GJ_DW_LA_RESERVE", "RDB_GJ_DW_HELPER", "RDB_GJ_DW_S0", "RDB_GJ_DW_SYNTH", "RDB_GJ_DW2")
 

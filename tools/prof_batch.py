@@ -17,7 +17,12 @@ ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--iters", type=int, default=1)
 ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--d-dtype", default="uint8", choices=["uint8", "int32"])
+ap.add_argument("--lib", default=None, help="another build of the library (A/B)")
 args = ap.parse_args()
+if args.lib:
+    from paper_2308_07403_b200 import _lib as L  # noqa: E402
+
+    L._lib = L.load_library(args.lib)
 
 bits, gammas, _ = wl.cfg2_batch(args.batch)
 dev = torch.device("cuda", 0)

@@ -68,7 +68,7 @@ def main():
     for _ in range(3):
         B.run_chunk(buf, 256, sh)
     torch.cuda.synchronize()
-    cap = 1 << 22
+    cap = 1 << 24
     tbuf = torch.zeros(cap * REC.itemsize, dtype=torch.uint8, device=dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for rep in range(a.reps):
@@ -90,6 +90,10 @@ def main():
         tbuf.zero_()
         L.check(lib.rdb_trace_attach(None, 0), "trace_detach")
         t_lo, t_hi = int(recs["t0"].min()), int(recs["t1"].max())
+        per_sm_n = np.bincount(recs["sm"], minlength=nsm)
+        print(json.dumps({"segment_capacity": cap // 4 // 192, "records_per_sm_max": int(per_sm_n.max()),
+                          "records_per_sm_min": int(per_sm_n.min()), "trace_counts": [int(cnt[0]), int(cnt[1])]}),
+              flush=True)
         wall = t_hi - t_lo
         busy = 0
         per_sm = {}
