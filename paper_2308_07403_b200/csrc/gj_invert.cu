@@ -1346,24 +1346,29 @@ RDB_DEV void s0_accumulate2(T& oa, T& ob, unsigned sbase, int cmax, unsigned pac
 // blockIdx.x). D's 16 rows sit transposed in shared memory (S[m][kk] =
 // D[k0 + kk][m], pitch 17: conflict-free both ways), so column j of the
 // result is the combination of the rows S[m] its edges m -> j select: a
-// half-warp per column, 16 columns per batch (their lists loaded QB columns
-// at a time, all loads in flight together), staged through a private 16 x 16
-// tile so the stores are 128-byte row segments. grid (B0 / 16, list
-// capacity), 256 threads, 2-3 CTAs per SM.
+// half-warp per column, CB = 8 columns per batch (their lists loaded QB
+// columns at a time, all loads in flight together), staged through a private
+// 16 x 8 tile so the stores are 64-byte row segments. grid (B0 / 16, list
+// capacity), 512 threads; 107 KB (B0 = 512: two CTAs, 32 warps per SM) or
+// 72 KB (B0 = 256: three CTAs) of shared memory.
+#ifndef RDB_S0_ROW_THREADS
+#define RDB_S0_ROW_THREADS 512
+#endif
 template <int B0>
 struct S0Row {
-  static constexpr int P = 17;
-  static constexpr size_t SMEM = ((size_t)(B0 + 1) * P + 16 * 16 * P) * sizeof(double);  // + the zero row
+  static constexpr int P = 17, THREADS = RDB_S0_ROW_THREADS, NH = THREADS / 16, CB = 8, PO = CB + 1;
+  static constexpr size_t SMEM = ((size_t)(B0 + 1) * P + NH * 16 * PO) * sizeof(double);  // + the zero row
 };
 
 template <int B0, bool CONSTV>
 RDB_DEV void s0_row_columns(const S0Args& g, const S0Lists& L, double* A, unsigned sbase, double* O, int R, int k0,
                             int hw, int c, double cv) {
-  constexpr int CAP = S0<B0>::CAP, P = S0Row<B0>::P, QB = CONSTV ? 16 : 4;
-  for (int t0 = hw * 16; t0 < R; t0 += 256) {  // this half-warp's 16 columns B0 + t0 ..
-    const int cnts = t0 + c < R ? L.nc[t0 + c] : 0;
+  using K = S0Row<B0>;
+  constexpr int CAP = S0<B0>::CAP, P = K::P, CB = K::CB, PO = K::PO, QB = CONSTV ? CB : 4;
+  for (int t0 = hw * CB; t0 < R; t0 += K::NH * CB) {  // this half-warp's CB columns B0 + t0 ..
+    const int cnts = (c < CB && t0 + c < R) ? L.nc[t0 + c] : 0;
 #pragma unroll 1
-    for (int q0 = 0; q0 < 16; q0 += QB) {
+    for (int q0 = 0; q0 < CB; q0 += QB) {
       unsigned pk[QB];
       double v0[QB], v1[QB];
 #pragma unroll
@@ -1387,23 +1392,25 @@ RDB_DEV void s0_row_columns(const S0Args& g, const S0Lists& L, double* A, unsign
         double oa = 0.0, ob = 0.0;
         s0_accumulate2<P * 8, CONSTV, double>(oa, ob, sbase, cmax, pk[q], pk[q + 1], v0[q], v1[q], v0[q + 1],
                                               v1[q + 1], cv);
-        O[c * P + q0 + q] = oa;
-        O[c * P + q0 + q + 1] = ob;
+        O[c * PO + q0 + q] = oa;
+        O[c * PO + q0 + q + 1] = ob;
       }
     }
     __syncwarp();
-    if (t0 + c < R) {
+    const int cc = c & (CB - 1), rr = c / CB;  // two rows of the tile per pass
+    if (t0 + cc < R) {
 #pragma unroll 4
-      for (int r = 0; r < 16; ++r) A[(int64_t)(k0 + r) * g.lda + B0 + t0 + c] = O[r * P + c];
+      for (int r = rr; r < 16; r += 16 / CB) A[(int64_t)(k0 + r) * g.lda + B0 + t0 + cc] = O[r * PO + cc];
     }
     __syncwarp();
   }
 }
 
 template <int B0>
-__global__ void __launch_bounds__(256) dw_s0_row_kernel(S0Args g) {
+__global__ void __launch_bounds__(S0Row<B0>::THREADS) dw_s0_row_kernel(S0Args g) {
   RDB_TRACE_SCOPE(6);
-  constexpr int CAP = S0<B0>::CAP, P = S0Row<B0>::P;
+  using K = S0Row<B0>;
+  constexpr int CAP = S0<B0>::CAP, P = K::P;
   if ((int)blockIdx.y >= g.count[1]) return;
   const int l = g.list[blockIdx.y];
   double* A = g.a + (int64_t)l * g.pstride;
@@ -1417,11 +1424,12 @@ __global__ void __launch_bounds__(256) dw_s0_row_kernel(S0Args g) {
   }
   extern __shared__ __align__(16) double s0_smem[];
   double* S = s0_smem;
-  for (int e = tid; e < 16 * B0; e += 256) S[(e % B0) * P + e / B0] = A[(int64_t)(k0 + e / B0) * g.lda + e % B0];
+  for (int e = tid; e < 16 * B0; e += K::THREADS)
+    S[(e % B0) * P + e / B0] = A[(int64_t)(k0 + e / B0) * g.lda + e % B0];
   if (tid < P) S[B0 * P + tid] = 0.0;
   __syncthreads();
   const int hw = tid >> 4, c = tid & 15;
-  double* O = s0_smem + (size_t)(B0 + 1) * P + hw * 16 * P;
+  double* O = s0_smem + (size_t)(B0 + 1) * P + hw * 16 * K::PO;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(S + c);
   if (g.gam)  // a_mj = -gamma
     s0_row_columns<B0, true>(g, L, A, sbase, O, R, k0, hw, c, -g.gam[(int64_t)l * g.gam_stride]);
@@ -1512,7 +1520,7 @@ static void s0_attrs() {
 template <int B0>
 static void launch_s0_row(const S0Args& g, int64_t pcnt, cudaStream_t st) {
   s0_attrs<B0>();
-  dw_s0_row_kernel<B0><<<dim3(B0 / 16, (unsigned)pcnt), 256, S0Row<B0>::SMEM, st>>>(g);
+  dw_s0_row_kernel<B0><<<dim3(B0 / 16, (unsigned)pcnt), S0Row<B0>::THREADS, S0Row<B0>::SMEM, st>>>(g);
 }
 
 template <int B0>
