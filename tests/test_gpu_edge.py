@@ -175,3 +175,55 @@ def test_mixed_batch_dense_wide_plan_and_band_paths(cuda, monkeypatch, n, count)
     for b in range(0, len(presents), 5):
         ref = orc.d_to_int32(orc.run_rdist(wl.weights_from_present(presents[b]), gam[b]))
         np.testing.assert_array_equal(d_dw[b], ref, err_msg=f"graph {b}")
+
+
+@pytest.mark.parametrize("n,p", [(512, 0.03), (1024, 0.02), (1536, 0.012)])
+def test_sparse_first_step_matches_dense_steps(cuda, monkeypatch, n, p):
+    """The sparse first step(s) of the dense-wide path (edge lists snapshotted,
+    half-warp-per-column row panel, warp-per-row update; two levels at
+    n = 1024) against the same matrices through dense tiles only
+    (RDB_GJ_DW_S0=0): the inverse agrees to rounding (the sums run in another
+    order), D is identical, and the APSP pipeline (M from the bits, every edge
+    -gamma) gives bitwise the inverse of the generic entry point (edge values
+    read from M). One graph exceeds the per-row edge cap and keeps the dense
+    step."""
+    from paper_2308_07403_b200 import batch as B
+
+    rng = np.random.default_rng(n)
+    count = 12
+    presents = []
+    for k in range(count):
+        q = rng.random((n, n)) < p
+        if k == 5:
+            q[n - 7, :200] = True  # 200 edges into block 0 from one row: over the cap
+        np.fill_diagonal(q, False)
+        presents.append(q)
+    bits = np.stack([wl.pack_bits(q) for q in presents])
+    gam = np.full(count, 1e-2)
+    dev = torch.device("cuda")
+    sh = torch.cuda.current_stream().cuda_stream
+    out = {}
+    for mode in ("default", "dense"):
+        monkeypatch.delenv("RDB_GJ_DW_S0", raising=False)
+        if mode == "dense":
+            monkeypatch.setenv("RDB_GJ_DW_S0", "0")
+        buf = B.BatchBuffers.allocate(n, count, dev)
+        buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+        buf.gammas.copy_(torch.from_numpy(gam))
+        buf.stage_build(count, sh)
+        buf.stage_invert(count, sh)
+        torch.cuda.synchronize()
+        y = buf.m.clone()
+        B.run_chunk(buf, count, sh)
+        torch.cuda.synchronize()
+        out[mode] = (y, buf.m.clone(), buf.d.clone())
+        del buf
+    y_s, y_pipe, d_s = out["default"]
+    y_d, _, d_d = out["dense"]
+    assert torch.equal(y_s, y_pipe)  # constant-value lists == values gathered from M
+    assert torch.equal(d_s, d_d)
+    rel = ((y_s - y_d).abs() / y_d.abs().clamp_min(1e-300)).max().item()
+    assert rel < 1e-12, rel
+    ref = orc.d_to_int32(orc.run_rdist(wl.weights_from_present(presents[5]), 1e-2))
+    got = rb.rounded_r_distance_batch(bits[5:6], gam[5:6], n)[0]
+    np.testing.assert_array_equal(got, ref)
