@@ -682,21 +682,48 @@ def main():
     e2e = e2e_run(args.d_dtype)
     e2e_other = e2e_run("int32" if args.d_dtype == "uint8" else "uint8")
 
-    # ---- config-5 inversion (BASELINE's "inversion FP64 TFLOP/s"): one GPU or the grid
+    # ---- config-5 inversion (BASELINE's "inversion FP64 TFLOP/s"): one GPU or the grid.
+    # At N > 1 the leg runs under a deadline (RDB_BENCH_CFG5_DEADLINE seconds,
+    # default 300): if the grid inversion or its collectives stall on some rank,
+    # rank 0 still prints the line (config-2 numbers, the leg marked as timed
+    # out) and every rank exits, instead of the whole run hanging.
     cfg5 = None
-    if not args.no_cfg5:
-        cfg5 = (cfg5_single(dev, sh, peak, max_over_ranks) if world == 1
-                else cfg5_distributed(dev, rank, world, local_world, peak, max_over_ranks))
-        if world > 1 and backend != "nccl":
-            cfg5["note"] = f"functional run over {backend} (ranks share GPUs): not a timing"
-        torch.cuda.empty_cache()
+    pending = {"line": None}
+    emit_lock = threading.Lock()
 
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return 0
+    def emit(line):
+        with emit_lock:
+            if pending.get("done"):
+                return
+            pending["done"] = True
+            print(json.dumps(line), flush=True)
 
-    traffic, traffic_src = ncu_traffic()
+    def cfg5_leg():
+        if args.no_cfg5:
+            return None
+        if world == 1:
+            return cfg5_single(dev, sh, peak, max_over_ranks)
+        deadline = float(os.environ.get("RDB_BENCH_CFG5_DEADLINE", "300"))
+
+        def on_timeout():
+            if rank == 0 and pending["line"] is not None:
+                pending["line"]["inversion_cfg5"] = {"error": f"config-5 grid leg exceeded {deadline:.0f} s: skipped"}
+                emit(pending["line"])
+            os._exit(0)
+
+        timer = threading.Timer(deadline, on_timeout)
+        timer.daemon = True
+        timer.start()
+        try:
+            out = cfg5_distributed(dev, rank, world, local_world, peak, max_over_ranks)
+            if backend != "nccl":
+                out["note"] = f"functional run over {backend} (ranks share GPUs): not a timing"
+        except Exception as exc:  # noqa: BLE001 - the config-2 line is still reported
+            out = {"error": f"{type(exc).__name__}: {exc}"}
+        timer.cancel()
+        return out
+
+    traffic, traffic_src = ncu_traffic() if rank == 0 else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -745,6 +772,13 @@ def main():
         "inversion_cfg5": cfg5,
         "clocks": clk,
     }
+    pending["line"] = line
+    line["inversion_cfg5"] = cfg5_leg()
+    torch.cuda.empty_cache()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
     if world == 1 and not args.no_cpu_baseline:
         pool = CpuPool(per_core=2)
         pool.run()  # worker start-up and graph generation, untimed
@@ -754,7 +788,7 @@ def main():
         line["cpu_baseline"] = {"value": len(pool.items) / dt, "unit": "graphs/s", "cores": pool.procs,
                                 "kind": pool.kind, "sample": pool.sample() + "; median of 5 samples",
                                 "host": cpu_host_info()}
-    print(json.dumps(line), flush=True)
+    emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
