@@ -16,7 +16,7 @@ from pathlib import Path
 import torch
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "librdist_b200.so"
+LIB_PATH = Path(os.environ.get("RDB_LIB_PATH") or _HERE / "librdist_b200.so")  # RDB_LIB_PATH: A/B builds (tools/)
 
 RDB_ABI_VERSION = 6  # include/rdist_b200.h; load_library refuses a library built from another header
 RDB_NB = 128

@@ -177,6 +177,9 @@ class CapturedPipeline:
         self.buf, self.count = buf, count
         run_chunk(buf, count)  # eager first: library setup (streams, attributes) stays outside the capture
         torch.cuda.synchronize()
+        self.graph = None
+        if os.environ.get("RDB_PIPELINE_EAGER") == "1":  # debugging: every replay is an eager call
+            return
         try:  # keep the cudaGraph_t so kernel_nodes() can inspect it
             self.graph = torch.cuda.CUDAGraph(keep_graph=True)
         except TypeError:
@@ -187,6 +190,9 @@ class CapturedPipeline:
             self.graph.instantiate()
 
     def replay(self) -> None:
+        if self.graph is None:
+            run_chunk(self.buf, self.count, torch.cuda.current_stream().cuda_stream)
+            return
         self.graph.replay()
 
     def kernel_nodes(self) -> int:

@@ -1026,6 +1026,12 @@ __global__ void __launch_bounds__(1024) dw_classify_kernel(DwClassifyArgs arg) {
     d.count[0] = base;
     d.count[1] = 0;
     d.count[2] = base;
+    // the two-level path's inner level reads its counts at count + 4: the
+    // sparse-first-step split refines them; without it (RDB_GJ_DW_S0=0, or a
+    // generic call whose split never runs) they are the classification's
+    d.count[4] = base;
+    d.count[5] = 0;
+    d.count[6] = base;
     d.ncounts[0] = d.ncounts[1] = base;          // nested row panels, steps 0 and 1
     d.ncounts[2] = d.ncounts[3] = 2 * base;      // nested update tiles
   }

@@ -479,22 +479,49 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
     auto block = [&](int j, double2 p, double2 q) {
       const double v[4] = {p.x, p.y, q.x, q.y};
       int d[4];
-      unsigned need = 0;
 #if RDB_K3_MUFU && RDB_K3_F32
+      // The estimates' `need` flags stay predicates and the estimates are used
+      // as they come: a block with a flag set (rare) resolves those elements
+      // on the exact path; uint8 D leaves through a saturating pack (two
+      // I2IP), so the common path has no per-element select, clamp or byte
+      // permute. A common-path D outside 0 .. RDB_D8_MAX (stored saturated;
+      // the matrix is redone in int32) is tracked by an unsigned max.
+      bool nd[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        bool nd;
-        const int de = dceil_estimate_f32(v[e], inv_lg2f, thr0, nd);
-        need |= (unsigned)nd << e;
-        d[e] = nd ? 0 : de;
+      for (int e = 0; e < 4; ++e) d[e] = dceil_estimate_f32(v[e], inv_lg2f, thr0, nd[e]);
+      // (the block holding the diagonal, one in n / 4, goes the rare way too: D = 0 there)
+      if (nd[0] | nd[1] | nd[2] | nd[3] | ((unsigned)(i - j) < 4u)) {  // rare (static indices keep v / d in registers)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (j + e == i) {
+            d[e] = 0;
+          } else if (nd[e]) {  // exact path
+            const double r = exact_value(v[e], g, lg, inv_lg);
+            d[e] = __double2int_ru(r);  // +inf -> INT32_MAX, the int32 sentinel
+            neg += v[e] < NEGATIVE_ENTRY_TOL;  // a negative entry always takes this path (sign bit -> need)
+            if (DK == DK_U8) {
+              const bool unreachable = r == __longlong_as_double(0x7FF0000000000000LL);
+              const bool ok = r == r && (unsigned)d[e] <= (unsigned)RDB_D8_MAX;  // NaN: out of range
+              bad += !ok && !unreachable;
+              d[e] = unreachable ? RDB_D8_UNREACHABLE : (ok ? d[e] : RDB_D8_MAX);
+            }
+          } else if (DK == DK_U8) {
+            dmax = max(dmax, (unsigned)d[e]);
+          }
+        }
+      } else if (DK == DK_U8) {
+        dmax = max(max(dmax, max((unsigned)d[0], (unsigned)d[1])), max((unsigned)d[2], (unsigned)d[3]));
       }
-      if ((unsigned)(i - j) < 4u) {  // the block holding the diagonal (one in n / 4): D = 0 there
-        need &= ~(1u << (i - j));
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (j + e == i) d[e] = 0;
+      if (DK == DK_U8) {
+        unsigned hi16, w;
+        asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(hi16) : "r"(d[3]), "r"(d[2]), "r"(0));
+        asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(w) : "r"(d[1]), "r"(d[0]), "r"(hi16));
+        *reinterpret_cast<unsigned*>(static_cast<uint8_t*>(dout) + orow + j) = w;
+      } else {
+        *reinterpret_cast<int4*>(static_cast<int32_t*>(dout) + orow + j) = make_int4(d[0], d[1], d[2], d[3]);
       }
 #else
+      unsigned need = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         bool nd;
@@ -510,7 +537,6 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
         neg += v[e] < NEGATIVE_ENTRY_TOL;
 #endif
       }
-#endif
       if (need) {  // rare: exact path (static indices keep v / d in registers)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
@@ -553,6 +579,7 @@ __global__ void __launch_bounds__(256, LEAN_MINB)
       } else {
         *reinterpret_cast<int4*>(static_cast<int32_t*>(dout) + orow + j) = make_int4(d[0], d[1], d[2], d[3]);
       }
+#endif
     };
     // LEAN_PF blocks of loads in flight ahead of the one being converted
     constexpr int PF = LEAN_PF;

@@ -220,7 +220,15 @@ def test_sparse_first_step_matches_dense_steps(cuda, monkeypatch, n, p):
         del buf
     y_s, y_pipe, d_s = out["default"]
     y_d, _, d_d = out["dense"]
-    assert torch.equal(y_s, y_pipe)  # constant-value lists == values gathered from M
+    if not torch.equal(y_s, y_pipe):  # constant-value lists == values gathered from M
+        msg = []
+        for b in range(count):
+            dd = y_s[b] != y_pipe[b]
+            if dd.any():
+                idx = dd.nonzero()
+                msg.append(f"graph {b}: {int(dd.sum())} entries, rows {int(idx[:, 0].min())}..{int(idx[:, 0].max())}, "
+                           f"cols {int(idx[:, 1].min())}..{int(idx[:, 1].max())}")
+        raise AssertionError("pipeline Y != generic Y: " + "; ".join(msg))
     assert torch.equal(d_s, d_d)
     rel = ((y_s - y_d).abs() / y_d.abs().clamp_min(1e-300)).max().item()
     assert rel < 1e-12, rel
