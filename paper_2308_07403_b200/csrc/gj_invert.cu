@@ -2135,13 +2135,15 @@ int invert_batched(double* a, int64_t n, int64_t lda, int64_t stride, int64_t ba
     if (cudaMemsetAsync(dyn, 0, 4 * MAX_PARTS * sizeof(int), st) != cudaSuccess) return RDB_ECUDA;
   }
   if (use_dw2) {
-    DevStreams* ds = dw_lookahead() ? dev_streams() : nullptr;
+    // (the events order the inline gathers too: needed with or without the look-ahead's side stream)
+    DevStreams* ds = dev_streams();
+    if (!ds) return RDB_ECUDA;
     const DwPart d2o = ws.dw2_outer(wb, 0, 0, (int)ntl), d2i = ws.dw2_inner(wb, 0, 0, (int)ntl);
     const S0Args g0 = use_s0 ? s0_args(d2i, 0, 1, n / 2, 1, dwp[0].count) : S0Args{};
     const S0Args g2 = use_s0 ? s0_args(d2o, 0, 1, n, 2, dwp[0].count) : S0Args{};
     const int rc = dw2_part(a, n, lda, stride, batch, d2o, d2i, info, 1, nonband, dyn, st,
-                            ds ? ds->dw_side[0] : nullptr, ds ? ds->dw_fork[0] : nullptr,
-                            ds ? ds->dw_join[0] : nullptr, dyn ? dyn + 2 * MAX_PARTS : nullptr,
+                            dw_lookahead() ? ds->dw_side[0] : nullptr, ds->dw_fork[0], ds->dw_join[0],
+                            dyn ? dyn + 2 * MAX_PARTS : nullptr,
                             use_s0 ? &g0 : nullptr, use_s0 ? &g2 : nullptr, nullptr);
     if (rc) return rc;
   } else if (use_dw) {

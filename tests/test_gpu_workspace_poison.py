@@ -1,0 +1,148 @@
+"""The batched pipeline must not read anything it has not written itself.
+
+`compute-sanitizer --tool initcheck` is closed on this GPU pool, so this is the
+repository's own initcheck for K2's workspace (row-block counters, ticket
+counters, block-sparse plan, dense-wide lists and counts, sparse-first-step
+lists, banded scratch): every buffer the caller hands over uninitialised — the
+workspace, M, D, the pivot records — is filled with a poison pattern before the
+call, for every schedule the A/B switches select, through both entry points
+(rdb_apsp_bits_batched from the bits, and K1 + rdb_invert_batched + K3), split
+and unsplit. D must equal, bitwise, the D of the default schedule on clean
+buffers (which tests/test_gpu_full_parity.py pins to the reference's digests).
+
+It found one such read: the two-level dense-wide path took the inner level's
+list count from a slot only the sparse-first-step split wrote, so
+RDB_GJ_DW_S0=0 ran with whatever the allocator had left there.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2308_07403_b200 import batch as B
+from paper_2308_07403_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+MODES = [
+    {},
+    {"RDB_GJ_DW_S0": "0"},
+    {"RDB_GJ_DW_SYNTH": "0"},
+    {"RDB_GJ_DW2": "0"},
+    {"RDB_GJ_DW2": "0", "RDB_GJ_DW_S0": "0"},
+    {"RDB_GJ_DW": "0"},
+    {"RDB_GJ_DW_LA": "0"},
+    {"RDB_GJ_DW_HELPER": "0"},
+    {"RDB_GJ_BAND": "0"},
+    {"RDB_GJ_SKIP": "0"},
+    {"RDB_GJ_DYNAMIC": "0"},
+    {"RDB_GJ_SPLIT_MIN": "0"},
+]
+SWITCHES = sorted({k for m in MODES for k in m})
+
+
+def _poison(buf, byte):
+    for t in (buf.work, buf.m, buf.d, buf.info):
+        t.view(torch.uint8).fill_(byte)
+    buf.counters.zero_()  # (the caller's contract for the uint8 range counters)
+
+
+def _run(buf, bits, gam, count, entry, sh):
+    buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+    buf.gammas.copy_(torch.from_numpy(gam))
+    if entry == "pipeline":
+        B.run_chunk(buf, count, sh)
+    else:
+        buf.stage_build(count, sh)
+        (buf.stage_invert if entry == "bits" else buf.stage_invert_generic)(count, sh)
+        buf.stage_log_ceil(count, sh)
+    torch.cuda.synchronize()
+    return buf.d.clone()
+
+
+@pytest.mark.parametrize("count", [12, 72])  # one stream / two sub-batch streams
+def test_poisoned_buffers_every_schedule(cuda, monkeypatch, count):
+    bits, gam, _ = wl.cfg2_batch(count)  # half ER (dense-wide, two levels), half lattices (banded)
+    n = wl.CFG2["n"]
+    dev = torch.device("cuda")
+    sh = torch.cuda.current_stream().cuda_stream
+    for k in SWITCHES:
+        monkeypatch.delenv(k, raising=False)
+    buf = B.BatchBuffers.allocate(n, count, dev)
+    _poison(buf, 0)
+    ref = _run(buf, bits, gam, count, "pipeline", sh)
+    del buf
+    bad = []
+    for mode in MODES:
+        for k in SWITCHES:
+            monkeypatch.delenv(k, raising=False)
+        for k, v in mode.items():
+            monkeypatch.setenv(k, v)
+        for entry in ("pipeline", "bits", "generic"):
+            for byte in (0xFF, 0x01, 0x5A):  # ints -1 / 16843009 / 1515870810; doubles NaN / tiny / 3e125
+                buf = B.BatchBuffers.allocate(n, count, dev)
+                _poison(buf, byte)
+                try:
+                    d = _run(buf, bits, gam, count, entry, sh)
+                except Exception as exc:
+                    raise AssertionError(f"{mode} {entry} poison {byte:#x}: {exc}") from exc
+                if not torch.equal(d, ref):
+                    wrong = (d != ref).flatten(1).any(1).nonzero().flatten().tolist()
+                    bad.append((mode, entry, hex(byte), wrong[:8]))
+                del buf, d
+    assert not bad, bad
+
+
+def _m_matrix(n, seed, dev):
+    p = wl.er_present(n, min(1.0, 12.0 / n), seed)
+    m = np.eye(n) - 0.03 * p
+    return torch.from_numpy(m).to(dev)
+
+
+@pytest.mark.parametrize("n", [128, 640, 2048, 8192])  # one panel / look-ahead path / wide 256-step path
+def test_poisoned_workspace_single_matrix(cuda, n):
+    """rdb_invert (single matrix: NB = 128 look-ahead, wide path with its R / C
+    scratches) on a poisoned workspace and pivot record equals the run on a
+    zeroed one, bitwise."""
+    from paper_2308_07403_b200 import _lib as L
+
+    dev = torch.device("cuda")
+    a0 = _m_matrix(n, n, dev)
+    outs = []
+    for byte in (0x00, 0xFF, 0x5A):
+        a = a0.clone()
+        work = torch.empty(L.lib().rdb_invert_workspace_bytes(n, 1), dtype=torch.uint8, device=dev).fill_(byte)
+        info = L.pivot_info_tensor(1, dev).fill_(byte)
+        L.check(L.lib().rdb_invert(a.data_ptr(), n, n, work.data_ptr(), info.data_ptr(), L.stream_handle()),
+                "rdb_invert")
+        torch.cuda.synchronize()
+        rec = L.read_pivot_info(info)[0]
+        outs.append((a, rec.min_pivot, rec.min_index, rec.flags))
+    for a, mp, mi, fl in outs[1:]:
+        assert torch.equal(a, outs[0][0])
+        assert (mp, mi, fl) == outs[0][1:]
+    assert outs[0][3] == 0
+
+
+@pytest.mark.parametrize("n", [5, 300, 1100])
+def test_poisoned_workspace_pivoted(cuda, n):
+    """rdb_invert_pivoted (blocked partial pivoting) on a poisoned workspace."""
+    from paper_2308_07403_b200 import _lib as L
+
+    dev = torch.device("cuda")
+    a0 = torch.from_numpy(np.random.default_rng(n).uniform(-1, 1, (n, n))).to(dev)
+    outs = []
+    for byte in (0x00, 0xFF, 0x5A):
+        a = a0.clone()
+        work = torch.empty(L.lib().rdb_invert_pivoted_workspace_bytes(n), dtype=torch.uint8, device=dev).fill_(byte)
+        info = L.pivot_info_tensor(1, dev).fill_(byte)
+        L.check(L.lib().rdb_invert_pivoted(a.data_ptr(), n, n, work.data_ptr(), info.data_ptr(), L.stream_handle()),
+                "rdb_invert_pivoted")
+        torch.cuda.synchronize()
+        rec = L.read_pivot_info(info)[0]
+        outs.append((a, rec.min_pivot, rec.min_index, rec.flags))
+    for a, mp, mi, fl in outs[1:]:
+        assert torch.equal(a, outs[0][0])
+        assert (mp, mi, fl) == outs[0][1:]
+    ref = np.linalg.inv(a0.cpu().numpy())
+    np.testing.assert_allclose(outs[0][0].cpu().numpy(), ref, rtol=1e-8, atol=1e-9)
