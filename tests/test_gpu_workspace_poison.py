@@ -146,3 +146,32 @@ def test_poisoned_workspace_pivoted(cuda, n):
         assert (mp, mi, fl) == outs[0][1:]
     ref = np.linalg.inv(a0.cpu().numpy())
     np.testing.assert_allclose(outs[0][0].cpu().numpy(), ref, rtol=1e-8, atol=1e-9)
+
+
+def test_bench_step_is_deterministic(cuda):
+    """The config-2 bench step (256 graphs, two sub-batch streams, side
+    streams, ticketed tiles, in-kernel waits) replayed 12 times, eagerly and
+    from the captured CUDA graph, gives bitwise the same inverse and D every
+    time: a missing dependency between the streams' kernels or a tile reading
+    an operand another tile is overwriting would show up as a differing run
+    (racecheck is closed on this pool with the other sanitizer tools)."""
+    bits, gam, _ = wl.cfg2_batch(256)
+    dev = torch.device("cuda")
+    sh = torch.cuda.current_stream().cuda_stream
+    buf = B.BatchBuffers.allocate(wl.CFG2["n"], 256, dev, d_dtype="uint8")
+    buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+    buf.gammas.copy_(torch.from_numpy(gam))
+    B.run_chunk(buf, 256, sh)
+    torch.cuda.synchronize()
+    y0, d0 = buf.m.clone(), buf.d.clone()
+    pipe = B.CapturedPipeline(buf, 256)
+    for it in range(12):
+        buf.m.fill_(float("nan"))
+        buf.d.fill_(77)
+        if it % 2:
+            pipe.replay()
+        else:
+            B.run_chunk(buf, 256, sh)
+        torch.cuda.synchronize()
+        assert torch.equal(buf.d, d0), it
+        assert torch.equal(buf.m.view(torch.int64), y0.view(torch.int64)), it
