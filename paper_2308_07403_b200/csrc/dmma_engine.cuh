@@ -90,12 +90,21 @@ struct Tile {
   int nk;                   // number of BK chunks
   int mode;                 // EPI_STORE / EPI_REDUCE
   int neg;                  // write -acc instead of acc
-  // Optional in-kernel dependency (tiles that overwrite another tile's A
+  // Optional in-kernel dependency (tiles that overwrite another tile's
   // operand): after its last k-chunk has landed in shared memory a tile
-  // increments *signal; a tile with wait != nullptr holds its epilogue until
-  // *wait >= wait_target. Waits only ever point at tiles with a smaller index,
-  // and every CTA processes its tiles in increasing order, so the smallest
-  // unfinished tile can always progress (no deadlock).
+  // increments *signal (the producer warp does, from the stage's full
+  // barrier); a tile with wait != nullptr holds its write until *wait >=
+  // wait_target. The awaited tiles are the tile's dependency group: tiles of
+  // smaller index, or the few tiles next to it in index order that share its
+  // operand (the G tiles of a row-panel column, the band tiles at the end of
+  // an update row; G <= 4). Forward progress: a CTA's producer takes no new
+  // tile while the last one's wait is open (its MMA warps never block inside
+  // a tile, so every taken tile is loaded and signalled); tiles are handed
+  // out in index order, so the lowest group with untaken tiles is held by at
+  // most G - 1 CTAs and every other CTA of the launch is released by groups
+  // that are fully taken, then takes the missing tiles. A launch therefore
+  // progresses whenever G of its CTAs can be resident, whatever else shares
+  // the GPU (its grid is never smaller than a group).
   int* signal;
   const int* wait;
   int wait_target;
@@ -316,6 +325,8 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
         break;
       }
       const Tile T = sched.tile(t);
+      int st_last = 0;
+      uint32_t ph_last = 0;
       for (int c = 0; c < T.nk; ++c) {
         mbar_wait(&s.empty[st], ph ^ 1);
         const int k0 = c * BK;
@@ -327,10 +338,29 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
         __syncwarp();
         if (lane < BK)
           bulk_g2s(&s.b[st][lane * BST], T.b + (int64_t)(k0 + lane) * T.ldb, BN * 8, &s.full[st]);
+        st_last = st;
+        ph_last = ph;
         if (++st == STAGES) {
           st = 0;
           ph ^= 1;
         }
+      }
+      // Dependency groups (see Tile::wait). The producer signals as soon as the
+      // tile's last chunk has landed (this stage's full barrier: it cannot be
+      // re-armed before the producer itself refills it), and takes no further
+      // tile until this tile's own wait is satisfied: the MMA warps then never
+      // spin on a counter in the middle of a tile, so the CTA never holds a
+      // tile it cannot finish while sitting on another one the same group
+      // needs (a CTA that drew two tiles of a group deadlocked otherwise).
+      if (T.signal || T.wait) {
+        if (lane == 0) {
+          if (T.signal) {
+            mbar_wait(&s.full[st_last], ph_last);
+            signal_done(T.signal);
+          }
+          if (T.wait) wait_count(T.wait, T.wait_target);
+        }
+        __syncwarp();
       }
     }
     return;
@@ -368,8 +398,6 @@ __device__ __forceinline__ void run(unsigned char* smem_raw, const CUtensorMap* 
 
     for (int c = 0; c < T.nk; ++c) {
       if (!dyn || c > 0) mbar_wait(&s.full[st], ph);
-      // all of this tile's operands are in shared memory: release dependents
-      if (c == T.nk - 1 && T.signal && warp == 0 && lane == 0) signal_done(T.signal);
       if constexpr (kDefer) {
         if (pend_t >= 0 && c == issue_at) {
           epi.issue(sched.tile(pend_t), wr, wc, 0, lane, true, stage_out);

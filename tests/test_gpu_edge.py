@@ -98,7 +98,32 @@ def test_resolvent_result_is_the_reference_dataclass(cuda):
     assert dataclasses.asdict(res)["health"]["inversion_residual"] == res.health.inversion_residual
 
 
-@pytest.mark.timeout(300)
+def _sync_or_die(seconds, what):
+    """Device synchronisation with a deadline. A kernel spinning on an in-kernel
+    wait never returns and no Python-level timeout can interrupt
+    cudaDeviceSynchronize, so a deadlock ends the process here (with a message)
+    instead of hanging the test run."""
+    import os
+    import sys
+    import time
+
+    done = torch.cuda.Event()
+    for st in _ALL_STREAMS:
+        torch.cuda.current_stream().wait_stream(st)
+    done.record()
+    t0 = time.monotonic()
+    while not done.query():
+        if time.monotonic() - t0 > seconds:
+            sys.stderr.write(f"\nDEADLOCK: {what}: the GPU work did not finish in {seconds:.0f} s\n")
+            sys.stderr.flush()
+            os._exit(3)
+        time.sleep(0.002)
+    torch.cuda.synchronize()
+
+
+_ALL_STREAMS: list = []
+
+
 def test_concurrent_inversions_on_three_streams_make_progress(cuda):
     """Forward progress of K2's in-kernel waits with several persistent update
     kernels in flight (gj_invert.cu: tiles by atomic ticket): two batched calls
@@ -126,7 +151,8 @@ def test_concurrent_inversions_on_three_streams_make_progress(cuda):
     m_ref = m0.clone()
     S.invert_in_place(m_ref, 1e-3)
     streams = [torch.cuda.Stream() for _ in range(3)]
-    for _ in range(3):
+    _ALL_STREAMS[:] = streams
+    for _ in range(6):
         m = m0.clone()
         torch.cuda.synchronize()
         for st, buf in zip(streams[:2], bufs):
@@ -137,10 +163,43 @@ def test_concurrent_inversions_on_three_streams_make_progress(cuda):
             info = L.pivot_info_tensor(1, cuda)
             L.check(L.lib().rdb_invert(m.data_ptr(), n, n, work.data_ptr(), info.data_ptr(), streams[2].cuda_stream),
                     "rdb_invert")
-        torch.cuda.synchronize()
+        _sync_or_die(120.0, "concurrent inversions on three streams")
         for buf, ref in zip(bufs, refs):
             assert torch.equal(buf.d, ref)
         assert torch.equal(m, m_ref)
+
+
+def test_four_concurrent_dense_batches_make_progress(cuda):
+    """Four batched calls of dense ER graphs (unsplit: one stream each plus the
+    shared side streams) in flight at once, so every persistent launch gets only
+    a few resident CTAs and a CTA often draws consecutive tiles: the case in
+    which a CTA used to spin on a dependency group whose next tile it held
+    itself (dmma_engine.cuh, Tile::wait). Results equal the serial runs."""
+    seeds = wl.cfg2_seeds(256)[:128]  # the ER half
+    bufs, refs = [], []
+    for k in range(4):
+        pick = seeds[12 * k: 12 * k + 12]
+        bits = np.stack([wl.pack_bits(wl.cfg2_present(kind, s)) for kind, s in pick])
+        gam = np.array([wl.cfg2_gamma(kind) for kind, _ in pick])
+        buf = B.BatchBuffers.allocate(1024, len(pick), cuda)
+        buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+        buf.gammas.copy_(torch.from_numpy(gam))
+        B.run_chunk(buf, len(pick))
+        torch.cuda.synchronize()
+        refs.append(buf.d.clone())
+        bufs.append(buf)
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    _ALL_STREAMS[:] = streams
+    for _ in range(8):
+        for buf in bufs:
+            buf.d.fill_(-1)
+        torch.cuda.synchronize()
+        for st, buf in zip(streams, bufs):
+            with torch.cuda.stream(st):
+                B.run_chunk(buf, buf.chunk, st.cuda_stream)
+        _sync_or_die(120.0, "four concurrent dense batches")
+        for buf, ref in zip(bufs, refs):
+            assert torch.equal(buf.d, ref)
 
 
 @pytest.mark.parametrize("n,count", [(512, 72), (1024, 24), (1536, 24)])  # 72: the two-stream split
