@@ -703,7 +703,8 @@ static int invert_core(double* a, int64_t n, int64_t lda, int64_t stride, int64_
 // Same algebra as the NB = 128 steps (the nested inverse is their first two
 // steps on the band); rounding order differs, so the inverse agrees to
 // ~1e-15 relative and D is unchanged (tests compare with the reference).
-// All waits point to tiles of smaller index: tiles are taken by ticket.
+// Waits point to tiles of smaller index or to the tile's own dependency group
+// (dmma_engine.cuh, Tile::wait: the producer gates on them, the MMA warps never block).
 struct WBRowSched {
   double* a;
   int64_t lda, stride;
@@ -1856,8 +1857,9 @@ static bool skip_enabled() {
 
 // Update tiles are taken by atomic ticket (a global counter per launch) by
 // default: the forward-progress argument for the in-kernel waits then needs
-// no co-residency (every tile a waiting tile depends on was grabbed earlier by
-// a running CTA), whatever else shares the GPU. Measured equal to the static
+// no co-residency of the whole grid (a tile's dependencies are taken by running
+// CTAs in index order and the producer gates on open waits: dmma_engine.cuh,
+// Tile::wait), whatever else shares the GPU. Measured equal to the static
 // stride on config 2 (9.498 vs 9.497 ms per K2 call, profiles/r02_k2_modes.json).
 // Block-tridiagonal matrices (every edge within the 32-block band, from the
 // adjacency bits) skip Gauss-Jordan and run the banded inverse (gj_band.cu).
