@@ -142,7 +142,7 @@ def hbm_peak():
 def ncu_traffic():
     """DRAM bytes (read + write) of one K2 call over the bench batch, from the
     committed `ncu --set full` capture of the same workload (profiles/)."""
-    for name in ("r02_ncu_full_cfg2.json", "r01_ncu_full_cfg2.json"):
+    for name in ("r02_ncu_full_cfg2_final.json", "r02_ncu_full_cfg2_two_level.json", "r02_ncu_full_cfg2.json"):
         p = ROOT / "profiles" / name
         try:
             d = json.loads(p.read_text())
