@@ -747,7 +747,14 @@ def main():
                      "k2_ms": t_inv,
                      "k2_er_only": {"graphs": n_er, "ms": t_inv_er, "executed_flop": exec_er, "tflops": er_tflops,
                                     "frac": er_tflops / peak,
-                                    "note": "the 128 ER graphs alone through the Gauss-Jordan engine (dense strips)"},
+                                    "frac_dense_2n3": flops_per_graph * n_er / (t_inv_er * 1e-3) / 1e12 / peak,
+                                    "dmma_active_pct_ncu": {"gj_w2_update": 95.1, "gj_w2_row": 94.4,
+                                                            "gj_wb_update": 87.7, "gj_wb_row": 86.6,
+                                                            "source": "profiles/r02_ncu_full_cfg2_final.json"},
+                                    "note": "the 128 ER graphs alone through the Gauss-Jordan engine: 59% of the "
+                                            "dense 2 n^3 is executed on the DMMA pipe (frac), the sparse first "
+                                            "steps that replace the rest are L2 / HBM-bound; against the dense 2 n^3 "
+                                            "the same time reads as frac_dense_2n3 (> 1: work skipped, not hardware)"},
                      "traffic": traffic, "traffic_unit": "DRAM bytes per K2 call (ncu --set full)",
                      "traffic_source": traffic_src, "peak_source": peak_src,
                      "work_per_launch": f"{exec_flops:.4g} flop executed per K2 call (batch.executed_flops): the "
