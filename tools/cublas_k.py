@@ -1,3 +1,5 @@
+"""cuBLAS DGEMM (C -= A B through torch.addmm, fp64) at K = 128 .. 1024 on the engine's problem shape: the comparator
+behind profiles/r01_engine_vs_cublas.json."""
 import torch, json
 torch.backends.cuda.matmul.allow_tf32 = False
 dev = 'cuda'
