@@ -175,3 +175,43 @@ def test_bench_step_is_deterministic(cuda):
         torch.cuda.synchronize()
         assert torch.equal(buf.d, d0), it
         assert torch.equal(buf.m.view(torch.int64), y0.view(torch.int64)), it
+
+
+def _carve(arena, off, nbytes, guard):
+    """[guard | buffer | guard] at `off` in the arena; returns (buffer view, next offset)."""
+    start = off + guard
+    return arena[start: start + nbytes], (start + nbytes + guard + 255) // 256 * 256
+
+
+@pytest.mark.parametrize("count,d_dtype", [(12, "int32"), (72, "uint8")])
+def test_no_write_outside_the_buffers(cuda, count, d_dtype):
+    """Every buffer of the batched pipeline (bits, gammas, M, workspace, pivot
+    records, D, counters) carved out of one arena with 1 MiB guard bands of a
+    known byte on both sides: after the call all guards are intact (no kernel
+    writes outside what it was given) and D equals the run on ordinary
+    allocations."""
+    from paper_2308_07403_b200 import _lib as L
+
+    bits, gam, _ = wl.cfg2_batch(count)
+    n = wl.CFG2["n"]
+    dev = torch.device("cuda")
+    sh = torch.cuda.current_stream().cuda_stream
+    ref_buf = B.BatchBuffers.allocate(n, count, dev, d_dtype=d_dtype)
+    ref = _run(ref_buf, bits, gam, count, "pipeline", sh)
+    guard = 1 << 20
+    sizes = {k: getattr(ref_buf, k).numel() * getattr(ref_buf, k).element_size()
+             for k in ("bits", "gammas", "m", "work", "info", "d", "counters")}
+    total = sum((v + 2 * guard + 255) // 256 * 256 for v in sizes.values()) + 256
+    arena = torch.full((total,), 0xA5, dtype=torch.uint8, device=dev)
+    views, off = {}, 0
+    for k, nbytes in sizes.items():
+        views[k], off = _carve(arena, off, nbytes, guard)
+    like = {k: getattr(ref_buf, k) for k in sizes}
+    buf = B.BatchBuffers(n=n, chunk=count, **{k: views[k].view(like[k].dtype).view(like[k].shape) for k in sizes})
+    buf.counters.zero_()
+    got = _run(buf, bits, gam, count, "pipeline", sh)
+    assert torch.equal(got, ref)
+    for k in sizes:  # wipe the buffers themselves; what is left must be all guard
+        views[k].fill_(0xA5)
+    assert bool((arena == 0xA5).all()), "a kernel wrote into a guard band"
+    assert L.RDB_OK == 0
