@@ -215,3 +215,18 @@ def test_no_write_outside_the_buffers(cuda, count, d_dtype):
         views[k].fill_(0xA5)
     assert bool((arena == 0xA5).all()), "a kernel wrote into a guard band"
     assert L.RDB_OK == 0
+
+
+@pytest.mark.parametrize("args", [("selftest",), ("12", "uint8"), ("72", "int32")])
+def test_electric_fence(cuda, args):
+    """tests/fence_run.py in a subprocess (a fault kills the CUDA context): every
+    buffer in its own virtual-memory mapping between unmapped address ranges,
+    flush against the end and then the start; `selftest` checks that an
+    overread really faults."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    script = Path(__file__).resolve().parent / "fence_run.py"
+    proc = subprocess.run([sys.executable, str(script), *args], capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, (proc.stdout[-1500:], proc.stderr[-1500:])
