@@ -202,6 +202,38 @@ def test_four_concurrent_dense_batches_make_progress(cuda):
             assert torch.equal(buf.d, ref)
 
 
+def test_progress_beside_a_gpu_hog(cuda):
+    """The config-2 style batch (split into two sub-batch streams) while another
+    stream keeps the SMs busy with large FP32 GEMMs: the persistent launches
+    then get their SMs a few at a time, in no particular order, and must still
+    finish with the same D."""
+    seeds = wl.cfg2_seeds(256)
+    pick = seeds[0:40] + seeds[128:168]
+    bits = np.stack([wl.pack_bits(wl.cfg2_present(kind, s)) for kind, s in pick])
+    gam = np.array([wl.cfg2_gamma(kind) for kind, _ in pick])
+    buf = B.BatchBuffers.allocate(1024, len(pick), cuda)
+    buf.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+    buf.gammas.copy_(torch.from_numpy(gam))
+    B.run_chunk(buf, len(pick))
+    torch.cuda.synchronize()
+    ref = buf.d.clone()
+    hog_a = torch.randn((6144, 6144), device=cuda)
+    hog_b = torch.randn((6144, 6144), device=cuda)
+    hog_c = torch.empty_like(hog_a)
+    hog, work = torch.cuda.Stream(), torch.cuda.Stream()
+    _ALL_STREAMS[:] = [hog, work]
+    for _ in range(5):
+        buf.d.fill_(-1)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(hog):
+            for _ in range(12):
+                torch.matmul(hog_a, hog_b, out=hog_c)
+        with torch.cuda.stream(work):
+            B.run_chunk(buf, buf.chunk, work.cuda_stream)
+        _sync_or_die(120.0, "batched inversion beside a GEMM hog")
+        assert torch.equal(buf.d, ref)
+
+
 @pytest.mark.parametrize("n,count", [(512, 72), (1024, 24), (1536, 24)])  # 72: the two-stream split
 def test_mixed_batch_dense_wide_plan_and_band_paths(cuda, monkeypatch, n, count):
     """One batched call whose matrices take all three inversion paths at once:
