@@ -190,8 +190,6 @@ def test_no_write_outside_the_buffers(cuda, count, d_dtype):
     known byte on both sides: after the call all guards are intact (no kernel
     writes outside what it was given) and D equals the run on ordinary
     allocations."""
-    from paper_2308_07403_b200 import _lib as L
-
     bits, gam, _ = wl.cfg2_batch(count)
     n = wl.CFG2["n"]
     dev = torch.device("cuda")
@@ -214,7 +212,6 @@ def test_no_write_outside_the_buffers(cuda, count, d_dtype):
     for k in sizes:  # wipe the buffers themselves; what is left must be all guard
         views[k].fill_(0xA5)
     assert bool((arena == 0xA5).all()), "a kernel wrote into a guard band"
-    assert L.RDB_OK == 0
 
 
 @pytest.mark.parametrize("args", [("selftest",), ("12", "uint8"), ("72", "int32")])
