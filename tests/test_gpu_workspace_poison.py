@@ -13,6 +13,15 @@ buffers (which tests/test_gpu_full_parity.py pins to the reference's digests).
 It found one such read: the two-level dense-wide path took the inner level's
 list count from a slot only the sparse-first-step split wrote, so
 RDB_GJ_DW_S0=0 ran with whatever the allocator had left there.
+
+Also here, for the same reason (no sanitizer on this pool): the bench step
+replayed into NaN-filled buffers is bitwise deterministic (racecheck), guard
+bands around every buffer stay intact, and an electric fence — every buffer in
+its own virtual-memory mapping between unmapped address ranges, flush against
+the end and the start (tests/fence_run.py, in a subprocess) — shows that no
+kernel reads or writes outside what it is given (memcheck). RDB_TEST_POISON /
+RDB_TEST_FENCE (tests/conftest.py) apply the first and the last to every
+torch.empty allocation of the whole GPU suite.
 """
 
 import numpy as np
