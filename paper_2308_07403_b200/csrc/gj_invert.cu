@@ -1639,7 +1639,9 @@ static int dw_part(double* a, int64_t n, int64_t lda, int64_t pstride, int64_t p
       // profiles/r02_sm_timeline_k2.json).
       const char* e = getenv("RDB_GJ_DW_LA_RESERVE");
       const int res = e ? atoi(e) : (sm_count() * 7) / 16;
-      if (res > 0 && (int)ugrid > sm_count() - res) ugrid = (unsigned)(sm_count() - res);
+      // (never below 8 CTAs: a launch must be able to hold a whole dependency group, dmma_engine.cuh)
+      const int keep = sm_count() - res > 8 ? sm_count() - res : 8;
+      if (res > 0 && (int)ugrid > keep) ugrid = (unsigned)keep;
       if (dyn && dw_helper() && full > ugrid) helper = full - ugrid;
       if (helper) us.dyn_ctas = (int)(ugrid + helper);
     }
